@@ -1,0 +1,202 @@
+/*
+ * hexsem_b200.h — C-ABI of the B200-native matrix-free SEM PCG solve.
+ *
+ * Drop-in boundary for the reference hexsem solver path (/root/reference/proj):
+ * plain pointers and sizes, no C++ or torch types, no exceptions across the
+ * ABI. Every entry point names the reference interface it replaces.
+ *
+ * Reference plug-in surface being replaced:
+ *   using LinearOp = std::function<void(span<const Real>, span<Real>)>   krylov.hpp:32
+ *   PcgResult pcg(const LinearOp& A, const LinearOp& P, span<const Real> b,
+ *                 const PcgConfig&)                                       krylov.hpp:37-38
+ *   SemSystem build_system(const ProblemConfig&)                          problem.hpp:81
+ *   PoissonResult solve_poisson(const ProblemConfig&)                     problem.hpp:93
+ *   SemOperator::apply                                                    operator.hpp:57
+ *   TwoScalePreconditioner::apply                                         precond.hpp:24
+ *   IndexMaps build_index_maps(const HexMesh&, const GllBasis&)           mesh.hpp:99
+ *
+ * Errors: every function returns HXB_OK (0) or an error code; the message is
+ * available from hxb_last_error() (thread-local). Non-convergence is NOT an
+ * error: it is reported in hxb_pcg_result.status (PcgStatus, krylov.hpp:22).
+ */
+#ifndef HEXSEM_B200_H
+#define HEXSEM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes (reference exception classes they replace). */
+enum {
+  HXB_OK = 0,
+  HXB_EINVAL = 1,   /* std::invalid_argument: bad sizes/params (operator.cpp:69-75, krylov.cpp:23-25) */
+  HXB_EMESH = 2,    /* std::runtime_error: inverted element (geometry.cpp:70-72), non-conforming (mesh.cpp:402-403) */
+  HXB_ENUMERIC = 3, /* std::runtime_error: Cholesky / AMG diagonal / pencil failure (coarse.cpp:126, amg.cpp:145) */
+  HXB_ECUDA = 4,    /* CUDA runtime failure or no sm_100 device */
+  HXB_ENCCL = 5     /* NCCL failure (multi-GPU plans) */
+};
+
+/* PrecondMode (precond.hpp:12) */
+enum { HXB_PRECOND_TWO_SCALE = 0, HXB_PRECOND_FINE_ONLY = 1, HXB_PRECOND_COARSE_ONLY = 2, HXB_PRECOND_NONE = 3 };
+/* CoarseSolve (coarse.hpp:28) */
+enum { HXB_COARSE_AUTOMATIC = 0, HXB_COARSE_DIRECT = 1, HXB_COARSE_AMG = 2 };
+/* OperatorVariant (operator.hpp:14) */
+enum { HXB_VARIANT_STORED = 0, HXB_VARIANT_ON_THE_FLY = 1 };
+/* MeshFamily (mesh.hpp:47) */
+enum { HXB_MESH_UNIFORM = 0, HXB_MESH_DISTORTED_DOMAIN = 1, HXB_MESH_DISTORTED_ELEMENTS = 2 };
+/* BoundaryTag (mesh.hpp:19) */
+enum { HXB_TAG_DIRICHLET = 0, HXB_TAG_NEUMANN = 1 };
+/* PcgStatus (krylov.hpp:22) */
+enum { HXB_PCG_CONVERGED = 0, HXB_PCG_MAX_ITERATIONS = 1, HXB_PCG_BREAKDOWN = 2 };
+
+/* HexMesh (mesh.hpp:38-45): vertices xyz[3*nv]; conn[8*ne] in Gmsh corner
+ * order (mesh.hpp:31-33); boundary faces as parallel arrays (mesh.hpp:24-29).
+ * Borrowed: hxb_plan_create copies what it needs. */
+typedef struct hxb_mesh {
+  int32_t num_vertices;
+  const double* xyz;
+  int32_t num_elements;
+  const int32_t* conn;
+  int32_t num_boundary_faces;
+  const int32_t* bface_element;
+  const int32_t* bface_face;
+  const uint8_t* bface_tag;
+} hxb_mesh;
+
+/* Owned mesh returned by the generators (generate_cube_mesh etc.). */
+typedef struct hxb_mesh_buf {
+  hxb_mesh view;
+  void* impl;
+} hxb_mesh_buf;
+
+/* ProblemConfig solver knobs (problem.hpp:44-53). */
+typedef struct hxb_options {
+  int precond_mode;            /* HXB_PRECOND_* (default two_scale) */
+  int coarse_solve;            /* HXB_COARSE_* (default automatic) */
+  int32_t direct_threshold;    /* vertices; default 64000 (coarse.hpp:36) */
+  int variant;                 /* HXB_VARIANT_* (default stored) */
+  int device;                  /* CUDA device ordinal for this plan */
+  int reserved[7];
+} hxb_options;
+
+/* PcgConfig (krylov.hpp:15-19) */
+typedef struct hxb_pcg_config {
+  double rel_tolerance;        /* (0,1), default 1e-6 */
+  int max_iterations;          /* >= 1, default 500 */
+  int record_history;
+} hxb_pcg_config;
+
+/* PcgResult (krylov.hpp:24-30). History/solution buffers are caller-owned:
+ * residual_history and zr_history hold max_iterations+1 doubles, u holds N.
+ * Any of them may be NULL. */
+typedef struct hxb_pcg_result {
+  int status;                  /* HXB_PCG_* */
+  int iterations;
+  int num_residuals;           /* entries written to residual_history */
+  int num_zr;                  /* entries written to zr_history */
+  double* residual_history;
+  double* zr_history;
+  double* u;
+  double solve_seconds;        /* device-timed solve (CUDA events) */
+  char diagnostic[256];
+} hxb_pcg_result;
+
+/* Plan facts (SolveReport fields, report.hpp:26-46). */
+typedef struct hxb_plan_info {
+  int64_t num_global;          /* N */
+  int64_t num_elements;        /* N_E */
+  int64_t num_vertices;
+  int32_t order;
+  int32_t coarse_uses_amg;
+  int64_t coarse_n;
+  int32_t amg_levels;          /* including the coarsest */
+  int32_t precond_mode;
+  int64_t amg_rows[16];
+  int64_t amg_nnz[16];
+  double setup_seconds;        /* host setup + upload */
+  int64_t device_bytes;        /* device memory held by the plan */
+} hxb_plan_info;
+
+typedef struct hxb_plan hxb_plan;
+
+const char* hxb_last_error(void);
+void hxb_default_options(hxb_options* opt);
+
+/* Mesh sources: generate_box_mesh / generate_cube_mesh / refine_uniform (mesh.hpp:49-62). */
+int hxb_generate_cube_mesh(int k, int family, int boundary_tag, hxb_mesh_buf** out);
+int hxb_generate_box_mesh(int kx, int ky, int kz, const double size[3], int boundary_tag, hxb_mesh_buf** out);
+int hxb_refine_uniform(const hxb_mesh* in, hxb_mesh_buf** out);
+void hxb_mesh_free(hxb_mesh_buf* m);
+
+/* build_system (problem.cpp:73-108) on a caller mesh with per-element kappa/c
+ * (operator.hpp:49-55). Uploads everything once; all vectors stay on the GPU. */
+int hxb_plan_create(const hxb_mesh* mesh, int order, const double* kappa_e, const double* c_e,
+                    const hxb_options* opt, hxb_plan** out);
+int hxb_plan_destroy(hxb_plan* plan);
+int hxb_plan_get_info(const hxb_plan* plan, hxb_plan_info* info);
+
+/* Host-pointer plug-ins: each is a drop-in LinearOp body (krylov.hpp:32). */
+int hxb_apply_A(hxb_plan* plan, const double* u, double* r);          /* SemOperator::apply */
+int hxb_apply_P(hxb_plan* plan, const double* r, double* z);          /* TwoScalePreconditioner::apply */
+int hxb_apply_fine(hxb_plan* plan, const double* r, double* z);       /* FinePreconditioner::apply */
+int hxb_apply_coarse(hxb_plan* plan, const double* r, double* z);     /* CoarsePreconditioner::apply */
+
+/* Device-pointer variants (inputs/outputs already in HBM; stream = cudaStream_t or NULL). */
+int hxb_apply_A_device(hxb_plan* plan, const double* d_u, double* d_r, void* stream);
+int hxb_apply_P_device(hxb_plan* plan, const double* d_r, double* d_z, void* stream);
+
+/* pcg(A, P, b, cfg) with u0 = 0 (krylov.cpp:20-71), entirely on the device.
+ * b = NULL uses the Poisson load b = m_N * 1, masked (problem.cpp:129, 38-46). */
+int hxb_solve(hxb_plan* plan, const double* b, const hxb_pcg_config* cfg, hxb_pcg_result* res);
+int hxb_solve_device(hxb_plan* plan, const double* d_b, const hxb_pcg_config* cfg, hxb_pcg_result* res);
+
+/* assemble_load(s = 1) and lumped_mass (problem.cpp:38-46, operator.hpp:60). */
+int hxb_load_ones(hxb_plan* plan, double* b);
+int hxb_lumped_mass(hxb_plan* plan, double* m);
+
+/* IndexMaps export for the bit-exact numbering check (mesh.hpp:66-97).
+ * Any pointer may be NULL. Sizes: l2g/g2l_elem/g2l_local NE*(n+1)^3,
+ * g2l_offsets N+1, sub_l2g NE*(n+3)^3, mask N. */
+int hxb_export_maps(hxb_plan* plan, int32_t* l2g, int64_t* g2l_offsets, int32_t* g2l_elem,
+                    int32_t* g2l_local, int32_t* sub_l2g, uint8_t* dirichlet_mask);
+
+/* AMG level export for the bit-exact aggregation check (amg.hpp:52-60). */
+int hxb_amg_level(hxb_plan* plan, int level, int64_t* rows, int64_t* nnz, int64_t* ptr, int32_t* col,
+                  double* val, int32_t* aggregate);
+
+/* GPU-free host setup (the build_system work minus the device upload): the
+ * numbering, coarse matrix and AMG aggregation are exported for the
+ * bit-exactness checks against the reference on machines without a GPU. */
+typedef struct hxb_setup hxb_setup;
+int hxb_setup_create(const hxb_mesh* mesh, int order, const double* kappa_e, const double* c_e,
+                     const hxb_options* opt, hxb_setup** out);
+void hxb_setup_destroy(hxb_setup* setup);
+int hxb_setup_info(const hxb_setup* setup, hxb_plan_info* info);
+int hxb_setup_export_maps(const hxb_setup* setup, int32_t* l2g, int64_t* g2l_offsets, int32_t* g2l_elem,
+                          int32_t* g2l_local, int32_t* sub_l2g, uint8_t* dirichlet_mask);
+int hxb_setup_amg_level(const hxb_setup* setup, int level, int64_t* rows, int64_t* nnz, int64_t* ptr,
+                        int32_t* col, double* val, int32_t* aggregate);
+int hxb_setup_lumped_mass(const hxb_setup* setup, double* m);
+
+/* GllBasis (gll.hpp:17-31) and PencilFactorization (fine.hpp:18-26) tables. */
+int hxb_gll(int order, double* nodes, double* weights, double* deriv);
+int hxb_pencil(int order, double* K, double* M, double* V, double* V_inv, double* lambda);
+
+/* Time `reps` back-to-back device Ax applications of the plan's p vector with
+ * CUDA events; returns mean ms per apply (kernel-level bench helper). */
+int hxb_bench_apply_A(hxb_plan* plan, int reps, double* ms_per_apply, double* ms_elem_kernel);
+
+/* Counter models (operator.cpp:20-37, fine.cpp:82-92). */
+uint64_t hxb_words_model(int64_t ne, int order, int variant);
+uint64_t hxb_flops_model(int64_t ne, int order);
+uint64_t hxb_fine_ops_model(int64_t ne, int order);
+uint64_t hxb_fine_words_model(int64_t ne, int order);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HEXSEM_B200_H */

@@ -1,0 +1,261 @@
+// Coarse two-scale component on the device:
+//   restrict_kernel + vertex_gather_kernel   CoarsePreconditioner::restrict_residual
+//                                            (coarse.cpp:138-162) + R[mask]=0 (:191-192)
+//   AMG K-cycle kernels                      AmgHierarchy cycle/ksolve (amg.cpp:198-263)
+//   dense_solve_kernel                       coarsest / direct solve (Eigen LLT in the
+//                                            reference, amg.cpp:188-194, coarse.cpp:201-206)
+// All sums over shared entities use sorted member lists (no atomics).
+#pragma once
+
+#include "kernels_common.cuh"
+
+namespace hxb {
+
+constexpr double kJacobiOmega = 2.0 / 3.0;  // amg.cpp:44
+
+// Per element: Rpart[e*8+cb] = sum_l B[cb][l] * (r/m_N)[l] * m[l]
+template <int NP, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) restrict_kernel(const double* __restrict__ r, const double* __restrict__ lumped,
+                                                         const int* __restrict__ l2g_surf, const double* __restrict__ mass,
+                                                         double* __restrict__ Rpart, int ne, int nsurf, int nsg)
+{
+  constexpr int NLOC = NP * NP * NP, n = NP - 1;
+  const OrderTables& T = c_tab[NP];
+  __shared__ double red[BLOCK / 32][8];
+  const int e = blockIdx.x;
+  const int* surf = l2g_surf + (long long)e * nsurf;
+  const long long ibase = (long long)nsg + (long long)e * (n - 1) * (n - 1) * (n - 1);
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int l = threadIdx.x; l < NLOC; l += BLOCK) {
+    const int i = l % NP, j = (l / NP) % NP, k = l / (NP * NP);
+    const int s = surface_slot(NP, i, j, k);
+    double y;
+    if (s < 0) {
+      const long long g = ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1);
+      y = __ldg(r + g) / __ldg(lumped + g);
+    } else {
+      const int code = __ldg(surf + s);
+      y = code >= 0 ? __ldg(r + code) / __ldg(lumped + code) : 0.0;  // masked r (precond.cpp:35)
+    }
+    const double ym = __ldg(mass + (std::size_t)e * NLOC + l);
+    const double hi[2] = {T.hat0[i], T.hat1[i]}, hj[2] = {T.hat0[j], T.hat1[j]}, hk[2] = {T.hat0[k], T.hat1[k]};
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb) acc[cb] += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[(cb >> 2) & 1] * y * ym;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int cb = 0; cb < 8; ++cb) {
+    double v = acc[cb];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][cb] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; ++w) s += red[w][threadIdx.x];
+    Rpart[8 * e + threadIdx.x] = s;
+  }
+}
+
+// R[v] = vmask[v] ? 0 : sum of Rpart over (e,cb) incidences in ascending order
+__global__ void vertex_gather_kernel(const double* __restrict__ Rpart, const unsigned* __restrict__ off,
+                                     const int* __restrict__ idx, const std::uint8_t* __restrict__ vmask,
+                                     double* __restrict__ R, int nv)
+{
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (unsigned q = __ldg(off + v); q < __ldg(off + v + 1); ++q) s += __ldg(Rpart + __ldg(idx + q));
+    R[v] = __ldg(vmask + v) ? 0.0 : s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// AMG level data (device pointers)
+struct DevCsr {
+  int n;
+  const int* ptr;
+  const int* col;
+  const double* val;
+};
+
+__device__ __forceinline__ double csr_row_dot(const DevCsr& A, int i, const double* __restrict__ x)
+{
+  double s = 0.0;
+  for (int q = __ldg(A.ptr + i); q < __ldg(A.ptr + i + 1); ++q) s += __ldg(A.val + q) * __ldg(x + __ldg(A.col + q));
+  return s;
+}
+
+// z = z1 + w d (r - A z1), z1 = w d r computed on the fly (amg.cpp:212-213)
+__global__ void amg_jacobi2_kernel(DevCsr A, const double* __restrict__ dinv, const double* __restrict__ r,
+                                   double* __restrict__ z)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = __ldg(A.ptr + i); q < __ldg(A.ptr + i + 1); ++q) {
+      const int c = __ldg(A.col + q);
+      s += __ldg(A.val + q) * (kJacobiOmega * __ldg(dinv + c) * __ldg(r + c));
+    }
+    const double z1 = kJacobiOmega * __ldg(dinv + i) * __ldg(r + i);
+    z[i] = z1 + kJacobiOmega * __ldg(dinv + i) * (__ldg(r + i) - s);
+  }
+}
+
+// rc[c] = sum over members i of aggregate c (ascending) of (r_i - (A z)_i)  (amg.cpp:214-218)
+__global__ void amg_resid_restrict_kernel(DevCsr A, const double* __restrict__ r, const double* __restrict__ z,
+                                          const int* __restrict__ agg_ptr, const int* __restrict__ agg_mem,
+                                          double* __restrict__ rc, int nc)
+{
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = __ldg(agg_ptr + c); q < __ldg(agg_ptr + c + 1); ++q) {
+      const int i = __ldg(agg_mem + q);
+      s += __ldg(r + i) - csr_row_dot(A, i, z);
+    }
+    rc[c] = s;
+  }
+}
+
+// zout = z3 + w d (r - A z3), z3 = zin + ec[agg] on the fly (amg.cpp:220-222)
+__global__ void amg_prolong_smooth_kernel(DevCsr A, const double* __restrict__ dinv, const double* __restrict__ r,
+                                          const double* __restrict__ zin, const double* __restrict__ ec,
+                                          const int* __restrict__ agg, double* __restrict__ zout)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int q = __ldg(A.ptr + i); q < __ldg(A.ptr + i + 1); ++q) {
+      const int c = __ldg(A.col + q);
+      s += __ldg(A.val + q) * (__ldg(zin + c) + __ldg(ec + __ldg(agg + c)));
+    }
+    const double z3 = __ldg(zin + i) + __ldg(ec + __ldg(agg + i));
+    zout[i] = z3 + kJacobiOmega * __ldg(dinv + i) * (__ldg(r + i) - s);
+  }
+}
+
+// zout = zin + w d (r - A zin)   (amg.cpp:204-208)
+__global__ void amg_smooth_kernel(DevCsr A, const double* __restrict__ dinv, const double* __restrict__ r,
+                                  const double* __restrict__ zin, double* __restrict__ zout)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+    const double s = csr_row_dot(A, i, zin);
+    zout[i] = __ldg(zin + i) + kJacobiOmega * __ldg(dinv + i) * (__ldg(r + i) - s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K-cycle inner PCG (amg.cpp:230-263). Scalars of one ksolve invocation:
+struct KScalars {
+  double zr, pf, zr_next;
+  int stopped;
+  int pad;
+};
+
+// r = b; x = 0; stopped = 0
+__global__ void amg_kinit_kernel(const double* __restrict__ b, double* __restrict__ r, double* __restrict__ x, int n,
+                                 KScalars* ks)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    r[i] = b[i];
+    x[i] = 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ks->stopped = 0;
+}
+
+// result = z.r, optionally p = z
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) amg_dot_kernel(const double* __restrict__ z, const double* __restrict__ r,
+                                                       double* __restrict__ p, int n, DotArgs d)
+{
+  __shared__ double red[BLOCK / 32];
+  double s = 0.0;
+  for (int i = blockIdx.x * BLOCK + threadIdx.x; i < n; i += gridDim.x * BLOCK) {
+    const double zi = z[i];
+    s += zi * r[i];
+    if (p) p[i] = zi;
+  }
+  dot_commit<BLOCK>(d, s, red);
+}
+
+// f = A p; result = p.f
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) amg_spmv_dot_kernel(DevCsr A, const double* __restrict__ p,
+                                                            double* __restrict__ f, DotArgs d)
+{
+  __shared__ double red[BLOCK / 32];
+  double s = 0.0;
+  for (int i = blockIdx.x * BLOCK + threadIdx.x; i < A.n; i += gridDim.x * BLOCK) {
+    const double fi = csr_row_dot(A, i, p);
+    f[i] = fi;
+    s += p[i] * fi;
+  }
+  dot_commit<BLOCK>(d, s, red);
+}
+
+// if (!(pf > 0) || !(|zr| > 0)) stop; else x += a p, r -= a f  (amg.cpp:244-253)
+__global__ void amg_kupdate_kernel(const double* __restrict__ p, const double* __restrict__ f, double* __restrict__ x,
+                                   double* __restrict__ r, int n, KScalars* ks)
+{
+  const double pf = ks->pf, zr = ks->zr;
+  const bool stop = ks->stopped || !(pf > 0) || !(fabs(zr) > 0);
+  if (stop) {
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) ks->stopped = 1;
+    return;
+  }
+  const double alpha = zr / pf;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    x[i] += alpha * p[i];
+    r[i] -= alpha * f[i];
+  }
+}
+
+// beta = zr_next/zr; zr = zr_next; p = z + beta p   (amg.cpp:256-260)
+__global__ void amg_kdir_kernel(const double* __restrict__ z, double* __restrict__ p, int n, KScalars* ks)
+{
+  if (ks->stopped) return;
+  const double beta = ks->zr_next / ks->zr;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = z[i] + beta * p[i];
+}
+
+// after kdir: zr <- zr_next (separate tiny kernel keeps kdir free of a grid-wide race)
+__global__ void amg_kshift_kernel(KScalars* ks)
+{
+  if (!ks->stopped) ks->zr = ks->zr_next;
+}
+
+// rho = R - K Z
+__global__ void amg_resid_kernel(DevCsr A, const double* __restrict__ R, const double* __restrict__ Z,
+                                 double* __restrict__ rho)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x)
+    rho[i] = __ldg(R + i) - csr_row_dot(A, i, Z);
+}
+
+__global__ void axpy1_kernel(double* __restrict__ y, const double* __restrict__ x, int n)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] += x[i];
+}
+
+// Dense coarse solve: z[coupled[r]] = sum_c Ainv[r][c] b[coupled[c]]; z[i] = b[i]*inv_diag[i] otherwise.
+// One warp per coupled row (coalesced row reads).
+__global__ void dense_solve_kernel(const double* __restrict__ ainv, const int* __restrict__ coupled, int m,
+                                   const double* __restrict__ inv_diag, const double* __restrict__ b,
+                                   double* __restrict__ z, int n)
+{
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int rr = warp; rr < m; rr += nwarps) {
+    const double* row = ainv + (std::size_t)rr * m;
+    double s = 0.0;
+    for (int c = lane; c < m; c += 32) s += row[c] * __ldg(b + __ldg(coupled + c));
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (lane == 0) z[__ldg(coupled + rr)] = s;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double di = __ldg(inv_diag + i);
+    if (di != 0.0) z[i] = __ldg(b + i) * di;
+  }
+}
+
+}  // namespace hxb

@@ -1,0 +1,112 @@
+// Shared device helpers: constant-memory operator tables, deterministic
+// reductions, index encodings. sm_100a, FP64 throughout.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hxb {
+
+constexpr int kMaxNP = 11;         // orders 1..10
+constexpr int kMaxP = kMaxNP + 2;  // FDM pencil size n+3
+
+// Per-order operator tables. Index [NP] selects the order so plans of
+// different orders can coexist; within a kernel NP is a template constant and
+// every loop over these tables is fully unrolled, so each entry becomes a
+// constant-bank operand of the DFMA (no register or shared-memory traffic).
+struct OrderTables {
+  double D[kMaxNP * kMaxNP];   // D[m*np+i] = phi'_m(t_i), gll.hpp:23-26
+  double V[kMaxP * kMaxP];     // pencil V     (fine.hpp:22)
+  double Vi[kMaxP * kMaxP];    // pencil V^-1  (fine.hpp:23)
+  double M[kMaxP];             // pencil lumped mass (fine.hpp:21)
+  double lam[kMaxP];           // pencil eigenvalues (fine.hpp:24)
+  double hat0[kMaxNP];         // 0.5*(1-t_i)  coarse hats (gll.cpp:92)
+  double hat1[kMaxNP];         // 0.5*(1+t_i)
+};
+// Single translation unit (plan.cu) includes the kernels, so this is the definition.
+__constant__ OrderTables c_tab[kMaxNP + 1];
+
+// Global-id encodings in the gather/scatter maps:
+//   v >= 0   free node v
+//   v == -1  no node (sentinel slot, IndexMaps::kNoNode)
+//   v <= -2  Dirichlet node (-v-2): reads as 0 (masked input, operator.cpp:264,
+//            precond.cpp:35)
+__host__ __device__ inline int encode_dirichlet(int g) { return -g - 2; }
+__device__ __forceinline__ double load_masked(const double* __restrict__ x, int code)
+{
+  return code >= 0 ? __ldg(x + code) : 0.0;
+}
+
+// Rank of local node (i,j,k) among element-surface nodes in ascending local
+// index, -1 for element-interior (mirrors setup_numbering.cpp).
+__host__ __device__ __forceinline__ int surface_slot(int np, int i, int j, int k)
+{
+  const int n = np - 1, mid = 4 * np - 4;
+  if (k == 0) return j * np + i;
+  if (k == n) return np * np + (np - 2) * mid + j * np + i;
+  const int base = np * np + (k - 1) * mid;
+  if (j == 0) return base + i;
+  if (j == n) return base + np + 2 * (np - 2) + i;
+  if (i == 0) return base + np + 2 * (j - 1);
+  if (i == n) return base + np + 2 * (j - 1) + 1;
+  return -1;
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic dot products. Each participating kernel block reduces its
+// partial in a fixed tree and stores it at partials[offset + blockIdx.x]; the
+// last block to finish (ticket) sums partials[0 .. offset+gridDim.x) in a
+// fixed order. Results are bitwise reproducible run to run.
+struct DotArgs {
+  double* partials = nullptr;  // null: no dot requested
+  unsigned* ticket = nullptr;
+  double* result = nullptr;    // null: only store partials (a later kernel finalizes)
+  int offset = 0;
+};
+
+template <int BLOCK>
+__device__ __forceinline__ double block_sum(double v, double* red)
+{
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int w = 0; w < BLOCK / 32; ++w) s += red[w];
+  }
+  return s;  // valid in thread 0
+}
+
+// Must be called by every thread of the block (linear block of BLOCK threads).
+template <int BLOCK>
+__device__ void dot_commit(const DotArgs& d, double v, double* red)
+{
+  if (d.partials == nullptr) return;
+  const double s = block_sum<BLOCK>(v, red);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    d.partials[d.offset + blockIdx.x] = s;
+    last = false;
+    if (d.result != nullptr) {
+      __threadfence();
+      const unsigned t = atomicAdd(d.ticket, 1u);
+      last = (t == gridDim.x - 1);
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int total = d.offset + gridDim.x;
+  double acc = 0;
+  for (int q = threadIdx.x; q < total; q += BLOCK) acc += __ldcg(d.partials + q);
+  const double tot = block_sum<BLOCK>(acc, red);
+  if (threadIdx.x == 0) {
+    *d.result = tot;
+    *d.ticket = 0;
+  }
+}
+
+}  // namespace hxb

@@ -1,0 +1,1036 @@
+// Device plan: setup upload, kernel orchestration, device-resident PCG, and
+// the C-ABI declared in include/hexsem_b200.h.
+//
+// A plan is the B200 counterpart of the reference SemSystem
+// (problem.hpp:68-85): built once from the mesh, it owns every device array;
+// the PCG loop (krylov.cpp:20-71) runs entirely on the GPU with one 16-byte
+// status read-back per iteration. The coarse correction runs on its own
+// stream as a captured CUDA graph, concurrently with the fine FDM solves
+// (the reference's std::async, precond.cpp:40-46).
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hexsem_b200.h"
+#include "kernels_ax.cuh"
+#include "kernels_coarse.cuh"
+#include "kernels_common.cuh"
+#include "kernels_fine.cuh"
+#include "kernels_vec.cuh"
+#include "capi_common.hpp"
+#include "setup.hpp"
+
+namespace hxb {
+
+namespace {
+
+
+#define HXB_CUDA(call)                                                                              \
+  do {                                                                                              \
+    cudaError_t err__ = (call);                                                                     \
+    if (err__ != cudaSuccess)                                                                       \
+      throw HxbError(HXB_ECUDA, std::string(#call) + ": " + cudaGetErrorString(err__));             \
+  } while (0)
+
+constexpr int kVecBlock = 256;
+
+int vec_grid(long long n)
+{
+  const long long b = (n + kVecBlock - 1) / kVecBlock;
+  return static_cast<int>(std::max(1LL, std::min(b, 148LL * 4)));
+}
+
+// --- device memory tracking -------------------------------------------------
+struct DeviceArena {
+  std::vector<void*> ptrs;
+  std::size_t bytes = 0;
+  template <class T>
+  T* alloc(std::size_t count)
+  {
+    if (count == 0) count = 1;
+    void* p = nullptr;
+    HXB_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    ptrs.push_back(p);
+    bytes += count * sizeof(T);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& h)
+  {
+    T* d = alloc<T>(h.size());
+    if (!h.empty()) HXB_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return d;
+  }
+  ~DeviceArena()
+  {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+struct DevLevel {
+  int n = 0, nc = 0;
+  DevCsr A{};
+  double* dinv = nullptr;
+  int* agg = nullptr;
+  int* agg_ptr = nullptr;
+  int* agg_mem = nullptr;
+  double *zA = nullptr, *zB = nullptr, *kr = nullptr, *kz = nullptr, *kp = nullptr, *kf = nullptr;
+  double *b = nullptr, *x = nullptr;  // rc/ec targets from the finer level's cycle
+  KScalars* ks = nullptr;
+};
+
+struct DevDense {
+  int n = 0, m = 0;
+  double* ainv = nullptr;
+  int* coupled = nullptr;
+  double* inv_diag = nullptr;
+};
+
+}  // namespace
+
+struct Plan {
+  int device = 0;
+  cudaStream_t s_main = nullptr, s_coarse = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_a = nullptr;
+  cudaGraphExec_t coarse_exec = nullptr;
+  DeviceArena mem;
+
+  int order = 0, np = 0, nloc = 0, nsurf = 0, P = 0;
+  int ne = 0, nv = 0, N = 0, nsg = 0;
+  int precond_mode = 0, variant = 0;
+  bool do_fine = false, do_coarse = false, use_amg = false;
+  double setup_seconds = 0;
+
+  // host state kept for exports (planes dropped after upload)
+  HostSetup hs;
+  gid coarse_n = 0;
+
+  // device arrays
+  double* wg = nullptr;
+  double* mass = nullptr;
+  double* c_e = nullptr;
+  double* kappa_e = nullptr;
+  double* h3 = nullptr;
+  int* l2g_surf = nullptr;
+  unsigned* ax_off = nullptr;
+  int* ax_idx = nullptr;
+  short* surf_local = nullptr;
+  std::uint8_t* mask = nullptr;
+  double* d_lumped = nullptr;
+  int* sub_face = nullptr;
+  unsigned* fine_off = nullptr;
+  int* fine_idx = nullptr;
+  double* zsub = nullptr;
+  int* conn = nullptr;
+  unsigned* vtx_off = nullptr;
+  int* vtx_idx = nullptr;
+  std::uint8_t* vmask = nullptr;
+  double *Rpart = nullptr, *R = nullptr, *Z = nullptr, *rho = nullptr, *dZ = nullptr;
+  std::vector<DevLevel> lv;  // AMG levels 0..L (L = coarsest, uses dense)
+  DevDense dense;
+  DevCsr Kc{};               // K_c on the device (AMG mode: residual between the two K-cycles)
+  std::uint8_t* zero_mask = nullptr;
+
+  // PCG vectors
+  double *u = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *f = nullptr, *b = nullptr, *rsurf = nullptr;
+  // scalars / reductions
+  double* partials = nullptr;
+  unsigned* ticket = nullptr;
+  double* cpartials = nullptr;
+  unsigned* cticket = nullptr;
+  double* zr_hist = nullptr;
+  double* pf_hist = nullptr;
+  double* res_hist = nullptr;
+  double* res2 = nullptr;
+  double* scratch = nullptr;
+  double* h_status = nullptr;  // pinned
+  int hist_cap = 0;
+
+  ~Plan()
+  {
+    if (coarse_exec) cudaGraphExecDestroy(coarse_exec);
+    for (cudaEvent_t e : {ev_fork, ev_join, ev_t0, ev_t1, ev_a})
+      if (e) cudaEventDestroy(e);
+    if (s_main) cudaStreamDestroy(s_main);
+    if (s_coarse) cudaStreamDestroy(s_coarse);
+    if (h_status) cudaFreeHost(h_status);
+  }
+};
+
+namespace {
+
+// --- template dispatch over the polynomial order --------------------------
+#define HXB_DISPATCH_NP(np, F, ...)                         \
+  switch (np) {                                             \
+    case 2: F<2>(__VA_ARGS__); break;                       \
+    case 3: F<3>(__VA_ARGS__); break;                       \
+    case 4: F<4>(__VA_ARGS__); break;                       \
+    case 5: F<5>(__VA_ARGS__); break;                       \
+    case 6: F<6>(__VA_ARGS__); break;                       \
+    case 7: F<7>(__VA_ARGS__); break;                       \
+    case 8: F<8>(__VA_ARGS__); break;                       \
+    case 9: F<9>(__VA_ARGS__); break;                       \
+    case 10: F<10>(__VA_ARGS__); break;                     \
+    case 11: F<11>(__VA_ARGS__); break;                     \
+    default: throw HxbError(HXB_EINVAL, "order out of range 1..10"); \
+  }
+
+DotArgs dot_args(Plan& pl, double* result, int offset = 0)
+{
+  DotArgs d;
+  d.partials = pl.partials;
+  d.ticket = pl.ticket;
+  d.result = result;
+  d.offset = offset;
+  return d;
+}
+
+DotArgs cdot_args(Plan& pl, double* result)
+{
+  DotArgs d;
+  d.partials = pl.cpartials;
+  d.ticket = pl.cticket;
+  d.result = result;
+  d.offset = 0;
+  return d;
+}
+
+template <int NP>
+void launch_ax_elem(Plan& pl, const double* u, double* r, DotArgs dot, cudaStream_t s)
+{
+  using Sh = AxShape<NP>;
+  AxArgs a;
+  a.u = u;
+  a.wg = pl.wg;
+  a.plane_stride = static_cast<std::size_t>(pl.ne) * pl.nloc;
+  a.mass = pl.mass;
+  a.c_e = pl.c_e;
+  a.l2g_surf = pl.l2g_surf;
+  a.rsurf = pl.rsurf;
+  a.r = r;
+  a.ne = pl.ne;
+  a.nsurf = pl.nsurf;
+  a.num_surface_global = pl.nsg;
+  a.dot = dot;
+  const int grid = (pl.ne + Sh::kEPB - 1) / Sh::kEPB;
+  const std::size_t smem = Sh::kSmemDoubles * sizeof(double);
+  ax_elem_kernel<NP><<<grid, Sh::kBlock, smem, s>>>(a);
+}
+
+int ax_elem_grid(const Plan& pl)
+{
+  int g = 0;
+  auto f = [&](auto tag) {
+    constexpr int NP = decltype(tag)::value;
+    g = (pl.ne + AxShape<NP>::kEPB - 1) / AxShape<NP>::kEPB;
+  };
+  switch (pl.np) {
+#define C(NPV) \
+  case NPV: f(std::integral_constant<int, NPV>{}); break;
+    C(2) C(3) C(4) C(5) C(6) C(7) C(8) C(9) C(10) C(11)
+#undef C
+  }
+  return g;
+}
+
+// f = A u (+ optional u.f into *dot_result)
+void enqueue_ax(Plan& pl, const double* u, double* r, double* dot_result, cudaStream_t s)
+{
+  const int g_elem = ax_elem_grid(pl);
+  DotArgs d1{}, d2{};
+  if (dot_result) {
+    d1 = dot_args(pl, nullptr, 0);
+    d2 = dot_args(pl, dot_result, g_elem);
+  }
+  HXB_DISPATCH_NP(pl.np, launch_ax_elem, pl, u, r, d1, s);
+  AxGatherArgs g;
+  g.rsurf = pl.rsurf;
+  g.off = pl.ax_off;
+  g.idx = pl.ax_idx;
+  g.u = u;
+  g.mask = pl.mask;
+  g.r = r;
+  g.num_surface_global = pl.nsg;
+  g.dot = d2;
+  ax_gather_kernel<kVecBlock><<<vec_grid(pl.nsg), kVecBlock, 0, s>>>(g);
+}
+
+template <int NP>
+void launch_fdm(Plan& pl, cudaStream_t s)
+{
+  FdmArgs a;
+  a.r = pl.r;
+  a.l2g_surf = pl.l2g_surf;
+  a.sub_face = pl.sub_face;
+  a.h3 = pl.h3;
+  a.kappa_e = pl.kappa_e;
+  a.c_e = pl.c_e;
+  a.zsub = pl.zsub;
+  a.ne = pl.ne;
+  a.nsurf = pl.nsurf;
+  a.num_surface_global = pl.nsg;
+  fdm_kernel<NP><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
+}
+
+template <int NP>
+void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse)
+{
+  CombineArgs a;
+  a.r = pl.r;
+  a.mask = pl.mask;
+  a.zsub = pl.zsub;
+  a.fine_off = pl.fine_off;
+  a.fine_idx = pl.fine_idx;
+  a.Z = pl.Z;
+  a.conn = pl.conn;
+  a.mass = pl.mass;
+  a.lumped = pl.d_lumped;
+  a.ax_off = pl.ax_off;
+  a.ax_idx = pl.ax_idx;
+  a.surf_local = pl.surf_local;
+  a.z = pl.z;
+  a.N = pl.N;
+  a.num_surface_global = pl.nsg;
+  a.nsurf = pl.nsurf;
+  a.do_fine = do_fine ? 1 : 0;
+  a.do_coarse = do_coarse ? 1 : 0;
+  a.dot = zr_result ? dot_args(pl, zr_result) : DotArgs{};
+  combine_kernel<NP, kVecBlock><<<vec_grid(pl.N), kVecBlock, 0, s>>>(a);
+}
+
+template <int NP>
+void launch_restrict(Plan& pl, cudaStream_t s)
+{
+  restrict_kernel<NP, 128><<<pl.ne, 128, 0, s>>>(pl.r, pl.d_lumped, pl.l2g_surf, pl.mass, pl.Rpart, pl.ne, pl.nsurf,
+                                                   pl.nsg);
+}
+
+// ---- AMG enqueue (captured into the coarse graph) --------------------------
+void enqueue_dense(Plan& pl, const double* b, double* x, cudaStream_t s)
+{
+  const DevDense& d = pl.dense;
+  const int threads = 256;
+  const int rows_per_block = threads / 32;
+  int grid = std::max((d.m + rows_per_block - 1) / rows_per_block, (d.n + threads - 1) / threads);
+  grid = std::max(1, std::min(grid, 148 * 8));
+  dense_solve_kernel<<<grid, threads, 0, s>>>(d.ainv, d.coupled, d.m, d.inv_diag, b, x, d.n);
+}
+
+void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s);
+
+void enqueue_cycle(Plan& pl, int l, const double* r, double* zout, cudaStream_t s)
+{
+  const int L = static_cast<int>(pl.lv.size()) - 1;
+  if (l == L) {
+    enqueue_dense(pl, r, zout, s);
+    return;
+  }
+  DevLevel& v = pl.lv[l];
+  DevLevel& c = pl.lv[l + 1];
+  const int g = vec_grid(v.n);
+  amg_jacobi2_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA);
+  amg_resid_restrict_kernel<<<vec_grid(v.nc), kVecBlock, 0, s>>>(v.A, r, v.zA, v.agg_ptr, v.agg_mem, c.b, v.nc);
+  enqueue_ksolve(pl, l + 1, c.b, c.x, s);
+  amg_prolong_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
+  amg_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout);
+}
+
+void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
+{
+  const int L = static_cast<int>(pl.lv.size()) - 1;
+  if (l == L) {
+    enqueue_dense(pl, b, x, s);
+    return;
+  }
+  DevLevel& v = pl.lv[l];
+  const int g = vec_grid(v.n);
+  amg_kinit_kernel<<<g, kVecBlock, 0, s>>>(b, v.kr, x, v.n, v.ks);
+  enqueue_cycle(pl, l, v.kr, v.kz, s);
+  amg_dot_kernel<kVecBlock><<<g, kVecBlock, 0, s>>>(v.kz, v.kr, v.kp, v.n, cdot_args(pl, &v.ks->zr));
+  for (int it = 0; it < 2; ++it) {
+    amg_spmv_dot_kernel<kVecBlock><<<g, kVecBlock, 0, s>>>(v.A, v.kp, v.kf, cdot_args(pl, &v.ks->pf));
+    amg_kupdate_kernel<<<g, kVecBlock, 0, s>>>(v.kp, v.kf, x, v.kr, v.n, v.ks);
+    if (it == 1) break;
+    enqueue_cycle(pl, l, v.kr, v.kz, s);
+    amg_dot_kernel<kVecBlock><<<g, kVecBlock, 0, s>>>(v.kz, v.kr, nullptr, v.n, cdot_args(pl, &v.ks->zr_next));
+    amg_kdir_kernel<<<g, kVecBlock, 0, s>>>(v.kz, v.kp, v.n, v.ks);
+    amg_kshift_kernel<<<1, 1, 0, s>>>(v.ks);
+  }
+}
+
+// restrict -> mask -> coarse solve; leaves Z (coarse.cpp:188-206)
+void enqueue_coarse(Plan& pl, cudaStream_t s)
+{
+  HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s);
+  vertex_gather_kernel<<<vec_grid(pl.nv), kVecBlock, 0, s>>>(pl.Rpart, pl.vtx_off, pl.vtx_idx, pl.vmask, pl.R, pl.nv);
+  if (pl.use_amg) {
+    enqueue_cycle(pl, 0, pl.R, pl.Z, s);
+    // two composed K-cycles: Z = B R + B (R - K_c B R)  (coarse.cpp:193-200)
+    const DevCsr K = pl.Kc;
+    amg_resid_kernel<<<vec_grid(K.n), kVecBlock, 0, s>>>(K, pl.R, pl.Z, pl.rho);
+    enqueue_cycle(pl, 0, pl.rho, pl.dZ, s);
+    axpy1_kernel<<<vec_grid(K.n), kVecBlock, 0, s>>>(pl.Z, pl.dZ, K.n);
+  } else {
+    enqueue_dense(pl, pl.R, pl.Z, s);
+  }
+}
+
+void capture_coarse_graph(Plan& pl)
+{
+  cudaGraph_t graph;
+  HXB_CUDA(cudaStreamBeginCapture(pl.s_coarse, cudaStreamCaptureModeThreadLocal));
+  enqueue_coarse(pl, pl.s_coarse);
+  HXB_CUDA(cudaStreamEndCapture(pl.s_coarse, &graph));
+  HXB_CUDA(cudaGraphInstantiate(&pl.coarse_exec, graph, 0));
+  cudaGraphDestroy(graph);
+}
+
+// z = P r (reads pl.r, writes pl.z); optional z.r into *zr_result
+void enqueue_precond(Plan& pl, double* zr_result)
+{
+  cudaStream_t s = pl.s_main;
+  if (pl.precond_mode == HXB_PRECOND_NONE) {
+    copy_dot_kernel<kVecBlock><<<vec_grid(pl.N), kVecBlock, 0, s>>>(pl.r, pl.r, pl.z, pl.N,
+                                                                     zr_result ? dot_args(pl, zr_result) : DotArgs{});
+    return;
+  }
+  if (pl.do_coarse) {
+    HXB_CUDA(cudaEventRecord(pl.ev_fork, s));
+    HXB_CUDA(cudaStreamWaitEvent(pl.s_coarse, pl.ev_fork, 0));
+    HXB_CUDA(cudaGraphLaunch(pl.coarse_exec, pl.s_coarse));
+    HXB_CUDA(cudaEventRecord(pl.ev_join, pl.s_coarse));
+  }
+  if (pl.do_fine) HXB_DISPATCH_NP(pl.np, launch_fdm, pl, s);
+  if (pl.do_coarse) HXB_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
+  HXB_DISPATCH_NP(pl.np, launch_combine, pl, zr_result, s, pl.do_fine, pl.do_coarse);
+}
+
+// ---------------------------------------------------------------------------
+// Setup
+
+void upload_tables(const GllBasis& basis, const Pencil& pencil)
+{
+  OrderTables t{};
+  const int np = basis.npts();
+  for (int q = 0; q < np * np; ++q) t.D[q] = basis.deriv[q];
+  for (int q = 0; q < pencil.p * pencil.p; ++q) {
+    t.V[q] = pencil.V[q];
+    t.Vi[q] = pencil.V_inv[q];
+  }
+  for (int q = 0; q < pencil.p; ++q) {
+    t.M[q] = pencil.M[q];
+    t.lam[q] = pencil.lambda[q];
+  }
+  for (int i = 0; i < np; ++i) {
+    t.hat0[i] = 0.5 * (1 - basis.nodes[i]);
+    t.hat1[i] = 0.5 * (1 + basis.nodes[i]);
+  }
+  HXB_CUDA(cudaMemcpyToSymbol(c_tab, &t, sizeof(OrderTables), sizeof(OrderTables) * np));
+}
+
+// CSR by counting sort of a flat (already ascending) source index stream.
+struct GatherCsr {
+  std::vector<unsigned> off;
+  std::vector<int> idx;
+};
+
+void dense_to_device(Plan& pl, const Csr& A)
+{
+  DenseCoarse dc = dense_coarse_setup(A, 1500);
+  DevDense& d = pl.dense;
+  d.n = dc.n;
+  d.m = static_cast<int>(dc.coupled.size());
+  d.coupled = pl.mem.upload(dc.coupled);
+  d.inv_diag = pl.mem.upload(dc.inv_diag);
+  const std::size_t mm = static_cast<std::size_t>(d.m) * d.m;
+  if (!dc.ainv.empty() || d.m == 0) {
+    d.ainv = pl.mem.upload(dc.ainv);
+    return;
+  }
+  // large coupled block: Cholesky + inverse on the device (cuSOLVER potrf/potri)
+  d.ainv = pl.mem.alloc<double>(mm);
+  HXB_CUDA(cudaMemcpy(d.ainv, dc.coupled_a.data(), mm * sizeof(double), cudaMemcpyHostToDevice));
+  cusolverDnHandle_t h;
+  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw HxbError(HXB_ECUDA, "cusolverDnCreate failed");
+  int lwork = 0, lwork2 = 0;
+  cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, d.m, d.ainv, d.m, &lwork);
+  cusolverDnDpotri_bufferSize(h, CUBLAS_FILL_MODE_LOWER, d.m, d.ainv, d.m, &lwork2);
+  lwork = std::max(lwork, lwork2);
+  double* work = nullptr;
+  int* info = nullptr;
+  HXB_CUDA(cudaMalloc(&work, sizeof(double) * std::max(1, lwork)));
+  HXB_CUDA(cudaMalloc(&info, sizeof(int)));
+  int hinfo = 0;
+  cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, d.m, d.ainv, d.m, work, lwork, info);
+  HXB_CUDA(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
+  if (hinfo == 0) {
+    cusolverDnDpotri(h, CUBLAS_FILL_MODE_LOWER, d.m, d.ainv, d.m, work, lwork, info);
+    HXB_CUDA(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
+  }
+  cudaFree(work);
+  cudaFree(info);
+  cusolverDnDestroy(h);
+  if (hinfo != 0) throw HxbError(HXB_ENUMERIC, "coarse matrix Cholesky failed (matrix not SPD?)");
+  // potri fills one triangle (column-major lower == row-major upper); mirror it
+  std::vector<double> hinv(mm);
+  HXB_CUDA(cudaMemcpy(hinv.data(), d.ainv, mm * sizeof(double), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < d.m; ++i)
+    for (int j = i + 1; j < d.m; ++j) hinv[static_cast<std::size_t>(j) * d.m + i] = hinv[static_cast<std::size_t>(i) * d.m + j];
+  HXB_CUDA(cudaMemcpy(d.ainv, hinv.data(), mm * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+DevCsr csr_to_device(Plan& pl, const Csr& A)
+{
+  if (A.nnz() > 0x7fffffffULL) throw HxbError(HXB_EINVAL, "coarse matrix too large");
+  std::vector<int> ptr(A.ptr.begin(), A.ptr.end());
+  DevCsr d;
+  d.n = A.n;
+  d.ptr = pl.mem.upload(ptr);
+  d.col = pl.mem.upload(A.col);
+  d.val = pl.mem.upload(A.val);
+  return d;
+}
+
+void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, const double* c_e, const hxb_options& opt)
+{
+  const auto t0 = std::chrono::steady_clock::now();
+  if (!m) throw HxbError(HXB_EINVAL, "mesh must be non-null");
+  if (opt.variant != HXB_VARIANT_STORED) throw HxbError(HXB_EINVAL, "only the stored operator variant is built");
+  pl.device = opt.device;
+  HXB_CUDA(cudaSetDevice(pl.device));
+  {
+    cudaDeviceProp prop;
+    HXB_CUDA(cudaGetDeviceProperties(&prop, pl.device));
+    if (prop.major != 10) throw HxbError(HXB_ECUDA, "hexsem_b200 requires an sm_100 (B200) device");
+  }
+  HostSetup& hs = pl.hs;
+  hs.mesh = mesh_from_arrays(m->num_vertices, m->xyz, m->num_elements, m->conn, m->num_boundary_faces,
+                             m->bface_element, m->bface_face, m->bface_tag);
+  const int ne = hs.mesh.num_elements();
+  hs.kappa.assign(kappa_e, kappa_e + ne);
+  hs.c.assign(c_e, c_e + ne);
+  SetupOptions so;
+  so.precond_mode = opt.precond_mode;
+  so.coarse_solve = opt.coarse_solve;
+  so.direct_threshold = opt.direct_threshold;
+  build_host_setup(hs, order, so);
+  const HexMesh& mesh = hs.mesh;
+  const Numbering& num = hs.num;
+
+  pl.order = order;
+  pl.np = order + 1;
+  pl.nloc = pl.np * pl.np * pl.np;
+  pl.nsurf = surface_slot_count(pl.np);
+  pl.P = order + 3;
+  pl.ne = ne;
+  pl.nv = mesh.num_vertices();
+  pl.precond_mode = opt.precond_mode;
+  pl.variant = opt.variant;
+  pl.do_fine = hs.do_fine;
+  pl.do_coarse = hs.do_coarse;
+  pl.use_amg = hs.use_amg;
+  pl.N = num.num_global;
+  pl.nsg = num.num_surface_global;
+  if (static_cast<std::size_t>(ne) * pl.nsurf > 0x7fffffffULL ||
+      static_cast<std::size_t>(ne) * pl.P * pl.P * pl.P > 0x7fffffffULL)
+    throw HxbError(HXB_EINVAL, "mesh too large for one device plan");
+
+  upload_tables(hs.basis, hs.pencil);
+
+  HXB_CUDA(cudaStreamCreateWithFlags(&pl.s_main, cudaStreamNonBlocking));
+  HXB_CUDA(cudaStreamCreateWithFlags(&pl.s_coarse, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&pl.ev_fork, &pl.ev_join}) HXB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  for (cudaEvent_t* e : {&pl.ev_t0, &pl.ev_t1, &pl.ev_a}) HXB_CUDA(cudaEventCreate(e));
+
+  DeviceArena& M = pl.mem;
+  pl.wg = M.upload(hs.geo.wg);
+  hs.geo.wg.clear();
+  hs.geo.wg.shrink_to_fit();
+  pl.mass = M.upload(hs.geo.mass);
+  pl.c_e = M.upload(hs.c);
+  pl.kappa_e = M.upload(hs.kappa);
+  pl.h3 = M.upload(hs.geo.h);
+  pl.mask = M.upload(num.dirichlet_mask);
+  pl.zero_mask = M.alloc<std::uint8_t>(pl.N);
+  HXB_CUDA(cudaMemset(pl.zero_mask, 0, pl.N));
+  pl.d_lumped = M.upload(hs.lumped);
+
+  // encoded surface map and Ax surface gather CSR (ascending e*nsurf+s)
+  {
+    std::vector<int> enc(num.l2g_surf.size());
+    for (std::size_t q = 0; q < enc.size(); ++q) {
+      const gid g = num.l2g_surf[q];
+      enc[q] = num.dirichlet_mask[g] ? encode_dirichlet(g) : g;
+    }
+    pl.l2g_surf = M.upload(enc);
+    std::vector<unsigned> off(static_cast<std::size_t>(pl.nsg) + 1, 0);
+    for (gid g : num.l2g_surf) off[g + 1]++;
+    for (int g = 0; g < pl.nsg; ++g) off[g + 1] += off[g];
+    std::vector<int> idx(num.l2g_surf.size());
+    std::vector<unsigned> cur(off.begin(), off.end() - 1);
+    for (std::size_t q = 0; q < num.l2g_surf.size(); ++q) idx[cur[num.l2g_surf[q]]++] = static_cast<int>(q);
+    pl.ax_off = M.upload(off);
+    pl.ax_idx = M.upload(idx);
+    std::vector<short> sl(pl.nsurf);
+    for (int k = 0; k < pl.np; ++k)
+      for (int j = 0; j < pl.np; ++j)
+        for (int i = 0; i < pl.np; ++i) {
+          const int s = surface_slot_of(pl.np, i, j, k);
+          if (s >= 0) sl[s] = static_cast<short>((k * pl.np + j) * pl.np + i);
+        }
+    pl.surf_local = M.upload(sl);
+  }
+  pl.rsurf = M.alloc<double>(num.l2g_surf.size());
+
+  // fine: encoded sub_face and the subdomain gather CSR in (e, slot) order
+  if (pl.do_fine) {
+    std::vector<int> enc(num.sub_face.size());
+    for (std::size_t q = 0; q < enc.size(); ++q) {
+      const gid g = num.sub_face[q];
+      enc[q] = g < 0 ? -1 : (num.dirichlet_mask[g] ? encode_dirichlet(g) : g);
+    }
+    pl.sub_face = M.upload(enc);
+    const std::size_t nsub = static_cast<std::size_t>(pl.P) * pl.P * pl.P;
+    std::vector<unsigned> cnt(static_cast<std::size_t>(pl.N) + 1, 0);
+    std::vector<gid> scratch(pl.nloc);
+    for (int e = 0; e < ne; ++e)
+      for_each_sub_slot(num, ne, e, scratch.data(), [&](gid g, int) {
+        if (g >= 0) cnt[g + 1]++;
+      });
+    for (int g = 0; g < pl.N; ++g) cnt[g + 1] += cnt[g];
+    std::vector<int> idx(cnt[pl.N]);
+    std::vector<unsigned> cur(cnt.begin(), cnt.end() - 1);
+    for (int e = 0; e < ne; ++e)
+      for_each_sub_slot(num, ne, e, scratch.data(), [&](gid g, int slot) {
+        if (g >= 0) idx[cur[g]++] = static_cast<int>(static_cast<std::size_t>(e) * nsub + slot);
+      });
+    pl.fine_off = M.upload(cnt);
+    pl.fine_idx = M.upload(idx);
+    pl.zsub = M.alloc<double>(static_cast<std::size_t>(ne) * nsub);
+  }
+
+  // coarse: connectivity, vertex incidence CSR (e, cb) order, coarse matrix, AMG / dense
+  if (pl.do_coarse) {
+    std::vector<int> conn(static_cast<std::size_t>(ne) * 8);
+    for (int e = 0; e < ne; ++e)
+      for (int q = 0; q < 8; ++q) conn[8 * static_cast<std::size_t>(e) + q] = mesh.elements[e][q];
+    pl.conn = M.upload(conn);
+    std::vector<unsigned> off(static_cast<std::size_t>(pl.nv) + 1, 0);
+    for (int e = 0; e < ne; ++e)
+      for (int cb = 0; cb < 8; ++cb) off[mesh.elements[e][kHexCornerFromBits[cb]] + 1]++;
+    for (int v = 0; v < pl.nv; ++v) off[v + 1] += off[v];
+    std::vector<int> idx(static_cast<std::size_t>(ne) * 8);
+    std::vector<unsigned> cur(off.begin(), off.end() - 1);
+    for (int e = 0; e < ne; ++e)
+      for (int cb = 0; cb < 8; ++cb) idx[cur[mesh.elements[e][kHexCornerFromBits[cb]]]++] = 8 * e + cb;
+    pl.vtx_off = M.upload(off);
+    pl.vtx_idx = M.upload(idx);
+    pl.vmask = M.upload(hs.vmask);
+    pl.Rpart = M.alloc<double>(static_cast<std::size_t>(ne) * 8);
+    pl.R = M.alloc<double>(pl.nv);
+    pl.Z = M.alloc<double>(pl.nv);
+    pl.rho = M.alloc<double>(pl.nv);
+    pl.dZ = M.alloc<double>(pl.nv);
+    pl.coarse_n = hs.Kc.n;
+    if (pl.use_amg) {
+      pl.Kc = csr_to_device(pl, hs.Kc);
+      const AmgSetup& amg = hs.amg;
+      const int L = static_cast<int>(amg.levels.size());
+      pl.lv.resize(L + 1);
+      for (int l = 0; l < L; ++l) {
+        const AmgLevel& h = amg.levels[l];
+        DevLevel& v = pl.lv[l];
+        v.n = h.A.n;
+        v.nc = h.n_coarse;
+        v.A = csr_to_device(pl, h.A);
+        v.dinv = M.upload(h.inv_diag);
+        v.agg = M.upload(h.aggregate);
+        std::vector<int> aptr(static_cast<std::size_t>(v.nc) + 1, 0), amem(v.n);
+        for (int i = 0; i < v.n; ++i) aptr[h.aggregate[i] + 1]++;
+        for (int c = 0; c < v.nc; ++c) aptr[c + 1] += aptr[c];
+        std::vector<int> cur2(aptr.begin(), aptr.end() - 1);
+        for (int i = 0; i < v.n; ++i) amem[cur2[h.aggregate[i]]++] = i;
+        v.agg_ptr = M.upload(aptr);
+        v.agg_mem = M.upload(amem);
+        for (double** b : {&v.zA, &v.zB, &v.kr, &v.kz, &v.kp, &v.kf}) *b = M.alloc<double>(v.n);
+        v.ks = M.alloc<KScalars>(1);
+      }
+      pl.lv[L].n = amg.coarsest.n;
+      for (int l = 1; l <= L; ++l) {
+        pl.lv[l].b = M.alloc<double>(pl.lv[l].n);
+        pl.lv[l].x = M.alloc<double>(pl.lv[l].n);
+      }
+      dense_to_device(pl, amg.coarsest);
+    } else {
+      dense_to_device(pl, hs.Kc);
+    }
+  }
+
+  // PCG vectors and reduction scratch
+  for (double** v : {&pl.u, &pl.r, &pl.z, &pl.p, &pl.f, &pl.b}) {
+    *v = M.alloc<double>(pl.N);
+    HXB_CUDA(cudaMemset(*v, 0, sizeof(double) * pl.N));
+  }
+  const int npart = ax_elem_grid(pl) + 8 * 148 * 4;
+  pl.partials = M.alloc<double>(npart);
+  pl.ticket = M.alloc<unsigned>(1);
+  pl.cpartials = M.alloc<double>(8 * 148 * 4);
+  pl.cticket = M.alloc<unsigned>(1);
+  HXB_CUDA(cudaMemset(pl.ticket, 0, sizeof(unsigned)));
+  HXB_CUDA(cudaMemset(pl.cticket, 0, sizeof(unsigned)));
+  pl.scratch = M.alloc<double>(64);
+  pl.res2 = pl.scratch;
+  HXB_CUDA(cudaMallocHost(&pl.h_status, 64 * sizeof(double)));
+  if (pl.do_coarse) capture_coarse_graph(pl);
+  HXB_CUDA(cudaDeviceSynchronize());
+  pl.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void ensure_hist(Plan& pl, int max_iterations)
+{
+  if (pl.hist_cap >= max_iterations + 2) return;
+  const int cap = max_iterations + 2;
+  pl.zr_hist = pl.mem.alloc<double>(cap);
+  pl.pf_hist = pl.mem.alloc<double>(cap);
+  pl.res_hist = pl.mem.alloc<double>(cap);
+  pl.hist_cap = cap;
+}
+
+// Mirrors pcg (krylov.cpp:20-71) statement by statement; the vectors never
+// leave the device.
+void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
+{
+  if (!(cfg.rel_tolerance > 0) || !(cfg.rel_tolerance < 1))
+    throw HxbError(HXB_EINVAL, "pcg: rel_tolerance must lie in (0,1)");
+  if (cfg.max_iterations < 1) throw HxbError(HXB_EINVAL, "pcg: max_iterations must be >= 1");
+  ensure_hist(pl, cfg.max_iterations);
+  cudaStream_t s = pl.s_main;
+  const int n = pl.N;
+  HXB_CUDA(cudaEventRecord(pl.ev_t0, s));
+  pcg_init_kernel<kVecBlock><<<vec_grid(n), kVecBlock, 0, s>>>(pl.b, pl.r, pl.u, n, dot_args(pl, pl.res2));
+  sqrt_store_kernel<<<1, 1, 0, s>>>(pl.res2, pl.res_hist);
+  HXB_CUDA(cudaMemcpyAsync(pl.h_status, pl.res_hist, sizeof(double), cudaMemcpyDeviceToHost, s));
+  HXB_CUDA(cudaStreamSynchronize(s));
+  const double r0 = pl.h_status[0];
+  int status = HXB_PCG_CONVERGED, iterations = 0;
+  std::string diag;
+  if (r0 != 0.0) {
+    enqueue_precond(pl, nullptr);
+    copy_dot_kernel<kVecBlock><<<vec_grid(n), kVecBlock, 0, s>>>(pl.z, pl.r, pl.p, n, dot_args(pl, pl.zr_hist));
+    status = HXB_PCG_MAX_ITERATIONS;
+    for (int k = 0; k < cfg.max_iterations; ++k) {
+      enqueue_ax(pl, pl.p, pl.f, pl.pf_hist + k, s);
+      pcg_update_kernel<kVecBlock><<<vec_grid(n), kVecBlock, 0, s>>>(pl.f, pl.r, n, pl.zr_hist, pl.pf_hist, k,
+                                                                     dot_args(pl, pl.res2));
+      sqrt_store_kernel<<<1, 1, 0, s>>>(pl.res2, pl.res_hist + k + 1);
+      HXB_CUDA(cudaMemcpyAsync(pl.h_status, pl.pf_hist + k, sizeof(double), cudaMemcpyDeviceToHost, s));
+      HXB_CUDA(cudaMemcpyAsync(pl.h_status + 1, pl.res_hist + k + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+      HXB_CUDA(cudaStreamSynchronize(s));
+      const double pf = pl.h_status[0], rn = pl.h_status[1];
+      if (!(pf > 0)) {
+        status = HXB_PCG_BREAKDOWN;
+        char buf[160];
+        std::snprintf(buf, sizeof(buf), "indefinite operator: p.Ap = %f at iteration %d", pf, k);
+        diag = buf;
+        iterations = k;
+        res->num_zr = k + 1;
+        break;
+      }
+      iterations = k + 1;
+      if (rn / r0 <= cfg.rel_tolerance) {
+        status = HXB_PCG_CONVERGED;
+        pcg_final_kernel<<<vec_grid(n), kVecBlock, 0, s>>>(pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
+        break;
+      }
+      if (k + 1 == cfg.max_iterations) {
+        pcg_final_kernel<<<vec_grid(n), kVecBlock, 0, s>>>(pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
+        diag = "not converged within " + std::to_string(cfg.max_iterations) + " iterations";
+        break;
+      }
+      enqueue_precond(pl, pl.zr_hist + k + 1);
+      pcg_dir_kernel<<<vec_grid(n), kVecBlock, 0, s>>>(pl.z, pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
+    }
+  }
+  HXB_CUDA(cudaEventRecord(pl.ev_t1, s));
+  HXB_CUDA(cudaEventSynchronize(pl.ev_t1));
+  float ms = 0;
+  HXB_CUDA(cudaEventElapsedTime(&ms, pl.ev_t0, pl.ev_t1));
+  res->solve_seconds = ms / 1000.0;
+  res->status = status;
+  res->iterations = iterations;
+  res->num_residuals = r0 == 0.0 ? 1 : iterations + 1;
+  if (status != HXB_PCG_BREAKDOWN) res->num_zr = r0 == 0.0 ? 0 : iterations;
+  std::snprintf(res->diagnostic, sizeof(res->diagnostic), "%s", diag.c_str());
+  if (cfg.record_history) {
+    if (res->residual_history)
+      HXB_CUDA(cudaMemcpy(res->residual_history, pl.res_hist, sizeof(double) * res->num_residuals, cudaMemcpyDeviceToHost));
+    if (res->zr_history && res->num_zr > 0)
+      HXB_CUDA(cudaMemcpy(res->zr_history, pl.zr_hist, sizeof(double) * res->num_zr, cudaMemcpyDeviceToHost));
+  }
+  if (res->u) HXB_CUDA(cudaMemcpy(res->u, pl.u, sizeof(double) * n, cudaMemcpyDeviceToHost));
+}
+
+Plan* as_plan(hxb_plan* p)
+{
+  if (!p) throw HxbError(HXB_EINVAL, "null plan");
+  return reinterpret_cast<Plan*>(p);
+}
+
+}  // namespace
+}  // namespace hxb
+
+using namespace hxb;
+
+extern "C" {
+
+int hxb_plan_create(const hxb_mesh* mesh, int order, const double* kappa_e, const double* c_e, const hxb_options* opt,
+                    hxb_plan** out)
+{
+  return guarded([&] {
+    if (!out) throw HxbError(HXB_EINVAL, "null output");
+    if (!kappa_e || !c_e) throw HxbError(HXB_EINVAL, "kappa/c must hold one value per element");
+    hxb_options o;
+    if (opt)
+      o = *opt;
+    else
+      hxb_default_options(&o);
+    auto pl = std::make_unique<Plan>();
+    build_plan(*pl, mesh, order, kappa_e, c_e, o);
+    *out = reinterpret_cast<hxb_plan*>(pl.release());
+  });
+}
+
+int hxb_plan_destroy(hxb_plan* plan)
+{
+  return guarded([&] {
+    if (plan) {
+      Plan* pl = as_plan(plan);
+      cudaSetDevice(pl->device);
+      cudaDeviceSynchronize();
+      delete pl;
+    }
+  });
+}
+
+int hxb_plan_get_info(const hxb_plan* plan, hxb_plan_info* info)
+{
+  return guarded([&] {
+    const Plan* pl = reinterpret_cast<const Plan*>(plan);
+    if (!pl || !info) throw HxbError(HXB_EINVAL, "null argument");
+    std::memset(info, 0, sizeof(*info));
+    info->num_global = pl->N;
+    info->num_elements = pl->ne;
+    info->num_vertices = pl->nv;
+    info->order = pl->order;
+    info->coarse_uses_amg = pl->use_amg ? 1 : 0;
+    info->coarse_n = pl->coarse_n;
+    info->precond_mode = pl->precond_mode;
+    fill_amg_info(pl->hs, &info->amg_levels, info->amg_rows, info->amg_nnz);
+    info->setup_seconds = pl->setup_seconds;
+    info->device_bytes = static_cast<int64_t>(pl->mem.bytes);
+  });
+}
+
+int hxb_apply_A_device(hxb_plan* plan, const double* d_u, double* d_r, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    cudaStream_t s = pl->s_main;
+    if (stream) {
+      HXB_CUDA(cudaEventRecord(pl->ev_a, static_cast<cudaStream_t>(stream)));
+      HXB_CUDA(cudaStreamWaitEvent(s, pl->ev_a, 0));
+    }
+    enqueue_ax(*pl, d_u, d_r, nullptr, s);
+    HXB_CUDA(cudaGetLastError());
+    if (stream) {
+      HXB_CUDA(cudaEventRecord(pl->ev_a, s));
+      HXB_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), pl->ev_a, 0));
+    } else {
+      HXB_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+int hxb_apply_A(hxb_plan* plan, const double* u, double* r)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    const std::size_t bytes = sizeof(double) * pl->N;
+    HXB_CUDA(cudaMemcpyAsync(pl->p, u, bytes, cudaMemcpyHostToDevice, pl->s_main));
+    enqueue_ax(*pl, pl->p, pl->f, nullptr, pl->s_main);
+    HXB_CUDA(cudaGetLastError());
+    HXB_CUDA(cudaMemcpyAsync(r, pl->f, bytes, cudaMemcpyDeviceToHost, pl->s_main));
+    HXB_CUDA(cudaStreamSynchronize(pl->s_main));
+  });
+}
+
+static int apply_precond_host(hxb_plan* plan, const double* r, double* z, int mode)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    if (mode == HXB_PRECOND_FINE_ONLY && !pl->do_fine) throw HxbError(HXB_EINVAL, "system has no fine preconditioner");
+    if (mode == HXB_PRECOND_COARSE_ONLY && !pl->do_coarse)
+      throw HxbError(HXB_EINVAL, "system has no coarse preconditioner");
+    const std::size_t bytes = sizeof(double) * pl->N;
+    HXB_CUDA(cudaMemcpyAsync(pl->r, r, bytes, cudaMemcpyHostToDevice, pl->s_main));
+    if (mode < 0) {
+      enqueue_precond(*pl, nullptr);
+    } else {
+      // component-only applies (FinePreconditioner::apply / CoarsePreconditioner::apply):
+      // run the requested branch and a combine without the mask/identity rows
+      const bool f = mode == HXB_PRECOND_FINE_ONLY, c = mode == HXB_PRECOND_COARSE_ONLY;
+      if (c) {
+        HXB_CUDA(cudaEventRecord(pl->ev_fork, pl->s_main));
+        HXB_CUDA(cudaStreamWaitEvent(pl->s_coarse, pl->ev_fork, 0));
+        HXB_CUDA(cudaGraphLaunch(pl->coarse_exec, pl->s_coarse));
+        HXB_CUDA(cudaEventRecord(pl->ev_join, pl->s_coarse));
+        HXB_CUDA(cudaStreamWaitEvent(pl->s_main, pl->ev_join, 0));
+      }
+      if (f) HXB_DISPATCH_NP(pl->np, launch_fdm, *pl, pl->s_main);
+      // FinePreconditioner::apply / CoarsePreconditioner::apply have no mask
+      // rows; emulate with a mask-free combine by temporarily pointing at a zero mask
+      std::uint8_t* saved = pl->mask;
+      pl->mask = pl->zero_mask;
+      HXB_DISPATCH_NP(pl->np, launch_combine, *pl, nullptr, pl->s_main, f, c);
+      pl->mask = saved;
+    }
+    HXB_CUDA(cudaGetLastError());
+    HXB_CUDA(cudaMemcpyAsync(z, pl->z, bytes, cudaMemcpyDeviceToHost, pl->s_main));
+    HXB_CUDA(cudaStreamSynchronize(pl->s_main));
+  });
+}
+
+int hxb_apply_P(hxb_plan* plan, const double* r, double* z) { return apply_precond_host(plan, r, z, -1); }
+int hxb_apply_fine(hxb_plan* plan, const double* r, double* z)
+{
+  return apply_precond_host(plan, r, z, HXB_PRECOND_FINE_ONLY);
+}
+int hxb_apply_coarse(hxb_plan* plan, const double* r, double* z)
+{
+  return apply_precond_host(plan, r, z, HXB_PRECOND_COARSE_ONLY);
+}
+
+int hxb_apply_P_device(hxb_plan* plan, const double* d_r, double* d_z, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    cudaStream_t s = pl->s_main;
+    if (stream) {
+      HXB_CUDA(cudaEventRecord(pl->ev_a, static_cast<cudaStream_t>(stream)));
+      HXB_CUDA(cudaStreamWaitEvent(s, pl->ev_a, 0));
+    }
+    if (d_r != pl->r) HXB_CUDA(cudaMemcpyAsync(pl->r, d_r, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice, s));
+    enqueue_precond(*pl, nullptr);
+    if (d_z != pl->z) HXB_CUDA(cudaMemcpyAsync(d_z, pl->z, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice, s));
+    HXB_CUDA(cudaGetLastError());
+    if (stream) {
+      HXB_CUDA(cudaEventRecord(pl->ev_a, s));
+      HXB_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), pl->ev_a, 0));
+    } else {
+      HXB_CUDA(cudaStreamSynchronize(s));
+    }
+  });
+}
+
+static void fill_default_b(Plan& pl)
+{
+  std::vector<double> b(pl.N);
+  for (int g = 0; g < pl.N; ++g) b[g] = pl.hs.num.dirichlet_mask[g] ? 0.0 : pl.hs.lumped[g] * 1.0;
+  HXB_CUDA(cudaMemcpy(pl.b, b.data(), sizeof(double) * pl.N, cudaMemcpyHostToDevice));
+}
+
+int hxb_solve(hxb_plan* plan, const double* b, const hxb_pcg_config* cfg, hxb_pcg_result* res)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (!cfg || !res) throw HxbError(HXB_EINVAL, "null argument");
+    HXB_CUDA(cudaSetDevice(pl->device));
+    if (b)
+      HXB_CUDA(cudaMemcpy(pl->b, b, sizeof(double) * pl->N, cudaMemcpyHostToDevice));
+    else
+      fill_default_b(*pl);
+    run_pcg(*pl, *cfg, res);
+  });
+}
+
+int hxb_solve_device(hxb_plan* plan, const double* d_b, const hxb_pcg_config* cfg, hxb_pcg_result* res)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (!cfg || !res) throw HxbError(HXB_EINVAL, "null argument");
+    HXB_CUDA(cudaSetDevice(pl->device));
+    if (d_b && d_b != pl->b)
+      HXB_CUDA(cudaMemcpy(pl->b, d_b, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice));
+    else if (!d_b)
+      fill_default_b(*pl);
+    run_pcg(*pl, *cfg, res);
+  });
+}
+
+int hxb_load_ones(hxb_plan* plan, double* b)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    for (int g = 0; g < pl->N; ++g) b[g] = pl->hs.num.dirichlet_mask[g] ? 0.0 : pl->hs.lumped[g] * 1.0;
+  });
+}
+
+int hxb_lumped_mass(hxb_plan* plan, double* m)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    std::memcpy(m, pl->hs.lumped.data(), sizeof(double) * pl->N);
+  });
+}
+
+int hxb_export_maps(hxb_plan* plan, int32_t* l2g, int64_t* g2l_offsets, int32_t* g2l_elem, int32_t* g2l_local,
+                    int32_t* sub_l2g, uint8_t* dirichlet_mask)
+{
+  return guarded([&] { export_index_maps(as_plan(plan)->hs, l2g, g2l_offsets, g2l_elem, g2l_local, sub_l2g, dirichlet_mask); });
+}
+
+int hxb_amg_level(hxb_plan* plan, int level, int64_t* rows, int64_t* nnz, int64_t* ptr, int32_t* col, double* val,
+                  int32_t* aggregate)
+{
+  return guarded([&] { export_amg_level(as_plan(plan)->hs, level, rows, nnz, ptr, col, val, aggregate); });
+}
+
+int hxb_bench_apply_A(hxb_plan* plan, int reps, double* ms_per_apply, double* ms_elem_kernel)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    cudaStream_t s = pl->s_main;
+    for (int w = 0; w < 3; ++w) enqueue_ax(*pl, pl->p, pl->f, nullptr, s);
+    HXB_CUDA(cudaStreamSynchronize(s));
+    HXB_CUDA(cudaEventRecord(pl->ev_t0, s));
+    for (int q = 0; q < reps; ++q) enqueue_ax(*pl, pl->p, pl->f, nullptr, s);
+    HXB_CUDA(cudaEventRecord(pl->ev_t1, s));
+    HXB_CUDA(cudaEventSynchronize(pl->ev_t1));
+    float ms = 0;
+    HXB_CUDA(cudaEventElapsedTime(&ms, pl->ev_t0, pl->ev_t1));
+    *ms_per_apply = ms / reps;
+    if (ms_elem_kernel) {
+      HXB_CUDA(cudaEventRecord(pl->ev_t0, s));
+      for (int q = 0; q < reps; ++q) HXB_DISPATCH_NP(pl->np, launch_ax_elem, *pl, pl->p, pl->f, DotArgs{}, s);
+      HXB_CUDA(cudaEventRecord(pl->ev_t1, s));
+      HXB_CUDA(cudaEventSynchronize(pl->ev_t1));
+      HXB_CUDA(cudaEventElapsedTime(&ms, pl->ev_t0, pl->ev_t1));
+      *ms_elem_kernel = ms / reps;
+    }
+    HXB_CUDA(cudaGetLastError());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,583 @@
+"""Python host mirror of the reference solver API over the B200 C-ABI.
+
+Mirrors the reference's Python surface ``_hexsem`` (python/src/module.cpp:73-143:
+``solve_poisson(**kwargs)``, ``mesh_info``, ``gll_nodes_weights``, counter
+models) and its C++ objects (``HexMesh``, ``ProblemConfig``, ``SemSystem`` with
+``operator_fn``/``preconditioner_fn``, ``pcg``) on top of
+``libhexsem_b200.so`` (include/hexsem_b200.h). Every numeric operation runs
+in the CUDA library; this module only marshals arguments. There is no CPU
+fallback: if the library is missing or no sm_100 GPU is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhexsem_b200.so")
+
+FAMILIES = {"uniform": 0, "distorted_domain": 1, "distorted_elements": 2}
+PRECONDS = {"two_scale": 0, "fine_only": 1, "coarse_only": 2, "none": 3}
+COARSE = {"automatic": 0, "direct": 1, "amg": 2}
+VARIANTS = {"stored": 0, "on_the_fly": 1}
+TAGS = {"dirichlet": 0, "neumann": 1}
+STATUS = {0: "converged", 1: "max_iterations", 2: "breakdown"}
+
+
+class HxbError(RuntimeError):
+    """Raised on a non-zero C-ABI return code (message from hxb_last_error)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class _Mesh(C.Structure):
+    _fields_ = [
+        ("num_vertices", C.c_int32), ("xyz", C.POINTER(C.c_double)),
+        ("num_elements", C.c_int32), ("conn", C.POINTER(C.c_int32)),
+        ("num_boundary_faces", C.c_int32), ("bface_element", C.POINTER(C.c_int32)),
+        ("bface_face", C.POINTER(C.c_int32)), ("bface_tag", C.POINTER(C.c_uint8)),
+    ]
+
+
+class _MeshBuf(C.Structure):
+    _fields_ = [("view", _Mesh), ("impl", C.c_void_p)]
+
+
+class _Options(C.Structure):
+    _fields_ = [("precond_mode", C.c_int), ("coarse_solve", C.c_int), ("direct_threshold", C.c_int32),
+                ("variant", C.c_int), ("device", C.c_int), ("reserved", C.c_int * 7)]
+
+
+class _PcgConfig(C.Structure):
+    _fields_ = [("rel_tolerance", C.c_double), ("max_iterations", C.c_int), ("record_history", C.c_int)]
+
+
+class _PcgResult(C.Structure):
+    _fields_ = [("status", C.c_int), ("iterations", C.c_int), ("num_residuals", C.c_int), ("num_zr", C.c_int),
+                ("residual_history", C.POINTER(C.c_double)), ("zr_history", C.POINTER(C.c_double)),
+                ("u", C.POINTER(C.c_double)), ("solve_seconds", C.c_double), ("diagnostic", C.c_char * 256)]
+
+
+class _PlanInfo(C.Structure):
+    _fields_ = [("num_global", C.c_int64), ("num_elements", C.c_int64), ("num_vertices", C.c_int64),
+                ("order", C.c_int32), ("coarse_uses_amg", C.c_int32), ("coarse_n", C.c_int64),
+                ("amg_levels", C.c_int32), ("precond_mode", C.c_int32), ("amg_rows", C.c_int64 * 16),
+                ("amg_nnz", C.c_int64 * 16), ("setup_seconds", C.c_double), ("device_bytes", C.c_int64)]
+
+
+# Exported symbols and their signatures (kept in sync with include/hexsem_b200.h).
+P = C.c_void_p
+SIGNATURES = {
+    "hxb_last_error": (C.c_char_p, []),
+    "hxb_default_options": (None, [C.POINTER(_Options)]),
+    "hxb_generate_cube_mesh": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.POINTER(_MeshBuf))]),
+    "hxb_generate_box_mesh": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double), C.c_int,
+                                        C.POINTER(C.POINTER(_MeshBuf))]),
+    "hxb_refine_uniform": (C.c_int, [C.POINTER(_Mesh), C.POINTER(C.POINTER(_MeshBuf))]),
+    "hxb_mesh_free": (None, [C.POINTER(_MeshBuf)]),
+    "hxb_plan_create": (C.c_int, [C.POINTER(_Mesh), C.c_int, P, P, C.POINTER(_Options), C.POINTER(P)]),
+    "hxb_plan_destroy": (C.c_int, [P]),
+    "hxb_plan_get_info": (C.c_int, [P, C.POINTER(_PlanInfo)]),
+    "hxb_apply_A": (C.c_int, [P, P, P]),
+    "hxb_apply_P": (C.c_int, [P, P, P]),
+    "hxb_apply_fine": (C.c_int, [P, P, P]),
+    "hxb_apply_coarse": (C.c_int, [P, P, P]),
+    "hxb_apply_A_device": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hxb_apply_P_device": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hxb_solve": (C.c_int, [P, P, C.POINTER(_PcgConfig), C.POINTER(_PcgResult)]),
+    "hxb_solve_device": (C.c_int, [P, C.c_void_p, C.POINTER(_PcgConfig), C.POINTER(_PcgResult)]),
+    "hxb_load_ones": (C.c_int, [P, P]),
+    "hxb_lumped_mass": (C.c_int, [P, P]),
+    "hxb_export_maps": (C.c_int, [P, P, P, P, P, P, P]),
+    "hxb_amg_level": (C.c_int, [P, C.c_int, P, P, P, P, P, P]),
+    "hxb_bench_apply_A": (C.c_int, [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "hxb_setup_create": (C.c_int, [C.POINTER(_Mesh), C.c_int, P, P, C.POINTER(_Options), C.POINTER(P)]),
+    "hxb_setup_destroy": (None, [P]),
+    "hxb_setup_info": (C.c_int, [P, C.POINTER(_PlanInfo)]),
+    "hxb_setup_export_maps": (C.c_int, [P, P, P, P, P, P, P]),
+    "hxb_setup_amg_level": (C.c_int, [P, C.c_int, P, P, P, P, P, P]),
+    "hxb_setup_lumped_mass": (C.c_int, [P, P]),
+    "hxb_gll": (C.c_int, [C.c_int, P, P, P]),
+    "hxb_pencil": (C.c_int, [C.c_int, P, P, P, P, P]),
+    "hxb_words_model": (C.c_uint64, [C.c_int64, C.c_int, C.c_int]),
+    "hxb_flops_model": (C.c_uint64, [C.c_int64, C.c_int]),
+    "hxb_fine_ops_model": (C.c_uint64, [C.c_int64, C.c_int]),
+    "hxb_fine_words_model": (C.c_uint64, [C.c_int64, C.c_int]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libhexsem_b200.so (fails loudly: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing; build it with `make -C paper_1506_05996_b200` "
+                          "or __graft_entry__.build()")
+    L = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise HxbError(rc, lib().hxb_last_error().decode())
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ---------------------------------------------------------------------------
+@dataclass
+class HexMesh:
+    """Conforming all-hex mesh (mesh.hpp:38-45) as numpy arrays."""
+    xyz: np.ndarray                      # (nv, 3) float64
+    conn: np.ndarray                     # (ne, 8) int32, Gmsh corner order
+    bf_elem: np.ndarray                  # (nbf,) int32
+    bf_face: np.ndarray                  # (nbf,) int32
+    bf_tag: np.ndarray                   # (nbf,) uint8 (0 dirichlet, 1 neumann)
+
+    @property
+    def num_elements(self) -> int:
+        return int(self.conn.shape[0])
+
+    @property
+    def num_vertices(self) -> int:
+        return int(self.xyz.shape[0])
+
+    def as_dict(self) -> dict:
+        return {"xyz": self.xyz, "conn": self.conn, "bf_elem": self.bf_elem, "bf_face": self.bf_face,
+                "bf_tag": self.bf_tag}
+
+    def _c(self) -> _Mesh:
+        self.xyz = np.ascontiguousarray(self.xyz, dtype=np.float64)
+        self.conn = np.ascontiguousarray(self.conn, dtype=np.int32)
+        self.bf_elem = np.ascontiguousarray(self.bf_elem, dtype=np.int32)
+        self.bf_face = np.ascontiguousarray(self.bf_face, dtype=np.int32)
+        self.bf_tag = np.ascontiguousarray(self.bf_tag, dtype=np.uint8)
+        m = _Mesh()
+        m.num_vertices = self.num_vertices
+        m.xyz = self.xyz.ctypes.data_as(C.POINTER(C.c_double))
+        m.num_elements = self.num_elements
+        m.conn = self.conn.ctypes.data_as(C.POINTER(C.c_int32))
+        m.num_boundary_faces = int(self.bf_elem.size)
+        m.bface_element = self.bf_elem.ctypes.data_as(C.POINTER(C.c_int32))
+        m.bface_face = self.bf_face.ctypes.data_as(C.POINTER(C.c_int32))
+        m.bface_tag = self.bf_tag.ctypes.data_as(C.POINTER(C.c_uint8))
+        return m
+
+
+def _take_mesh(buf) -> HexMesh:
+    v = buf.contents.view
+    nv, ne, nb = v.num_vertices, v.num_elements, v.num_boundary_faces
+    m = HexMesh(
+        xyz=np.ctypeslib.as_array(v.xyz, shape=(nv * 3,)).reshape(nv, 3).copy(),
+        conn=np.ctypeslib.as_array(v.conn, shape=(ne * 8,)).reshape(ne, 8).copy(),
+        bf_elem=np.ctypeslib.as_array(v.bface_element, shape=(max(nb, 1),))[:nb].copy(),
+        bf_face=np.ctypeslib.as_array(v.bface_face, shape=(max(nb, 1),))[:nb].copy(),
+        bf_tag=np.ctypeslib.as_array(v.bface_tag, shape=(max(nb, 1),))[:nb].copy(),
+    )
+    lib().hxb_mesh_free(buf)
+    return m
+
+
+def generate_cube_mesh(k: int, family: str = "uniform", boundary: str = "dirichlet") -> HexMesh:
+    """generate_cube_mesh (mesh.hpp:53-54, mesh.cpp:110-139)."""
+    out = C.POINTER(_MeshBuf)()
+    _check(lib().hxb_generate_cube_mesh(k, FAMILIES[family], TAGS[boundary], C.byref(out)))
+    return _take_mesh(out)
+
+
+def generate_box_mesh(kx: int, ky: int, kz: int, size=(1.0, 1.0, 1.0), boundary: str = "dirichlet") -> HexMesh:
+    """generate_box_mesh (mesh.hpp:57-58, mesh.cpp:67-108)."""
+    out = C.POINTER(_MeshBuf)()
+    sz = (C.c_double * 3)(*[float(x) for x in size])
+    _check(lib().hxb_generate_box_mesh(kx, ky, kz, sz, TAGS[boundary], C.byref(out)))
+    return _take_mesh(out)
+
+
+def refine_uniform(mesh: HexMesh) -> HexMesh:
+    """refine_uniform (mesh.hpp:60-62, mesh.cpp:141-234)."""
+    out = C.POINTER(_MeshBuf)()
+    cm = mesh._c()
+    _check(lib().hxb_refine_uniform(C.byref(cm), C.byref(out)))
+    return _take_mesh(out)
+
+
+@dataclass
+class ProblemConfig:
+    """Solver-path subset of hexsem::ProblemConfig (problem.hpp:35-62)."""
+    label: str = "poisson"
+    family: str = "uniform"
+    k: int = 8
+    refine: int = 0
+    bar: tuple = (0, 0, 0)
+    bar_size: tuple = (1.0, 1.0, 8.0)
+    boundary: str = "dirichlet"
+    order: int = 3
+    kappa: float = 1.0
+    c: float = 0.0
+    tol: float = 1e-6
+    max_iterations: int = 500
+    precond: str = "two_scale"
+    variant: str = "stored"
+    coarse_solve: str = "automatic"
+    coarse_direct_threshold: int = 64000
+    device: int = 0
+
+
+def make_mesh(cfg: ProblemConfig) -> HexMesh:
+    """make_mesh (problem.cpp:13-26) for generated meshes."""
+    if cfg.bar[0] > 0:
+        mesh = generate_box_mesh(cfg.bar[0], cfg.bar[1], cfg.bar[2], cfg.bar_size, cfg.boundary)
+    else:
+        mesh = generate_cube_mesh(cfg.k, cfg.family, cfg.boundary)
+    for _ in range(cfg.refine):
+        mesh = refine_uniform(mesh)
+    return mesh
+
+
+class Plan:
+    """Device-resident SemSystem (problem.hpp:68-85): operator, two-scale
+    preconditioner and PCG on one B200. Arrays in, arrays out."""
+
+    def __init__(self, mesh: HexMesh, order: int, kappa_e=None, c_e=None, *, precond: str = "two_scale",
+                 coarse_solve: str = "automatic", direct_threshold: int = 64000, variant: str = "stored",
+                 device: int = 0):
+        L = lib()
+        ne = mesh.num_elements
+        self.mesh = mesh
+        self.kappa_e = np.ascontiguousarray(np.full(ne, 1.0) if kappa_e is None else kappa_e, dtype=np.float64)
+        self.c_e = np.ascontiguousarray(np.zeros(ne) if c_e is None else c_e, dtype=np.float64)
+        opt = _Options()
+        L.hxb_default_options(C.byref(opt))
+        opt.precond_mode = PRECONDS[precond]
+        opt.coarse_solve = COARSE[coarse_solve]
+        opt.direct_threshold = direct_threshold
+        opt.variant = VARIANTS[variant]
+        opt.device = device
+        cm = mesh._c()
+        h = C.c_void_p()
+        _check(L.hxb_plan_create(C.byref(cm), order, _ptr(self.kappa_e), _ptr(self.c_e), C.byref(opt), C.byref(h)))
+        self._h = h
+        self.precond = precond
+        info = _PlanInfo()
+        _check(L.hxb_plan_get_info(self._h, C.byref(info)))
+        self.N = int(info.num_global)
+        self.NE = int(info.num_elements)
+        self.NV = int(info.num_vertices)
+        self.order = int(info.order)
+        self.coarse_amg = bool(info.coarse_uses_amg)
+        self.coarse_n = int(info.coarse_n)
+        self.amg_levels = int(info.amg_levels)
+        self.amg_rows = [int(info.amg_rows[i]) for i in range(self.amg_levels)]
+        self.amg_nnz = [int(info.amg_nnz[i]) for i in range(self.amg_levels)]
+        self.setup_seconds = float(info.setup_seconds)
+        self.device_bytes = int(info.device_bytes)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hxb_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # --- LinearOp plug-ins (host arrays) ------------------------------------
+    def _op(self, name, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.shape != (self.N,):
+            raise ValueError(f"{name}: vector length mismatch")
+        y = np.empty(self.N)
+        _check(getattr(lib(), name)(self._h, _ptr(x), _ptr(y)))
+        return y
+
+    def apply_A(self, u):
+        """SemOperator::apply (operator.cpp:255-287)."""
+        return self._op("hxb_apply_A", u)
+
+    def apply_P(self, r):
+        """TwoScalePreconditioner::apply (precond.cpp:27-67)."""
+        return self._op("hxb_apply_P", r)
+
+    def apply_fine(self, r):
+        """FinePreconditioner::apply on the masked residual (fine.cpp:210-231)."""
+        return self._op("hxb_apply_fine", r)
+
+    def apply_coarse(self, r):
+        """CoarsePreconditioner::apply on the masked residual (coarse.cpp:188-208)."""
+        return self._op("hxb_apply_coarse", r)
+
+    def operator_fn(self):
+        return self.apply_A
+
+    def preconditioner_fn(self):
+        return self.apply_P
+
+    # --- device-pointer entry points (for the bench; data already in HBM) -----
+    def apply_A_device(self, d_u: int, d_r: int, stream: int = 0):
+        _check(lib().hxb_apply_A_device(self._h, C.c_void_p(d_u), C.c_void_p(d_r), C.c_void_p(stream or None)))
+
+    def apply_P_device(self, d_r: int, d_z: int, stream: int = 0):
+        _check(lib().hxb_apply_P_device(self._h, C.c_void_p(d_r), C.c_void_p(d_z), C.c_void_p(stream or None)))
+
+    # --- solve ------------------------------------------------------------------
+    def _solve(self, fn, bptr, tol, max_iterations, want_u=True):
+        cfg = _PcgConfig(float(tol), int(max_iterations), 1)
+        rh = np.zeros(max_iterations + 1)
+        zh = np.zeros(max_iterations + 1)
+        u = np.zeros(self.N) if want_u else None
+        res = _PcgResult()
+        res.residual_history = rh.ctypes.data_as(C.POINTER(C.c_double))
+        res.zr_history = zh.ctypes.data_as(C.POINTER(C.c_double))
+        res.u = u.ctypes.data_as(C.POINTER(C.c_double)) if want_u else C.POINTER(C.c_double)()
+        _check(fn(self._h, bptr, C.byref(cfg), C.byref(res)))
+        return {"status": STATUS[res.status], "iterations": int(res.iterations),
+                "residual_history": rh[:res.num_residuals].copy(), "zr_history": zh[:res.num_zr].copy(),
+                "u": u, "solve_seconds": float(res.solve_seconds), "diagnostic": res.diagnostic.decode()}
+
+    def pcg(self, b=None, tol: float = 1e-6, max_iterations: int = 500, want_u: bool = True) -> dict:
+        """pcg(operator_fn, preconditioner_fn, b, cfg) (krylov.cpp:20-71) on the device.
+        b=None uses the Poisson load m_N*1 masked (problem.cpp:129)."""
+        bb = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
+        if bb is not None and bb.shape != (self.N,):
+            raise ValueError("pcg: vector length mismatch")
+        return self._solve(lib().hxb_solve, _ptr(bb), tol, max_iterations, want_u)
+
+    def pcg_device(self, d_b: int | None, tol: float = 1e-6, max_iterations: int = 500, want_u: bool = False):
+        return self._solve(lib().hxb_solve_device, C.c_void_p(d_b) if d_b else None, tol, max_iterations, want_u)
+
+    # --- data ---------------------------------------------------------------------
+    def load_ones(self):
+        b = np.empty(self.N)
+        _check(lib().hxb_load_ones(self._h, _ptr(b)))
+        return b
+
+    def lumped_mass(self):
+        m = np.empty(self.N)
+        _check(lib().hxb_lumped_mass(self._h, _ptr(m)))
+        return m
+
+    def maps(self, sub: bool = True) -> dict:
+        n = self.order
+        nloc, nsub = (n + 1) ** 3, (n + 3) ** 3
+        out = {
+            "l2g": np.zeros(self.NE * nloc, dtype=np.int32),
+            "g2l_offsets": np.zeros(self.N + 1, dtype=np.int64),
+            "g2l_elem": np.zeros(self.NE * nloc, dtype=np.int32),
+            "g2l_local": np.zeros(self.NE * nloc, dtype=np.int32),
+            "sub_l2g": np.zeros(self.NE * nsub, dtype=np.int32) if sub else None,
+            "dirichlet_mask": np.zeros(self.N, dtype=np.uint8),
+        }
+        _check(lib().hxb_export_maps(self._h, _ptr(out["l2g"]), _ptr(out["g2l_offsets"]), _ptr(out["g2l_elem"]),
+                                     _ptr(out["g2l_local"]), _ptr(out["sub_l2g"]), _ptr(out["dirichlet_mask"])))
+        return out
+
+    def amg_level(self, l: int) -> dict:
+        rows, nnz = C.c_int64(), C.c_int64()
+        _check(lib().hxb_amg_level(self._h, l, C.byref(rows), C.byref(nnz), None, None, None, None))
+        ptr = np.zeros(rows.value + 1, dtype=np.int64)
+        col = np.zeros(nnz.value, dtype=np.int32)
+        val = np.zeros(nnz.value)
+        agg = np.full(rows.value, -1, dtype=np.int32)
+        _check(lib().hxb_amg_level(self._h, l, C.byref(rows), C.byref(nnz), _ptr(ptr), _ptr(col), _ptr(val),
+                                   _ptr(agg)))
+        return {"ptr": ptr, "col": col, "val": val, "aggregate": agg}
+
+    def bench_apply_A(self, reps: int = 20):
+        ms, ms_elem = C.c_double(), C.c_double()
+        _check(lib().hxb_bench_apply_A(self._h, reps, C.byref(ms), C.byref(ms_elem)))
+        return ms.value, ms_elem.value
+
+
+class HostSetup:
+    """GPU-free setup (build_system minus the device upload): numbering,
+    lumped mass, coarse matrix and AMG hierarchy, for bit-exact checks."""
+
+    def __init__(self, mesh: HexMesh, order: int, kappa_e=None, c_e=None, *, precond: str = "two_scale",
+                 coarse_solve: str = "automatic", direct_threshold: int = 64000):
+        L = lib()
+        ne = mesh.num_elements
+        self.kappa_e = np.ascontiguousarray(np.full(ne, 1.0) if kappa_e is None else kappa_e, dtype=np.float64)
+        self.c_e = np.ascontiguousarray(np.zeros(ne) if c_e is None else c_e, dtype=np.float64)
+        opt = _Options()
+        L.hxb_default_options(C.byref(opt))
+        opt.precond_mode = PRECONDS[precond]
+        opt.coarse_solve = COARSE[coarse_solve]
+        opt.direct_threshold = direct_threshold
+        cm = mesh._c()
+        h = C.c_void_p()
+        _check(L.hxb_setup_create(C.byref(cm), order, _ptr(self.kappa_e), _ptr(self.c_e), C.byref(opt), C.byref(h)))
+        self._h = h
+        info = _PlanInfo()
+        _check(L.hxb_setup_info(self._h, C.byref(info)))
+        self.N = int(info.num_global)
+        self.NE = int(info.num_elements)
+        self.NV = int(info.num_vertices)
+        self.order = int(info.order)
+        self.coarse_amg = bool(info.coarse_uses_amg)
+        self.coarse_n = int(info.coarse_n)
+        self.amg_levels = int(info.amg_levels)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hxb_setup_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def maps(self, sub: bool = True) -> dict:
+        n = self.order
+        nloc, nsub = (n + 1) ** 3, (n + 3) ** 3
+        out = {
+            "l2g": np.zeros(self.NE * nloc, dtype=np.int32),
+            "g2l_offsets": np.zeros(self.N + 1, dtype=np.int64),
+            "g2l_elem": np.zeros(self.NE * nloc, dtype=np.int32),
+            "g2l_local": np.zeros(self.NE * nloc, dtype=np.int32),
+            "sub_l2g": np.zeros(self.NE * nsub, dtype=np.int32) if sub else None,
+            "dirichlet_mask": np.zeros(self.N, dtype=np.uint8),
+        }
+        _check(lib().hxb_setup_export_maps(self._h, _ptr(out["l2g"]), _ptr(out["g2l_offsets"]),
+                                           _ptr(out["g2l_elem"]), _ptr(out["g2l_local"]), _ptr(out["sub_l2g"]),
+                                           _ptr(out["dirichlet_mask"])))
+        return out
+
+    def amg_level(self, l: int) -> dict:
+        rows, nnz = C.c_int64(), C.c_int64()
+        _check(lib().hxb_setup_amg_level(self._h, l, C.byref(rows), C.byref(nnz), None, None, None, None))
+        ptr = np.zeros(rows.value + 1, dtype=np.int64)
+        col = np.zeros(nnz.value, dtype=np.int32)
+        val = np.zeros(nnz.value)
+        agg = np.full(rows.value, -1, dtype=np.int32)
+        _check(lib().hxb_setup_amg_level(self._h, l, C.byref(rows), C.byref(nnz), _ptr(ptr), _ptr(col), _ptr(val),
+                                         _ptr(agg)))
+        return {"ptr": ptr, "col": col, "val": val, "aggregate": agg}
+
+    def lumped_mass(self):
+        m = np.empty(self.N)
+        _check(lib().hxb_setup_lumped_mass(self._h, _ptr(m)))
+        return m
+
+
+def gll(order: int):
+    """GllBasis tables (gll.cpp:106-114): nodes, weights, D[i][j] = phi'_i(t_j)."""
+    np1 = order + 1
+    t, w, d = np.zeros(np1), np.zeros(np1), np.zeros(np1 * np1)
+    _check(lib().hxb_gll(order, _ptr(t), _ptr(w), _ptr(d)))
+    return t, w, d.reshape(np1, np1)
+
+
+def gll_nodes_weights(n: int):
+    t, w, _ = gll(n)
+    return list(t), list(w)
+
+
+def derivation_matrix(n: int):
+    return gll(n)[2].tolist()
+
+
+def pencil(order: int) -> dict:
+    """PencilFactorization (fine.cpp:15-80)."""
+    p = order + 3
+    K, M, V, Vi, lam = np.zeros(p * p), np.zeros(p), np.zeros(p * p), np.zeros(p * p), np.zeros(p)
+    _check(lib().hxb_pencil(order, _ptr(K), _ptr(M), _ptr(V), _ptr(Vi), _ptr(lam)))
+    return {"K": K.reshape(p, p), "M": M, "V": V.reshape(p, p), "V_inv": Vi.reshape(p, p), "lambda": lam}
+
+
+# ---------------------------------------------------------------------------
+# Reference Python-module mirror (python/src/module.cpp)
+
+def _config_from_kwargs(kw) -> ProblemConfig:
+    cfg = ProblemConfig()
+    for key in ("k", "refine", "order", "kappa", "c", "family", "precond", "variant", "boundary", "tol",
+                "max_iterations", "coarse_solve", "coarse_direct_threshold", "device", "label"):
+        if key in kw:
+            setattr(cfg, key, kw[key])
+    if "bar" in kw:
+        cfg.bar = tuple(kw["bar"])
+    if "bar_size" in kw:
+        cfg.bar_size = tuple(kw["bar_size"])
+    return cfg
+
+
+def build_system(config: ProblemConfig | None = None, **kw) -> Plan:
+    """build_system (problem.cpp:73-108): kappa/c broadcast per element."""
+    cfg = config or _config_from_kwargs(kw)
+    mesh = make_mesh(cfg)
+    ne = mesh.num_elements
+    return Plan(mesh, cfg.order, np.full(ne, float(cfg.kappa)), np.full(ne, float(cfg.c)), precond=cfg.precond,
+                coarse_solve=cfg.coarse_solve, direct_threshold=cfg.coarse_direct_threshold, variant=cfg.variant,
+                device=cfg.device)
+
+
+def solve_poisson(**kw) -> dict:
+    """solve_poisson (problem.cpp:126-143 / module.cpp:106-114): s = 1."""
+    cfg = _config_from_kwargs(kw)
+    with build_system(cfg) as plan:
+        res = plan.pcg(None, cfg.tol, cfg.max_iterations)
+        report = {
+            "label": cfg.label, "status": res["status"], "iterations": res["iterations"], "N": plan.N,
+            "N_E": plan.NE, "n": plan.order, "residual_history": res["residual_history"].tolist(),
+            "zr_history": res["zr_history"].tolist(),
+            "operator": {"variant": cfg.variant, "n": plan.order, "N_E": plan.NE,
+                         "flops_model": residual_flops_model(plan.NE, plan.order),
+                         "bytes_model": residual_words_model(plan.NE, plan.order, cfg.variant) * 8},
+            "timings": {"setup_seconds": plan.setup_seconds, "solve_seconds": res["solve_seconds"]},
+        }
+        if plan.coarse_n > 0:
+            report["coarse"] = {"unknowns": plan.coarse_n, "solver": "amg" if plan.coarse_amg else "direct"}
+            if plan.coarse_amg:
+                report["coarse"]["hierarchy"] = {"levels": [{"rows": r, "nnz": z} for r, z in
+                                                            zip(plan.amg_rows, plan.amg_nnz)]}
+        if res["diagnostic"]:
+            report["diagnostic"] = res["diagnostic"]
+        return {"report": report, "u": res["u"]}
+
+
+def mesh_info(**kw) -> dict:
+    cfg = _config_from_kwargs(kw)
+    mesh = make_mesh(cfg)
+    n = cfg.order
+    with Plan(mesh, n, precond="none") as plan:
+        return {"num_elements": mesh.num_elements, "num_vertices": mesh.num_vertices, "num_nodes": plan.N}
+
+
+def residual_flops_model(ne: int, n: int) -> int:
+    return int(lib().hxb_flops_model(ne, n))
+
+
+def residual_words_model(ne: int, n: int, variant: str = "stored") -> int:
+    return int(lib().hxb_words_model(ne, n, VARIANTS[variant]))
+
+
+def fine_ops_model(ne: int, n: int) -> int:
+    return int(lib().hxb_fine_ops_model(ne, n))
+
+
+def fine_words_model(ne: int, n: int) -> int:
+    return int(lib().hxb_fine_words_model(ne, n))
