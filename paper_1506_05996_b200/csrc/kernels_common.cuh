@@ -16,6 +16,7 @@ constexpr int kMaxP = kMaxNP + 2;  // FDM pencil size n+3
 // constant-bank operand of the DFMA (no register or shared-memory traffic).
 struct OrderTables {
   double D[kMaxNP * kMaxNP];   // D[m*np+i] = phi'_m(t_i), gll.hpp:23-26
+  double DT[kMaxNP * kMaxNP];  // DT[m*np+i] = D[i*np+m] (adjoint contractions read rows)
   double V[kMaxP * kMaxP];     // pencil V     (fine.hpp:22)
   double Vi[kMaxP * kMaxP];    // pencil V^-1  (fine.hpp:23)
   double M[kMaxP];             // pencil lumped mass (fine.hpp:21)

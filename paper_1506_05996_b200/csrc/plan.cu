@@ -104,6 +104,7 @@ struct Plan {
 
   int order = 0, np = 0, nloc = 0, nsurf = 0, P = 0;
   int ne = 0, nv = 0, N = 0, nsg = 0;
+  int num_sms = 148, ax_grid = 1;
   int precond_mode = 0, variant = 0;
   bool do_fine = false, do_coarse = false, use_amg = false;
   double setup_seconds = 0;
@@ -203,6 +204,12 @@ DotArgs cdot_args(Plan& pl, double* result)
 }
 
 template <int NP>
+int ax_persistent_grid(const Plan& pl)
+{
+  return (pl.ne + AxShape<NP>::kEPB - 1) / AxShape<NP>::kEPB;
+}
+
+template <int NP>
 void launch_ax_elem(Plan& pl, const double* u, double* r, DotArgs dot, cudaStream_t s)
 {
   using Sh = AxShape<NP>;
@@ -219,26 +226,17 @@ void launch_ax_elem(Plan& pl, const double* u, double* r, DotArgs dot, cudaStrea
   a.nsurf = pl.nsurf;
   a.num_surface_global = pl.nsg;
   a.dot = dot;
-  const int grid = (pl.ne + Sh::kEPB - 1) / Sh::kEPB;
   const std::size_t smem = Sh::kSmemDoubles * sizeof(double);
-  ax_elem_kernel<NP><<<grid, Sh::kBlock, smem, s>>>(a);
+  ax_elem_kernel<NP><<<pl.ax_grid, Sh::kBlock, smem, s>>>(a);
 }
 
-int ax_elem_grid(const Plan& pl)
+template <int NP>
+void init_ax_grid(Plan& pl)
 {
-  int g = 0;
-  auto f = [&](auto tag) {
-    constexpr int NP = decltype(tag)::value;
-    g = (pl.ne + AxShape<NP>::kEPB - 1) / AxShape<NP>::kEPB;
-  };
-  switch (pl.np) {
-#define C(NPV) \
-  case NPV: f(std::integral_constant<int, NPV>{}); break;
-    C(2) C(3) C(4) C(5) C(6) C(7) C(8) C(9) C(10) C(11)
-#undef C
-  }
-  return g;
+  pl.ax_grid = ax_persistent_grid<NP>(pl);
 }
+
+int ax_elem_grid(const Plan& pl) { return pl.ax_grid; }
 
 // f = A u (+ optional u.f into *dot_result)
 void enqueue_ax(Plan& pl, const double* u, double* r, double* dot_result, cudaStream_t s)
@@ -420,6 +418,8 @@ void upload_tables(const GllBasis& basis, const Pencil& pencil)
   OrderTables t{};
   const int np = basis.npts();
   for (int q = 0; q < np * np; ++q) t.D[q] = basis.deriv[q];
+  for (int m = 0; m < np; ++m)
+    for (int i = 0; i < np; ++i) t.DT[m * np + i] = basis.deriv[i * np + m];
   for (int q = 0; q < pencil.p * pencil.p; ++q) {
     t.V[q] = pencil.V[q];
     t.Vi[q] = pencil.V_inv[q];
@@ -509,6 +509,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     cudaDeviceProp prop;
     HXB_CUDA(cudaGetDeviceProperties(&prop, pl.device));
     if (prop.major != 10) throw HxbError(HXB_ECUDA, "hexsem_b200 requires an sm_100 (B200) device");
+    pl.num_sms = prop.multiProcessorCount;
   }
   HostSetup& hs = pl.hs;
   hs.mesh = mesh_from_arrays(m->num_vertices, m->xyz, m->num_elements, m->conn, m->num_boundary_faces,
@@ -543,6 +544,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     throw HxbError(HXB_EINVAL, "mesh too large for one device plan");
 
   upload_tables(hs.basis, hs.pencil);
+  HXB_DISPATCH_NP(pl.np, init_ax_grid, pl);
 
   HXB_CUDA(cudaStreamCreateWithFlags(&pl.s_main, cudaStreamNonBlocking));
   HXB_CUDA(cudaStreamCreateWithFlags(&pl.s_coarse, cudaStreamNonBlocking));

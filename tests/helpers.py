@@ -25,7 +25,7 @@ def history_parity(ours: dict, ref: dict, tol=1e-10, iters_slack=1):
     ra, rb = np.asarray(ours["residual_history"]), np.asarray(ref["residual_history"])
     k = min(len(ra), len(rb))
     r0 = rb[0]
-    assert abs(ra[0] - r0) <= 1e-14 * r0
+    assert abs(ra[0] - r0) <= 1e-13 * r0
     dr = float(np.max(np.abs(ra[:k] - rb[:k])) / r0)
     assert dr <= tol, dr
     if ours.get("u") is not None:

@@ -1,0 +1,17 @@
+"""Profiling driver (run under ncu on the GPU box): one plan, a few Ax and
+P applications and a short PCG. Not a bench — numbers printed here are
+never reported."""
+import sys
+
+sys.path.insert(0, ".")
+import paper_1506_05996_b200 as hx
+from oracle import splitmix_vector
+
+k = int(sys.argv[1]) if len(sys.argv) > 1 else 30
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 7
+plan = hx.Plan(hx.generate_cube_mesh(k), n)
+u = splitmix_vector(plan.N, 12345)
+for _ in range(2):
+    plan.apply_A(u)
+plan.apply_P(u)
+plan.pcg(None, tol=1e-8, max_iterations=3, want_u=False)
