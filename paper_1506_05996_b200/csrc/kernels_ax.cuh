@@ -222,35 +222,4 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
   dot_commit<Sh::kBlock>(a.dot, dot, red);
 }
 
-// Surface assembly over element-surface copies, in ascending (e,l) order
-// (gather, mesh.cpp:463-475), plus the Dirichlet identity rows
-// (operator.cpp:279-280) and the optional fused p.Ap partial.
-struct AxGatherArgs {
-  const double* rsurf;
-  const unsigned* off;   // num_surface_global + 1
-  const int* idx;        // e*nsurf + slot, sorted per node
-  const double* u;
-  const std::uint8_t* mask;
-  double* r;
-  int num_surface_global;
-  DotArgs dot;
-};
-
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) ax_gather_kernel(AxGatherArgs a)
-{
-  __shared__ double red[BLOCK / 32];
-  double dot = 0.0;
-  for (int g = blockIdx.x * BLOCK + threadIdx.x; g < a.num_surface_global; g += gridDim.x * BLOCK) {
-    const unsigned q0 = __ldg(a.off + g), q1 = __ldg(a.off + g + 1);
-    double s = 0.0;
-    for (unsigned q = q0; q < q1; ++q) s += __ldg(a.rsurf + __ldg(a.idx + q));
-    const double ug = __ldg(a.u + g);
-    if (__ldg(a.mask + g)) s = ug;
-    a.r[g] = s;
-    dot += ug * s;
-  }
-  dot_commit<BLOCK>(a.dot, dot, red);
-}
-
 }  // namespace hxb

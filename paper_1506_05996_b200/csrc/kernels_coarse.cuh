@@ -58,15 +58,41 @@ __global__ void __launch_bounds__(BLOCK) restrict_kernel(const double* __restric
   }
 }
 
-// R[v] = vmask[v] ? 0 : sum of Rpart over (e,cb) incidences in ascending order
-__global__ void vertex_gather_kernel(const double* __restrict__ Rpart, const unsigned* __restrict__ off,
-                                     const int* __restrict__ idx, const std::uint8_t* __restrict__ vmask,
-                                     double* __restrict__ R, int nv)
+// Prolongation per element copy (coarse.cpp:164-182): p_l = (sum_cb B[cb][l]
+// Z[v_cb]) * m_l, stored like Ax outputs (element-interior nodes direct into
+// pint, element-surface copies into psurf) for the deterministic gather in
+// combine_kernel. The 8 corner values are loaded once per element.
+template <int NP, int EPB, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) prolong_elem_kernel(const double* __restrict__ Z, const int* __restrict__ conn,
+                                                             const double* __restrict__ mass, double* __restrict__ psurf,
+                                                             double* __restrict__ pint, int ne, int nsurf, int nsg)
 {
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1);
+  const OrderTables& T = c_tab[NP];
+  const int tid = threadIdx.x;
+  const int el = tid / (NP * NP), loc = tid % (NP * NP);
+  const int i = loc % NP, j = loc / NP;
+  const int e = blockIdx.x * EPB + el;
+  if (el >= EPB || e >= ne) return;
+  constexpr int kCorner[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // kHexCornerFromBits, mesh.hpp:33
+  double zc[8];
+#pragma unroll
+  for (int cb = 0; cb < 8; ++cb) zc[cb] = __ldg(Z + __ldg(conn + 8 * e + kCorner[cb]));
+  const double hi[2] = {T.hat0[i], T.hat1[i]}, hj[2] = {T.hat0[j], T.hat1[j]};
+  const long long ibase = (long long)nsg + (long long)e * NI;
+  const double* m0 = mass + (std::size_t)e * NP * NP * NP + j * NP + i;
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const double hk[2] = {T.hat0[k], T.hat1[k]};
     double s = 0.0;
-    for (unsigned q = __ldg(off + v); q < __ldg(off + v + 1); ++q) s += __ldg(Rpart + __ldg(idx + q));
-    R[v] = __ldg(vmask + v) ? 0.0 : s;
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb) s += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[cb >> 2] * zc[cb];
+    const double v = s * __ldg(m0 + k * NP * NP);
+    const int sl = surface_slot(NP, i, j, k);
+    if (sl >= 0)
+      psurf[(long long)e * nsurf + sl] = v;
+    else
+      pint[ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1)] = v;
   }
 }
 
@@ -101,17 +127,14 @@ __global__ void amg_jacobi2_kernel(DevCsr A, const double* __restrict__ dinv, co
   }
 }
 
-// rc[c] = sum over members i of aggregate c (ascending) of (r_i - (A z)_i)  (amg.cpp:214-218)
-__global__ void amg_resid_restrict_kernel(DevCsr A, const double* __restrict__ r, const double* __restrict__ z,
-                                          const int* __restrict__ agg_ptr, const int* __restrict__ agg_mem,
-                                          double* __restrict__ rc, int nc)
+// rc[c] = sum over members i of aggregate c (ascending) of rho_i
+// (rho = r - A z from amg_resid_kernel; amg.cpp:214-218)
+__global__ void amg_agg_sum_kernel(const double* __restrict__ rho, const int* __restrict__ agg_ptr,
+                                   const int* __restrict__ agg_mem, double* __restrict__ rc, int nc)
 {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
     double s = 0.0;
-    for (int q = __ldg(agg_ptr + c); q < __ldg(agg_ptr + c + 1); ++q) {
-      const int i = __ldg(agg_mem + q);
-      s += __ldg(r + i) - csr_row_dot(A, i, z);
-    }
+    for (int q = __ldg(agg_ptr + c); q < __ldg(agg_ptr + c + 1); ++q) s += __ldg(rho + __ldg(agg_mem + q));
     rc[c] = s;
   }
 }

@@ -17,8 +17,8 @@ constexpr int kMaxP = kMaxNP + 2;  // FDM pencil size n+3
 struct OrderTables {
   double D[kMaxNP * kMaxNP];   // D[m*np+i] = phi'_m(t_i), gll.hpp:23-26
   double DT[kMaxNP * kMaxNP];  // DT[m*np+i] = D[i*np+m] (adjoint contractions read rows)
-  double V[kMaxP * kMaxP];     // pencil V     (fine.hpp:22)
-  double Vi[kMaxP * kMaxP];    // pencil V^-1  (fine.hpp:23)
+  double VT[kMaxP * kMaxP];    // pencil V transposed: VT[x*p+d] = V[d][x] (fine.hpp:22)
+  double ViT[kMaxP * kMaxP];   // pencil V^-1 transposed (fine.hpp:23)
   double M[kMaxP];             // pencil lumped mass (fine.hpp:21)
   double lam[kMaxP];           // pencil eigenvalues (fine.hpp:24)
   double hat0[kMaxNP];         // 0.5*(1-t_i)  coarse hats (gll.cpp:92)

@@ -23,6 +23,7 @@
 #include "kernels_coarse.cuh"
 #include "kernels_common.cuh"
 #include "kernels_fine.cuh"
+#include "kernels_gather.cuh"
 #include "kernels_vec.cuh"
 #include "capi_common.hpp"
 #include "setup.hpp"
@@ -40,6 +41,12 @@ namespace {
   } while (0)
 
 constexpr int kVecBlock = 256;
+
+int gather_grid(long long n)
+{
+  const long long b = (n + kGatherBlock - 1) / kGatherBlock;
+  return static_cast<int>(std::max(1LL, std::min(b, 148LL * 8)));
+}
 
 int vec_grid(long long n)
 {
@@ -134,6 +141,7 @@ struct Plan {
   int* vtx_idx = nullptr;
   std::uint8_t* vmask = nullptr;
   double *Rpart = nullptr, *R = nullptr, *Z = nullptr, *rho = nullptr, *dZ = nullptr;
+  double *psurf = nullptr, *pint = nullptr;
   std::vector<DevLevel> lv;  // AMG levels 0..L (L = coarsest, uses dense)
   DevDense dense;
   DevCsr Kc{};               // K_c on the device (AMG mode: residual between the two K-cycles)
@@ -257,7 +265,7 @@ void enqueue_ax(Plan& pl, const double* u, double* r, double* dot_result, cudaSt
   g.r = r;
   g.num_surface_global = pl.nsg;
   g.dot = d2;
-  ax_gather_kernel<kVecBlock><<<vec_grid(pl.nsg), kVecBlock, 0, s>>>(g);
+  ax_gather_kernel<<<gather_grid(pl.nsg), kGatherBlock, 0, s>>>(g);
 }
 
 template <int NP>
@@ -277,7 +285,6 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   fdm_kernel<NP><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
 }
 
-template <int NP>
 void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse)
 {
   CombineArgs a;
@@ -286,21 +293,26 @@ void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, b
   a.zsub = pl.zsub;
   a.fine_off = pl.fine_off;
   a.fine_idx = pl.fine_idx;
-  a.Z = pl.Z;
-  a.conn = pl.conn;
-  a.mass = pl.mass;
-  a.lumped = pl.d_lumped;
+  a.psurf = pl.psurf;
+  a.pint = pl.pint;
   a.ax_off = pl.ax_off;
   a.ax_idx = pl.ax_idx;
-  a.surf_local = pl.surf_local;
+  a.lumped = pl.d_lumped;
   a.z = pl.z;
   a.N = pl.N;
-  a.num_surface_global = pl.nsg;
-  a.nsurf = pl.nsurf;
+  a.nsg = pl.nsg;
   a.do_fine = do_fine ? 1 : 0;
   a.do_coarse = do_coarse ? 1 : 0;
   a.dot = zr_result ? dot_args(pl, zr_result) : DotArgs{};
-  combine_kernel<NP, kVecBlock><<<vec_grid(pl.N), kVecBlock, 0, s>>>(a);
+  combine_kernel<<<gather_grid(pl.N), kGatherBlock, 0, s>>>(a);
+}
+
+template <int NP>
+void launch_prolong(Plan& pl, cudaStream_t s)
+{
+  using Sh = AxShape<NP>;
+  prolong_elem_kernel<NP, Sh::kEPB, Sh::kBlock><<<(pl.ne + Sh::kEPB - 1) / Sh::kEPB, Sh::kBlock, 0, s>>>(
+      pl.Z, pl.conn, pl.mass, pl.psurf, pl.pint, pl.ne, pl.nsurf, pl.nsg);
 }
 
 template <int NP>
@@ -334,7 +346,8 @@ void enqueue_cycle(Plan& pl, int l, const double* r, double* zout, cudaStream_t 
   DevLevel& c = pl.lv[l + 1];
   const int g = vec_grid(v.n);
   amg_jacobi2_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA);
-  amg_resid_restrict_kernel<<<vec_grid(v.nc), kVecBlock, 0, s>>>(v.A, r, v.zA, v.agg_ptr, v.agg_mem, c.b, v.nc);
+  amg_resid_kernel<<<g, kVecBlock, 0, s>>>(v.A, r, v.zA, v.kf);  // kf is free during the cycle
+  amg_agg_sum_kernel<<<vec_grid(v.nc), kVecBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
   enqueue_ksolve(pl, l + 1, c.b, c.x, s);
   amg_prolong_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
   amg_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout);
@@ -367,7 +380,7 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
 void enqueue_coarse(Plan& pl, cudaStream_t s)
 {
   HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s);
-  vertex_gather_kernel<<<vec_grid(pl.nv), kVecBlock, 0, s>>>(pl.Rpart, pl.vtx_off, pl.vtx_idx, pl.vmask, pl.R, pl.nv);
+  vertex_gather_kernel<<<gather_grid(pl.nv), kGatherBlock, 0, s>>>(pl.Rpart, pl.vtx_off, pl.vtx_idx, pl.vmask, pl.R, pl.nv);
   if (pl.use_amg) {
     enqueue_cycle(pl, 0, pl.R, pl.Z, s);
     // two composed K-cycles: Z = B R + B (R - K_c B R)  (coarse.cpp:193-200)
@@ -378,6 +391,7 @@ void enqueue_coarse(Plan& pl, cudaStream_t s)
   } else {
     enqueue_dense(pl, pl.R, pl.Z, s);
   }
+  HXB_DISPATCH_NP(pl.np, launch_prolong, pl, s);
 }
 
 void capture_coarse_graph(Plan& pl)
@@ -407,7 +421,7 @@ void enqueue_precond(Plan& pl, double* zr_result)
   }
   if (pl.do_fine) HXB_DISPATCH_NP(pl.np, launch_fdm, pl, s);
   if (pl.do_coarse) HXB_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
-  HXB_DISPATCH_NP(pl.np, launch_combine, pl, zr_result, s, pl.do_fine, pl.do_coarse);
+  launch_combine(pl, zr_result, s, pl.do_fine, pl.do_coarse);
 }
 
 // ---------------------------------------------------------------------------
@@ -420,10 +434,11 @@ void upload_tables(const GllBasis& basis, const Pencil& pencil)
   for (int q = 0; q < np * np; ++q) t.D[q] = basis.deriv[q];
   for (int m = 0; m < np; ++m)
     for (int i = 0; i < np; ++i) t.DT[m * np + i] = basis.deriv[i * np + m];
-  for (int q = 0; q < pencil.p * pencil.p; ++q) {
-    t.V[q] = pencil.V[q];
-    t.Vi[q] = pencil.V_inv[q];
-  }
+  for (int d = 0; d < pencil.p; ++d)
+    for (int x = 0; x < pencil.p; ++x) {
+      t.VT[x * pencil.p + d] = pencil.V[d * pencil.p + x];
+      t.ViT[x * pencil.p + d] = pencil.V_inv[d * pencil.p + x];
+    }
   for (int q = 0; q < pencil.p; ++q) {
     t.M[q] = pencil.M[q];
     t.lam[q] = pencil.lambda[q];
@@ -640,6 +655,8 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.Z = M.alloc<double>(pl.nv);
     pl.rho = M.alloc<double>(pl.nv);
     pl.dZ = M.alloc<double>(pl.nv);
+    pl.psurf = M.alloc<double>(num.l2g_surf.size());
+    pl.pint = M.alloc<double>(pl.N);
     pl.coarse_n = hs.Kc.n;
     if (pl.use_amg) {
       pl.Kc = csr_to_device(pl, hs.Kc);
@@ -903,7 +920,7 @@ static int apply_precond_host(hxb_plan* plan, const double* r, double* z, int mo
       // rows; emulate with a mask-free combine by temporarily pointing at a zero mask
       std::uint8_t* saved = pl->mask;
       pl->mask = pl->zero_mask;
-      HXB_DISPATCH_NP(pl->np, launch_combine, *pl, nullptr, pl->s_main, f, c);
+      launch_combine(*pl, nullptr, pl->s_main, f, c);
       pl->mask = saved;
     }
     HXB_CUDA(cudaGetLastError());
