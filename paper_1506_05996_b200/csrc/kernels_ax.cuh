@@ -2,8 +2,8 @@
 // (operator.cpp:255-287) with the element contraction of
 // contraction_kernel (operator.cpp:124-163), restructured for sm_100a.
 //
-// Each CTA works on EPB elements, each element an NP x NP thread tile (i,j)
-// owning the k-column of its element. Per element:
+// Each CTA works on one element at a time, an NP x NP thread tile (i,j) with
+// each thread owning the k-column of the element. Per element:
 //   A  gather u (masked) into registers (k-column) and two shared copies laid
 //      out for x-line and y-line access
 //   B  r- and s-derivatives as line contractions: thread -> one x-line and one
@@ -28,17 +28,22 @@ namespace hxb {
 
 template <int NP>
 struct AxShape {
-  static constexpr int kLocal = NP * NP;  // threads per element
-  static constexpr int kEPB = NP <= 3 ? 8 : (NP <= 6 ? 4 : (NP <= 8 ? 2 : 1));
-  static constexpr int kBlock = ((kLocal * kEPB + 31) / 32) * 32;
-  static constexpr int kS = NP | 1;  // generic padded row stride
+  static constexpr int kLocal = NP * NP;              // threads per element
+  static constexpr int kBlock = ((kLocal + 31) / 32) * 32;
+  static constexpr int kEPB = 1;                      // one element per CTA (persistent)
+  static constexpr int kS = NP | 1;                   // generic padded row stride
+  static constexpr int kNloc = NP * NP * NP;
+  static constexpr int kNlocP = (kNloc + 1) & ~1;     // 16-byte aligned plane blocks
+  static constexpr int kNsurf = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2);
+  static constexpr int kNsurfP = (kNsurf + 3) & ~3;   // 16-byte aligned index blocks
   // per-element shared doubles for the x-layout (sa) and y-layout (sb) buffers
   static constexpr int kBufA = NP == 8 ? 512 : NP * NP * kS;
   static constexpr int kBufB = NP == 8 ? 576 : NP * NP * kS;
-  static constexpr int kSmemDoubles = (kBufA + kBufB) * kEPB;
-  // register budget per thread (>= 20 resident warps per SM at NP=8)
+  static constexpr std::size_t kGBytes = 6ull * kNlocP * sizeof(double);
+  static constexpr std::size_t kIdxBytes = kNsurfP * sizeof(int);
+  static constexpr std::size_t kSmemBytes =
+      kGBytes + (kBufA + kBufB) * sizeof(double) + kIdxBytes + 2 * sizeof(unsigned long long);
   static constexpr int kRegs = NP >= 9 ? 128 : 96;
-  static constexpr int kMinBlocks = 65536 / (kBlock * kRegs) > 0 ? 65536 / (kBlock * kRegs) : 1;
 };
 
 // x-layout: owner (i,j | k) and x-line (j,k | m) accesses conflict free
@@ -62,15 +67,13 @@ __device__ __forceinline__ int lay_b(int k, int j, int i)
 
 struct AxArgs {
   const double* u;          // N, input (p in PCG)
-  const double* wg;         // 6 planes, plane stride = plane_stride
-  std::size_t plane_stride; // NE * nloc
+  const double* wg;         // [e][6][nlocp]: kappa*m*Gt planes per element (TMA-staged)
   const double* mass;       // NE * nloc
   const double* c_e;        // NE
-  const int* l2g_surf;      // NE * nsurf, Dirichlet-encoded
-  double* rsurf;            // NE * nsurf surface E-vector (output)
+  const int* l2g_surf;      // [e][nsurfp], Dirichlet-encoded (TMA-staged)
+  double* rsurf;            // [e][nsurfp] surface E-vector (output)
   double* r;                // N output (interior nodes written here)
   int ne;
-  int nsurf;
   int num_surface_global;   // first element-interior global id
   DotArgs dot;              // optional: sum over interior nodes of u*r
 };
@@ -107,115 +110,144 @@ __device__ __forceinline__ void contract3(const double* __restrict__ M, FX&& in_
   }
 }
 
+// Persistent: CTA b processes elements b, b+grid, ... . The element's six
+// metric planes (6*nloc FP64, the bulk of Ax traffic) and its surface index
+// block are streamed into shared memory by TMA bulk copies issued one element
+// ahead: indices for e' as soon as phase A of e has consumed them, planes for
+// e' as soon as phase C of e has — so HBM streams while the CTA computes.
 template <int NP>
-__global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) ax_elem_kernel(AxArgs a)
+__global__ void __launch_bounds__(AxShape<NP>::kBlock) ax_elem_kernel(AxArgs a)
 {
   using Sh = AxShape<NP>;
-  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1);
-  extern __shared__ double smem[];
+  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NLP = Sh::kNlocP;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* sG = reinterpret_cast<double*>(smem_raw);                  // [6][nlocp]
+  double* sa = sG + 6 * NLP;
+  double* sb = sa + Sh::kBufA;
+  int* sidx = reinterpret_cast<int*>(sb + Sh::kBufB);                // [nsurfp]
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sidx + Sh::kNsurfP);  // [0]=G, [1]=idx
   __shared__ double red[Sh::kBlock / 32];
   const double* D = c_tab[NP].D;
   const double* DT = c_tab[NP].DT;
 
   const int tid = threadIdx.x;
-  const int el = tid / Sh::kLocal;
-  const bool lane_ok = el < Sh::kEPB;
-  const int loc = tid - el * Sh::kLocal;
+  const bool lane_ok = tid < Sh::kLocal;
+  const int loc = lane_ok ? tid : 0;
   const int i = loc % NP, j = loc / NP;  // owner column; also x-line (j'=i,k'=j) and y-line (i'=i,k'=j)
-  const int elc = lane_ok ? el : 0;
-  double* sa = smem + elc * (Sh::kBufA + Sh::kBufB);
-  double* sb = sa + Sh::kBufA;
-  const int e = blockIdx.x * Sh::kEPB + el;
-  const bool active = lane_ok && e < a.ne;
-  const long long ibase = (long long)a.num_surface_global + (long long)e * NI;
-  const int* surf = a.l2g_surf + (long long)e * a.nsurf;
 
-  // ---- A: gather u (masked, operator.cpp:264-265) ---------------------------
-  double ucol[NP];
-#pragma unroll
-  for (int k = 0; k < NP; ++k) {
-    double v = 0.0;
-    if (active) {
-      const int s = surface_slot(NP, i, j, k);
-      v = s >= 0 ? load_masked(a.u, __ldg(surf + s))
-                 : __ldg(a.u + ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1));
-    }
-    ucol[k] = v;
-    if (lane_ok) {
-      sa[lay_a<NP>(k, j, i)] = v;
-      sb[lay_b<NP>(k, j, i)] = v;
-    }
+  int e = blockIdx.x;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
   }
   __syncthreads();
-
-  // ---- B: derivatives (operator.cpp:136-138): x-line, y-line, owner z-column
-  double fz[NP];
-  {
-    double ox[NP], oy[NP];
-    contract3<NP>(D, [&](int m) { return sa[lay_a<NP>(j, i, m)]; }, [&](int m) { return sb[lay_b<NP>(j, m, i)]; },
-                  ucol, ox, oy, fz);
-    __syncthreads();  // all lines read before any is overwritten
-    if (lane_ok) {
-#pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        sa[lay_a<NP>(j, i, q)] = ox[q];
-        sb[lay_b<NP>(j, q, i)] = oy[q];
-      }
-    }
+  if (tid == 0 && e < a.ne) {
+    mbar_expect_tx(&bar[1], Sh::kIdxBytes);
+    bulk_g2s(sidx, a.l2g_surf + (long long)e * Sh::kNsurfP, Sh::kIdxBytes, &bar[1]);
+    mbar_expect_tx(&bar[0], Sh::kGBytes);
+    bulk_g2s(sG, a.wg + (long long)e * 6 * NLP, Sh::kGBytes, &bar[0]);
   }
-  __syncthreads();
-
-  // ---- C: metric fluxes (operator.cpp:142-144) ------------------------------
-  if (active) {
-    const std::size_t ps = a.plane_stride;
-    const double* g0 = a.wg + (std::size_t)e * NP * NP * NP + j * NP + i;
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const double* gk = g0 + k * NP * NP;
-      const double w0 = __ldg(gk), w1 = __ldg(gk + ps), w2 = __ldg(gk + 2 * ps);
-      const double w3 = __ldg(gk + 3 * ps), w4 = __ldg(gk + 4 * ps), w5 = __ldg(gk + 5 * ps);
-      const int pa = lay_a<NP>(k, j, i), pb = lay_b<NP>(k, j, i);
-      const double sx = sa[pa], sy = sb[pb], sz = fz[k];
-      sa[pa] = w0 * sx + w1 * sy + w2 * sz;
-      sb[pb] = w1 * sx + w3 * sy + w4 * sz;
-      fz[k] = w2 * sx + w4 * sy + w5 * sz;
-    }
-  }
-  __syncthreads();
-
-  // ---- D: adjoint contractions (operator.cpp:152-157), rows of D^T ------------
-  double tz[NP];
-  {
-    double ox[NP], oy[NP];
-    contract3<NP>(DT, [&](int m) { return sa[lay_a<NP>(j, i, m)]; }, [&](int m) { return sb[lay_b<NP>(j, m, i)]; },
-                  fz, ox, oy, tz);
-    __syncthreads();
-    if (lane_ok) {
-#pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        sa[lay_a<NP>(j, i, q)] = ox[q];
-        sb[lay_b<NP>(j, q, i)] = oy[q];
-      }
-    }
-  }
-  __syncthreads();
-
-  // ---- E: sum, mass term, store ---------------------------------------------
   double dot = 0.0;
-  if (active) {
-    const double ce = __ldg(a.c_e + e);
-    const double* m0 = a.mass + (std::size_t)e * NP * NP * NP + j * NP + i;
-    double* rs = a.rsurf + (long long)e * a.nsurf;
+  unsigned phase = 0;
+  for (; e < a.ne; e += gridDim.x, phase ^= 1u) {
+    const int en = e + gridDim.x;
+    const long long ibase = (long long)a.num_surface_global + (long long)e * NI;
+
+    // ---- A: gather u (masked, operator.cpp:264-265) ---------------------------
+    mbar_wait(&bar[1], phase);
+    double ucol[NP];
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
-      double r = (sa[lay_a<NP>(k, j, i)] + sb[lay_b<NP>(k, j, i)]) + tz[k];
-      if (ce != 0.0) r += (ce * ucol[k]) * __ldg(m0 + k * NP * NP);  // operator.cpp:159
       const int s = surface_slot(NP, i, j, k);
-      if (s >= 0) {
-        rs[s] = r;
-      } else {
-        a.r[ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1)] = r;
-        dot += ucol[k] * r;
+      ucol[k] = s >= 0 ? load_masked(a.u, sidx[s])
+                       : __ldg(a.u + ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1));
+    }
+    __syncthreads();  // sidx consumed; previous element's phase E done with sa/sb
+    if (tid == 0 && en < a.ne) {
+      mbar_expect_tx(&bar[1], Sh::kIdxBytes);
+      bulk_g2s(sidx, a.l2g_surf + (long long)en * Sh::kNsurfP, Sh::kIdxBytes, &bar[1]);
+    }
+    if (lane_ok) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        sa[lay_a<NP>(k, j, i)] = ucol[k];
+        sb[lay_b<NP>(k, j, i)] = ucol[k];
+      }
+    }
+    __syncthreads();
+
+    // ---- B: derivatives (operator.cpp:136-138): x-line, y-line, owner z-column
+    double fz[NP];
+    {
+      double ox[NP], oy[NP];
+      contract3<NP>(D, [&](int m) { return sa[lay_a<NP>(j, i, m)]; }, [&](int m) { return sb[lay_b<NP>(j, m, i)]; },
+                    ucol, ox, oy, fz);
+      __syncthreads();  // all lines read before any is overwritten
+      if (lane_ok) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          sa[lay_a<NP>(j, i, q)] = ox[q];
+          sb[lay_b<NP>(j, q, i)] = oy[q];
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- C: metric fluxes (operator.cpp:142-144), planes from shared ----------
+    mbar_wait(&bar[0], phase);
+    if (lane_ok) {
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        const int l = (k * NP + j) * NP + i;
+        const double w0 = sG[l], w1 = sG[NLP + l], w2 = sG[2 * NLP + l];
+        const double w3 = sG[3 * NLP + l], w4 = sG[4 * NLP + l], w5 = sG[5 * NLP + l];
+        const int pa = lay_a<NP>(k, j, i), pb = lay_b<NP>(k, j, i);
+        const double sx = sa[pa], sy = sb[pb], sz = fz[k];
+        sa[pa] = w0 * sx + w1 * sy + w2 * sz;
+        sb[pb] = w1 * sx + w3 * sy + w4 * sz;
+        fz[k] = w2 * sx + w4 * sy + w5 * sz;
+      }
+    }
+    __syncthreads();  // sG consumed
+    if (tid == 0 && en < a.ne) {
+      mbar_expect_tx(&bar[0], Sh::kGBytes);
+      bulk_g2s(sG, a.wg + (long long)en * 6 * NLP, Sh::kGBytes, &bar[0]);
+    }
+
+    // ---- D: adjoint contractions (operator.cpp:152-157), rows of D^T ------------
+    double tz[NP];
+    {
+      double ox[NP], oy[NP];
+      contract3<NP>(DT, [&](int m) { return sa[lay_a<NP>(j, i, m)]; }, [&](int m) { return sb[lay_b<NP>(j, m, i)]; },
+                    fz, ox, oy, tz);
+      __syncthreads();
+      if (lane_ok) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          sa[lay_a<NP>(j, i, q)] = ox[q];
+          sb[lay_b<NP>(j, q, i)] = oy[q];
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- E: sum, mass term, store ---------------------------------------------
+    if (lane_ok) {
+      const double ce = __ldg(a.c_e + e);
+      const double* m0 = a.mass + (std::size_t)e * Sh::kNloc + j * NP + i;
+      double* rs = a.rsurf + (long long)e * Sh::kNsurfP;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        double r = (sa[lay_a<NP>(k, j, i)] + sb[lay_b<NP>(k, j, i)]) + tz[k];
+        if (ce != 0.0) r += (ce * ucol[k]) * __ldg(m0 + k * NP * NP);  // operator.cpp:159
+        const int s = surface_slot(NP, i, j, k);
+        if (s >= 0) {
+          rs[s] = r;
+        } else {
+          a.r[ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1)] = r;
+          dot += ucol[k] * r;
+        }
       }
     }
   }

@@ -214,7 +214,13 @@ DotArgs cdot_args(Plan& pl, double* result)
 template <int NP>
 int ax_persistent_grid(const Plan& pl)
 {
-  return (pl.ne + AxShape<NP>::kEPB - 1) / AxShape<NP>::kEPB;
+  using Sh = AxShape<NP>;
+  HXB_CUDA(cudaFuncSetAttribute(ax_elem_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(Sh::kSmemBytes)));
+  int per_sm = 0;
+  HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ax_elem_kernel<NP>, Sh::kBlock, Sh::kSmemBytes));
+  per_sm = std::max(per_sm, 1);
+  return std::max(1, std::min(pl.ne, per_sm * pl.num_sms));
 }
 
 template <int NP>
@@ -224,18 +230,15 @@ void launch_ax_elem(Plan& pl, const double* u, double* r, DotArgs dot, cudaStrea
   AxArgs a;
   a.u = u;
   a.wg = pl.wg;
-  a.plane_stride = static_cast<std::size_t>(pl.ne) * pl.nloc;
   a.mass = pl.mass;
   a.c_e = pl.c_e;
   a.l2g_surf = pl.l2g_surf;
   a.rsurf = pl.rsurf;
   a.r = r;
   a.ne = pl.ne;
-  a.nsurf = pl.nsurf;
   a.num_surface_global = pl.nsg;
   a.dot = dot;
-  const std::size_t smem = Sh::kSmemDoubles * sizeof(double);
-  ax_elem_kernel<NP><<<pl.ax_grid, Sh::kBlock, smem, s>>>(a);
+  ax_elem_kernel<NP><<<pl.ax_grid, Sh::kBlock, Sh::kSmemBytes, s>>>(a);
 }
 
 template <int NP>
@@ -543,7 +546,8 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   pl.order = order;
   pl.np = order + 1;
   pl.nloc = pl.np * pl.np * pl.np;
-  pl.nsurf = surface_slot_count(pl.np);
+  const int nsurf_raw = surface_slot_count(pl.np);
+  pl.nsurf = (nsurf_raw + 3) & ~3;  // padded element stride of every surface-slot array (16 B aligned)
   pl.P = order + 3;
   pl.ne = ne;
   pl.nv = mesh.num_vertices();
@@ -567,7 +571,16 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   for (cudaEvent_t* e : {&pl.ev_t0, &pl.ev_t1, &pl.ev_a}) HXB_CUDA(cudaEventCreate(e));
 
   DeviceArena& M = pl.mem;
-  pl.wg = M.upload(hs.geo.wg);
+  {  // kappa*m*Gt planes regrouped per element: [e][6][nlocp] (one TMA stream per element)
+    const int nlocp = (pl.nloc + 1) & ~1;
+    const std::size_t total = static_cast<std::size_t>(ne) * pl.nloc;
+    std::vector<double> wge(static_cast<std::size_t>(ne) * 6 * nlocp, 0.0);
+    for (int e = 0; e < ne; ++e)
+      for (int p = 0; p < 6; ++p)
+        std::memcpy(&wge[(static_cast<std::size_t>(e) * 6 + p) * nlocp],
+                    &hs.geo.wg[p * total + static_cast<std::size_t>(e) * pl.nloc], pl.nloc * sizeof(double));
+    pl.wg = M.upload(wge);
+  }
   hs.geo.wg.clear();
   hs.geo.wg.shrink_to_fit();
   pl.mass = M.upload(hs.geo.mass);
@@ -579,32 +592,35 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   HXB_CUDA(cudaMemset(pl.zero_mask, 0, pl.N));
   pl.d_lumped = M.upload(hs.lumped);
 
-  // encoded surface map and Ax surface gather CSR (ascending e*nsurf+s)
+  // encoded surface map and Ax surface gather CSR (ascending e*nsurf+s, padded stride)
   {
-    std::vector<int> enc(num.l2g_surf.size());
-    for (std::size_t q = 0; q < enc.size(); ++q) {
-      const gid g = num.l2g_surf[q];
-      enc[q] = num.dirichlet_mask[g] ? encode_dirichlet(g) : g;
-    }
+    std::vector<int> enc(static_cast<std::size_t>(ne) * pl.nsurf, 0);
+    for (int e = 0; e < ne; ++e)
+      for (int q = 0; q < nsurf_raw; ++q) {
+        const gid g = num.l2g_surf[static_cast<std::size_t>(e) * nsurf_raw + q];
+        enc[static_cast<std::size_t>(e) * pl.nsurf + q] = num.dirichlet_mask[g] ? encode_dirichlet(g) : g;
+      }
     pl.l2g_surf = M.upload(enc);
     std::vector<unsigned> off(static_cast<std::size_t>(pl.nsg) + 1, 0);
     for (gid g : num.l2g_surf) off[g + 1]++;
     for (int g = 0; g < pl.nsg; ++g) off[g + 1] += off[g];
     std::vector<int> idx(num.l2g_surf.size());
     std::vector<unsigned> cur(off.begin(), off.end() - 1);
-    for (std::size_t q = 0; q < num.l2g_surf.size(); ++q) idx[cur[num.l2g_surf[q]]++] = static_cast<int>(q);
+    for (int e = 0; e < ne; ++e)
+      for (int q = 0; q < nsurf_raw; ++q)
+        idx[cur[num.l2g_surf[static_cast<std::size_t>(e) * nsurf_raw + q]]++] = e * pl.nsurf + q;
     pl.ax_off = M.upload(off);
     pl.ax_idx = M.upload(idx);
-    std::vector<short> sl(pl.nsurf);
+    std::vector<short> sl(pl.nsurf, 0);
     for (int k = 0; k < pl.np; ++k)
       for (int j = 0; j < pl.np; ++j)
         for (int i = 0; i < pl.np; ++i) {
-          const int s = surface_slot_of(pl.np, i, j, k);
-          if (s >= 0) sl[s] = static_cast<short>((k * pl.np + j) * pl.np + i);
+          const int sq = surface_slot_of(pl.np, i, j, k);
+          if (sq >= 0) sl[sq] = static_cast<short>((k * pl.np + j) * pl.np + i);
         }
     pl.surf_local = M.upload(sl);
   }
-  pl.rsurf = M.alloc<double>(num.l2g_surf.size());
+  pl.rsurf = M.alloc<double>(static_cast<std::size_t>(ne) * pl.nsurf);
 
   // fine: encoded sub_face and the subdomain gather CSR in (e, slot) order
   if (pl.do_fine) {
@@ -655,7 +671,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.Z = M.alloc<double>(pl.nv);
     pl.rho = M.alloc<double>(pl.nv);
     pl.dZ = M.alloc<double>(pl.nv);
-    pl.psurf = M.alloc<double>(num.l2g_surf.size());
+    pl.psurf = M.alloc<double>(static_cast<std::size_t>(ne) * pl.nsurf);
     pl.pint = M.alloc<double>(pl.N);
     pl.coarse_n = hs.Kc.n;
     if (pl.use_amg) {
