@@ -41,9 +41,9 @@ struct AxShape {
   static constexpr int kBufB = NP == 8 ? 576 : NP * NP * kS;
   static constexpr std::size_t kGBytes = 6ull * kNlocP * sizeof(double);
   static constexpr std::size_t kIdxBytes = kNsurfP * sizeof(int);
-  static constexpr std::size_t kSmemBytes =
-      kGBytes + (kBufA + kBufB) * sizeof(double) + kIdxBytes + 2 * sizeof(unsigned long long);
-  static constexpr int kRegs = NP >= 9 ? 128 : 96;
+  static constexpr std::size_t kSmemBytes = kGBytes + (kBufA + kBufB + 2 * NP * NP) * sizeof(double) + kIdxBytes +
+                                            2 * sizeof(unsigned long long);
+  static constexpr int kMinBlocks = NP <= 8 ? 6 : 2;  // caps registers; shared memory sets the real limit
 };
 
 // x-layout: owner (i,j | k) and x-line (j,k | m) accesses conflict free
@@ -113,10 +113,13 @@ __device__ __forceinline__ void contract3(const double* __restrict__ M, FX&& in_
 // Persistent: CTA b processes elements b, b+grid, ... . The element's six
 // metric planes (6*nloc FP64, the bulk of Ax traffic) and its surface index
 // block are streamed into shared memory by TMA bulk copies issued one element
-// ahead: indices for e' as soon as phase A of e has consumed them, planes for
-// e' as soon as phase C of e has — so HBM streams while the CTA computes.
+// ahead (planes for e' once phase C of e has consumed them, indices for e''
+// once u(e') has been gathered), and u(e') is gathered into registers during
+// phase D of e, so HBM traffic overlaps the contractions. D and D^T live in
+// shared memory and are read as warp-uniform broadcasts, keeping registers
+// low enough for 6 CTAs per SM.
 template <int NP>
-__global__ void __launch_bounds__(AxShape<NP>::kBlock) ax_elem_kernel(AxArgs a)
+__global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) ax_elem_kernel(AxArgs a)
 {
   using Sh = AxShape<NP>;
   constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NLP = Sh::kNlocP;
@@ -124,18 +127,29 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock) ax_elem_kernel(AxArgs a)
   double* sG = reinterpret_cast<double*>(smem_raw);                  // [6][nlocp]
   double* sa = sG + 6 * NLP;
   double* sb = sa + Sh::kBufA;
-  int* sidx = reinterpret_cast<int*>(sb + Sh::kBufB);                // [nsurfp]
+  double* sD = sb + Sh::kBufB;                                       // D, then D^T
+  double* sDT = sD + NP * NP;
+  int* sidx = reinterpret_cast<int*>(sDT + NP * NP);                 // [nsurfp]
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(sidx + Sh::kNsurfP);  // [0]=G, [1]=idx
   __shared__ double red[Sh::kBlock / 32];
-  const double* D = c_tab[NP].D;
-  const double* DT = c_tab[NP].DT;
 
   const int tid = threadIdx.x;
   const bool lane_ok = tid < Sh::kLocal;
   const int loc = lane_ok ? tid : 0;
   const int i = loc % NP, j = loc / NP;  // owner column; also x-line (j'=i,k'=j) and y-line (i'=i,k'=j)
+  // node classification of this thread's column: surface slot, or -1-(interior offset)
+  int code[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    const int s = surface_slot(NP, i, j, k);
+    code[k] = s >= 0 ? s : -1 - (((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1));
+  }
 
   int e = blockIdx.x;
+  for (int q = tid; q < NP * NP; q += Sh::kBlock) {
+    sD[q] = c_tab[NP].D[q];
+    sDT[q] = c_tab[NP].DT[q];
+  }
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -148,26 +162,32 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock) ax_elem_kernel(AxArgs a)
     mbar_expect_tx(&bar[0], Sh::kGBytes);
     bulk_g2s(sG, a.wg + (long long)e * 6 * NLP, Sh::kGBytes, &bar[0]);
   }
-  double dot = 0.0;
+  // gather u for element ee (masked, operator.cpp:264-265) using the staged indices
+  auto gather_u = [&](int ee, double (&dst)[NP]) {
+    const long long ib = (long long)a.num_surface_global + (long long)ee * NI;
+#pragma unroll
+    for (int k = 0; k < NP; ++k)
+      dst[k] = code[k] >= 0 ? load_masked(a.u, sidx[code[k]]) : __ldg(a.u + ib - 1 - code[k]);
+  };
+  double ucol[NP];
+  double ce = 0.0;
   unsigned phase = 0;
+  if (e < a.ne) {
+    mbar_wait(&bar[1], 0);
+    gather_u(e, ucol);
+    ce = __ldg(a.c_e + e);
+    __syncthreads();
+    if (tid == 0 && e + (int)gridDim.x < a.ne) {
+      mbar_expect_tx(&bar[1], Sh::kIdxBytes);
+      bulk_g2s(sidx, a.l2g_surf + (long long)(e + gridDim.x) * Sh::kNsurfP, Sh::kIdxBytes, &bar[1]);
+    }
+  }
+  double dot = 0.0;
   for (; e < a.ne; e += gridDim.x, phase ^= 1u) {
     const int en = e + gridDim.x;
     const long long ibase = (long long)a.num_surface_global + (long long)e * NI;
 
-    // ---- A: gather u (masked, operator.cpp:264-265) ---------------------------
-    mbar_wait(&bar[1], phase);
-    double ucol[NP];
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const int s = surface_slot(NP, i, j, k);
-      ucol[k] = s >= 0 ? load_masked(a.u, sidx[s])
-                       : __ldg(a.u + ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1));
-    }
-    __syncthreads();  // sidx consumed; previous element's phase E done with sa/sb
-    if (tid == 0 && en < a.ne) {
-      mbar_expect_tx(&bar[1], Sh::kIdxBytes);
-      bulk_g2s(sidx, a.l2g_surf + (long long)en * Sh::kNsurfP, Sh::kIdxBytes, &bar[1]);
-    }
+    // ---- A: u column -> shared (two layouts) ------------------------------------
     if (lane_ok) {
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
@@ -181,7 +201,7 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock) ax_elem_kernel(AxArgs a)
     double fz[NP];
     {
       double ox[NP], oy[NP];
-      contract3<NP>(D, [&](int m) { return sa[lay_a<NP>(j, i, m)]; }, [&](int m) { return sb[lay_b<NP>(j, m, i)]; },
+      contract3<NP>(sD, [&](int m) { return sa[lay_a<NP>(j, i, m)]; }, [&](int m) { return sb[lay_b<NP>(j, m, i)]; },
                     ucol, ox, oy, fz);
       __syncthreads();  // all lines read before any is overwritten
       if (lane_ok) {
@@ -214,14 +234,26 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock) ax_elem_kernel(AxArgs a)
       mbar_expect_tx(&bar[0], Sh::kGBytes);
       bulk_g2s(sG, a.wg + (long long)en * 6 * NLP, Sh::kGBytes, &bar[0]);
     }
+    // prefetch u(e') and c(e') while the adjoint contractions run
+    double unext[NP];
+    double cnext = 0.0;
+    if (en < a.ne) {
+      mbar_wait(&bar[1], phase ^ 1u);
+      gather_u(en, unext);
+      cnext = __ldg(a.c_e + en);
+    }
 
     // ---- D: adjoint contractions (operator.cpp:152-157), rows of D^T ------------
     double tz[NP];
     {
       double ox[NP], oy[NP];
-      contract3<NP>(DT, [&](int m) { return sa[lay_a<NP>(j, i, m)]; }, [&](int m) { return sb[lay_b<NP>(j, m, i)]; },
+      contract3<NP>(sDT, [&](int m) { return sa[lay_a<NP>(j, i, m)]; }, [&](int m) { return sb[lay_b<NP>(j, m, i)]; },
                     fz, ox, oy, tz);
-      __syncthreads();
+      __syncthreads();  // lines read; sidx(e') consumed
+      if (tid == 0 && en + (int)gridDim.x < a.ne) {
+        mbar_expect_tx(&bar[1], Sh::kIdxBytes);
+        bulk_g2s(sidx, a.l2g_surf + (long long)(en + gridDim.x) * Sh::kNsurfP, Sh::kIdxBytes, &bar[1]);
+      }
       if (lane_ok) {
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
@@ -234,22 +266,24 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock) ax_elem_kernel(AxArgs a)
 
     // ---- E: sum, mass term, store ---------------------------------------------
     if (lane_ok) {
-      const double ce = __ldg(a.c_e + e);
       const double* m0 = a.mass + (std::size_t)e * Sh::kNloc + j * NP + i;
       double* rs = a.rsurf + (long long)e * Sh::kNsurfP;
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         double r = (sa[lay_a<NP>(k, j, i)] + sb[lay_b<NP>(k, j, i)]) + tz[k];
         if (ce != 0.0) r += (ce * ucol[k]) * __ldg(m0 + k * NP * NP);  // operator.cpp:159
-        const int s = surface_slot(NP, i, j, k);
-        if (s >= 0) {
-          rs[s] = r;
+        if (code[k] >= 0) {
+          rs[code[k]] = r;
         } else {
-          a.r[ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1)] = r;
+          a.r[ibase - 1 - code[k]] = r;
           dot += ucol[k] * r;
         }
       }
     }
+    __syncthreads();  // sa/sb reads done before the next element's phase A
+#pragma unroll
+    for (int k = 0; k < NP; ++k) ucol[k] = unext[k];
+    ce = cnext;
   }
   dot_commit<Sh::kBlock>(a.dot, dot, red);
 }

@@ -10,22 +10,29 @@ namespace hxb {
 constexpr int kMaxNP = 11;         // orders 1..10
 constexpr int kMaxP = kMaxNP + 2;  // FDM pencil size n+3
 
-// Per-order operator tables. Index [NP] selects the order so plans of
-// different orders can coexist; within a kernel NP is a template constant and
-// every loop over these tables is fully unrolled, so each entry becomes a
-// constant-bank operand of the DFMA (no register or shared-memory traffic).
+// Per-order operator tables (device global memory, ~6.5 KB per order). Index
+// [NP] selects the order so plans of different orders coexist. Kernels copy
+// the rows they contract with into shared memory once per CTA and read them
+// as warp-uniform broadcasts (one LDS.128 feeds two DFMA columns), which on
+// sm_100a is cheaper than staging FP64 constants through uniform registers.
 struct OrderTables {
   double D[kMaxNP * kMaxNP];   // D[m*np+i] = phi'_m(t_i), gll.hpp:23-26
   double DT[kMaxNP * kMaxNP];  // DT[m*np+i] = D[i*np+m] (adjoint contractions read rows)
   double VT[kMaxP * kMaxP];    // pencil V transposed: VT[x*p+d] = V[d][x] (fine.hpp:22)
   double ViT[kMaxP * kMaxP];   // pencil V^-1 transposed (fine.hpp:23)
   double M[kMaxP];             // pencil lumped mass (fine.hpp:21)
+  double invM[kMaxP];          // 1/M
+  // even/odd split of the pencil transforms (eigenvectors of the reflection-
+  // symmetric pencil are even (d even) or odd (d odd)); see fdm_kernel
+  double FE[49], FO[36];       // forward: FE[x*NE+a] = V[2a][x], FO[x*NO+a] = V[2a+1][x]
+  double IE[49], IO[36];       // inverse: IE[a*(h+mid)+x] = Vi[x][2a], IO[a*h+x] = Vi[x][2a+1]
+  int eo_ok;                   // 1 when the split is exact to rounding (checked at setup)
   double lam[kMaxP];           // pencil eigenvalues (fine.hpp:24)
   double hat0[kMaxNP];         // 0.5*(1-t_i)  coarse hats (gll.cpp:92)
   double hat1[kMaxNP];         // 0.5*(1+t_i)
 };
 // Single translation unit (plan.cu) includes the kernels, so this is the definition.
-__constant__ OrderTables c_tab[kMaxNP + 1];
+__device__ OrderTables c_tab[kMaxNP + 1];
 
 // Global-id encodings in the gather/scatter maps:
 //   v >= 0   free node v

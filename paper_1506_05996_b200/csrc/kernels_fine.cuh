@@ -51,6 +51,7 @@ struct FdmArgs {
   int ne, nsurf, num_surface_global;
 };
 
+// out[q] = sum_m MT[m*P+q] in[m] (dense, m ascending = tensor_pass order)
 template <int P>
 __device__ __forceinline__ void pencil_apply(const double* __restrict__ MT, const double (&in)[P], double (&out)[P])
 {
@@ -62,22 +63,123 @@ __device__ __forceinline__ void pencil_apply(const double* __restrict__ MT, cons
     for (int q = 0; q < P; ++q) out[q] += MT[m * P + q] * in[m];
 }
 
-template <int NP>
+// Forward transform out = V in with the even/odd split: the pencil is
+// reflection symmetric, so row d of V is even (d even) or odd (d odd) and
+// V in = [FE^T (in + flip in) ; FO^T (in - flip in)] at half the FMAs.
+template <int P>
+__device__ __forceinline__ void pencil_fwd_eo(const double* __restrict__ FE, const double* __restrict__ FO,
+                                              const double (&in)[P], double (&out)[P])
+{
+  constexpr int h = P / 2, mid = P & 1, NE = (P + 1) / 2, NO = P / 2;
+  double ev[h + mid], od[h];
+#pragma unroll
+  for (int x = 0; x < h; ++x) {
+    ev[x] = in[x] + in[P - 1 - x];
+    od[x] = in[x] - in[P - 1 - x];
+  }
+  if constexpr (mid) ev[h] = in[h];
+  double oe[NE], oo[NO];
+#pragma unroll
+  for (int a = 0; a < NE; ++a) oe[a] = FE[a] * ev[0];
+#pragma unroll
+  for (int x = 1; x < h + mid; ++x)
+#pragma unroll
+    for (int a = 0; a < NE; ++a) oe[a] += FE[x * NE + a] * ev[x];
+#pragma unroll
+  for (int a = 0; a < NO; ++a) oo[a] = FO[a] * od[0];
+#pragma unroll
+  for (int x = 1; x < h; ++x)
+#pragma unroll
+    for (int a = 0; a < NO; ++a) oo[a] += FO[x * NO + a] * od[x];
+#pragma unroll
+  for (int a = 0; a < NE; ++a) out[2 * a] = oe[a];
+#pragma unroll
+  for (int a = 0; a < NO; ++a) out[2 * a + 1] = oo[a];
+}
+
+// Inverse transform out = V^-1 in with the split: columns of V^-1 are even/odd.
+template <int P>
+__device__ __forceinline__ void pencil_inv_eo(const double* __restrict__ IE, const double* __restrict__ IO,
+                                              const double (&in)[P], double (&out)[P])
+{
+  constexpr int h = P / 2, mid = P & 1, NE = (P + 1) / 2, NO = P / 2;
+  double E[h + mid], O[h];
+#pragma unroll
+  for (int x = 0; x < h + mid; ++x) E[x] = IE[x] * in[0];
+#pragma unroll
+  for (int a = 1; a < NE; ++a)
+#pragma unroll
+    for (int x = 0; x < h + mid; ++x) E[x] += IE[a * (h + mid) + x] * in[2 * a];
+#pragma unroll
+  for (int x = 0; x < h; ++x) O[x] = IO[x] * in[1];
+#pragma unroll
+  for (int a = 1; a < NO; ++a)
+#pragma unroll
+    for (int x = 0; x < h; ++x) O[x] += IO[a * h + x] * in[2 * a + 1];
+#pragma unroll
+  for (int x = 0; x < h; ++x) {
+    out[x] = E[x] + O[x];
+    out[P - 1 - x] = E[x] - O[x];
+  }
+  if constexpr (mid) out[h] = E[h];
+}
+
+template <int NP, bool EO>
 __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
 {
   using Sh = FdmShape<NP>;
   constexpr int P = Sh::kP, S = Sh::kS, PS = Sh::kPS, n = NP - 1;
+  constexpr int h = P / 2, mid = P & 1, NE = (P + 1) / 2, NO = P / 2;
+  constexpr int kTab = EO ? (2 * (h + mid) * NE + 2 * h * NO) : 2 * P * P;
   __shared__ double buf[Sh::kBuf];
+  __shared__ double tab[kTab];  // transform tables, read as warp-uniform broadcasts
+  __shared__ double s_lam[P], s_invM[P];
   const OrderTables& T = c_tab[NP];
   const int e = blockIdx.x;
   const int tid = threadIdx.x;
   const bool lt = tid < Sh::kLines;
   const int la = tid % P, lb = tid / P;
   auto at = [](int x, int y, int z) { return z * PS + y * S + x; };
+  double* tFE = tab;                       // EO: FE, FO, IE, IO ; dense: VT, ViT
+  double* tFO = tab + (h + mid) * NE;
+  double* tIE = tFO + h * NO;
+  double* tIO = tIE + (h + mid) * NE;
+  if constexpr (EO) {
+    for (int q = tid; q < (h + mid) * NE; q += Sh::kBlock) {
+      tFE[q] = T.FE[q];
+      tIE[q] = T.IE[q];
+    }
+    for (int q = tid; q < h * NO; q += Sh::kBlock) {
+      tFO[q] = T.FO[q];
+      tIO[q] = T.IO[q];
+    }
+  } else {
+    for (int q = tid; q < P * P; q += Sh::kBlock) {
+      tab[q] = T.VT[q];
+      tab[P * P + q] = T.ViT[q];
+    }
+  }
+  for (int q = tid; q < P; q += Sh::kBlock) {
+    s_lam[q] = T.lam[q];
+    s_invM[q] = T.invM[q];
+  }
+  auto fwd = [&](const double (&in)[P], double (&out)[P]) {
+    if constexpr (EO)
+      pencil_fwd_eo<P>(tFE, tFO, in, out);
+    else
+      pencil_apply<P>(tab, in, out);
+  };
+  auto inv = [&](const double (&in)[P], double (&out)[P]) {
+    if constexpr (EO)
+      pencil_inv_eo<P>(tIE, tIO, in, out);
+    else
+      pencil_apply<P>(tab + P * P, in, out);
+  };
 
   const double hx = __ldg(a.h3 + 3 * e), hy = __ldg(a.h3 + 3 * e + 1), hz = __ldg(a.h3 + 3 * e + 2);
   const double svol = 8.0 / (hx * hy * hz);  // fine.cpp:154
   double in[P], out[P];
+  __syncthreads();
 
   // ---- 1: gather + r' scaling + V along x (thread = x-line (y=la, z=lb)) -------
   if (lt) {
@@ -106,10 +208,11 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
 #pragma unroll
       for (int ii = 0; ii <= n; ++ii) in[ii + 1] = load_masked(a.r, __ldg(sf + (f * NP + jj) * NP + ii));
     }
-    const double syz = T.M[y] * T.M[z];
+    // r' = 8/(hx hy hz) r / (M_i M_j M_k) (fine.cpp:161-166), as products of reciprocals
+    const double syz = svol * s_invM[y] * s_invM[z];
 #pragma unroll
-    for (int x = 0; x < P; ++x) in[x] = svol * in[x] / (T.M[x] * syz);
-    pencil_apply<P>(T.VT, in, out);
+    for (int x = 0; x < P; ++x) in[x] = in[x] * (syz * s_invM[x]);
+    fwd(in, out);
 #pragma unroll
     for (int x = 0; x < P; ++x) buf[at(x, y, z)] = out[x];
   }
@@ -119,7 +222,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
   if (lt) {
 #pragma unroll
     for (int y = 0; y < P; ++y) in[y] = buf[at(la, y, lb)];
-    pencil_apply<P>(T.VT, in, out);
+    fwd(in, out);
 #pragma unroll
     for (int y = 0; y < P; ++y) buf[at(la, y, lb)] = out[y];
   }
@@ -129,13 +232,13 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
   if (lt) {
     const double ihx2 = 1.0 / (hx * hx), ihy2 = 1.0 / (hy * hy), ihz2 = 1.0 / (hz * hz);
     const double kappa4 = 4.0 * __ldg(a.kappa_e + e), ce = __ldg(a.c_e + e);
-    const double lxy = T.lam[la] * ihx2 + T.lam[lb] * ihy2;
+    const double lxy = s_lam[la] * ihx2 + s_lam[lb] * ihy2;
 #pragma unroll
     for (int z = 0; z < P; ++z) in[z] = buf[at(la, lb, z)];
-    pencil_apply<P>(T.VT, in, out);
+    fwd(in, out);
 #pragma unroll
-    for (int z = 0; z < P; ++z) out[z] = out[z] / (kappa4 * (lxy + T.lam[z] * ihz2) + ce);
-    pencil_apply<P>(T.ViT, out, in);
+    for (int z = 0; z < P; ++z) out[z] = out[z] * __drcp_rn(kappa4 * (lxy + s_lam[z] * ihz2) + ce);
+    inv(out, in);
 #pragma unroll
     for (int z = 0; z < P; ++z) buf[at(la, lb, z)] = in[z];
   }
@@ -145,7 +248,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
   if (lt) {
 #pragma unroll
     for (int y = 0; y < P; ++y) in[y] = buf[at(la, y, lb)];
-    pencil_apply<P>(T.ViT, in, out);
+    inv(in, out);
 #pragma unroll
     for (int y = 0; y < P; ++y) buf[at(la, y, lb)] = out[y];
   }
@@ -155,7 +258,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
   if (lt) {
 #pragma unroll
     for (int x = 0; x < P; ++x) in[x] = buf[at(x, la, lb)];
-    pencil_apply<P>(T.ViT, in, out);
+    inv(in, out);
     double* o = a.zsub + (long long)e * P * P * P + (lb * P + la) * P;
 #pragma unroll
     for (int x = 0; x < P; ++x) o[x] = out[x];

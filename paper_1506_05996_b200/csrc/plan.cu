@@ -112,6 +112,7 @@ struct Plan {
   int order = 0, np = 0, nloc = 0, nsurf = 0, P = 0;
   int ne = 0, nv = 0, N = 0, nsg = 0;
   int num_sms = 148, ax_grid = 1;
+  bool fdm_eo = false;
   int precond_mode = 0, variant = 0;
   bool do_fine = false, do_coarse = false, use_amg = false;
   double setup_seconds = 0;
@@ -217,6 +218,7 @@ int ax_persistent_grid(const Plan& pl)
   using Sh = AxShape<NP>;
   HXB_CUDA(cudaFuncSetAttribute(ax_elem_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(Sh::kSmemBytes)));
+  HXB_CUDA(cudaFuncSetAttribute(ax_elem_kernel<NP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int per_sm = 0;
   HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ax_elem_kernel<NP>, Sh::kBlock, Sh::kSmemBytes));
   per_sm = std::max(per_sm, 1);
@@ -285,7 +287,10 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   a.ne = pl.ne;
   a.nsurf = pl.nsurf;
   a.num_surface_global = pl.nsg;
-  fdm_kernel<NP><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
+  if (pl.fdm_eo)
+    fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
+  else
+    fdm_kernel<NP, false><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
 }
 
 void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse)
@@ -430,7 +435,7 @@ void enqueue_precond(Plan& pl, double* zr_result)
 // ---------------------------------------------------------------------------
 // Setup
 
-void upload_tables(const GllBasis& basis, const Pencil& pencil)
+bool upload_tables(const GllBasis& basis, const Pencil& pencil)
 {
   OrderTables t{};
   const int np = basis.npts();
@@ -444,13 +449,39 @@ void upload_tables(const GllBasis& basis, const Pencil& pencil)
     }
   for (int q = 0; q < pencil.p; ++q) {
     t.M[q] = pencil.M[q];
+    t.invM[q] = 1.0 / pencil.M[q];
     t.lam[q] = pencil.lambda[q];
+  }
+  {  // even/odd split (fdm_kernel): eigenvector d must be even for even d, odd for odd d
+    const int P = pencil.p, h = P / 2, mid = P & 1, NE = (P + 1) / 2, NO = P / 2;
+    double vmax = 0;
+    for (double v : pencil.V) vmax = std::max(vmax, std::fabs(v));
+    double wmax = 0;
+    for (double v : pencil.V_inv) wmax = std::max(wmax, std::fabs(v));
+    bool ok = true;
+    for (int d = 0; d < P; ++d) {
+      const double sgn = (d % 2 == 0) ? 1.0 : -1.0;
+      for (int x = 0; x < P; ++x) {
+        if (std::fabs(pencil.V[d * P + x] - sgn * pencil.V[d * P + (P - 1 - x)]) > 1e-12 * vmax) ok = false;
+        if (std::fabs(pencil.V_inv[x * P + d] - sgn * pencil.V_inv[(P - 1 - x) * P + d]) > 1e-12 * wmax) ok = false;
+      }
+    }
+    t.eo_ok = ok ? 1 : 0;
+    for (int x = 0; x < h + mid; ++x)
+      for (int a = 0; a < NE; ++a) t.FE[x * NE + a] = pencil.V[(2 * a) * P + x];
+    for (int x = 0; x < h; ++x)
+      for (int a = 0; a < NO; ++a) t.FO[x * NO + a] = pencil.V[(2 * a + 1) * P + x];
+    for (int a = 0; a < NE; ++a)
+      for (int x = 0; x < h + mid; ++x) t.IE[a * (h + mid) + x] = pencil.V_inv[x * P + 2 * a];
+    for (int a = 0; a < NO; ++a)
+      for (int x = 0; x < h; ++x) t.IO[a * h + x] = pencil.V_inv[x * P + 2 * a + 1];
   }
   for (int i = 0; i < np; ++i) {
     t.hat0[i] = 0.5 * (1 - basis.nodes[i]);
     t.hat1[i] = 0.5 * (1 + basis.nodes[i]);
   }
   HXB_CUDA(cudaMemcpyToSymbol(c_tab, &t, sizeof(OrderTables), sizeof(OrderTables) * np));
+  return t.eo_ok != 0;
 }
 
 // CSR by counting sort of a flat (already ascending) source index stream.
@@ -562,7 +593,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
       static_cast<std::size_t>(ne) * pl.P * pl.P * pl.P > 0x7fffffffULL)
     throw HxbError(HXB_EINVAL, "mesh too large for one device plan");
 
-  upload_tables(hs.basis, hs.pencil);
+  pl.fdm_eo = upload_tables(hs.basis, hs.pencil);
   HXB_DISPATCH_NP(pl.np, init_ax_grid, pl);
 
   HXB_CUDA(cudaStreamCreateWithFlags(&pl.s_main, cudaStreamNonBlocking));
