@@ -14,35 +14,58 @@ namespace hxb {
 constexpr double kJacobiOmega = 2.0 / 3.0;  // amg.cpp:44
 
 // Per element: Rpart[e*8+cb] = sum_l B[cb][l] * (r/m_N)[l] * m[l]
+// (restrict_residual, coarse.cpp:144-160; r masked, precond.cpp:35). Element
+// tile of NP x NP threads, each owning a k-column; the 8 corner sums are
+// reduced across the tile in a fixed tree.
 template <int NP, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) restrict_kernel(const double* __restrict__ r, const double* __restrict__ lumped,
-                                                         const int* __restrict__ l2g_surf, const double* __restrict__ mass,
-                                                         double* __restrict__ Rpart, int ne, int nsurf, int nsg)
+                                                         const int* __restrict__ smap, const double* __restrict__ mass,
+                                                         double* __restrict__ Rpart, int ne, int sstride, int nsg)
 {
-  constexpr int NLOC = NP * NP * NP, n = NP - 1;
+  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NW = BLOCK / 32;
   const OrderTables& T = c_tab[NP];
-  __shared__ double red[BLOCK / 32][8];
+  __shared__ double red[NW][8];
+  __shared__ double hk0[NP], hk1[NP];
+  const int tid = threadIdx.x;
   const int e = blockIdx.x;
-  const int* surf = l2g_surf + (long long)e * nsurf;
-  const long long ibase = (long long)nsg + (long long)e * (n - 1) * (n - 1) * (n - 1);
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int l = threadIdx.x; l < NLOC; l += BLOCK) {
-    const int i = l % NP, j = (l / NP) % NP, k = l / (NP * NP);
-    const int s = surface_slot(NP, i, j, k);
-    double y;
-    if (s < 0) {
-      const long long g = ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1);
-      y = __ldg(r + g) / __ldg(lumped + g);
-    } else {
-      const int code = __ldg(surf + s);
-      y = code >= 0 ? __ldg(r + code) / __ldg(lumped + code) : 0.0;  // masked r (precond.cpp:35)
-    }
-    const double ym = __ldg(mass + (std::size_t)e * NLOC + l);
-    const double hi[2] = {T.hat0[i], T.hat1[i]}, hj[2] = {T.hat0[j], T.hat1[j]}, hk[2] = {T.hat0[k], T.hat1[k]};
-#pragma unroll
-    for (int cb = 0; cb < 8; ++cb) acc[cb] += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[(cb >> 2) & 1] * y * ym;
+  const bool ok = tid < NP * NP;
+  const int i = (ok ? tid : 0) % NP, j = (ok ? tid : 0) / NP;
+  if (tid < NP) {
+    hk0[tid] = T.hat0[tid];
+    hk1[tid] = T.hat1[tid];
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double hi[2] = {T.hat0[i], T.hat1[i]}, hj[2] = {T.hat0[j], T.hat1[j]};
+  const int* surf = smap + (long long)e * sstride;
+  const long long ibase = (long long)nsg + (long long)e * NI;
+  const double* m0 = mass + (std::size_t)e * NP * NP * NP + j * NP + i;
+  double y[NP];
+#pragma unroll
+  for (int k = 0; k < NP; ++k) {
+    double v = 0.0;
+    if (ok) {
+      const int s = surface_slot(NP, i, j, k);
+      if (s < 0) {
+        const long long g = ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1);
+        v = __ldg(r + g) / __ldg(lumped + g);
+      } else {
+        const int code = __ldg(surf + s);
+        v = code >= 0 ? __ldg(r + code) / __ldg(lumped + code) : 0.0;
+      }
+    }
+    y[k] = v;
+  }
+  __syncthreads();
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (ok) {
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const double ym = __ldg(m0 + k * NP * NP);
+      const double hk[2] = {hk0[k], hk1[k]};
+#pragma unroll
+      for (int cb = 0; cb < 8; ++cb) acc[cb] += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[cb >> 2] * y[k] * ym;
+    }
+  }
+  const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
   for (int cb = 0; cb < 8; ++cb) {
     double v = acc[cb];
@@ -50,22 +73,24 @@ __global__ void __launch_bounds__(BLOCK) restrict_kernel(const double* __restric
     if (lane == 0) red[warp][cb] = v;
   }
   __syncthreads();
-  if (threadIdx.x < 8) {
+  if (tid < 8) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < BLOCK / 32; ++w) s += red[w][threadIdx.x];
-    Rpart[8 * e + threadIdx.x] = s;
+    for (int w = 0; w < NW; ++w) s += red[w][tid];
+    Rpart[8 * e + tid] = s;
   }
 }
 
 // Prolongation per element copy (coarse.cpp:164-182): p_l = (sum_cb B[cb][l]
 // Z[v_cb]) * m_l, stored like Ax outputs (element-interior nodes direct into
-// pint, element-surface copies into psurf) for the deterministic gather in
-// combine_kernel. The 8 corner values are loaded once per element.
+// pint, element-surface copies at their CSR position in psort) for the
+// deterministic gather in combine_kernel. The 8 corner values are loaded once
+// per element.
 template <int NP, int EPB, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) prolong_elem_kernel(const double* __restrict__ Z, const int* __restrict__ conn,
-                                                             const double* __restrict__ mass, double* __restrict__ psurf,
-                                                             double* __restrict__ pint, int ne, int nsurf, int nsg)
+                                                             const double* __restrict__ mass, const int* __restrict__ smap,
+                                                             double* __restrict__ psort, double* __restrict__ pint, int ne,
+                                                             int nsurfp, int nsg)
 {
   constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1);
   const OrderTables& T = c_tab[NP];
@@ -90,7 +115,7 @@ __global__ void __launch_bounds__(BLOCK) prolong_elem_kernel(const double* __res
     const double v = s * __ldg(m0 + k * NP * NP);
     const int sl = surface_slot(NP, i, j, k);
     if (sl >= 0)
-      psurf[(long long)e * nsurf + sl] = v;
+      psort[__ldg(smap + (long long)e * 2 * nsurfp + nsurfp + sl)] = v;  // CSR position
     else
       pint[ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1)] = v;
   }

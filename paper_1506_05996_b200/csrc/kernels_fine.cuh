@@ -12,7 +12,8 @@
 //   2  V along y
 //   3  V along z, pointwise 1/(4k(lx+ly+lz)+c) (fine.cpp:172-177), V^-1 along z
 //   4  V^-1 along y
-//   5  V^-1 along x and store z_sub[e][slot] (every slot)
+//   5  V^-1 along x and store each slot's value at its CSR position (sorted
+//      by destination node, so the combine kernel streams it)
 // The transforms along different axes commute, so running V^-1 z-first is
 // the reference's x,y,z order up to rounding. V/V^-1 rows are uniform
 // constant loads (transposed tables), and the padded strides below were
@@ -42,13 +43,14 @@ struct FdmShape {
 
 struct FdmArgs {
   const double* r;          // N (PCG residual; masked on read)
-  const int* l2g_surf;      // NE*nsurf, Dirichlet-encoded
+  const int* smap;          // [e][2][nsurfp]: row 0 Dirichlet-encoded global ids
   const int* sub_face;      // NE*6*np^2, -1 none, Dirichlet-encoded
   const double* h3;         // NE*3 element dimensions
   const double* kappa_e;
   const double* c_e;
-  double* zsub;             // NE*P^3
-  int ne, nsurf, num_surface_global;
+  const int* pos;           // [e][P^3] CSR position of each slot's contribution (-1: sentinel)
+  double* zsort;            // contributions in CSR order (combine streams them)
+  int ne, sstride, num_surface_global;
 };
 
 // out[q] = sum_m MT[m*P+q] in[m] (dense, m ascending = tensor_pass order)
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
   if (lt) {
     const int y = la, z = lb, jj = y - 1, kk = z - 1;
     const bool iny = jj >= 0 && jj <= n, inz = kk >= 0 && kk <= n;
-    const int* surf = a.l2g_surf + (long long)e * a.nsurf;
+    const int* surf = a.smap + (long long)e * a.sstride;
     const int* sf = a.sub_face + (long long)e * 6 * NP * NP;
     const long long ibase = (long long)a.num_surface_global + (long long)e * (n - 1) * (n - 1) * (n - 1);
 #pragma unroll
@@ -259,9 +261,12 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
 #pragma unroll
     for (int x = 0; x < P; ++x) in[x] = buf[at(x, la, lb)];
     inv(in, out);
-    double* o = a.zsub + (long long)e * P * P * P + (lb * P + la) * P;
+    const int* ps = a.pos + (long long)e * P * P * P + (lb * P + la) * P;
 #pragma unroll
-    for (int x = 0; x < P; ++x) o[x] = out[x];
+    for (int x = 0; x < P; ++x) {
+      const int q = __ldg(ps + x);
+      if (q >= 0) a.zsort[q] = out[x];
+    }
   }
 }
 

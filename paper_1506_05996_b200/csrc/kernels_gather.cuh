@@ -17,9 +17,12 @@ namespace hxb {
 constexpr int kGatherBlock = 256;
 constexpr int kGatherCap = 320;  // staged values per warp (avg ~1.5-2.6 per node)
 
-template <class Src>
-__device__ __forceinline__ double warp_csr_sum(const unsigned* __restrict__ off, const int* __restrict__ idx, Src&& src,
-                                               int g0, int n, double* __restrict__ stage)
+// Sum vals[off[g] .. off[g+1]) left to right for the warp's 32 consecutive
+// nodes. The producers wrote each contribution at its CSR position, so the
+// warp's whole segment is contiguous: one coalesced sweep into the staging
+// buffer, then a sequential per-lane sum (reference order).
+__device__ __forceinline__ double warp_seg_sum(const unsigned* __restrict__ off, const double* __restrict__ vals, int g0,
+                                               int n, double* __restrict__ stage)
 {
   const int lane = threadIdx.x & 31;
   const int g = g0 + lane;
@@ -31,12 +34,12 @@ __device__ __forceinline__ double warp_csr_sum(const unsigned* __restrict__ off,
   double s = 0.0;
   if (cnt <= static_cast<unsigned>(kGatherCap)) {
 #pragma unroll 4
-    for (unsigned c = lane; c < cnt; c += 32) stage[c] = src(__ldg(idx + base + c));
+    for (unsigned c = lane; c < cnt; c += 32) stage[c] = __ldcs(vals + base + c);
     __syncwarp();
     for (unsigned q = my0 - base; q < my1 - base; ++q) s += stage[q];
     __syncwarp();
   } else {
-    for (unsigned q = my0; q < my1; ++q) s += src(__ldg(idx + q));
+    for (unsigned q = my0; q < my1; ++q) s += __ldcs(vals + q);
   }
   return s;
 }
@@ -45,9 +48,8 @@ __device__ __forceinline__ double warp_csr_sum(const unsigned* __restrict__ off,
 // Ax surface assembly (gather, mesh.cpp:463-475) + Dirichlet identity rows
 // (operator.cpp:279-280) + the optional fused p.Ap partial.
 struct AxGatherArgs {
-  const double* rsurf;
+  const double* rsort;   // surface copies in CSR order (written by ax_elem_kernel)
   const unsigned* off;   // num_surface_global + 1
-  const int* idx;        // e*nsurf + slot, sorted per node
   const double* u;
   const std::uint8_t* mask;
   double* r;
@@ -63,8 +65,7 @@ __global__ void __launch_bounds__(kGatherBlock) ax_gather_kernel(AxGatherArgs a)
   const int nwarps = gridDim.x * (kGatherBlock / 32);
   double dot = 0.0;
   for (int g0 = (blockIdx.x * (kGatherBlock / 32) + warp) * 32; g0 < a.num_surface_global; g0 += nwarps * 32) {
-    const double s = warp_csr_sum(a.off, a.idx, [&](int q) { return __ldg(a.rsurf + q); }, g0,
-                                  a.num_surface_global, stage[warp]);
+    const double s = warp_seg_sum(a.off, a.rsort, g0, a.num_surface_global, stage[warp]);
     const int g = g0 + lane;
     if (g < a.num_surface_global) {
       const double ug = __ldg(a.u + g);
@@ -87,13 +88,11 @@ __global__ void __launch_bounds__(kGatherBlock) ax_gather_kernel(AxGatherArgs a)
 struct CombineArgs {
   const double* r;
   const std::uint8_t* mask;
-  const double* zsub;        // fine subdomain outputs
+  const double* zsort;       // fine subdomain outputs in CSR order (fdm_kernel)
   const unsigned* fine_off;  // N+1
-  const int* fine_idx;       // e*P^3 + slot
-  const double* psurf;       // prolongated surface copies (NE*nsurf)
+  const double* psort;       // prolongated surface copies in CSR order (prolong_elem_kernel)
   const double* pint;        // prolongated element-interior nodes (N, [nsg,N) used)
   const unsigned* ax_off;    // nsg+1
-  const int* ax_idx;         // e*nsurf + slot
   const double* lumped;      // m_N
   double* z;
   int N, nsg;
@@ -112,10 +111,10 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_kernel(CombineArgs a)
     const int g = g0 + lane;
     double zf = 0.0, zc = 0.0;
     if (a.do_fine)
-      zf = warp_csr_sum(a.fine_off, a.fine_idx, [&](int q) { return __ldg(a.zsub + q); }, g0, a.N, stage[warp]);
+      zf = warp_seg_sum(a.fine_off, a.zsort, g0, a.N, stage[warp]);
     if (a.do_coarse) {
       if (g0 < a.nsg)
-        zc = warp_csr_sum(a.ax_off, a.ax_idx, [&](int q) { return __ldg(a.psurf + q); }, g0, a.nsg, stage[warp]);
+        zc = warp_seg_sum(a.ax_off, a.psort, g0, a.nsg, stage[warp]);
       if (g >= a.nsg && g < a.N) zc = __ldg(a.pint + g);
     }
     if (g < a.N) {
@@ -138,19 +137,14 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_kernel(CombineArgs a)
 
 // R[v] = vmask[v] ? 0 : sum of Rpart over (e,cb) incidences in ascending order
 // (restrict_residual accumulation, coarse.cpp:155-160, then coarse.cpp:191-192)
-__global__ void __launch_bounds__(kGatherBlock) vertex_gather_kernel(const double* __restrict__ Rpart,
-                                                                     const unsigned* __restrict__ off,
-                                                                     const int* __restrict__ idx,
-                                                                     const std::uint8_t* __restrict__ vmask,
-                                                                     double* __restrict__ R, int nv)
+__global__ void vertex_gather_kernel(const double* __restrict__ Rpart, const unsigned* __restrict__ off,
+                                     const int* __restrict__ idx, const std::uint8_t* __restrict__ vmask,
+                                     double* __restrict__ R, int nv)
 {
-  __shared__ double stage[kGatherBlock / 32][kGatherCap];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = gridDim.x * (kGatherBlock / 32);
-  for (int g0 = (blockIdx.x * (kGatherBlock / 32) + warp) * 32; g0 < nv; g0 += nwarps * 32) {
-    const double s = warp_csr_sum(off, idx, [&](int q) { return __ldg(Rpart + q); }, g0, nv, stage[warp]);
-    const int v = g0 + lane;
-    if (v < nv) R[v] = __ldg(vmask + v) ? 0.0 : s;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (unsigned q = __ldg(off + v); q < __ldg(off + v + 1); ++q) s += __ldg(Rpart + __ldg(idx + q));
+    R[v] = __ldg(vmask + v) ? 0.0 : s;
   }
 }
 

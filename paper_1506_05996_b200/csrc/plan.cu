@@ -112,6 +112,7 @@ struct Plan {
   int order = 0, np = 0, nloc = 0, nsurf = 0, P = 0;
   int ne = 0, nv = 0, N = 0, nsg = 0;
   int num_sms = 148, ax_grid = 1;
+  std::size_t n_ax_entries = 0;
   bool fdm_eo = false;
   int precond_mode = 0, variant = 0;
   bool do_fine = false, do_coarse = false, use_amg = false;
@@ -127,29 +128,27 @@ struct Plan {
   double* c_e = nullptr;
   double* kappa_e = nullptr;
   double* h3 = nullptr;
-  int* l2g_surf = nullptr;
+  int* smap = nullptr;        // [e][2][nsurf]: encoded l2g codes, Ax CSR positions
   unsigned* ax_off = nullptr;
-  int* ax_idx = nullptr;
-  short* surf_local = nullptr;
   std::uint8_t* mask = nullptr;
   double* d_lumped = nullptr;
   int* sub_face = nullptr;
   unsigned* fine_off = nullptr;
-  int* fine_idx = nullptr;
-  double* zsub = nullptr;
+  int* fine_pos = nullptr;    // [e][P^3] CSR position (-1 sentinel)
+  double* zsort = nullptr;
   int* conn = nullptr;
   unsigned* vtx_off = nullptr;
   int* vtx_idx = nullptr;
   std::uint8_t* vmask = nullptr;
   double *Rpart = nullptr, *R = nullptr, *Z = nullptr, *rho = nullptr, *dZ = nullptr;
-  double *psurf = nullptr, *pint = nullptr;
+  double *psort = nullptr, *pint = nullptr;
   std::vector<DevLevel> lv;  // AMG levels 0..L (L = coarsest, uses dense)
   DevDense dense;
   DevCsr Kc{};               // K_c on the device (AMG mode: residual between the two K-cycles)
   std::uint8_t* zero_mask = nullptr;
 
   // PCG vectors
-  double *u = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *f = nullptr, *b = nullptr, *rsurf = nullptr;
+  double *u = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *f = nullptr, *b = nullptr, *rsort = nullptr;
   // scalars / reductions
   double* partials = nullptr;
   unsigned* ticket = nullptr;
@@ -234,8 +233,8 @@ void launch_ax_elem(Plan& pl, const double* u, double* r, DotArgs dot, cudaStrea
   a.wg = pl.wg;
   a.mass = pl.mass;
   a.c_e = pl.c_e;
-  a.l2g_surf = pl.l2g_surf;
-  a.rsurf = pl.rsurf;
+  a.smap = pl.smap;
+  a.rsort = pl.rsort;
   a.r = r;
   a.ne = pl.ne;
   a.num_surface_global = pl.nsg;
@@ -262,9 +261,8 @@ void enqueue_ax(Plan& pl, const double* u, double* r, double* dot_result, cudaSt
   }
   HXB_DISPATCH_NP(pl.np, launch_ax_elem, pl, u, r, d1, s);
   AxGatherArgs g;
-  g.rsurf = pl.rsurf;
+  g.rsort = pl.rsort;
   g.off = pl.ax_off;
-  g.idx = pl.ax_idx;
   g.u = u;
   g.mask = pl.mask;
   g.r = r;
@@ -278,14 +276,15 @@ void launch_fdm(Plan& pl, cudaStream_t s)
 {
   FdmArgs a;
   a.r = pl.r;
-  a.l2g_surf = pl.l2g_surf;
+  a.smap = pl.smap;
   a.sub_face = pl.sub_face;
   a.h3 = pl.h3;
   a.kappa_e = pl.kappa_e;
   a.c_e = pl.c_e;
-  a.zsub = pl.zsub;
+  a.pos = pl.fine_pos;
+  a.zsort = pl.zsort;
   a.ne = pl.ne;
-  a.nsurf = pl.nsurf;
+  a.sstride = 2 * pl.nsurf;
   a.num_surface_global = pl.nsg;
   if (pl.fdm_eo)
     fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
@@ -298,13 +297,11 @@ void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, b
   CombineArgs a;
   a.r = pl.r;
   a.mask = pl.mask;
-  a.zsub = pl.zsub;
+  a.zsort = pl.zsort;
   a.fine_off = pl.fine_off;
-  a.fine_idx = pl.fine_idx;
-  a.psurf = pl.psurf;
+  a.psort = pl.psort;
   a.pint = pl.pint;
   a.ax_off = pl.ax_off;
-  a.ax_idx = pl.ax_idx;
   a.lumped = pl.d_lumped;
   a.z = pl.z;
   a.N = pl.N;
@@ -320,13 +317,14 @@ void launch_prolong(Plan& pl, cudaStream_t s)
 {
   using Sh = AxShape<NP>;
   prolong_elem_kernel<NP, Sh::kEPB, Sh::kBlock><<<(pl.ne + Sh::kEPB - 1) / Sh::kEPB, Sh::kBlock, 0, s>>>(
-      pl.Z, pl.conn, pl.mass, pl.psurf, pl.pint, pl.ne, pl.nsurf, pl.nsg);
+      pl.Z, pl.conn, pl.mass, pl.smap, pl.psort, pl.pint, pl.ne, pl.nsurf, pl.nsg);
 }
 
 template <int NP>
 void launch_restrict(Plan& pl, cudaStream_t s)
 {
-  restrict_kernel<NP, 128><<<pl.ne, 128, 0, s>>>(pl.r, pl.d_lumped, pl.l2g_surf, pl.mass, pl.Rpart, pl.ne, pl.nsurf,
+  constexpr int B = AxShape<NP>::kBlock;
+  restrict_kernel<NP, B><<<pl.ne, B, 0, s>>>(pl.r, pl.d_lumped, pl.smap, pl.mass, pl.Rpart, pl.ne, 2 * pl.nsurf,
                                                    pl.nsg);
 }
 
@@ -623,35 +621,27 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   HXB_CUDA(cudaMemset(pl.zero_mask, 0, pl.N));
   pl.d_lumped = M.upload(hs.lumped);
 
-  // encoded surface map and Ax surface gather CSR (ascending e*nsurf+s, padded stride)
+  // surface map [e][2][nsurf]: Dirichlet-encoded global ids and each copy's
+  // position in the Ax surface CSR (copies of a node in ascending (e,l) order,
+  // mesh.cpp:358-367) - producers write there, gathers stream contiguously
   {
-    std::vector<int> enc(static_cast<std::size_t>(ne) * pl.nsurf, 0);
-    for (int e = 0; e < ne; ++e)
-      for (int q = 0; q < nsurf_raw; ++q) {
-        const gid g = num.l2g_surf[static_cast<std::size_t>(e) * nsurf_raw + q];
-        enc[static_cast<std::size_t>(e) * pl.nsurf + q] = num.dirichlet_mask[g] ? encode_dirichlet(g) : g;
-      }
-    pl.l2g_surf = M.upload(enc);
     std::vector<unsigned> off(static_cast<std::size_t>(pl.nsg) + 1, 0);
     for (gid g : num.l2g_surf) off[g + 1]++;
     for (int g = 0; g < pl.nsg; ++g) off[g + 1] += off[g];
-    std::vector<int> idx(num.l2g_surf.size());
     std::vector<unsigned> cur(off.begin(), off.end() - 1);
+    std::vector<int> smap(static_cast<std::size_t>(ne) * 2 * pl.nsurf, 0);
     for (int e = 0; e < ne; ++e)
-      for (int q = 0; q < nsurf_raw; ++q)
-        idx[cur[num.l2g_surf[static_cast<std::size_t>(e) * nsurf_raw + q]]++] = e * pl.nsurf + q;
+      for (int q = 0; q < nsurf_raw; ++q) {
+        const gid g = num.l2g_surf[static_cast<std::size_t>(e) * nsurf_raw + q];
+        int* row = &smap[static_cast<std::size_t>(e) * 2 * pl.nsurf];
+        row[q] = num.dirichlet_mask[g] ? encode_dirichlet(g) : g;
+        row[pl.nsurf + q] = static_cast<int>(cur[g]++);
+      }
+    pl.smap = M.upload(smap);
     pl.ax_off = M.upload(off);
-    pl.ax_idx = M.upload(idx);
-    std::vector<short> sl(pl.nsurf, 0);
-    for (int k = 0; k < pl.np; ++k)
-      for (int j = 0; j < pl.np; ++j)
-        for (int i = 0; i < pl.np; ++i) {
-          const int sq = surface_slot_of(pl.np, i, j, k);
-          if (sq >= 0) sl[sq] = static_cast<short>((k * pl.np + j) * pl.np + i);
-        }
-    pl.surf_local = M.upload(sl);
+    pl.n_ax_entries = off[pl.nsg];
   }
-  pl.rsurf = M.alloc<double>(static_cast<std::size_t>(ne) * pl.nsurf);
+  pl.rsort = M.alloc<double>(pl.n_ax_entries);
 
   // fine: encoded sub_face and the subdomain gather CSR in (e, slot) order
   if (pl.do_fine) {
@@ -669,15 +659,17 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
         if (g >= 0) cnt[g + 1]++;
       });
     for (int g = 0; g < pl.N; ++g) cnt[g + 1] += cnt[g];
-    std::vector<int> idx(cnt[pl.N]);
+    // each (e, slot) contribution's position in the per-node list, ascending
+    // (e, slot) = the reference accumulation order (fine.cpp:224-227)
+    std::vector<int> pos(static_cast<std::size_t>(ne) * nsub, -1);
     std::vector<unsigned> cur(cnt.begin(), cnt.end() - 1);
     for (int e = 0; e < ne; ++e)
       for_each_sub_slot(num, ne, e, scratch.data(), [&](gid g, int slot) {
-        if (g >= 0) idx[cur[g]++] = static_cast<int>(static_cast<std::size_t>(e) * nsub + slot);
+        if (g >= 0) pos[static_cast<std::size_t>(e) * nsub + slot] = static_cast<int>(cur[g]++);
       });
     pl.fine_off = M.upload(cnt);
-    pl.fine_idx = M.upload(idx);
-    pl.zsub = M.alloc<double>(static_cast<std::size_t>(ne) * nsub);
+    pl.fine_pos = M.upload(pos);
+    pl.zsort = M.alloc<double>(cnt[pl.N]);
   }
 
   // coarse: connectivity, vertex incidence CSR (e, cb) order, coarse matrix, AMG / dense
@@ -702,7 +694,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.Z = M.alloc<double>(pl.nv);
     pl.rho = M.alloc<double>(pl.nv);
     pl.dZ = M.alloc<double>(pl.nv);
-    pl.psurf = M.alloc<double>(static_cast<std::size_t>(ne) * pl.nsurf);
+    pl.psort = M.alloc<double>(pl.n_ax_entries);
     pl.pint = M.alloc<double>(pl.N);
     pl.coarse_n = hs.Kc.n;
     if (pl.use_amg) {
@@ -1070,6 +1062,48 @@ int hxb_amg_level(hxb_plan* plan, int level, int64_t* rows, int64_t* nnz, int64_
                   int32_t* aggregate)
 {
   return guarded([&] { export_amg_level(as_plan(plan)->hs, level, rows, nnz, ptr, col, val, aggregate); });
+}
+
+// Per-component device times (ms, CUDA events, warm caches, mean of reps):
+// out[0] Ax element kernel, [1] Ax gather, [2] FDM subdomain solves,
+// [3] coarse branch graph (restrict + solve + prolong), [4] combine,
+// [5] full P apply (fine || coarse, combine), [6] PCG vector update,
+// [7] PCG direction update.
+int hxb_profile(hxb_plan* plan, int reps, double* out)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    cudaStream_t s = pl->s_main;
+    auto timeit = [&](auto&& fn) {
+      for (int w = 0; w < 2; ++w) fn();
+      HXB_CUDA(cudaStreamSynchronize(s));
+      HXB_CUDA(cudaEventRecord(pl->ev_t0, s));
+      for (int q = 0; q < reps; ++q) fn();
+      HXB_CUDA(cudaEventRecord(pl->ev_t1, s));
+      HXB_CUDA(cudaEventSynchronize(pl->ev_t1));
+      float ms = 0;
+      HXB_CUDA(cudaEventElapsedTime(&ms, pl->ev_t0, pl->ev_t1));
+      return static_cast<double>(ms) / reps;
+    };
+    for (int q = 0; q < 8; ++q) out[q] = 0;
+    ensure_hist(*pl, 4);
+    out[0] = timeit([&] { HXB_DISPATCH_NP(pl->np, launch_ax_elem, *pl, pl->p, pl->f, DotArgs{}, s); });
+    out[1] = timeit([&] { enqueue_ax(*pl, pl->p, pl->f, nullptr, s); }) - out[0];
+    if (pl->do_fine) out[2] = timeit([&] { HXB_DISPATCH_NP(pl->np, launch_fdm, *pl, s); });
+    if (pl->do_coarse) out[3] = timeit([&] { HXB_CUDA(cudaGraphLaunch(pl->coarse_exec, s)); });
+    out[4] = timeit([&] { launch_combine(*pl, pl->zr_hist, s, pl->do_fine, pl->do_coarse); });
+    out[5] = timeit([&] { enqueue_precond(*pl, pl->zr_hist); });
+    HXB_CUDA(cudaMemcpy(pl->pf_hist, pl->zr_hist, sizeof(double), cudaMemcpyDeviceToDevice));
+    out[6] = timeit([&] {
+      pcg_update_kernel<kVecBlock><<<vec_grid(pl->N), kVecBlock, 0, s>>>(pl->f, pl->r, pl->N, pl->zr_hist, pl->pf_hist,
+                                                                         0, dot_args(*pl, pl->res2));
+    });
+    out[7] = timeit([&] {
+      pcg_dir_kernel<<<vec_grid(pl->N), kVecBlock, 0, s>>>(pl->z, pl->p, pl->u, pl->N, pl->zr_hist, pl->pf_hist, 0);
+    });
+    HXB_CUDA(cudaGetLastError());
+  });
 }
 
 int hxb_bench_apply_A(hxb_plan* plan, int reps, double* ms_per_apply, double* ms_elem_kernel)

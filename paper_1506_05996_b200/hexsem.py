@@ -96,6 +96,7 @@ SIGNATURES = {
     "hxb_export_maps": (C.c_int, [P, P, P, P, P, P, P]),
     "hxb_amg_level": (C.c_int, [P, C.c_int, P, P, P, P, P, P]),
     "hxb_bench_apply_A": (C.c_int, [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "hxb_profile": (C.c_int, [P, C.c_int, P]),
     "hxb_setup_create": (C.c_int, [C.POINTER(_Mesh), C.c_int, P, P, C.POINTER(_Options), C.POINTER(P)]),
     "hxb_setup_destroy": (None, [P]),
     "hxb_setup_info": (C.c_int, [P, C.POINTER(_PlanInfo)]),
@@ -404,6 +405,13 @@ class Plan:
         _check(lib().hxb_amg_level(self._h, l, C.byref(rows), C.byref(nnz), _ptr(ptr), _ptr(col), _ptr(val),
                                    _ptr(agg)))
         return {"ptr": ptr, "col": col, "val": val, "aggregate": agg}
+
+    def profile(self, reps: int = 10) -> dict:
+        """Per-component device times in ms (CUDA events, warm caches)."""
+        out = np.zeros(8)
+        _check(lib().hxb_profile(self._h, reps, _ptr(out)))
+        keys = ["ax_elem", "ax_gather", "fdm", "coarse", "combine", "precond", "pcg_update", "pcg_dir"]
+        return dict(zip(keys, out.tolist()))
 
     def bench_apply_A(self, reps: int = 20):
         ms, ms_elem = C.c_double(), C.c_double()

@@ -21,6 +21,7 @@ out["amg"] = [plan.amg_rows, plan.amg_nnz]
 u = splitmix_vector(plan.N, 12345)
 r = plan.apply_A(u)
 out["ax_checksum"] = float(r.sum())
+out["profile_ms"] = plan.profile(10)
 ms, ms_elem = plan.bench_apply_A(20)
 words = hx.residual_words_model(plan.NE, n)
 out["ax_ms"] = ms
