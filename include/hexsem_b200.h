@@ -189,8 +189,9 @@ int hxb_pencil(int order, double* K, double* M, double* V, double* V_inv, double
  * CUDA events; returns mean ms per apply (kernel-level bench helper). */
 int hxb_bench_apply_A(hxb_plan* plan, int reps, double* ms_per_apply, double* ms_elem_kernel);
 
-/* Per-component device timings (ms): Ax element, Ax gather, FDM, coarse
- * branch, combine, full P, PCG update, PCG direction (out[8]). */
+/* Per-component device timings (ms), out[12]: Ax element, Ax gather, FDM,
+ * coarse branch, combine, full P, PCG update, PCG direction, restrict,
+ * prolong, AMG solve. */
 int hxb_profile(hxb_plan* plan, int reps, double* out);
 
 /* Counter models (operator.cpp:20-37, fine.cpp:82-92). */

@@ -40,7 +40,7 @@ struct AxShape {
   static constexpr int kBufA = NP == 8 ? 512 : NP * NP * kS;
   static constexpr int kBufB = NP == 8 ? 576 : NP * NP * kS;
   static constexpr std::size_t kGBytes = 6ull * kNlocP * sizeof(double);
-  static constexpr std::size_t kIdxBytes = 2 * kNsurfP * sizeof(int);  // codes + CSR positions
+  static constexpr std::size_t kIdxBytes = kNsurfP * sizeof(int);  // Dirichlet-encoded codes
   static constexpr std::size_t kSmemBytes = kGBytes + (kBufA + kBufB + 2 * NP * NP) * sizeof(double) + kIdxBytes +
                                             2 * sizeof(unsigned long long);
   static constexpr int kMinBlocks = NP <= 8 ? 6 : 2;  // caps registers; shared memory sets the real limit
@@ -70,8 +70,8 @@ struct AxArgs {
   const double* wg;         // [e][6][nlocp]: kappa*m*Gt planes per element (TMA-staged)
   const double* mass;       // NE * nloc
   const double* c_e;        // NE
-  const int* smap;          // [e][2][nsurfp]: Dirichlet-encoded global ids, CSR positions (TMA-staged)
-  double* rsort;            // surface copies in assembly (CSR) order (output)
+  const int* smap;          // [e][2][nsurfp]: row 0 Dirichlet-encoded global ids (TMA-staged)
+  double* rsurf;            // [e][nsurfp] surface E-vector (output)
   double* r;                // N output (interior nodes written here)
   int ne;
   int num_surface_global;   // first element-interior global id
@@ -129,8 +129,8 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
   double* sb = sa + Sh::kBufA;
   double* sD = sb + Sh::kBufB;                                       // D, then D^T
   double* sDT = sD + NP * NP;
-  int* sidx = reinterpret_cast<int*>(sDT + NP * NP);                 // [2][nsurfp]
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sidx + 2 * Sh::kNsurfP);  // [0]=G, [1]=idx
+  int* sidx = reinterpret_cast<int*>(sDT + NP * NP);                 // [nsurfp]
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sidx + Sh::kNsurfP);  // [0]=G, [1]=idx
   __shared__ double red[Sh::kBlock / 32];
 
   const int tid = threadIdx.x;
@@ -163,22 +163,18 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
     bulk_g2s(sG, a.wg + (long long)e * 6 * NLP, Sh::kGBytes, &bar[0]);
   }
   // gather u for element ee (masked, operator.cpp:264-265) using the staged indices
-  // (also reads the element's output positions from the same staged block)
-  auto gather_u = [&](int ee, double (&dst)[NP], int (&pos)[NP]) {
+  auto gather_u = [&](int ee, double (&dst)[NP]) {
     const long long ib = (long long)a.num_surface_global + (long long)ee * NI;
 #pragma unroll
-    for (int k = 0; k < NP; ++k) {
+    for (int k = 0; k < NP; ++k)
       dst[k] = code[k] >= 0 ? load_masked(a.u, sidx[code[k]]) : __ldg(a.u + ib - 1 - code[k]);
-      pos[k] = code[k] >= 0 ? sidx[Sh::kNsurfP + code[k]] : 0;
-    }
   };
   double ucol[NP];
-  int posk[NP];
   double ce = 0.0;
   unsigned phase = 0;
   if (e < a.ne) {
     mbar_wait(&bar[1], 0);
-    gather_u(e, ucol, posk);
+    gather_u(e, ucol);
     ce = __ldg(a.c_e + e);
     __syncthreads();
     if (tid == 0 && e + (int)gridDim.x < a.ne) {
@@ -238,13 +234,12 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
       mbar_expect_tx(&bar[0], Sh::kGBytes);
       bulk_g2s(sG, a.wg + (long long)en * 6 * NLP, Sh::kGBytes, &bar[0]);
     }
-    // prefetch u(e'), its output positions and c(e') while the adjoint contractions run
+    // prefetch u(e') and c(e') while the adjoint contractions run
     double unext[NP];
-    int posnext[NP];
     double cnext = 0.0;
     if (en < a.ne) {
       mbar_wait(&bar[1], phase ^ 1u);
-      gather_u(en, unext, posnext);
+      gather_u(en, unext);
       cnext = __ldg(a.c_e + en);
     }
 
@@ -272,12 +267,13 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
     // ---- E: sum, mass term, store ---------------------------------------------
     if (lane_ok) {
       const double* m0 = a.mass + (std::size_t)e * Sh::kNloc + j * NP + i;
+      double* rs = a.rsurf + (long long)e * Sh::kNsurfP;
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         double r = (sa[lay_a<NP>(k, j, i)] + sb[lay_b<NP>(k, j, i)]) + tz[k];
         if (ce != 0.0) r += (ce * ucol[k]) * __ldg(m0 + k * NP * NP);  // operator.cpp:159
         if (code[k] >= 0) {
-          a.rsort[posk[k]] = r;  // CSR position: the gather then streams
+          rs[code[k]] = r;
         } else {
           a.r[ibase - 1 - code[k]] = r;
           dot += ucol[k] * r;
@@ -286,10 +282,7 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
     }
     __syncthreads();  // sa/sb reads done before the next element's phase A
 #pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      ucol[k] = unext[k];
-      posk[k] = posnext[k];
-    }
+    for (int k = 0; k < NP; ++k) ucol[k] = unext[k];
     ce = cnext;
   }
   dot_commit<Sh::kBlock>(a.dot, dot, red);

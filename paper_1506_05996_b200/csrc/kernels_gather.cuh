@@ -44,12 +44,39 @@ __device__ __forceinline__ double warp_seg_sum(const unsigned* __restrict__ off,
   return s;
 }
 
+// Same, for values scattered in an E-vector: src(idx[q]) gathered by the warp
+// (coalesced index segment, parallel value loads), then per-lane sequential sums.
+template <class Src>
+__device__ __forceinline__ double warp_csr_sum(const unsigned* __restrict__ off, const int* __restrict__ idx, Src&& src,
+                                               int g0, int n, double* __restrict__ stage)
+{
+  const int lane = threadIdx.x & 31;
+  const int g = g0 + lane;
+  const unsigned my0 = __ldg(off + min(g, n));
+  const unsigned my1 = __ldg(off + min(g + 1, n));
+  const unsigned base = __shfl_sync(0xffffffffu, my0, 0);
+  const unsigned end = __shfl_sync(0xffffffffu, my1, 31);
+  const unsigned cnt = end - base;
+  double s = 0.0;
+  if (cnt <= static_cast<unsigned>(kGatherCap)) {
+#pragma unroll 4
+    for (unsigned c = lane; c < cnt; c += 32) stage[c] = src(__ldg(idx + base + c));
+    __syncwarp();
+    for (unsigned q = my0 - base; q < my1 - base; ++q) s += stage[q];
+    __syncwarp();
+  } else {
+    for (unsigned q = my0; q < my1; ++q) s += src(__ldg(idx + q));
+  }
+  return s;
+}
+
 // ---------------------------------------------------------------------------
 // Ax surface assembly (gather, mesh.cpp:463-475) + Dirichlet identity rows
 // (operator.cpp:279-280) + the optional fused p.Ap partial.
 struct AxGatherArgs {
-  const double* rsort;   // surface copies in CSR order (written by ax_elem_kernel)
+  const double* rsurf;   // [e][nsurfp] surface E-vector (ax_elem_kernel)
   const unsigned* off;   // num_surface_global + 1
+  const int* idx;        // e*nsurfp + slot, ascending per node
   const double* u;
   const std::uint8_t* mask;
   double* r;
@@ -65,7 +92,8 @@ __global__ void __launch_bounds__(kGatherBlock) ax_gather_kernel(AxGatherArgs a)
   const int nwarps = gridDim.x * (kGatherBlock / 32);
   double dot = 0.0;
   for (int g0 = (blockIdx.x * (kGatherBlock / 32) + warp) * 32; g0 < a.num_surface_global; g0 += nwarps * 32) {
-    const double s = warp_seg_sum(a.off, a.rsort, g0, a.num_surface_global, stage[warp]);
+    const double s = warp_csr_sum(a.off, a.idx, [&](int q) { return __ldg(a.rsurf + q); }, g0,
+                                  a.num_surface_global, stage[warp]);
     const int g = g0 + lane;
     if (g < a.num_surface_global) {
       const double ug = __ldg(a.u + g);

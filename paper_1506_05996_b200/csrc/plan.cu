@@ -148,7 +148,8 @@ struct Plan {
   std::uint8_t* zero_mask = nullptr;
 
   // PCG vectors
-  double *u = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *f = nullptr, *b = nullptr, *rsort = nullptr;
+  double *u = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *f = nullptr, *b = nullptr, *rsurf = nullptr;
+  int* ax_idx = nullptr;
   // scalars / reductions
   double* partials = nullptr;
   unsigned* ticket = nullptr;
@@ -234,7 +235,7 @@ void launch_ax_elem(Plan& pl, const double* u, double* r, DotArgs dot, cudaStrea
   a.mass = pl.mass;
   a.c_e = pl.c_e;
   a.smap = pl.smap;
-  a.rsort = pl.rsort;
+  a.rsurf = pl.rsurf;
   a.r = r;
   a.ne = pl.ne;
   a.num_surface_global = pl.nsg;
@@ -261,8 +262,9 @@ void enqueue_ax(Plan& pl, const double* u, double* r, double* dot_result, cudaSt
   }
   HXB_DISPATCH_NP(pl.np, launch_ax_elem, pl, u, r, d1, s);
   AxGatherArgs g;
-  g.rsort = pl.rsort;
+  g.rsurf = pl.rsurf;
   g.off = pl.ax_off;
+  g.idx = pl.ax_idx;
   g.u = u;
   g.mask = pl.mask;
   g.r = r;
@@ -640,8 +642,13 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.smap = M.upload(smap);
     pl.ax_off = M.upload(off);
     pl.n_ax_entries = off[pl.nsg];
+    std::vector<int> idx(off[pl.nsg]);
+    for (int e = 0; e < ne; ++e)
+      for (int q = 0; q < nsurf_raw; ++q)
+        idx[smap[static_cast<std::size_t>(e) * 2 * pl.nsurf + pl.nsurf + q]] = e * pl.nsurf + q;
+    pl.ax_idx = M.upload(idx);
   }
-  pl.rsort = M.alloc<double>(pl.n_ax_entries);
+  pl.rsurf = M.alloc<double>(static_cast<std::size_t>(ne) * pl.nsurf);
 
   // fine: encoded sub_face and the subdomain gather CSR in (e, slot) order
   if (pl.do_fine) {
@@ -1086,7 +1093,7 @@ int hxb_profile(hxb_plan* plan, int reps, double* out)
       HXB_CUDA(cudaEventElapsedTime(&ms, pl->ev_t0, pl->ev_t1));
       return static_cast<double>(ms) / reps;
     };
-    for (int q = 0; q < 8; ++q) out[q] = 0;
+    for (int q = 0; q < 12; ++q) out[q] = 0;
     ensure_hist(*pl, 4);
     out[0] = timeit([&] { HXB_DISPATCH_NP(pl->np, launch_ax_elem, *pl, pl->p, pl->f, DotArgs{}, s); });
     out[1] = timeit([&] { enqueue_ax(*pl, pl->p, pl->f, nullptr, s); }) - out[0];
@@ -1102,6 +1109,15 @@ int hxb_profile(hxb_plan* plan, int reps, double* out)
     out[7] = timeit([&] {
       pcg_dir_kernel<<<vec_grid(pl->N), kVecBlock, 0, s>>>(pl->z, pl->p, pl->u, pl->N, pl->zr_hist, pl->pf_hist, 0);
     });
+    if (pl->do_coarse) {
+      out[8] = timeit([&] {
+        HXB_DISPATCH_NP(pl->np, launch_restrict, *pl, s);
+        vertex_gather_kernel<<<vec_grid(pl->nv), kVecBlock, 0, s>>>(pl->Rpart, pl->vtx_off, pl->vtx_idx, pl->vmask,
+                                                                     pl->R, pl->nv);
+      });
+      out[9] = timeit([&] { HXB_DISPATCH_NP(pl->np, launch_prolong, *pl, s); });
+      out[10] = out[3] - out[8] - out[9];
+    }
     HXB_CUDA(cudaGetLastError());
   });
 }

@@ -408,9 +408,10 @@ class Plan:
 
     def profile(self, reps: int = 10) -> dict:
         """Per-component device times in ms (CUDA events, warm caches)."""
-        out = np.zeros(8)
+        out = np.zeros(12)
         _check(lib().hxb_profile(self._h, reps, _ptr(out)))
-        keys = ["ax_elem", "ax_gather", "fdm", "coarse", "combine", "precond", "pcg_update", "pcg_dir"]
+        keys = ["ax_elem", "ax_gather", "fdm", "coarse", "combine", "precond", "pcg_update", "pcg_dir",
+                "restrict", "prolong", "amg"]
         return dict(zip(keys, out.tolist()))
 
     def bench_apply_A(self, reps: int = 20):

@@ -84,3 +84,25 @@ def test_pcg_amg_path():
     ref, plan = _pair(k=8, order=3, coarse_solve="amg")
     b = ref.load_ones()
     history_parity(plan.pcg(b, tol=1e-8), ref.pcg(b, tol=1e-8))
+
+
+@pytest.mark.slow
+def test_pcg_cfg2_against_golden():
+    """cfg2 (52^3, N=7, ~48.6M DOF) two-scale PCG to 1e-8 vs the reference's
+    history recorded in tests/golden/cfg2_pcg.json (make_cfg2_golden.py)."""
+    import json
+    import os
+
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cfg2_pcg.json")))
+    mesh = hx.generate_cube_mesh(52)
+    with hx.Plan(mesh, 7) as plan:
+        assert plan.N == gold["N"]
+        u = splitmix_vector(plan.N, 12345)
+        r = plan.apply_A(u)
+        assert abs(r.sum() - gold["ax_checksum_seed12345"]) <= 1e-9 * gold["ax_norm_seed12345"]
+        assert abs(np.linalg.norm(r) - gold["ax_norm_seed12345"]) <= 1e-12 * gold["ax_norm_seed12345"]
+        res = plan.pcg(None, tol=1e-8, max_iterations=500)
+    ref = {"status": gold["status"], "iterations": gold["iterations"],
+           "residual_history": np.array(gold["residual_history"]), "u": None}
+    history_parity(res, ref, tol=1e-10)
+    assert abs(np.linalg.norm(res["u"]) - gold["u_norm2"]) <= 1e-10 * gold["u_norm2"]
