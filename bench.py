@@ -1,0 +1,397 @@
+"""bench.py — B200 matrix-free SEM PCG (hexsem solver path) benchmark.
+
+Workload (BASELINE.json configs[1], "cfg2"): 52^3 uniform hexes, N=7
+(48,627,125 DOF), Poisson (kappa=1, c=0, s=1), all-Dirichlet, two-scale
+Schwarz PCG to 1e-8.
+
+A "step" is one Ax = SemOperator::apply (operator.cpp:255-287) over the full
+mesh: the element contraction kernel plus the deterministic CSR gather. The
+headline `value` is Ax GDOF/s = N / (ms per step) with u already in HBM;
+`e2e` is the same metric through the reference-facing C-ABI call
+`hxb_apply_A` on pinned HOST buffers (H2D of u and D2H of r inside the timed
+region). The PCG solve to 1e-8 (the metric's second half) is measured in the
+same run and reported under "pcg" (device-timed, plus the host-API e2e).
+
+`roofline` is for the dominant kernel (ax_elem_kernel): algorithmic bytes =
+the reference's own model B_R = 8*NE*(10 np^3 + np^2 + 2)
+(operator.cpp:31-37) per launch / its CUDA-event duration measured
+live over the timed region, against MEASURED_PEAKS.json hbm_gbs.
+
+`cpu_baseline`: the unmodified reference (oracle/_ref/libhexsem_ref.so,
+compiled from /root/reference sources by oracle/Makefile) timed on this box's
+host cores on a bounded sample (26^3 hexes, N=7; the reference Ax is
+single-threaded by design, so cores=1).
+
+`--impl reference` times that same reference library's SemOperator::apply on
+the bounded sample, rank 0 only.
+
+Multi-GPU (torchrun, N>1): each rank runs its own cfg2 replica (weak scaling,
+no data-path collective); element-slab domain decomposition with halo
+exchange is not in this round.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Ax GDOF/s (FP64) and PCG solve time to 1e-8 at N=7, ~50M DOF, 1/2/4/8 B200"
+SAMPLE_K = 26  # bounded CPU sample: 26^3 hexes at N=7 (6.1M DOF, 1/8 of cfg2)
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 10:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        load = [r for r in rows if (num(r[4]) or 0) >= 50] or rows
+        sm = [num(r[1]) for r in load if num(r[1]) is not None]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in load:
+            for name, v in zip(names, r[6:10]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": num(rows[0][2]),
+                "reasons": sorted(reasons), "samples": len(rows), "samples_under_load": len(load),
+                "power_w_max": max((num(r[3]) or 0) for r in rows)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference_ax(k: int, order: int, steps: int, warmup: int):
+    """Reference SemOperator::apply (oracle/_ref, unmodified sources) on a k^3 mesh."""
+    from oracle import RefConfig, RefSystem, ref_available, splitmix_vector, OracleSystem
+
+    kind = "reference" if ref_available() else "port"
+    cls = RefSystem if kind == "reference" else OracleSystem
+    t0 = time.time()
+    sys_ = cls(RefConfig(k=k, order=order, precond="none"))
+    setup_s = time.time() - t0
+    u = splitmix_vector(sys_.N, 12345)
+    for _ in range(warmup):
+        sys_.apply_A(u)
+    times = []
+    for _ in range(steps):
+        t = time.perf_counter()
+        sys_.apply_A(u)
+        times.append(time.perf_counter() - t)
+    N = sys_.N
+    sys_.close()
+    mean = sum(times) / len(times)
+    return {"kind": kind, "N": N, "mean_s": mean, "best_s": min(times), "setup_s": setup_s, "steps": steps}
+
+
+def cpu_reference_pcg(k: int, order: int, iters: int, threads: int):
+    """Reference two-scale pcg (krylov.cpp:20-71) in its fastest legal mode
+    (fine_threads = cores-1, concurrent coarse), capped at `iters` iterations."""
+    from oracle import RefConfig, RefSystem, ref_available
+
+    if not ref_available():
+        return None
+    s = RefSystem(RefConfig(k=k, order=order, precond="two_scale", concurrent_precond=True,
+                            fine_threads=max(1, threads - 1)))
+    b = s.load_ones()
+    res = s.pcg(b, tol=1e-8, max_iterations=iters)
+    out = {"N": s.N, "iterations": res["iterations"], "solve_s": res["solve_seconds"],
+           "s_per_iteration": res["solve_seconds"] / max(1, res["iterations"])}
+    s.close()
+    return out
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    r = cpu_reference_ax(SAMPLE_K, args.order, args.steps, args.warmup)
+    gdofs = r["N"] / r["mean_s"] / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gdofs, "unit": "GDOF/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["mean_s"] * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated mesh, splitmix64 u)",
+        "config": {"workload": f"cfg2 Ax (SemOperator::apply), bounded sample {SAMPLE_K}^3 hexes N={args.order}",
+                   "k": SAMPLE_K, "order": args.order, "N": r["N"], "parallelism": "1 host thread"},
+        "cpu_baseline": {"value": gdofs, "unit": "GDOF/s", "cores": 1, "kind": r["kind"],
+                         "sample": f"SemOperator::apply on {SAMPLE_K}^3 hexes N={args.order} ({r['N']} DOF), "
+                                   f"mean of {args.steps} after {args.warmup} warm-up; reference Ax is "
+                                   f"single-threaded (host has {cores} cores)"},
+        "e2e": {"value": gdofs, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_1506_05996_b200 as hx
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the B200 path has no CPU fallback)")
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    k, order = args.k, args.order
+    t0 = time.time()
+    mesh = hx.generate_cube_mesh(k)
+    plan = hx.Plan(mesh, order, device=local_rank)
+    setup_s = time.time() - t0
+    N, NE = plan.N, plan.NE
+    np1 = order + 1
+    bytes_ax = 8 * NE * (10 * np1 ** 3 + np1 ** 2 + 2)  # B_R, operator.cpp:31-37
+    bytes_fdm = 8 * NE * (3 * (order + 3) ** 3 + 4 * (order + 3) ** 2)  # B_P, fine.cpp:88-92
+
+    # u: splitmix64 seed 12345 (oracles.cpp:126-139), Dirichlet entries zeroed
+    from oracle import splitmix_vector  # input generator only (same vector the reference is fed)
+
+    u_host = splitmix_vector(N, 12345)
+    mask = plan.maps(sub=False)["dirichlet_mask"].astype(bool)
+    u_host[mask] = 0.0
+    d_u = torch.from_numpy(u_host).to("cuda")
+    d_r = torch.empty(N, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+
+    # ---- device-resident Ax: W warm-up, K timed --------------------------
+    for _ in range(args.warmup):
+        plan.apply_A_device(d_u.data_ptr(), d_r.data_ptr(), stream)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    plan.kernel_timing(True, max_launches=4 * args.steps + 16)
+    launches0 = plan.launch_count()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        plan.apply_A_device(d_u.data_ptr(), d_r.data_ptr(), stream)
+    ev1.record()
+    barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = plan.launch_count() - launches0
+    elem_ms, elem_n = plan.kernel_time("ax_elem")
+    gath_ms, gath_n = plan.kernel_time("ax_gather")
+    plan.kernel_timing(False)
+    ms_step = max_over_ranks(ms_total / args.steps)
+    value = world * N / (ms_step * 1e-3) / 1e9
+    r_dev = d_r.cpu().numpy()
+
+    # ---- e2e through the C-ABI with pinned host buffers -------------------
+    h_u = torch.from_numpy(u_host).pin_memory()
+    h_r = torch.empty(N, dtype=torch.float64).pin_memory()
+    for _ in range(min(args.warmup, 3)):
+        plan.apply_A_host_ptr(h_u.data_ptr(), h_r.data_ptr())
+    barrier()
+    e2e_steps = max(3, min(args.steps, 20))
+    t = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.apply_A_host_ptr(h_u.data_ptr(), h_r.data_ptr())
+    e2e_s = max_over_ranks((time.perf_counter() - t) / e2e_steps)
+    e2e_parity = float(np.max(np.abs(h_r.numpy() - r_dev)))
+
+    # ---- FDM (fine Schwarz) kernel timing from the same plan ---------------
+    fdm = None
+    try:
+        prof = plan.profile(5)
+        fdm = {"ms": prof["fdm"], "algorithmic_bytes": bytes_fdm,
+               "gbs": bytes_fdm / (prof["fdm"] * 1e-3) / 1e9 if prof["fdm"] > 0 else None,
+               "components_ms": prof}
+    except Exception as exc:  # noqa: BLE001
+        fdm = {"error": str(exc)}
+
+    # ---- PCG solve to 1e-8 (device-resident) + e2e (host b in, host u out) --
+    pcg = None
+    if not args.no_pcg:
+        res = plan.pcg_device(None, tol=1e-8, max_iterations=500, want_u=False)  # warm-up solve
+        barrier()
+        l0 = plan.launch_count()
+        res = plan.pcg_device(None, tol=1e-8, max_iterations=500, want_u=False)
+        pcg_launches = plan.launch_count() - l0
+        solve_s = max_over_ranks(res["solve_seconds"])
+        b_host = plan.load_ones()
+        t = time.perf_counter()
+        res_e2e = plan.pcg(b_host, tol=1e-8, max_iterations=500, want_u=True)
+        e2e_solve = max_over_ranks(time.perf_counter() - t)
+        pcg = {"tol": 1e-8, "iterations": res["iterations"], "status": res["status"],
+               "solve_s": solve_s, "ms_per_iteration": solve_s * 1e3 / max(1, res["iterations"]),
+               "gpu_launches": pcg_launches,
+               "e2e_solve_s": e2e_solve, "e2e_h2d_bytes": 8 * N, "e2e_d2h_bytes": 8 * N,
+               "r0": float(res["residual_history"][0]), "r_final": float(res["residual_history"][-1]),
+               "u_norm2": float(np.linalg.norm(res_e2e["u"]))}
+        gold_path = os.path.join(ROOT, "tests", "golden", "cfg2_pcg.json")
+        if (k, order) == (52, 7) and os.path.exists(gold_path):
+            gold = json.load(open(gold_path))
+            rh = np.asarray(res["residual_history"])
+            gh = np.asarray(gold["residual_history"])
+            m = min(len(rh), len(gh))
+            pcg["parity_vs_reference"] = {
+                "ref_iterations": gold["iterations"],
+                "max_abs_dr_over_r0": float(np.max(np.abs(rh[:m] - gh[:m])) / gh[0]),
+                "u_norm2_rel_diff": abs(pcg["u_norm2"] - gold["u_norm2"]) / gold["u_norm2"],
+                "ref_cpu_solve_s_build_host": gold["timing"]["solve_s"],
+            }
+    clocks = sampler.stop()
+
+    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        try:
+            r = cpu_reference_ax(SAMPLE_K, order, 3, 1)
+            cpu = {"value": r["N"] / r["mean_s"] / 1e9, "unit": "GDOF/s", "cores": 1, "kind": r["kind"],
+                   "sample": f"reference SemOperator::apply on {SAMPLE_K}^3 hexes N={order} ({r['N']} DOF), "
+                             f"mean of 3 after 1 warm-up, single-threaded by design; host has {cores} cores"}
+            if not args.no_pcg:
+                pr = cpu_reference_pcg(SAMPLE_K, order, 4, cores)
+                if pr:
+                    cpu["pcg_sample"] = {
+                        **pr, "threads": cores,
+                        "note": f"two-scale pcg, {pr['iterations']} iterations on {SAMPLE_K}^3 N={order}, "
+                                f"fine_threads={max(1, cores - 1)} + concurrent coarse (reference fastest mode)",
+                        "cfg2_solve_s_extrapolated": pr["s_per_iteration"] * (N / pr["N"]) *
+                                                     (pcg["iterations"] if pcg else 46)}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "GDOF/s", "cores": 1, "kind": "reference", "sample": f"failed: {exc}"}
+
+    peak, peak_src = _peaks()
+    elem_avg_ms = elem_ms / max(1, elem_n)
+    achieved = bytes_ax / (elem_avg_ms * 1e-3) / 1e9 if elem_n else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated 52^3 mesh, splitmix64 u, s=1 load)",
+        "config": {"workload": f"cfg2: {k}^3 uniform hexes, N={order}, Poisson kappa=1 c=0, all-Dirichlet; "
+                               "step = one Ax (SemOperator::apply)",
+                   "k": k, "order": order, "N": N, "NE": NE,
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (weak)",
+                   "l2": f"inputs larger than L2 ({bytes_ax / 1e9:.2f} GB per Ax vs 126 MB L2); no flush"},
+        "e2e": {"value": N * world / e2e_s / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * N,
+                "d2h_bytes_per_step": 8 * N, "api": "hxb_apply_A (host pointers, pinned)",
+                "ms_per_step": e2e_s * 1e3, "max_abs_diff_vs_device_path": e2e_parity},
+        "gpu_launches": launches,
+        "roofline": {"kernel": "ax_elem_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_ax,
+                     "avg_launch_ms": elem_avg_ms, "launches_timed": elem_n,
+                     "share_of_step": elem_ms / ms_total if ms_total else None,
+                     "ax_gather_avg_ms": gath_ms / max(1, gath_n),
+                     "whole_ax_gbs": bytes_ax / (ms_step * 1e-3) / 1e9},
+        "fdm": fdm,
+        "pcg": pcg,
+        "clocks": clocks,
+        "setup_s": setup_s,
+        "cpu_baseline": cpu,
+    }
+    plan.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--k", type=int, default=52)
+    ap.add_argument("--order", type=int, default=7)
+    ap.add_argument("--no-pcg", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local_rank = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -194,6 +194,17 @@ int hxb_bench_apply_A(hxb_plan* plan, int reps, double* ms_per_apply, double* ms
  * prolong, AMG solve. */
 int hxb_profile(hxb_plan* plan, int reps, double* out);
 
+/* Live kernel timing for the bench roofline: while enabled, the plan brackets
+ * each tagged launch on its main stream with a CUDA event pair (up to
+ * max_launches launches). _read sums the durations of one tag. The reference
+ * equivalent is the wall-clock counter of SemOperator::apply
+ * (operator.cpp:262,285-286), per kernel instead of per apply. */
+enum { HXB_KT_AX_ELEM = 0, HXB_KT_AX_GATHER = 1, HXB_KT_FDM = 2, HXB_KT_COMBINE = 3 };
+int hxb_kernel_timing(hxb_plan* plan, int enable, int max_launches);
+int hxb_kernel_timing_read(hxb_plan* plan, int tag, double* total_ms, int* count);
+/* Kernels the plan has enqueued since creation (coarse-graph nodes counted per launch). */
+int hxb_launch_count(hxb_plan* plan, int64_t* launches);
+
 /* Counter models (operator.cpp:20-37, fine.cpp:82-92). */
 uint64_t hxb_words_model(int64_t ne, int order, int variant);
 uint64_t hxb_flops_model(int64_t ne, int order);

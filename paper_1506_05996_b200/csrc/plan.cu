@@ -163,6 +163,14 @@ struct Plan {
   double* h_status = nullptr;  // pinned
   int hist_cap = 0;
 
+  // live kernel timing (bench roofline): event pairs around tagged launches on s_main
+  bool kt_on = false;
+  std::vector<cudaEvent_t> kt_ev;
+  std::vector<int> kt_tag;
+  std::size_t kt_used = 0;
+  long long launches = 0;      // kernels enqueued by the plan (graph nodes counted per launch)
+  int coarse_graph_nodes = 0;
+
   ~Plan()
   {
     if (coarse_exec) cudaGraphExecDestroy(coarse_exec);
@@ -171,6 +179,7 @@ struct Plan {
     if (s_main) cudaStreamDestroy(s_main);
     if (s_coarse) cudaStreamDestroy(s_coarse);
     if (h_status) cudaFreeHost(h_status);
+    for (cudaEvent_t e : kt_ev) cudaEventDestroy(e);
   }
 };
 
@@ -191,6 +200,27 @@ namespace {
     case 11: F<11>(__VA_ARGS__); break;                     \
     default: throw HxbError(HXB_EINVAL, "order out of range 1..10"); \
   }
+
+// tagged event pair around one launch (hxb_kernel_timing); no-op unless enabled
+struct KtScope {
+  Plan& pl;
+  cudaStream_t s;
+  bool on;
+  KtScope(Plan& p, int tag, cudaStream_t st) : pl(p), s(st), on(p.kt_on && p.kt_used + 2 <= p.kt_ev.size())
+  {
+    if (on) {
+      pl.kt_tag[pl.kt_used / 2] = tag;
+      HXB_CUDA(cudaEventRecord(pl.kt_ev[pl.kt_used], s));
+    }
+  }
+  ~KtScope()
+  {
+    if (on) {
+      cudaEventRecord(pl.kt_ev[pl.kt_used + 1], s);
+      pl.kt_used += 2;
+    }
+  }
+};
 
 DotArgs dot_args(Plan& pl, double* result, int offset = 0)
 {
@@ -260,7 +290,10 @@ void enqueue_ax(Plan& pl, const double* u, double* r, double* dot_result, cudaSt
     d1 = dot_args(pl, nullptr, 0);
     d2 = dot_args(pl, dot_result, g_elem);
   }
-  HXB_DISPATCH_NP(pl.np, launch_ax_elem, pl, u, r, d1, s);
+  {
+    KtScope kt(pl, HXB_KT_AX_ELEM, s);
+    HXB_DISPATCH_NP(pl.np, launch_ax_elem, pl, u, r, d1, s);
+  }
   AxGatherArgs g;
   g.rsurf = pl.rsurf;
   g.off = pl.ax_off;
@@ -270,7 +303,11 @@ void enqueue_ax(Plan& pl, const double* u, double* r, double* dot_result, cudaSt
   g.r = r;
   g.num_surface_global = pl.nsg;
   g.dot = d2;
-  ax_gather_kernel<<<gather_grid(pl.nsg), kGatherBlock, 0, s>>>(g);
+  {
+    KtScope kt(pl, HXB_KT_AX_GATHER, s);
+    ax_gather_kernel<<<gather_grid(pl.nsg), kGatherBlock, 0, s>>>(g);
+  }
+  pl.launches += 2;
 }
 
 template <int NP>
@@ -288,6 +325,8 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   a.ne = pl.ne;
   a.sstride = 2 * pl.nsurf;
   a.num_surface_global = pl.nsg;
+  KtScope kt(pl, HXB_KT_FDM, s);
+  pl.launches += 1;
   if (pl.fdm_eo)
     fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
   else
@@ -311,6 +350,8 @@ void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, b
   a.do_fine = do_fine ? 1 : 0;
   a.do_coarse = do_coarse ? 1 : 0;
   a.dot = zr_result ? dot_args(pl, zr_result) : DotArgs{};
+  KtScope kt(pl, HXB_KT_COMBINE, s);
+  pl.launches += 1;
   combine_kernel<<<gather_grid(pl.N), kGatherBlock, 0, s>>>(a);
 }
 
@@ -408,6 +449,9 @@ void capture_coarse_graph(Plan& pl)
   HXB_CUDA(cudaStreamBeginCapture(pl.s_coarse, cudaStreamCaptureModeThreadLocal));
   enqueue_coarse(pl, pl.s_coarse);
   HXB_CUDA(cudaStreamEndCapture(pl.s_coarse, &graph));
+  std::size_t nodes = 0;
+  HXB_CUDA(cudaGraphGetNodes(graph, nullptr, &nodes));
+  pl.coarse_graph_nodes = static_cast<int>(nodes);
   HXB_CUDA(cudaGraphInstantiate(&pl.coarse_exec, graph, 0));
   cudaGraphDestroy(graph);
 }
@@ -419,6 +463,7 @@ void enqueue_precond(Plan& pl, double* zr_result)
   if (pl.precond_mode == HXB_PRECOND_NONE) {
     copy_dot_kernel<kVecBlock><<<vec_grid(pl.N), kVecBlock, 0, s>>>(pl.r, pl.r, pl.z, pl.N,
                                                                      zr_result ? dot_args(pl, zr_result) : DotArgs{});
+    pl.launches += 1;
     return;
   }
   if (pl.do_coarse) {
@@ -426,6 +471,7 @@ void enqueue_precond(Plan& pl, double* zr_result)
     HXB_CUDA(cudaStreamWaitEvent(pl.s_coarse, pl.ev_fork, 0));
     HXB_CUDA(cudaGraphLaunch(pl.coarse_exec, pl.s_coarse));
     HXB_CUDA(cudaEventRecord(pl.ev_join, pl.s_coarse));
+    pl.launches += pl.coarse_graph_nodes;
   }
   if (pl.do_fine) HXB_DISPATCH_NP(pl.np, launch_fdm, pl, s);
   if (pl.do_coarse) HXB_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
@@ -781,6 +827,7 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
   HXB_CUDA(cudaEventRecord(pl.ev_t0, s));
   pcg_init_kernel<kVecBlock><<<vec_grid(n), kVecBlock, 0, s>>>(pl.b, pl.r, pl.u, n, dot_args(pl, pl.res2));
   sqrt_store_kernel<<<1, 1, 0, s>>>(pl.res2, pl.res_hist);
+  pl.launches += 2;
   HXB_CUDA(cudaMemcpyAsync(pl.h_status, pl.res_hist, sizeof(double), cudaMemcpyDeviceToHost, s));
   HXB_CUDA(cudaStreamSynchronize(s));
   const double r0 = pl.h_status[0];
@@ -789,12 +836,14 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
   if (r0 != 0.0) {
     enqueue_precond(pl, nullptr);
     copy_dot_kernel<kVecBlock><<<vec_grid(n), kVecBlock, 0, s>>>(pl.z, pl.r, pl.p, n, dot_args(pl, pl.zr_hist));
+    pl.launches += 1;
     status = HXB_PCG_MAX_ITERATIONS;
     for (int k = 0; k < cfg.max_iterations; ++k) {
       enqueue_ax(pl, pl.p, pl.f, pl.pf_hist + k, s);
       pcg_update_kernel<kVecBlock><<<vec_grid(n), kVecBlock, 0, s>>>(pl.f, pl.r, n, pl.zr_hist, pl.pf_hist, k,
                                                                      dot_args(pl, pl.res2));
       sqrt_store_kernel<<<1, 1, 0, s>>>(pl.res2, pl.res_hist + k + 1);
+      pl.launches += 2;
       HXB_CUDA(cudaMemcpyAsync(pl.h_status, pl.pf_hist + k, sizeof(double), cudaMemcpyDeviceToHost, s));
       HXB_CUDA(cudaMemcpyAsync(pl.h_status + 1, pl.res_hist + k + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
       HXB_CUDA(cudaStreamSynchronize(s));
@@ -812,15 +861,18 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
       if (rn / r0 <= cfg.rel_tolerance) {
         status = HXB_PCG_CONVERGED;
         pcg_final_kernel<<<vec_grid(n), kVecBlock, 0, s>>>(pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
+        pl.launches += 1;
         break;
       }
       if (k + 1 == cfg.max_iterations) {
         pcg_final_kernel<<<vec_grid(n), kVecBlock, 0, s>>>(pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
+        pl.launches += 1;
         diag = "not converged within " + std::to_string(cfg.max_iterations) + " iterations";
         break;
       }
       enqueue_precond(pl, pl.zr_hist + k + 1);
       pcg_dir_kernel<<<vec_grid(n), kVecBlock, 0, s>>>(pl.z, pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
+      pl.launches += 1;
     }
   }
   HXB_CUDA(cudaEventRecord(pl.ev_t1, s));
@@ -1146,6 +1198,56 @@ int hxb_bench_apply_A(hxb_plan* plan, int reps, double* ms_per_apply, double* ms
       *ms_elem_kernel = ms / reps;
     }
     HXB_CUDA(cudaGetLastError());
+  });
+}
+
+int hxb_kernel_timing(hxb_plan* plan, int enable, int max_launches)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    if (enable) {
+      if (max_launches < 1) throw HxbError(HXB_EINVAL, "max_launches must be >= 1");
+      const std::size_t want = 2 * static_cast<std::size_t>(max_launches);
+      while (pl->kt_ev.size() < want) {
+        cudaEvent_t e;
+        HXB_CUDA(cudaEventCreate(&e));
+        pl->kt_ev.push_back(e);
+      }
+      pl->kt_tag.assign(pl->kt_ev.size() / 2, -1);
+      pl->kt_used = 0;
+    }
+    pl->kt_on = enable != 0;
+  });
+}
+
+int hxb_kernel_timing_read(hxb_plan* plan, int tag, double* total_ms, int* count)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (!total_ms || !count) throw HxbError(HXB_EINVAL, "null argument");
+    HXB_CUDA(cudaSetDevice(pl->device));
+    HXB_CUDA(cudaStreamSynchronize(pl->s_main));
+    double ms = 0;
+    int c = 0;
+    for (std::size_t i = 0; 2 * i + 1 < pl->kt_used; ++i) {
+      if (pl->kt_tag[i] != tag) continue;
+      float m = 0;
+      HXB_CUDA(cudaEventElapsedTime(&m, pl->kt_ev[2 * i], pl->kt_ev[2 * i + 1]));
+      ms += m;
+      ++c;
+    }
+    *total_ms = ms;
+    *count = c;
+  });
+}
+
+int hxb_launch_count(hxb_plan* plan, int64_t* launches)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (!launches) throw HxbError(HXB_EINVAL, "null argument");
+    *launches = pl->launches;
   });
 }
 

@@ -97,6 +97,9 @@ SIGNATURES = {
     "hxb_amg_level": (C.c_int, [P, C.c_int, P, P, P, P, P, P]),
     "hxb_bench_apply_A": (C.c_int, [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "hxb_profile": (C.c_int, [P, C.c_int, P]),
+    "hxb_kernel_timing": (C.c_int, [P, C.c_int, C.c_int]),
+    "hxb_kernel_timing_read": (C.c_int, [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
+    "hxb_launch_count": (C.c_int, [P, C.POINTER(C.c_int64)]),
     "hxb_setup_create": (C.c_int, [C.POINTER(_Mesh), C.c_int, P, P, C.POINTER(_Options), C.POINTER(P)]),
     "hxb_setup_destroy": (None, [P]),
     "hxb_setup_info": (C.c_int, [P, C.POINTER(_PlanInfo)]),
@@ -413,6 +416,27 @@ class Plan:
         keys = ["ax_elem", "ax_gather", "fdm", "coarse", "combine", "precond", "pcg_update", "pcg_dir",
                 "restrict", "prolong", "amg"]
         return dict(zip(keys, out.tolist()))
+
+    KT_TAGS = {"ax_elem": 0, "ax_gather": 1, "fdm": 2, "combine": 3}
+
+    def kernel_timing(self, enable: bool, max_launches: int = 4096):
+        """Bracket tagged launches with CUDA events (hxb_kernel_timing)."""
+        _check(lib().hxb_kernel_timing(self._h, 1 if enable else 0, int(max_launches)))
+
+    def kernel_time(self, tag: str):
+        """(total ms, launches) of one tagged kernel since kernel_timing(True)."""
+        ms, cnt = C.c_double(), C.c_int()
+        _check(lib().hxb_kernel_timing_read(self._h, self.KT_TAGS[tag], C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _check(lib().hxb_launch_count(self._h, C.byref(n)))
+        return n.value
+
+    def apply_A_host_ptr(self, h_u: int, h_r: int):
+        """hxb_apply_A on raw (pinned) host pointers: H2D, Ax, D2H."""
+        _check(lib().hxb_apply_A(self._h, C.c_void_p(h_u), C.c_void_p(h_r)))
 
     def bench_apply_A(self, reps: int = 20):
         ms, ms_elem = C.c_double(), C.c_double()
