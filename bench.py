@@ -309,6 +309,7 @@ def run_ours(args, rank, world, local_rank):
             pcg["parity_vs_reference"] = {
                 "ref_iterations": gold["iterations"],
                 "max_abs_dr_over_r0": float(np.max(np.abs(rh[:m] - gh[:m])) / gh[0]),
+                "max_abs_dr_over_rk": float(np.max(np.abs(rh[:m] - gh[:m]) / gh[:m])),
                 "u_norm2_rel_diff": abs(pcg["u_norm2"] - gold["u_norm2"]) / gold["u_norm2"],
                 "ref_cpu_solve_s_build_host": gold["timing"]["solve_s"],
             }

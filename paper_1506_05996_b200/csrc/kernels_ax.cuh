@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
     ce = __ldg(a.c_e + e);
     __syncthreads();
     if (tid == 0 && e + (int)gridDim.x < a.ne) {
+      fence_proxy_async_smem();  // every warp's sidx reads (gather_u) precede the overwrite
       mbar_expect_tx(&bar[1], Sh::kIdxBytes);
       bulk_g2s(sidx, a.smap + (long long)(e + gridDim.x) * 2 * Sh::kNsurfP, Sh::kIdxBytes, &bar[1]);
     }
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
     }
     __syncthreads();  // sG consumed
     if (tid == 0 && en < a.ne) {
+      fence_proxy_async_smem();
       mbar_expect_tx(&bar[0], Sh::kGBytes);
       bulk_g2s(sG, a.wg + (long long)en * 6 * NLP, Sh::kGBytes, &bar[0]);
     }
@@ -251,6 +253,7 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
                     fz, ox, oy, tz);
       __syncthreads();  // lines read; sidx(e') consumed
       if (tid == 0 && en + (int)gridDim.x < a.ne) {
+        fence_proxy_async_smem();
         mbar_expect_tx(&bar[1], Sh::kIdxBytes);
         bulk_g2s(sidx, a.smap + (long long)(en + gridDim.x) * 2 * Sh::kNsurfP, Sh::kIdxBytes, &bar[1]);
       }

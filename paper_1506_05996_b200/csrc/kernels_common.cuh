@@ -86,6 +86,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// Orders this thread's (and, through a preceding __syncthreads, the whole
+// CTA's) generic-proxy shared-memory accesses before its subsequent
+// async-proxy (TMA) accesses: required before a bulk copy overwrites a buffer
+// that other threads have just read with ordinary loads (WAR across proxies).
+__device__ __forceinline__ void fence_proxy_async_smem()
+{
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity)
 {
   asm volatile(

@@ -18,15 +18,23 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))
 
 
-def history_parity(ours: dict, ref: dict, tol=1e-10, iters_slack=1):
-    """SURVEY §8c parity rule: iterations +-1, max_k |dr_k|/r_0 <= tol, rel-L2(u) <= tol."""
+def history_parity(ours: dict, ref: dict, tol=1e-10, iters_slack=1, per_rk=False):
+    """SURVEY §8c parity rule: iterations +-1, max_k |dr_k|/r_0 <= tol, rel-L2(u) <= tol.
+
+    per_rk=True judges each residual relative to itself, |dr_k|/r_k <= tol (the
+    north star's "per-iteration residuals within 1e-10 relative"); used at
+    cfg2, where early residuals exceed r_0 by 11x and the reference's own
+    sequential 48.6M-term norms carry ~6e-11 relative rounding."""
     assert ours["status"] == ref["status"], (ours["status"], ref["status"])
     assert abs(ours["iterations"] - ref["iterations"]) <= iters_slack, (ours["iterations"], ref["iterations"])
     ra, rb = np.asarray(ours["residual_history"]), np.asarray(ref["residual_history"])
     k = min(len(ra), len(rb))
     r0 = rb[0]
-    assert abs(ra[0] - r0) <= 1e-13 * r0
-    dr = float(np.max(np.abs(ra[:k] - rb[:k])) / r0)
+    assert abs(ra[0] - r0) <= tol * r0  # r_0 = ||b||: sequential vs tree summation of N terms
+    if per_rk:
+        dr = float(np.max(np.abs(ra[:k] - rb[:k]) / rb[:k]))
+    else:
+        dr = float(np.max(np.abs(ra[:k] - rb[:k])) / r0)
     assert dr <= tol, dr
     if ours.get("u") is not None:
         assert rel(ours["u"], ref["u"]) <= tol, rel(ours["u"], ref["u"])
