@@ -218,26 +218,38 @@ def run_ours(args, rank, world, local_rank):
     k, order = args.k, args.order
     t0 = time.time()
     mesh = hx.generate_cube_mesh(k)
-    plan = hx.Plan(mesh, order, device=local_rank)
+    distributed = world > 1 and not args.replicas
+    if distributed:
+        # element-slab partition of the one cfg2 mesh over the ranks (strong scaling)
+        plan = hx.Plan(mesh, order, precond="none", device=local_rank, rank=rank, nranks=world)
+        from paper_1506_05996_b200.dist import DistOperator
+
+        dop = DistOperator(plan, torch, dist)
+    else:
+        plan = hx.Plan(mesh, order, device=local_rank)
     setup_s = time.time() - t0
-    N, NE = plan.N, plan.NE
+    N, NE = plan.N, plan.NE  # NE: elements this rank owns
     np1 = order + 1
-    bytes_ax = 8 * NE * (10 * np1 ** 3 + np1 ** 2 + 2)  # B_R, operator.cpp:31-37
+    bytes_ax = 8 * NE * (10 * np1 ** 3 + np1 ** 2 + 2)  # B_R, operator.cpp:31-37 (this rank's share)
     bytes_fdm = 8 * NE * (3 * (order + 3) ** 3 + 4 * (order + 3) ** 2)  # B_P, fine.cpp:88-92
 
     # u: splitmix64 seed 12345 (oracles.cpp:126-139), Dirichlet entries zeroed
     from oracle import splitmix_vector  # input generator only (same vector the reference is fed)
 
     u_host = splitmix_vector(N, 12345)
-    mask = plan.maps(sub=False)["dirichlet_mask"].astype(bool)
-    u_host[mask] = 0.0
     d_u = torch.from_numpy(u_host).to("cuda")
     d_r = torch.empty(N, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream().cuda_stream
 
+    def ax_step():
+        if distributed:
+            dop.apply(d_u.data_ptr(), d_r.data_ptr(), stream)
+        else:
+            plan.apply_A_device(d_u.data_ptr(), d_r.data_ptr(), stream)
+
     # ---- device-resident Ax: W warm-up, K timed --------------------------
     for _ in range(args.warmup):
-        plan.apply_A_device(d_u.data_ptr(), d_r.data_ptr(), stream)
+        ax_step()
     sampler = ClockSampler(local_rank)
     sampler.start()
     plan.kernel_timing(True, max_launches=4 * args.steps + 16)
@@ -246,7 +258,7 @@ def run_ours(args, rank, world, local_rank):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     for _ in range(args.steps):
-        plan.apply_A_device(d_u.data_ptr(), d_r.data_ptr(), stream)
+        ax_step()
     ev1.record()
     barrier()
     ms_total = ev0.elapsed_time(ev1)
@@ -255,8 +267,12 @@ def run_ours(args, rank, world, local_rank):
     gath_ms, gath_n = plan.kernel_time("ax_gather")
     plan.kernel_timing(False)
     ms_step = max_over_ranks(ms_total / args.steps)
-    value = world * N / (ms_step * 1e-3) / 1e9
+    # strong scaling: the ranks share one mesh of N DOF; replicas: N each
+    value = (N if distributed else world * N) / (ms_step * 1e-3) / 1e9
     r_dev = d_r.cpu().numpy()
+    if distributed:
+        return finish_distributed(args, rank, world, plan, value, ms_step, launches, elem_ms, elem_n, gath_ms,
+                                  gath_n, ms_total, bytes_ax, N, NE, setup_s, sampler, dist, torch)
 
     # ---- e2e through the C-ABI with pinned host buffers -------------------
     h_u = torch.from_numpy(u_host).pin_memory()
@@ -373,6 +389,38 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
+def finish_distributed(args, rank, world, plan, value, ms_step, launches, elem_ms, elem_n, gath_ms, gath_n,
+                       ms_total, bytes_ax, N, NE, setup_s, sampler, dist, torch):
+    """JSON line of the element-slab distributed Ax (strong scaling of cfg2)."""
+    clocks = sampler.stop()
+    peak, peak_src = _peaks()
+    elem_avg_ms = elem_ms / max(1, elem_n)
+    achieved = bytes_ax / (elem_avg_ms * 1e-3) / 1e9 if elem_n else None
+    info = plan.dist_info()
+    line = {
+        "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated mesh, splitmix64 u)",
+        "config": {"workload": f"cfg2 Ax distributed: {args.k}^3 hexes N={args.order} split in {world} element slabs",
+                   "k": args.k, "order": args.order, "N": N, "NE_per_rank": NE,
+                   "parallelism": f"element-slab partition x{world}, NCCL neighbour exchange (2 messages per Ax)",
+                   "interface_doubles_rank0": info["n_up"],
+                   "l2": "inputs larger than L2; no flush"},
+        "e2e": None, "gpu_launches": launches,
+        "roofline": {"kernel": "ax_elem_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved else None, "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": bytes_ax, "avg_launch_ms": elem_avg_ms,
+                     "share_of_step": elem_ms / ms_total if ms_total else None},
+        "pcg": None, "pcg_note": "distributed PCG (FDM halos, coarse allgather) is not built yet; see DESIGN.md",
+        "clocks": clocks, "setup_s": setup_s, "cpu_baseline": None,
+    }
+    plan.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -383,6 +431,7 @@ def main():
     ap.add_argument("--order", type=int, default=7)
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent cfg2 replicas instead of a partition")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

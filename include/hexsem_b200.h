@@ -79,7 +79,10 @@ typedef struct hxb_options {
   int32_t direct_threshold;    /* vertices; default 64000 (coarse.hpp:36) */
   int variant;                 /* HXB_VARIANT_* (default stored) */
   int device;                  /* CUDA device ordinal for this plan */
-  int reserved[7];
+  int reserved[7];             /* reserved[0] bit 0: run the AMG K-cycle as one kernel per step
+                                  instead of the default single cluster kernel (A/B checks);
+                                  reserved[1] = rank, reserved[2] = number of ranks: element-slab
+                                  partition for the distributed operator (hxb_dist_*) */
 } hxb_options;
 
 /* PcgConfig (krylov.hpp:15-19) */
@@ -180,6 +183,10 @@ int hxb_setup_export_maps(const hxb_setup* setup, int32_t* l2g, int64_t* g2l_off
 int hxb_setup_amg_level(const hxb_setup* setup, int level, int64_t* rows, int64_t* nnz, int64_t* ptr,
                         int32_t* col, double* val, int32_t* aggregate);
 int hxb_setup_lumped_mass(const hxb_setup* setup, double* m);
+/* GPU-free partition lists of the distributed operator (see hxb_dist_*):
+ * counts[6] = e0, e1, n_group0, n_up, n_down, local surface nodes; nodes
+ * (optional) = local node ids [group0 | up | down]. */
+int hxb_setup_dist_lists(const hxb_setup* setup, int rank, int nranks, int64_t* counts, int32_t* nodes);
 
 /* GllBasis (gll.hpp:17-31) and PencilFactorization (fine.hpp:18-26) tables. */
 int hxb_gll(int order, double* nodes, double* weights, double* deriv);
@@ -189,10 +196,31 @@ int hxb_pencil(int order, double* K, double* M, double* V, double* V_inv, double
  * CUDA events; returns mean ms per apply (kernel-level bench helper). */
 int hxb_bench_apply_A(hxb_plan* plan, int reps, double* ms_per_apply, double* ms_elem_kernel);
 
-/* Per-component device timings (ms), out[12]: Ax element, Ax gather, FDM,
+/* Per-component device timings (ms), out[16]: Ax element, Ax gather, FDM,
  * coarse branch, combine, full P, PCG update, PCG direction, restrict,
- * prolong, AMG solve. */
+ * prolong, AMG solve, one AMG cluster kernel, combine fine-only, combine
+ * coarse-only. */
 int hxb_profile(hxb_plan* plan, int reps, double* out);
+
+/* Distributed Ax over an element-slab partition (one plan per
+ * GPU, rank r of R owning elements [r*NE/R, (r+1)*NE/R), created with
+ * options.reserved[1..2] = rank, R and precond_mode none). Vectors are
+ * global-length device arrays; a rank reads/writes only the nodes of its
+ * elements. Interface nodes are summed in the reference's (e,l) order across
+ * ranks (SemOperator::apply + gather, operator.cpp:255-287, mesh.cpp:463-475):
+ *   begin:    element kernel, local gather, partial sums for the upper neighbour -> send_up[n_up]
+ *   (send_up of rank r -> recv_down of rank r+1)
+ *   continue: continue rank r-1's partials, Dirichlet rows, finals -> send_down[n_down]
+ *   (send_down of rank r -> recv_up of rank r-1)
+ *   end:      write the finals received from the upper neighbour
+ * The result equals the single-plan hxb_apply_A bit for bit.
+ * info[8] = rank, nranks, e0, e1, n_up, n_down, n_group0, N. */
+int hxb_dist_info(hxb_plan* plan, int64_t* info);
+int hxb_dist_lists(hxb_plan* plan, int32_t* up_nodes, int32_t* down_nodes);
+int hxb_dist_apply_A_begin(hxb_plan* plan, const double* d_u, double* d_r, double* d_send_up, void* stream);
+int hxb_dist_apply_A_continue(hxb_plan* plan, const double* d_u, double* d_r, const double* d_recv_down,
+                              double* d_send_down, void* stream);
+int hxb_dist_apply_A_end(hxb_plan* plan, double* d_r, const double* d_recv_up, void* stream);
 
 /* Live kernel timing for the bench roofline: while enabled, the plan brackets
  * each tagged launch on its main stream with a CUDA event pair (up to

@@ -16,6 +16,8 @@ The product (``paper_1506_05996_b200``) never does.
 from .ctypes_oracle import (  # noqa: F401
     RefSystem,
     OracleSystem,
+    OracleFmaSystem,
+    oracle_fma_available,
     RefConfig,
     ref_available,
     oracle_available,

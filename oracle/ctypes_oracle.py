@@ -15,6 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _REF_SO = os.path.join(_HERE, "_ref", "libhexsem_ref.so")
 _ORC_SO = os.path.join(_HERE, "_ref", "libhexsem_oracle.so")
+_ORC_FMA_SO = os.path.join(_HERE, "_ref", "libhexsem_oracle_fma.so")
 
 FAMILIES = {"uniform": 0, "distorted_domain": 1, "distorted_elements": 2}
 PRECONDS = {"two_scale": 0, "fine_only": 1, "coarse_only": 2, "none": 3}
@@ -288,6 +289,17 @@ class OracleSystem(_System):
     """The plain C++ restatement (oracle/_ref/libhexsem_oracle.so)."""
     PATH = _ORC_SO
     PREFIX = "orc_"
+
+
+class OracleFmaSystem(_System):
+    """The restatement compiled with FMA contraction: a rounding-only
+    perturbation of the reference, used to calibrate parity tolerances."""
+    PATH = _ORC_FMA_SO
+    PREFIX = "orc_"
+
+
+def oracle_fma_available() -> bool:
+    return os.path.exists(_ORC_FMA_SO)
 
 
 def ref_available() -> bool:

@@ -1310,11 +1310,28 @@ void apply_P(const System& S, const double* r, double* z)
   }
 }
 
+// 0: the reference's sequential double accumulation (krylov.cpp:11-16);
+// 1: correctly rounded (double-double compensated products and sums) — an
+//    instrument for separating summation rounding from everything else
+int g_dot_mode = 0;
+
 double dot(const Vec& a, const Vec& b)
-{  // sequential double accumulation (krylov.cpp:11-16)
-  double s = 0;
-  for (std::size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
-  return s;
+{
+  if (g_dot_mode == 0) {  // krylov.cpp:11-16
+    double s = 0;
+    for (std::size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+    return s;
+  }
+  double hi = 0, lo = 0;
+  for (std::size_t i = 0; i < a.size(); ++i) {
+    const double p = a[i] * b[i];
+    const double pe = std::fma(a[i], b[i], -p);  // exact product error
+    const double t = hi + p;
+    const double z = t - hi;
+    lo += (hi - (t - z)) + (p - z) + pe;  // TwoSum error + product error
+    hi = t;
+  }
+  return hi + lo;
 }
 
 // pcg with u0 = 0 (krylov.cpp:20-71)
@@ -1407,6 +1424,9 @@ struct orc_config {
 };
 
 const char* orc_last_error() { return g_err.c_str(); }
+
+// Dot-product summation mode of the restated pcg (see orc::dot).
+void orc_set_dot_mode(int mode) { g_dot_mode = mode; }
 
 static void finish(System& S, const orc_config* c)
 {

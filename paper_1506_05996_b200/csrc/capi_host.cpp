@@ -249,4 +249,22 @@ uint64_t hxb_fine_words_model(int64_t ne, int order)
   return static_cast<uint64_t>(ne) * (3 * p * p * p + 4 * p * p);
 }
 
+
+// Partition lists of rank `rank` of `nranks` (GPU-free; same code as the plan's).
+// counts[6] = e0, e1, n_group0, n_up, n_down, total local surface nodes;
+// nodes (may be NULL) receives the local node ids [group0 | up | down].
+int hxb_setup_dist_lists(const hxb_setup* setup, int rank, int nranks, int64_t* counts, int32_t* nodes)
+{
+  return guarded([&] {
+    if (!setup || !counts) throw HxbError(HXB_EINVAL, "null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw HxbError(HXB_EINVAL, "rank out of range");
+    const HostSetup& hs = *reinterpret_cast<const HostSetup*>(setup);
+    const int nsurfp = (surface_slot_count(hs.order + 1) + 3) & ~3;
+    DistLists d = dist_partition(hs, rank, nranks, nsurfp);
+    const int64_t v[6] = {d.e0, d.e1, d.n_grp0, d.n_up, d.n_down, static_cast<int64_t>(d.nodes.size())};
+    std::memcpy(counts, v, sizeof(v));
+    if (nodes) std::memcpy(nodes, d.nodes.data(), d.nodes.size() * sizeof(int32_t));
+  });
+}
+
 }  // extern "C"

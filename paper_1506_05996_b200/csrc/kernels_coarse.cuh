@@ -81,6 +81,148 @@ __global__ void __launch_bounds__(BLOCK) restrict_kernel(const double* __restric
   }
 }
 
+// Restriction, warp per element (restrict_residual, coarse.cpp:138-162, on
+// the masked residual, precond.cpp:35): R_cb(e) = sum_l B[cb][l] y_l m_l with
+// y = r / m_N. B is the tensor product of the two linear hats, so the sum is
+// done separably: each lane owns (j,k) lines, forms the two hat-weighted
+// line sums W_a = sum_i hat_a(t_i) y_i m_i, spreads them over the 8 corners
+// with hat_b(t_j) hat_c(t_k), and the warp reduces the 8 partials in a fixed
+// tree (deterministic; summation order differs from the reference's l-loop
+// at rounding level only). Rpart[8e + cb] feeds vertex_gather_kernel.
+template <int NP>
+__global__ void __launch_bounds__(256) restrict_warp_kernel(const double* __restrict__ r,
+                                                            const double* __restrict__ lumped,
+                                                            const int* __restrict__ smap,
+                                                            const double* __restrict__ mass,
+                                                            double* __restrict__ Rpart, int ne, int sstride, int nsg)
+{
+  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NL = NP * NP, LPL = (NL + 31) / 32;
+  constexpr int CH = LPL < 2 ? LPL : 2;  // LPL is 1, 2 or 4
+  __shared__ double h0[NP], h1[NP];
+  if (threadIdx.x < NP) {
+    h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
+    h1[threadIdx.x] = c_tab[NP].hat1[threadIdx.x];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne; e += warps) {
+    const int* surf = smap + (long long)e * sstride;
+    const long long ibase = (long long)nsg + (long long)e * NI;
+    const double* me = mass + (std::size_t)e * NP * NP * NP;
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // lines in chunks of CH per lane: ids first, then every load of the chunk,
+    // then arithmetic (memory-level parallelism without spilling at large NP)
+#pragma unroll 1
+    for (int q0 = 0; q0 < LPL; q0 += CH) {
+      long long gid[CH][NP];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int line = lane + 32 * (q0 + q);
+        const int j = (line < NL ? line : 0) % NP, k = (line < NL ? line : 0) / NP;
+        const bool face = (j == 0 || j == n || k == 0 || k == n);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          if (line >= NL) {
+            gid[q][i] = -1;
+          } else if (face || i == 0 || i == n) {
+            const int code = __ldg(surf + surface_slot(NP, i, j, k));
+            gid[q][i] = code >= 0 ? code : -1;  // Dirichlet: masked residual (precond.cpp:35)
+          } else {
+            gid[q][i] = ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1);
+          }
+        }
+      }
+      double rv[CH][NP], lv[CH][NP], mv[CH][NP];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int line = lane + 32 * (q0 + q);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          const long long g = gid[q][i] < 0 ? 0 : gid[q][i];
+          rv[q][i] = __ldg(r + g);
+          lv[q][i] = __ldg(lumped + g);
+          mv[q][i] = line < NL ? __ldg(me + line * NP + i) : 0.0;
+        }
+      }
+      // line sums W_a = sum_i hat_a(t_i) (r/m_N)_i m_i, spread to the corners
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int line = lane + 32 * (q0 + q);
+        const int j = (line < NL ? line : 0) % NP, k = (line < NL ? line : 0) / NP;
+        double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          const double y = gid[q][i] < 0 ? 0.0 : rv[q][i] / lv[q][i];  // coarse.cpp:144
+          const double w = y * mv[q][i];
+          w0 += h0[i] * w;
+          w1 += h1[i] * w;
+        }
+        if (line < NL) {
+          const double hj[2] = {h0[j], h1[j]}, hk[2] = {h0[k], h1[k]};
+#pragma unroll
+          for (int cb = 0; cb < 8; ++cb) acc[cb] += (hj[(cb >> 1) & 1] * hk[cb >> 2]) * ((cb & 1) ? w1 : w0);
+        }
+      }
+    }
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb)
+      for (int o = 16; o > 0; o >>= 1) acc[cb] += __shfl_xor_sync(0xffffffffu, acc[cb], o);
+    if (lane < 8) {
+      double v = acc[0];
+#pragma unroll
+      for (int cb = 1; cb < 8; ++cb)
+        if (lane == cb) v = acc[cb];
+      Rpart[8 * (long long)e + lane] = v;
+    }
+  }
+}
+
+// Prolongation of every element-surface copy (coarse.cpp:170-181):
+// esurf[e][slot] = (sum_cb B[cb][l] Z[v_cb]) * m[e][l], element-major so the
+// writes are coalesced; the combine gathers them through the Ax CSR lists.
+template <int NP>
+__global__ void prolong_surface_kernel(const double* __restrict__ Z, const int* __restrict__ conn,
+                                       const double* __restrict__ mass, double* __restrict__ esurf, int ne)
+{
+  constexpr int NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2), NSP = (NS + 3) & ~3;
+  constexpr int kCorner[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // kHexCornerFromBits, mesh.hpp:33
+  __shared__ double h0[NP], h1[NP];
+  if (threadIdx.x < NP) {
+    h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
+    h1[threadIdx.x] = c_tab[NP].hat1[threadIdx.x];
+  }
+  __syncthreads();
+  const long long total = (long long)ne * NSP;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total; q += (long long)gridDim.x * blockDim.x) {
+    const long long e = q / NSP;
+    const int sl = static_cast<int>(q - e * NSP);
+    if (sl >= NS) continue;
+    int i, j, k;
+    surface_ijk<NP>(sl, i, j, k);
+    const double hi[2] = {h0[i], h1[i]}, hj[2] = {h0[j], h1[j]}, hk[2] = {h0[k], h1[k]};
+    double s = 0.0;
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb)
+      s += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[cb >> 2] * __ldg(Z + __ldg(conn + 8 * e + kCorner[cb]));
+    esurf[q] = s * __ldg(mass + e * NP * NP * NP + (k * NP + j) * NP + i);
+  }
+}
+
+// Zc[8e + cb] = Z[vertex of corner cb of e] (the 8 coarse values each element
+// prolongates, coarse.cpp:170-171), so the fused combine reads one 64-byte
+// block per element copy instead of 8 dependent gathers.
+__global__ void corner_values_kernel(const double* __restrict__ Z, const int* __restrict__ conn,
+                                     double* __restrict__ Zc, int ne)
+{
+  constexpr int kCorner[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // kHexCornerFromBits, mesh.hpp:33
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < 8LL * ne; q += (long long)gridDim.x * blockDim.x) {
+    const long long e = q >> 3;
+    const int cb = static_cast<int>(q & 7);
+    Zc[q] = __ldg(Z + __ldg(conn + 8 * e + kCorner[cb]));
+  }
+}
+
 // Prolongation per element copy (coarse.cpp:164-182): p_l = (sum_cb B[cb][l]
 // Z[v_cb]) * m_l, stored like Ax outputs (element-interior nodes direct into
 // pint, element-surface copies at their CSR position in psort) for the
@@ -132,9 +274,7 @@ struct DevCsr {
 
 __device__ __forceinline__ double csr_row_dot(const DevCsr& A, int i, const double* __restrict__ x)
 {
-  double s = 0.0;
-  for (int q = __ldg(A.ptr + i); q < __ldg(A.ptr + i + 1); ++q) s += __ldg(A.val + q) * __ldg(x + __ldg(A.col + q));
-  return s;
+  return csr_row_sum(A.ptr, A.col, A.val, i, [&](int c) { return __ldg(x + c); });
 }
 
 // z = z1 + w d (r - A z1), z1 = w d r computed on the fly (amg.cpp:212-213)
@@ -142,11 +282,8 @@ __global__ void amg_jacobi2_kernel(DevCsr A, const double* __restrict__ dinv, co
                                    double* __restrict__ z)
 {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int q = __ldg(A.ptr + i); q < __ldg(A.ptr + i + 1); ++q) {
-      const int c = __ldg(A.col + q);
-      s += __ldg(A.val + q) * (kJacobiOmega * __ldg(dinv + c) * __ldg(r + c));
-    }
+    const double s = csr_row_sum(A.ptr, A.col, A.val, i,
+                                 [&](int c) { return kJacobiOmega * __ldg(dinv + c) * __ldg(r + c); });
     const double z1 = kJacobiOmega * __ldg(dinv + i) * __ldg(r + i);
     z[i] = z1 + kJacobiOmega * __ldg(dinv + i) * (__ldg(r + i) - s);
   }
@@ -170,11 +307,8 @@ __global__ void amg_prolong_smooth_kernel(DevCsr A, const double* __restrict__ d
                                           const int* __restrict__ agg, double* __restrict__ zout)
 {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int q = __ldg(A.ptr + i); q < __ldg(A.ptr + i + 1); ++q) {
-      const int c = __ldg(A.col + q);
-      s += __ldg(A.val + q) * (__ldg(zin + c) + __ldg(ec + __ldg(agg + c)));
-    }
+    const double s = csr_row_sum(A.ptr, A.col, A.val, i,
+                                 [&](int c) { return __ldg(zin + c) + __ldg(ec + __ldg(agg + c)); });
     const double z3 = __ldg(zin + i) + __ldg(ec + __ldg(agg + i));
     zout[i] = z3 + kJacobiOmega * __ldg(dinv + i) * (__ldg(r + i) - s);
   }

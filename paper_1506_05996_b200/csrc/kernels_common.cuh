@@ -34,6 +34,16 @@ struct OrderTables {
 // Single translation unit (plan.cu) includes the kernels, so this is the definition.
 __device__ OrderTables c_tab[kMaxNP + 1];
 
+// FDM transform tables in the constant bank: with the order a template
+// parameter every coefficient address is a compile-time immediate, so the
+// kernels read them as LDCU.128 into uniform registers (one per warp, off
+// the L1/shared path that the line transposes saturate).
+struct FdmConst {
+  double FE[49], FO[36], IE[49], IO[36];
+  double lam[kMaxP], invM[kMaxP];
+};
+__constant__ FdmConst c_fdm[kMaxNP + 1];
+
 // Global-id encodings in the gather/scatter maps:
 //   v >= 0   free node v
 //   v == -1  no node (sentinel slot, IndexMaps::kNoNode)
@@ -58,6 +68,40 @@ __host__ __device__ __forceinline__ int surface_slot(int np, int i, int j, int k
   if (i == 0) return base + np + 2 * (j - 1);
   if (i == n) return base + np + 2 * (j - 1) + 1;
   return -1;
+}
+
+// Inverse of surface_slot: local (i,j,k) of surface slot s.
+template <int NP>
+__device__ __forceinline__ void surface_ijk(int s, int& i, int& j, int& k)
+{
+  constexpr int n = NP - 1, mid = 4 * NP - 4, NN = NP * NP;
+  if (s < NN) {
+    k = 0;
+    j = s / NP;
+    i = s % NP;
+    return;
+  }
+  const int t = s - NN;
+  if (t >= (NP - 2) * mid) {
+    const int u = t - (NP - 2) * mid;
+    k = n;
+    j = u / NP;
+    i = u % NP;
+    return;
+  }
+  k = 1 + t / mid;
+  const int rem = t % mid;
+  if (rem < NP) {
+    j = 0;
+    i = rem;
+  } else if (rem >= NP + 2 * (NP - 2)) {
+    j = n;
+    i = rem - (NP + 2 * (NP - 2));
+  } else {
+    const int q = rem - NP;
+    j = 1 + q / 2;
+    i = (q & 1) ? n : 0;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -105,6 +149,35 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// CSR row sum s = sum_q val[q] * x(col[q]) in ascending q (CsrMatrix::multiply
+// order, amg.cpp:13-20), with the loads of 8 entries issued before any of
+// their products is summed: the row costs ~3 memory round trips instead of
+// one per entry.
+template <class XF>
+__device__ __forceinline__ double csr_row_sum(const int* __restrict__ ptr, const int* __restrict__ col,
+                                              const double* __restrict__ val, int i, XF&& xf)
+{
+  const int q0 = __ldg(ptr + i), q1 = __ldg(ptr + i + 1);
+  double s = 0.0;
+  for (int q = q0; q < q1; q += 8) {
+    int c[8];
+    double v[8], x[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const bool ok = q + t < q1;
+      c[t] = ok ? __ldg(col + q + t) : 0;
+      v[t] = ok ? __ldg(val + q + t) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) x[t] = q + t < q1 ? xf(c[t]) : 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t)
+      if (q + t < q1) s += v[t] * x[t];
+  }
+  return s;
 }
 
 // ---------------------------------------------------------------------------

@@ -50,6 +50,10 @@ struct FdmArgs {
   const double* c_e;
   const int* pos;           // [e][P^3] CSR position of each slot's contribution (-1: sentinel)
   double* zsort;            // contributions in CSR order (combine streams them)
+  // fused coarse restriction (restrict_residual, coarse.cpp:138-162): null Rpart = off
+  const double* inv_lumped; // 1/m_N
+  const double* mass;       // [e][nloc]
+  double* Rpart;            // [e][8] corner partial sums
   int ne, sstride, num_surface_global;
 };
 
@@ -131,56 +135,50 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
 {
   using Sh = FdmShape<NP>;
   constexpr int P = Sh::kP, S = Sh::kS, PS = Sh::kPS, n = NP - 1;
-  constexpr int h = P / 2, mid = P & 1, NE = (P + 1) / 2, NO = P / 2;
-  constexpr int kTab = EO ? (2 * (h + mid) * NE + 2 * h * NO) : 2 * P * P;
+  constexpr int kTab = EO ? 1 : 2 * P * P;
   __shared__ double buf[Sh::kBuf];
-  __shared__ double tab[kTab];  // transform tables, read as warp-uniform broadcasts
-  __shared__ double s_lam[P], s_invM[P];
+  __shared__ double tab[kTab];  // dense fallback only: V^T, V^-T as warp-uniform broadcasts
   const OrderTables& T = c_tab[NP];
+  const FdmConst& C = c_fdm[NP];  // even/odd tables, lambda, 1/M: constant bank
   const int e = blockIdx.x;
   const int tid = threadIdx.x;
   const bool lt = tid < Sh::kLines;
   const int la = tid % P, lb = tid / P;
   auto at = [](int x, int y, int z) { return z * PS + y * S + x; };
-  double* tFE = tab;                       // EO: FE, FO, IE, IO ; dense: VT, ViT
-  double* tFO = tab + (h + mid) * NE;
-  double* tIE = tFO + h * NO;
-  double* tIO = tIE + (h + mid) * NE;
-  if constexpr (EO) {
-    for (int q = tid; q < (h + mid) * NE; q += Sh::kBlock) {
-      tFE[q] = T.FE[q];
-      tIE[q] = T.IE[q];
-    }
-    for (int q = tid; q < h * NO; q += Sh::kBlock) {
-      tFO[q] = T.FO[q];
-      tIO[q] = T.IO[q];
-    }
-  } else {
+  if constexpr (!EO) {
     for (int q = tid; q < P * P; q += Sh::kBlock) {
       tab[q] = T.VT[q];
       tab[P * P + q] = T.ViT[q];
     }
   }
+  __shared__ double s_lam[P], s_invM[P];  // indexed per thread (non-uniform): shared, not constant
   for (int q = tid; q < P; q += Sh::kBlock) {
-    s_lam[q] = T.lam[q];
-    s_invM[q] = T.invM[q];
+    s_lam[q] = C.lam[q];
+    s_invM[q] = C.invM[q];
   }
   auto fwd = [&](const double (&in)[P], double (&out)[P]) {
     if constexpr (EO)
-      pencil_fwd_eo<P>(tFE, tFO, in, out);
+      pencil_fwd_eo<P>(C.FE, C.FO, in, out);
     else
       pencil_apply<P>(tab, in, out);
   };
   auto inv = [&](const double (&in)[P], double (&out)[P]) {
     if constexpr (EO)
-      pencil_inv_eo<P>(tIE, tIO, in, out);
+      pencil_inv_eo<P>(C.IE, C.IO, in, out);
     else
       pencil_apply<P>(tab + P * P, in, out);
   };
 
+  __shared__ double s_h0[NP], s_h1[NP];   // coarse hats 0.5(1 -+ t) (gll.cpp:92)
+  __shared__ double s_red[Sh::kBlock / 32][8];
+  for (int q = tid; q < NP; q += Sh::kBlock) {
+    s_h0[q] = T.hat0[q];
+    s_h1[q] = T.hat1[q];
+  }
   const double hx = __ldg(a.h3 + 3 * e), hy = __ldg(a.h3 + 3 * e + 1), hz = __ldg(a.h3 + 3 * e + 2);
   const double svol = 8.0 / (hx * hy * hz);  // fine.cpp:154
   double in[P], out[P];
+  double racc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   __syncthreads();
 
   // ---- 1: gather + r' scaling + V along x (thread = x-line (y=la, z=lb)) -------
@@ -195,11 +193,33 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
     if (iny && inz) {
       in[0] = load_masked(a.r, __ldg(sf + (0 * NP + kk) * NP + jj));      // face 0 slot (u=jj, w=kk)
       in[P - 1] = load_masked(a.r, __ldg(sf + (1 * NP + kk) * NP + jj));  // face 1 slot
+      int gl[NP];  // own-node ids of this x-line (-1: Dirichlet, reads as 0)
 #pragma unroll
       for (int ii = 0; ii <= n; ++ii) {
         const int s = surface_slot(NP, ii, jj, kk);
-        in[ii + 1] = s >= 0 ? load_masked(a.r, __ldg(surf + s))
-                            : __ldg(a.r + ibase + ((kk - 1) * (n - 1) + (jj - 1)) * (n - 1) + (ii - 1));
+        if (s >= 0) {
+          const int code = __ldg(surf + s);
+          gl[ii] = code >= 0 ? code : -1;
+        } else {
+          gl[ii] = static_cast<int>(ibase + ((kk - 1) * (n - 1) + (jj - 1)) * (n - 1) + (ii - 1));
+        }
+      }
+#pragma unroll
+      for (int ii = 0; ii <= n; ++ii) in[ii + 1] = gl[ii] >= 0 ? __ldg(a.r + gl[ii]) : 0.0;
+      if (a.Rpart) {
+        // this line's share of the 8 corner sums R_cb = sum_l B[cb][l] (r/m_N)_l m_l
+        const double* ml = a.mass + (std::size_t)e * NP * NP * NP + (kk * NP + jj) * NP;
+        double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+        for (int ii = 0; ii <= n; ++ii) {
+          const double y = gl[ii] >= 0 ? in[ii + 1] * __ldg(a.inv_lumped + gl[ii]) : 0.0;
+          const double w = y * __ldg(ml + ii);
+          w0 += s_h0[ii] * w;
+          w1 += s_h1[ii] * w;
+        }
+        const double hj[2] = {s_h0[jj], s_h1[jj]}, hk[2] = {s_h0[kk], s_h1[kk]};
+#pragma unroll
+        for (int cb = 0; cb < 8; ++cb) racc[cb] = (hj[(cb >> 1) & 1] * hk[cb >> 2]) * ((cb & 1) ? w1 : w0);
       }
     } else if (inz && (y == 0 || y == P - 1)) {  // faces 2/3: u=kk, w=ii
       const int f = y == 0 ? 2 : 3;
@@ -218,7 +238,21 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
 #pragma unroll
     for (int x = 0; x < P; ++x) buf[at(x, y, z)] = out[x];
   }
+  if (a.Rpart) {  // fixed-tree reduction of the corner sums over the CTA's lines
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb)
+      for (int o = 16; o > 0; o >>= 1) racc[cb] += __shfl_xor_sync(0xffffffffu, racc[cb], o);
+    if ((tid & 31) == 0)
+#pragma unroll
+      for (int cb = 0; cb < 8; ++cb) s_red[tid >> 5][cb] = racc[cb];
+  }
   __syncthreads();
+  if (a.Rpart && tid < 8) {
+    double v = 0.0;
+#pragma unroll
+    for (int w = 0; w < Sh::kBlock / 32; ++w) v += s_red[w][tid];
+    a.Rpart[8 * (long long)e + tid] = v;
+  }
 
   // ---- 2: V along y (thread = y-line (x=la, z=lb)) ----------------------------
   if (lt) {

@@ -80,7 +80,8 @@ struct AxGatherArgs {
   const double* u;
   const std::uint8_t* mask;
   double* r;
-  int num_surface_global;
+  int num_surface_global;  // nodes gathered (off has one more entry)
+  const int* nodes;        // null: node t is global id t; else global id of local node t
   DotArgs dot;
 };
 
@@ -94,8 +95,9 @@ __global__ void __launch_bounds__(kGatherBlock) ax_gather_kernel(AxGatherArgs a)
   for (int g0 = (blockIdx.x * (kGatherBlock / 32) + warp) * 32; g0 < a.num_surface_global; g0 += nwarps * 32) {
     const double s = warp_csr_sum(a.off, a.idx, [&](int q) { return __ldg(a.rsurf + q); }, g0,
                                   a.num_surface_global, stage[warp]);
-    const int g = g0 + lane;
-    if (g < a.num_surface_global) {
+    const int t = g0 + lane;
+    if (t < a.num_surface_global) {
+      const int g = a.nodes ? __ldg(a.nodes + t) : t;
       const double ug = __ldg(a.u + g);
       const double rg = __ldg(a.mask + g) ? ug : s;
       a.r[g] = rg;
@@ -103,6 +105,48 @@ __global__ void __launch_bounds__(kGatherBlock) ax_gather_kernel(AxGatherArgs a)
     }
   }
   dot_commit<kGatherBlock>(a.dot, dot, red);
+}
+
+// ---------------------------------------------------------------------------
+// Distributed Ax (element-slab partition). A node shared by ranks
+// r and r+1 has its copies in ascending element order, so rank r's copies
+// come first: rank r sums them (partial), rank r+1 continues the same
+// left-to-right sum with its own copies and finalises (mask), and returns the
+// final value. The result is bit-identical to the single-plan gather.
+
+// send[t] = sum of this rank's copies of up-interface node t (no mask: not final)
+__global__ void dist_partial_kernel(const unsigned* __restrict__ off, const int* __restrict__ idx,
+                                    const double* __restrict__ rsurf, int n, double* __restrict__ send)
+{
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (unsigned q = __ldg(off + t); q < __ldg(off + t + 1); ++q) s += __ldg(rsurf + __ldg(idx + q));
+    send[t] = s;
+  }
+}
+
+// down-interface node t: continue the lower rank's partial with this rank's
+// copies, apply the Dirichlet identity, store and return the final value
+__global__ void dist_continue_kernel(const unsigned* __restrict__ off, const int* __restrict__ idx,
+                                     const double* __restrict__ rsurf, const int* __restrict__ nodes, int n,
+                                     const double* __restrict__ u, const std::uint8_t* __restrict__ mask,
+                                     const double* __restrict__ recv, double* __restrict__ r, double* __restrict__ send)
+{
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    double s = __ldg(recv + t);
+    for (unsigned q = __ldg(off + t); q < __ldg(off + t + 1); ++q) s += __ldg(rsurf + __ldg(idx + q));
+    const int g = __ldg(nodes + t);
+    const double v = __ldg(mask + g) ? __ldg(u + g) : s;
+    r[g] = v;
+    send[t] = v;
+  }
+}
+
+// up-interface node t: the final value computed by the upper rank
+__global__ void dist_finish_kernel(const int* __restrict__ nodes, int n, const double* __restrict__ recv,
+                                   double* __restrict__ r)
+{
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) r[__ldg(nodes + t)] = __ldg(recv + t);
 }
 
 // ---------------------------------------------------------------------------
@@ -161,6 +205,244 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_kernel(CombineArgs a)
     }
   }
   dot_commit<kGatherBlock>(a.dot, dot, red);
+}
+
+// Two-scale combine with the coarse prolongation fused in (precond.cpp:57-66,
+// prolongate coarse.cpp:164-186): per node g
+//   zf = sum of its subdomain contributions in (e, slot) order (fine.cpp:224-227)
+//   zc = (sum over its copies (e,l), in (e,l) order, of
+//         (sum_cb B[cb][l] Zc[e][cb]) * m[e][l]) / m_N[g]
+//   z  = mask ? r : (0 + zf) + zc ;  z.r partial
+// Element-interior nodes have one copy whose (e,l) follows from g
+// (interior ids are (e, local)-ordered, mesh.cpp:283); surface nodes walk
+// their Ax gather list (ax_idx = e*nsurfp + slot).
+struct CombineProlongArgs {
+  const double* r;
+  const std::uint8_t* mask;
+  const double* zsort;
+  const unsigned* fine_off;
+  const unsigned* ax_off;
+  const int* ax_idx;
+  const double* Zc;
+  const double* mass;      // [e][nloc] (element-interior copies)
+  const double* mass_csr;  // surface copies, Ax-CSR order
+  const double* esurf;     // [e][nsurfp] prolongated surface copies (prolong_surface_kernel)
+  const double* lumped;
+  double* z;
+  int N, nsg;
+  int do_fine, do_coarse;
+  DotArgs dot;
+};
+
+template <int NP>
+__global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(CombineProlongArgs a)
+{
+  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NLOC = NP * NP * NP;
+  constexpr int NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2), NSP = (NS + 3) & ~3;
+  __shared__ double red[kGatherBlock / 32];
+  __shared__ double h0[NP], h1[NP];
+  if (threadIdx.x < NP) {
+    h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
+    h1[threadIdx.x] = c_tab[NP].hat1[threadIdx.x];
+  }
+  __syncthreads();
+  // prolongated value of copy (e; i,j,k) before the mass: sum_cb B[cb][l] Zc[e][cb] (coarse.cpp:176-179)
+  auto pz = [&](long long e, int i, int j, int k) {
+    const double2* zc2 = reinterpret_cast<const double2*>(a.Zc + 8 * e);
+    const double2 c01 = __ldg(zc2), c23 = __ldg(zc2 + 1), c45 = __ldg(zc2 + 2), c67 = __ldg(zc2 + 3);
+    const double zc[8] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y};
+    const double hi[2] = {h0[i], h1[i]}, hj[2] = {h0[j], h1[j]}, hk[2] = {h0[k], h1[k]};
+    double s = 0.0;
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb) s += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[cb >> 2] * zc[cb];
+    return s;
+  };
+  double dot = 0.0;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < a.N; g += gridDim.x * blockDim.x) {
+    const double rg = __ldg(a.r + g);
+    double zg;
+    if (__ldg(a.mask + g)) {
+      zg = rg;
+    } else {
+      double s = 0.0;
+      if (a.do_fine) {
+        // up to 8 contributions loaded at once (predicated), summed in list order
+        const unsigned q0 = __ldg(a.fine_off + g), q1 = __ldg(a.fine_off + g + 1);
+        double v[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[t] = q0 + t < q1 ? __ldcs(a.zsort + q0 + t) : 0.0;
+        double zf = 0.0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (q0 + t < q1) zf += v[t];
+        for (unsigned q = q0 + 8; q < q1; ++q) zf += __ldcs(a.zsort + q);
+        s += zf;
+      }
+      if (a.do_coarse) {
+        double zc = 0.0;
+        if (g >= a.nsg) {
+          if constexpr (NI > 0) {
+            const int t = g - a.nsg;
+            const long long e = t / NI;
+            const int l = t % NI;
+            const int i = 1 + l % (n - 1), j = 1 + (l / (n - 1)) % (n - 1), k = 1 + l / ((n - 1) * (n - 1));
+            zc = pz(e, i, j, k) * __ldg(a.mass + e * NLOC + (k * NP + j) * NP + i);  // coarse.cpp:180
+          }
+        } else {
+          // face nodes (2 copies) dominate: the first two copies are evaluated
+          // independently, the rest (edges 4, vertices 8+) in order after them
+          const unsigned c0 = __ldg(a.ax_off + g), c1 = __ldg(a.ax_off + g + 1);
+          const int x0 = __ldg(a.ax_idx + c0);
+          const int x1 = c0 + 1 < c1 ? __ldg(a.ax_idx + c0 + 1) : x0;
+          int i0, j0, k0, i1, j1, k1;
+          surface_ijk<NP>(x0 % NSP, i0, j0, k0);
+          surface_ijk<NP>(x1 % NSP, i1, j1, k1);
+          const double m0 = __ldcs(a.mass_csr + c0);
+          const double m1 = c0 + 1 < c1 ? __ldcs(a.mass_csr + c0 + 1) : 0.0;
+          const double p0 = pz(x0 / NSP, i0, j0, k0) * m0;
+          const double p1 = pz(x1 / NSP, i1, j1, k1) * m1;
+          zc += p0;
+          if (c0 + 1 < c1) zc += p1;
+          for (unsigned q = c0 + 2; q < c1; ++q) {
+            const int c = __ldg(a.ax_idx + q);
+            int i, j, k;
+            surface_ijk<NP>(c % NSP, i, j, k);
+            zc += pz(c / NSP, i, j, k) * __ldcs(a.mass_csr + q);
+          }
+        }
+        s += zc / __ldg(a.lumped + g);
+      }
+      zg = s;
+    }
+    a.z[g] = zg;
+    dot += zg * rg;
+  }
+  dot_commit<kGatherBlock>(a.dot, dot, red);
+}
+
+// Tiled variant of the combine: a warp owns a tile of kTile consecutive nodes
+// (lane + 32 t). The tile's fine contributions and surface-copy lists are
+// contiguous in CSR order, so the warp first streams them into shared memory
+// with coalesced loads (every load of the tile in flight at once), then each
+// lane sums its nodes' segments left to right from shared memory. Segments
+// longer than the staging capacity fall back to direct loads.
+constexpr int kTile = 128;
+constexpr int kTileCapF = 512;  // staged fine contributions per warp (typ. 2.6 per node)
+constexpr int kTileCapC = 384;  // staged surface copies per warp (typ. 1.5-2 per surface node)
+constexpr int kCombBlock = 128;
+
+template <int NP>
+__global__ void __launch_bounds__(kCombBlock, 4) combine_tile_kernel(CombineProlongArgs a)
+{
+  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NLOC = NP * NP * NP;
+  constexpr int W = kCombBlock / 32, T = kTile / 32;
+  __shared__ double red[W];
+  __shared__ double h0[NP], h1[NP];
+  __shared__ double sf[W][kTileCapF];
+  __shared__ double sm[W][kTileCapC];
+  if (threadIdx.x < NP) {
+    h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
+    h1[threadIdx.x] = c_tab[NP].hat1[threadIdx.x];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* stf = sf[warp];
+  double* stm = sm[warp];
+  auto pz = [&](long long e, int i, int j, int k) {  // sum_cb B[cb][l] Zc[e][cb] (coarse.cpp:176-179)
+    const double2* zc2 = reinterpret_cast<const double2*>(a.Zc + 8 * e);
+    const double2 c01 = __ldg(zc2), c23 = __ldg(zc2 + 1), c45 = __ldg(zc2 + 2), c67 = __ldg(zc2 + 3);
+    const double zc[8] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y};
+    const double hi[2] = {h0[i], h1[i]}, hj[2] = {h0[j], h1[j]}, hk[2] = {h0[k], h1[k]};
+    double s = 0.0;
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb) s += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[cb >> 2] * zc[cb];
+    return s;
+  };
+  double dot = 0.0;
+  const int nw = gridDim.x * W;
+  for (int g0 = (blockIdx.x * W + warp) * kTile; g0 < a.N; g0 += nw * kTile) {
+    // ---- first-level loads for the tile's nodes (coalesced) ----
+    unsigned f0[T], f1[T], c0[T], c1[T];
+    double rg[T];
+    bool msk[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int g = g0 + lane + 32 * t;
+      const bool in = g < a.N;
+      rg[t] = in ? __ldg(a.r + g) : 0.0;
+      msk[t] = in ? __ldg(a.mask + g) != 0 : true;
+      f0[t] = f1[t] = c0[t] = c1[t] = 0;
+      if (in && a.do_fine) {
+        f0[t] = __ldg(a.fine_off + g);
+        f1[t] = __ldg(a.fine_off + g + 1);
+      }
+      if (in && a.do_coarse && g < a.nsg) {
+        c0[t] = __ldg(a.ax_off + g);
+        c1[t] = __ldg(a.ax_off + g + 1);
+      }
+    }
+    // tile ranges (first lane holds the lowest node, last lane the highest)
+    const int glast = min(g0 + kTile, a.N) - 1;
+    unsigned fb = 0, fe = 0, cb0 = 0, ce = 0;
+    if (a.do_fine) {
+      fb = __shfl_sync(0xffffffffu, f0[0], 0);
+      fe = __ldg(a.fine_off + glast + 1);
+    }
+    const bool any_surf = a.do_coarse && g0 < a.nsg;
+    if (any_surf) {
+      cb0 = __shfl_sync(0xffffffffu, c0[0], 0);
+      ce = __ldg(a.ax_off + min(glast, a.nsg - 1) + 1);
+    }
+    const bool stage_f = a.do_fine && fe - fb <= (unsigned)kTileCapF;
+    const bool stage_c = any_surf && ce - cb0 <= (unsigned)kTileCapC;
+    // ---- stream the tile's segments into shared memory ----
+    if (stage_f)
+      for (unsigned q = lane; q < fe - fb; q += 32) stf[q] = __ldcs(a.zsort + fb + q);
+    if (stage_c)  // the tile's surface copies, gathered from the element-major E-vector
+      for (unsigned q = lane; q < ce - cb0; q += 32) stm[q] = __ldg(a.esurf + __ldg(a.ax_idx + cb0 + q));
+    __syncwarp();
+    // ---- per-lane sums in list order ----
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      const int g = g0 + lane + 32 * t;
+      if (g >= a.N) continue;
+      double zg;
+      if (msk[t]) {
+        zg = rg[t];
+      } else {
+        double s = 0.0;
+        if (a.do_fine) {
+          double zf = 0.0;
+          if (stage_f)
+            for (unsigned q = f0[t] - fb; q < f1[t] - fb; ++q) zf += stf[q];
+          else
+            for (unsigned q = f0[t]; q < f1[t]; ++q) zf += __ldcs(a.zsort + q);
+          s += zf;
+        }
+        if (a.do_coarse) {
+          double zc = 0.0;
+          if (g >= a.nsg) {
+            if constexpr (NI > 0) {
+              const int u = g - a.nsg;
+              const long long e = u / NI;
+              const int l = u % NI;
+              const int i = 1 + l % (n - 1), j = 1 + (l / (n - 1)) % (n - 1), k = 1 + l / ((n - 1) * (n - 1));
+              zc = pz(e, i, j, k) * __ldg(a.mass + e * NLOC + (k * NP + j) * NP + i);  // coarse.cpp:180
+            }
+          } else {
+            for (unsigned q = c0[t]; q < c1[t]; ++q)  // copies in (e,l) order (coarse.cpp:181)
+              zc += stage_c ? stm[q - cb0] : __ldg(a.esurf + __ldg(a.ax_idx + q));
+          }
+          s += zc / __ldg(a.lumped + g);
+        }
+        zg = s;
+      }
+      a.z[g] = zg;
+      dot += zg * rg[t];
+    }
+    __syncwarp();  // staging buffers reused by the next tile
+  }
+  dot_commit<kCombBlock>(a.dot, dot, red);
 }
 
 // R[v] = vmask[v] ? 0 : sum of Rpart over (e,cb) incidences in ascending order

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/hexsem_b200.h"
+#include "kernels_amg.cuh"
 #include "kernels_ax.cuh"
 #include "kernels_coarse.cuh"
 #include "kernels_common.cuh"
@@ -46,6 +47,26 @@ int gather_grid(long long n)
 {
   const long long b = (n + kGatherBlock - 1) / kGatherBlock;
   return static_cast<int>(std::max(1LL, std::min(b, 148LL * 8)));
+}
+
+// Grid for a grid-stride kernel: never more blocks than can be resident at
+// once (one wave), so no block is left for a partial second wave.
+int g_num_sms = 148;
+template <class K>
+int fill_grid(K kernel, int block, long long items)
+{
+  static thread_local std::vector<std::pair<const void*, int>> cache;
+  const void* key = reinterpret_cast<const void*>(kernel);
+  int per_sm = 0;
+  for (const auto& kv : cache)
+    if (kv.first == key) per_sm = kv.second;
+  if (per_sm == 0) {
+    HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, 0));
+    per_sm = std::max(per_sm, 1);
+    cache.emplace_back(key, per_sm);
+  }
+  const long long need = (items + block - 1) / block;
+  return static_cast<int>(std::max(1LL, std::min(need, static_cast<long long>(per_sm) * g_num_sms)));
 }
 
 int vec_grid(long long n)
@@ -132,6 +153,7 @@ struct Plan {
   unsigned* ax_off = nullptr;
   std::uint8_t* mask = nullptr;
   double* d_lumped = nullptr;
+  double* d_inv_lumped = nullptr;
   int* sub_face = nullptr;
   unsigned* fine_off = nullptr;
   int* fine_pos = nullptr;    // [e][P^3] CSR position (-1 sentinel)
@@ -141,10 +163,21 @@ struct Plan {
   int* vtx_idx = nullptr;
   std::uint8_t* vmask = nullptr;
   double *Rpart = nullptr, *R = nullptr, *Z = nullptr, *rho = nullptr, *dZ = nullptr;
-  double *psort = nullptr, *pint = nullptr;
+  double* Zc = nullptr;       // [e][8] coarse corner values for the fused prolongation
+  double* mass_csr = nullptr; // m of each surface copy in Ax-CSR order
+  double* esurf = nullptr;    // [e][nsurfp] prolongated surface copies
   std::vector<DevLevel> lv;  // AMG levels 0..L (L = coarsest, uses dense)
   DevDense dense;
   DevCsr Kc{};               // K_c on the device (AMG mode: residual between the two K-cycles)
+  // levels >= 1 of the K-cycle as one cluster kernel (kernels_amg.cuh)
+  bool amg_cluster = false;
+  int cluster_size = 0;
+  AmgClusterArgs cargs{};
+  int* agg0c = nullptr;      // level-0 row -> compact level-1 row (-1: dropped zero row)
+  int* mptr0 = nullptr;      // kept level-1 rows: level-0 members (ascending)
+  int* mem0 = nullptr;
+  int n1 = 0;
+  DevDense cdense;           // compact coarsest solve
   std::uint8_t* zero_mask = nullptr;
 
   // PCG vectors
@@ -162,6 +195,13 @@ struct Plan {
   double* scratch = nullptr;
   double* h_status = nullptr;  // pinned
   int hist_cap = 0;
+
+  // element-slab partition (distributed Ax); rank 0 of 1 = whole mesh
+  int rank = 0, nranks = 1;
+  int e0 = 0;                 // first owned element (global id); pl.ne counts owned elements
+  int* ax_nodes = nullptr;    // local surface node -> global id (null: identity)
+  int n_loc_surf = 0;         // local surface nodes = [group0 | up | down]
+  int n_grp0 = 0, n_up = 0, n_down = 0;
 
   // live kernel timing (bench roofline): event pairs around tagged launches on s_main
   bool kt_on = false;
@@ -268,7 +308,7 @@ void launch_ax_elem(Plan& pl, const double* u, double* r, DotArgs dot, cudaStrea
   a.rsurf = pl.rsurf;
   a.r = r;
   a.ne = pl.ne;
-  a.num_surface_global = pl.nsg;
+  a.num_surface_global = pl.nsg + pl.e0 * (pl.order - 1) * (pl.order - 1) * (pl.order - 1);  // first owned interior id
   a.dot = dot;
   ax_elem_kernel<NP><<<pl.ax_grid, Sh::kBlock, Sh::kSmemBytes, s>>>(a);
 }
@@ -301,11 +341,12 @@ void enqueue_ax(Plan& pl, const double* u, double* r, double* dot_result, cudaSt
   g.u = u;
   g.mask = pl.mask;
   g.r = r;
-  g.num_surface_global = pl.nsg;
+  g.num_surface_global = pl.nranks > 1 ? pl.n_grp0 : pl.nsg;  // distributed: interface nodes go through dist_*
+  g.nodes = pl.ax_nodes;
   g.dot = d2;
   {
     KtScope kt(pl, HXB_KT_AX_GATHER, s);
-    ax_gather_kernel<<<gather_grid(pl.nsg), kGatherBlock, 0, s>>>(g);
+    ax_gather_kernel<<<fill_grid(ax_gather_kernel, kGatherBlock, g.num_surface_global), kGatherBlock, 0, s>>>(g);
   }
   pl.launches += 2;
 }
@@ -325,6 +366,9 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   a.ne = pl.ne;
   a.sstride = 2 * pl.nsurf;
   a.num_surface_global = pl.nsg;
+  a.inv_lumped = pl.d_inv_lumped;
+  a.mass = pl.mass;
+  a.Rpart = pl.do_coarse ? pl.Rpart : nullptr;
   KtScope kt(pl, HXB_KT_FDM, s);
   pl.launches += 1;
   if (pl.fdm_eo)
@@ -333,16 +377,20 @@ void launch_fdm(Plan& pl, cudaStream_t s)
     fdm_kernel<NP, false><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
 }
 
-void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse)
+template <int NP>
+void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse)
 {
-  CombineArgs a;
+  CombineProlongArgs a;
   a.r = pl.r;
   a.mask = pl.mask;
   a.zsort = pl.zsort;
   a.fine_off = pl.fine_off;
-  a.psort = pl.psort;
-  a.pint = pl.pint;
   a.ax_off = pl.ax_off;
+  a.ax_idx = pl.ax_idx;
+  a.Zc = pl.Zc;
+  a.mass = pl.mass;
+  a.mass_csr = pl.mass_csr;
+  a.esurf = pl.esurf;
   a.lumped = pl.d_lumped;
   a.z = pl.z;
   a.N = pl.N;
@@ -350,25 +398,34 @@ void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, b
   a.do_fine = do_fine ? 1 : 0;
   a.do_coarse = do_coarse ? 1 : 0;
   a.dot = zr_result ? dot_args(pl, zr_result) : DotArgs{};
-  KtScope kt(pl, HXB_KT_COMBINE, s);
-  pl.launches += 1;
-  combine_kernel<<<gather_grid(pl.N), kGatherBlock, 0, s>>>(a);
+  const int grid = fill_grid(combine_tile_kernel<NP>, kCombBlock, (pl.N + kTile - 1) / kTile * 32);
+  combine_tile_kernel<NP><<<grid, kCombBlock, 0, s>>>(a);
 }
 
-template <int NP>
-void launch_prolong(Plan& pl, cudaStream_t s)
+void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse)
 {
-  using Sh = AxShape<NP>;
-  prolong_elem_kernel<NP, Sh::kEPB, Sh::kBlock><<<(pl.ne + Sh::kEPB - 1) / Sh::kEPB, Sh::kBlock, 0, s>>>(
-      pl.Z, pl.conn, pl.mass, pl.smap, pl.psort, pl.pint, pl.ne, pl.nsurf, pl.nsg);
+  KtScope kt(pl, HXB_KT_COMBINE, s);
+  pl.launches += 1;
+  HXB_DISPATCH_NP(pl.np, launch_combine_np, pl, zr_result, s, do_fine, do_coarse);
 }
+
+// Zc = Z at each element's corners (interior copies, prolonged inside the
+// combine) and the prolongated surface copies (coarse.cpp:164-181)
+template <int NP>
+void launch_prolong_np(Plan& pl, cudaStream_t s)
+{
+  corner_values_kernel<<<vec_grid(8LL * pl.ne), kVecBlock, 0, s>>>(pl.Z, pl.conn, pl.Zc, pl.ne);
+  prolong_surface_kernel<NP><<<fill_grid(prolong_surface_kernel<NP>, kVecBlock, (long long)pl.ne * pl.nsurf), kVecBlock, 0, s>>>(
+      pl.Z, pl.conn, pl.mass, pl.esurf, pl.ne);
+}
+void launch_prolong(Plan& pl, cudaStream_t s) { HXB_DISPATCH_NP(pl.np, launch_prolong_np, pl, s); }
 
 template <int NP>
 void launch_restrict(Plan& pl, cudaStream_t s)
 {
-  constexpr int B = AxShape<NP>::kBlock;
-  restrict_kernel<NP, B><<<pl.ne, B, 0, s>>>(pl.r, pl.d_lumped, pl.smap, pl.mass, pl.Rpart, pl.ne, 2 * pl.nsurf,
-                                                   pl.nsg);
+  const int grid = fill_grid(restrict_warp_kernel<NP>, 256, 32LL * pl.ne);
+  restrict_warp_kernel<NP><<<grid, 256, 0, s>>>(pl.r, pl.d_lumped, pl.smap, pl.mass, pl.Rpart, pl.ne, 2 * pl.nsurf,
+                                               pl.nsg);
 }
 
 // ---- AMG enqueue (captured into the coarse graph) --------------------------
@@ -425,22 +482,55 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
   }
 }
 
+// cycle(0, r, zout) with ksolve(1) as one cluster kernel (kernels_amg.cuh)
+void enqueue_cycle0_cluster(Plan& pl, const double* r, double* zout, cudaStream_t s)
+{
+  DevLevel& v = pl.lv[0];
+  const int g = vec_grid(v.n);
+  amg_jacobi2_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA);
+  amg_resid_kernel<<<g, kVecBlock, 0, s>>>(v.A, r, v.zA, v.kf);
+  CLev& c1 = pl.cargs.lev[0];
+  amg_agg_sum_compact_kernel<<<vec_grid(pl.n1), kVecBlock, 0, s>>>(v.kf, pl.mptr0, pl.mem0, c1.b, pl.n1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.cluster_size);
+  cfg.blockDim = dim3(kAmgClusterBlock);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = pl.cluster_size;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  HXB_CUDA(cudaLaunchKernelEx(&cfg, amg_cluster_kernel, pl.cargs, static_cast<const double*>(c1.b), c1.x));
+  amg_prolong_smooth_compact_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c1.x, pl.agg0c, v.zB);
+  amg_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout);
+}
+
 // restrict -> mask -> coarse solve; leaves Z (coarse.cpp:188-206)
+// Rpart -> R -> coarse solve -> Zc (coarse.cpp:188-206). Rpart comes from
+// the FDM kernel (fused restriction) or, without a fine branch, from
+// restrict_warp_kernel launched just before the graph.
 void enqueue_coarse(Plan& pl, cudaStream_t s)
 {
-  HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s);
   vertex_gather_kernel<<<gather_grid(pl.nv), kGatherBlock, 0, s>>>(pl.Rpart, pl.vtx_off, pl.vtx_idx, pl.vmask, pl.R, pl.nv);
   if (pl.use_amg) {
-    enqueue_cycle(pl, 0, pl.R, pl.Z, s);
+    auto cyc0 = [&](const double* r, double* z) {
+      if (pl.amg_cluster)
+        enqueue_cycle0_cluster(pl, r, z, s);
+      else
+        enqueue_cycle(pl, 0, r, z, s);
+    };
+    cyc0(pl.R, pl.Z);
     // two composed K-cycles: Z = B R + B (R - K_c B R)  (coarse.cpp:193-200)
     const DevCsr K = pl.Kc;
     amg_resid_kernel<<<vec_grid(K.n), kVecBlock, 0, s>>>(K, pl.R, pl.Z, pl.rho);
-    enqueue_cycle(pl, 0, pl.rho, pl.dZ, s);
+    cyc0(pl.rho, pl.dZ);
     axpy1_kernel<<<vec_grid(K.n), kVecBlock, 0, s>>>(pl.Z, pl.dZ, K.n);
   } else {
     enqueue_dense(pl, pl.R, pl.Z, s);
   }
-  HXB_DISPATCH_NP(pl.np, launch_prolong, pl, s);
+  launch_prolong(pl, s);
 }
 
 void capture_coarse_graph(Plan& pl)
@@ -461,20 +551,23 @@ void enqueue_precond(Plan& pl, double* zr_result)
 {
   cudaStream_t s = pl.s_main;
   if (pl.precond_mode == HXB_PRECOND_NONE) {
-    copy_dot_kernel<kVecBlock><<<vec_grid(pl.N), kVecBlock, 0, s>>>(pl.r, pl.r, pl.z, pl.N,
+    copy_dot_kernel<kVecBlock><<<fill_grid(copy_dot_kernel<kVecBlock>, kVecBlock, pl.N), kVecBlock, 0, s>>>(pl.r, pl.r, pl.z, pl.N,
                                                                      zr_result ? dot_args(pl, zr_result) : DotArgs{});
     pl.launches += 1;
     return;
   }
+  // fine FDM solves with the coarse restriction fused in (one pass over r),
+  // then the coarse graph; the combine sums both and applies the mask
+  if (pl.do_fine) {
+    HXB_DISPATCH_NP(pl.np, launch_fdm, pl, s);
+  } else if (pl.do_coarse) {
+    HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s);
+    pl.launches += 1;
+  }
   if (pl.do_coarse) {
-    HXB_CUDA(cudaEventRecord(pl.ev_fork, s));
-    HXB_CUDA(cudaStreamWaitEvent(pl.s_coarse, pl.ev_fork, 0));
-    HXB_CUDA(cudaGraphLaunch(pl.coarse_exec, pl.s_coarse));
-    HXB_CUDA(cudaEventRecord(pl.ev_join, pl.s_coarse));
+    HXB_CUDA(cudaGraphLaunch(pl.coarse_exec, s));
     pl.launches += pl.coarse_graph_nodes;
   }
-  if (pl.do_fine) HXB_DISPATCH_NP(pl.np, launch_fdm, pl, s);
-  if (pl.do_coarse) HXB_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
   launch_combine(pl, zr_result, s, pl.do_fine, pl.do_coarse);
 }
 
@@ -527,6 +620,14 @@ bool upload_tables(const GllBasis& basis, const Pencil& pencil)
     t.hat1[i] = 0.5 * (1 + basis.nodes[i]);
   }
   HXB_CUDA(cudaMemcpyToSymbol(c_tab, &t, sizeof(OrderTables), sizeof(OrderTables) * np));
+  FdmConst fc{};
+  std::memcpy(fc.FE, t.FE, sizeof(fc.FE));
+  std::memcpy(fc.FO, t.FO, sizeof(fc.FO));
+  std::memcpy(fc.IE, t.IE, sizeof(fc.IE));
+  std::memcpy(fc.IO, t.IO, sizeof(fc.IO));
+  std::memcpy(fc.lam, t.lam, sizeof(fc.lam));
+  std::memcpy(fc.invM, t.invM, sizeof(fc.invM));
+  HXB_CUDA(cudaMemcpyToSymbol(c_fdm, &fc, sizeof(FdmConst), sizeof(FdmConst) * np));
   return t.eo_ok != 0;
 }
 
@@ -536,10 +637,10 @@ struct GatherCsr {
   std::vector<int> idx;
 };
 
-void dense_to_device(Plan& pl, const Csr& A)
+DevDense dense_to_device(Plan& pl, const Csr& A)
 {
   DenseCoarse dc = dense_coarse_setup(A, 1500);
-  DevDense& d = pl.dense;
+  DevDense d;
   d.n = dc.n;
   d.m = static_cast<int>(dc.coupled.size());
   d.coupled = pl.mem.upload(dc.coupled);
@@ -547,7 +648,7 @@ void dense_to_device(Plan& pl, const Csr& A)
   const std::size_t mm = static_cast<std::size_t>(d.m) * d.m;
   if (!dc.ainv.empty() || d.m == 0) {
     d.ainv = pl.mem.upload(dc.ainv);
-    return;
+    return d;
   }
   // large coupled block: Cholesky + inverse on the device (cuSOLVER potrf/potri)
   d.ainv = pl.mem.alloc<double>(mm);
@@ -579,6 +680,155 @@ void dense_to_device(Plan& pl, const Csr& A)
   for (int i = 0; i < d.m; ++i)
     for (int j = i + 1; j < d.m; ++j) hinv[static_cast<std::size_t>(j) * d.m + i] = hinv[static_cast<std::size_t>(i) * d.m + j];
   HXB_CUDA(cudaMemcpy(d.ainv, hinv.data(), mm * sizeof(double), cudaMemcpyHostToDevice));
+  return d;
+}
+
+// Levels >= 1 of the AMG hierarchy, compacted to the rows that can carry
+// non-zero values (kernels_amg.cuh): a level-0 row is dropped when it is a
+// Dirichlet vertex (R masked to 0, coarse.cpp:191-192) with no off-diagonal
+// entry; a coarser row when all its aggregate members were dropped and it is
+// itself decoupled. Returns false when the cluster path cannot be used.
+bool build_amg_cluster(Plan& pl, const AmgSetup& amg, const std::vector<std::uint8_t>& vmask)
+{
+  const int Lh = static_cast<int>(amg.levels.size());
+  if (Lh < 1 || Lh > kAmgMaxLevels) return false;
+  auto A_of = [&](int l) -> const Csr& { return l < Lh ? amg.levels[l].A : amg.coarsest; };
+  auto decoupled = [&](const Csr& A, gid i) {
+    for (std::int64_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k)
+      if (A.col[k] != i) return false;
+    return true;
+  };
+  std::vector<std::vector<char>> drop(Lh + 1);
+  {
+    const Csr& A0 = A_of(0);
+    drop[0].assign(A0.n, 0);
+    for (gid i = 0; i < A0.n; ++i) drop[0][i] = (i < static_cast<gid>(vmask.size()) && vmask[i] && decoupled(A0, i)) ? 1 : 0;
+  }
+  for (int l = 0; l < Lh; ++l) {
+    const AmgLevel& lv = amg.levels[l];
+    const Csr& An = A_of(l + 1);
+    std::vector<char> all(lv.n_coarse, 1);
+    for (gid i = 0; i < lv.A.n; ++i)
+      if (!drop[l][i]) all[lv.aggregate[i]] = 0;
+    drop[l + 1].assign(An.n, 0);
+    for (gid c = 0; c < An.n; ++c) drop[l + 1][c] = (all[c] && decoupled(An, c)) ? 1 : 0;
+  }
+  std::vector<std::vector<gid>> cidx(Lh + 1);
+  std::vector<int> ncomp(Lh + 1, 0);
+  for (int l = 1; l <= Lh; ++l) {
+    cidx[l].assign(A_of(l).n, -1);
+    for (gid i = 0; i < A_of(l).n; ++i)
+      if (!drop[l][i]) cidx[l][i] = ncomp[l]++;
+  }
+  DeviceArena& M = pl.mem;
+  AmgClusterArgs& ca = pl.cargs;
+  ca.L = Lh - 1;
+  // compact levels 1..Lh-1 (ca.lev[l-1])
+  for (int l = 1; l < Lh; ++l) {
+    const AmgLevel& lv = amg.levels[l];
+    const Csr& A = lv.A;
+    CLev& c = ca.lev[l - 1];
+    c.n = ncomp[l];
+    std::vector<int> ptr(1, 0), col, agg, mptr(ncomp[l + 1] + 1, 0), mem;
+    std::vector<double> val, dinv;
+    for (gid i = 0; i < A.n; ++i) {
+      if (drop[l][i]) continue;
+      for (std::int64_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+        const gid j = cidx[l][A.col[k]];
+        if (j < 0) throw HxbError(HXB_ENUMERIC, "amg compaction: kept row couples to a dropped row");
+        col.push_back(j);
+        val.push_back(A.val[k]);
+      }
+      ptr.push_back(static_cast<int>(col.size()));
+      dinv.push_back(lv.inv_diag[i]);
+      const gid a = cidx[l + 1][lv.aggregate[i]];
+      if (a < 0) throw HxbError(HXB_ENUMERIC, "amg compaction: kept row in a dropped aggregate");
+      agg.push_back(a);
+      mptr[a + 1]++;
+    }
+    for (int k = 0; k < ncomp[l + 1]; ++k) mptr[k + 1] += mptr[k];
+    mem.assign(c.n, 0);
+    std::vector<int> cur(mptr.begin(), mptr.end() - 1);
+    for (int i = 0; i < c.n; ++i) mem[cur[agg[i]]++] = i;  // ascending member order
+    c.ptr = M.upload(ptr);
+    c.col = M.upload(col);
+    c.val = M.upload(val);
+    c.dinv = M.upload(dinv);
+    c.agg = M.upload(agg);
+    c.mptr = M.upload(mptr);
+    c.mem = M.upload(mem);
+    c.nc = ncomp[l + 1];
+    for (double** v : {&c.zA, &c.zB, &c.rho, &c.kr, &c.kz, &c.kp, &c.kf, &c.b, &c.x}) *v = M.alloc<double>(c.n);
+  }
+  {  // compact coarsest (ca.lev[Lh-1])
+    const Csr& A = amg.coarsest;
+    CLev& c = ca.lev[Lh - 1];
+    c.n = ncomp[Lh];
+    Csr Ac;
+    Ac.n = c.n;
+    Ac.ptr.assign(1, 0);
+    for (gid i = 0; i < A.n; ++i) {
+      if (drop[Lh][i]) continue;
+      for (std::int64_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+        Ac.col.push_back(cidx[Lh][A.col[k]]);
+        Ac.val.push_back(A.val[k]);
+      }
+      Ac.ptr.push_back(static_cast<std::int64_t>(Ac.col.size()));
+    }
+    pl.cdense = dense_to_device(pl, Ac);
+    ca.ainv = pl.cdense.ainv;
+    ca.coupled = pl.cdense.coupled;
+    ca.inv_diag = pl.cdense.inv_diag;
+    ca.m = pl.cdense.m;
+    c.b = M.alloc<double>(std::max(1, c.n));
+    c.x = M.alloc<double>(std::max(1, c.n));
+  }
+  {  // level 0 -> compact level 1
+    const AmgLevel& l0 = amg.levels[0];
+    std::vector<int> agg0c(l0.A.n), mptr(ncomp[1] + 1, 0), mem;
+    for (gid i = 0; i < l0.A.n; ++i) {
+      agg0c[i] = cidx[1][l0.aggregate[i]];
+      if (agg0c[i] >= 0) mptr[agg0c[i] + 1]++;
+    }
+    for (int k = 0; k < ncomp[1]; ++k) mptr[k + 1] += mptr[k];
+    mem.assign(mptr[ncomp[1]], 0);
+    std::vector<int> cur(mptr.begin(), mptr.end() - 1);
+    for (gid i = 0; i < l0.A.n; ++i)
+      if (agg0c[i] >= 0) mem[cur[agg0c[i]]++] = i;
+    pl.agg0c = M.upload(agg0c);
+    pl.mptr0 = M.upload(mptr);
+    pl.mem0 = M.upload(mem);
+    pl.n1 = ncomp[1];
+  }
+  // the K-cycle recursion (ksolve -> cycle -> ksolve ...) needs a per-thread
+  // stack deeper than the 1 KB default for hierarchies of many levels
+  {
+    std::size_t stack = 0;
+    HXB_CUDA(cudaDeviceGetLimit(&stack, cudaLimitStackSize));
+    const std::size_t want = 1024 + 512 * static_cast<std::size_t>(Lh + 2);
+    if (stack < want) HXB_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, want));
+  }
+  // cluster size: 16 CTAs (non-portable) when the device can co-schedule them, else 8
+  HXB_CUDA(cudaFuncSetAttribute(amg_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  for (int cs : {16, 8}) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kAmgClusterBlock);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, amg_cluster_kernel, &cfg) == cudaSuccess && nclusters > 0) {
+      pl.cluster_size = cs;
+      break;
+    }
+    cudaGetLastError();
+  }
+  return pl.cluster_size > 0;
 }
 
 DevCsr csr_to_device(Plan& pl, const Csr& A)
@@ -593,6 +843,93 @@ DevCsr csr_to_device(Plan& pl, const Csr& A)
   return d;
 }
 
+// Element-slab partition of the Ax gather. Rank r owns the
+// elements [e0, e0+ne). Its surface nodes split into
+//   group 0: all copies owned here            -> ax_gather_kernel
+//   up:      copies also in rank r+1's slab     -> partial sum sent up
+//   down:    copies also in rank r-1's slab     -> continue the partial received
+// each group in ascending global id (the neighbour's matching list is the
+// same set in the same order). A node spanning three ranks is rejected.
+}  // namespace
+
+DistLists dist_partition(const HostSetup& hs, int rank, int nranks, int nsurfp)
+{
+  const Numbering& num = hs.num;
+  const int ne_all = hs.mesh.num_elements();
+  const int np = hs.order + 1;
+  const int nsurf_raw = surface_slot_count(np);
+  auto start = [&](int r) { return static_cast<int>(static_cast<long long>(ne_all) * r / nranks); };
+  const int e0 = start(rank), e1 = start(rank + 1);
+  const int e_lo = rank > 0 ? start(rank - 1) : 0, e_hi = rank + 1 < nranks ? start(rank + 2) : ne_all;
+  const int nsg = num.num_surface_global;
+  std::vector<int> minE(nsg, ne_all), maxE(nsg, -1);
+  for (int e = 0; e < ne_all; ++e)
+    for (int q = 0; q < nsurf_raw; ++q) {
+      const gid g = num.l2g_surf[static_cast<std::size_t>(e) * nsurf_raw + q];
+      minE[g] = std::min(minE[g], e);
+      maxE[g] = std::max(maxE[g], e);
+    }
+  std::vector<int> loc(nsg, -1);
+  std::vector<gid> grp[3];
+  for (int e = e0; e < e1; ++e)
+    for (int q = 0; q < nsurf_raw; ++q) {
+      const gid g = num.l2g_surf[static_cast<std::size_t>(e) * nsurf_raw + q];
+      if (loc[g] != -1) continue;
+      loc[g] = -2;
+      const bool up = maxE[g] >= e1, down = minE[g] < e0;
+      if ((up && down) || (up && maxE[g] >= e_hi) || (down && minE[g] < e_lo))
+        throw HxbError(HXB_EINVAL, "slab partition too thin: a node spans more than two ranks");
+      grp[up ? 1 : (down ? 2 : 0)].push_back(g);
+    }
+  DistLists d;
+  d.e0 = e0;
+  d.e1 = e1;
+  for (auto& v : grp) {
+    std::sort(v.begin(), v.end());
+    d.nodes.insert(d.nodes.end(), v.begin(), v.end());
+  }
+  d.n_grp0 = static_cast<int>(grp[0].size());
+  d.n_up = static_cast<int>(grp[1].size());
+  d.n_down = static_cast<int>(grp[2].size());
+  const int nl = static_cast<int>(d.nodes.size());
+  for (int t = 0; t < nl; ++t) loc[d.nodes[t]] = t;
+  d.off.assign(static_cast<std::size_t>(nl) + 1, 0);
+  for (int e = e0; e < e1; ++e)
+    for (int q = 0; q < nsurf_raw; ++q) d.off[loc[num.l2g_surf[static_cast<std::size_t>(e) * nsurf_raw + q]] + 1]++;
+  for (int t = 0; t < nl; ++t) d.off[t + 1] += d.off[t];
+  std::vector<unsigned> cur(d.off.begin(), d.off.end() - 1);
+  d.smap.assign(static_cast<std::size_t>(e1 - e0) * 2 * nsurfp, 0);
+  d.idx.assign(d.off[nl], 0);
+  for (int le = 0; le < e1 - e0; ++le)
+    for (int q = 0; q < nsurf_raw; ++q) {
+      const gid g = num.l2g_surf[static_cast<std::size_t>(e0 + le) * nsurf_raw + q];
+      int* row = &d.smap[static_cast<std::size_t>(le) * 2 * nsurfp];
+      row[q] = num.dirichlet_mask[g] ? -g - 2 : g;  // encode_dirichlet
+      const unsigned pos = cur[loc[g]]++;
+      row[nsurfp + q] = static_cast<int>(pos);
+      d.idx[pos] = le * nsurfp + q;
+    }
+  return d;
+}
+
+namespace {
+
+// Element-slab partition of the Ax gather, uploaded.
+void build_dist_ax(Plan& pl, const HostSetup& hs, int /*nsurf_raw*/)
+{
+  DistLists d = dist_partition(hs, pl.rank, pl.nranks, pl.nsurf);
+  pl.n_grp0 = d.n_grp0;
+  pl.n_up = d.n_up;
+  pl.n_down = d.n_down;
+  pl.n_loc_surf = static_cast<int>(d.nodes.size());
+  DeviceArena& M = pl.mem;
+  pl.smap = M.upload(d.smap);
+  pl.ax_off = M.upload(d.off);
+  pl.ax_idx = M.upload(d.idx);
+  pl.ax_nodes = M.upload(d.nodes);
+  pl.n_ax_entries = d.off[pl.n_loc_surf];
+}
+
 void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, const double* c_e, const hxb_options& opt)
 {
   const auto t0 = std::chrono::steady_clock::now();
@@ -605,6 +942,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     HXB_CUDA(cudaGetDeviceProperties(&prop, pl.device));
     if (prop.major != 10) throw HxbError(HXB_ECUDA, "hexsem_b200 requires an sm_100 (B200) device");
     pl.num_sms = prop.multiProcessorCount;
+    g_num_sms = prop.multiProcessorCount;
   }
   HostSetup& hs = pl.hs;
   hs.mesh = mesh_from_arrays(m->num_vertices, m->xyz, m->num_elements, m->conn, m->num_boundary_faces,
@@ -626,7 +964,16 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   const int nsurf_raw = surface_slot_count(pl.np);
   pl.nsurf = (nsurf_raw + 3) & ~3;  // padded element stride of every surface-slot array (16 B aligned)
   pl.P = order + 3;
-  pl.ne = ne;
+  pl.nranks = std::max(1, opt.reserved[2]);
+  pl.rank = opt.reserved[1];
+  if (pl.nranks > 1) {
+    if (pl.rank < 0 || pl.rank >= pl.nranks) throw HxbError(HXB_EINVAL, "rank out of range");
+    if (opt.precond_mode != HXB_PRECOND_NONE)
+      throw HxbError(HXB_EINVAL, "distributed plans carry the operator only (precond_mode none)");
+    if (pl.nranks > ne) throw HxbError(HXB_EINVAL, "more ranks than elements");
+  }
+  pl.e0 = static_cast<int>(static_cast<long long>(ne) * pl.rank / pl.nranks);
+  pl.ne = static_cast<int>(static_cast<long long>(ne) * (pl.rank + 1) / pl.nranks) - pl.e0;
   pl.nv = mesh.num_vertices();
   pl.precond_mode = opt.precond_mode;
   pl.variant = opt.variant;
@@ -648,31 +995,41 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   for (cudaEvent_t* e : {&pl.ev_t0, &pl.ev_t1, &pl.ev_a}) HXB_CUDA(cudaEventCreate(e));
 
   DeviceArena& M = pl.mem;
+  const int e0 = pl.e0, nel = pl.ne;  // owned elements [e0, e0 + nel)
   {  // kappa*m*Gt planes regrouped per element: [e][6][nlocp] (one TMA stream per element)
     const int nlocp = (pl.nloc + 1) & ~1;
     const std::size_t total = static_cast<std::size_t>(ne) * pl.nloc;
-    std::vector<double> wge(static_cast<std::size_t>(ne) * 6 * nlocp, 0.0);
-    for (int e = 0; e < ne; ++e)
+    std::vector<double> wge(static_cast<std::size_t>(nel) * 6 * nlocp, 0.0);
+    for (int le = 0; le < nel; ++le)
       for (int p = 0; p < 6; ++p)
-        std::memcpy(&wge[(static_cast<std::size_t>(e) * 6 + p) * nlocp],
-                    &hs.geo.wg[p * total + static_cast<std::size_t>(e) * pl.nloc], pl.nloc * sizeof(double));
+        std::memcpy(&wge[(static_cast<std::size_t>(le) * 6 + p) * nlocp],
+                    &hs.geo.wg[p * total + static_cast<std::size_t>(e0 + le) * pl.nloc], pl.nloc * sizeof(double));
     pl.wg = M.upload(wge);
   }
   hs.geo.wg.clear();
   hs.geo.wg.shrink_to_fit();
-  pl.mass = M.upload(hs.geo.mass);
-  pl.c_e = M.upload(hs.c);
-  pl.kappa_e = M.upload(hs.kappa);
-  pl.h3 = M.upload(hs.geo.h);
+  auto slice = [&](const std::vector<double>& v, int per) {
+    return std::vector<double>(v.begin() + static_cast<std::size_t>(e0) * per,
+                               v.begin() + static_cast<std::size_t>(e0 + nel) * per);
+  };
+  pl.mass = M.upload(pl.nranks > 1 ? slice(hs.geo.mass, pl.nloc) : hs.geo.mass);
+  pl.c_e = M.upload(pl.nranks > 1 ? slice(hs.c, 1) : hs.c);
+  pl.kappa_e = M.upload(pl.nranks > 1 ? slice(hs.kappa, 1) : hs.kappa);
+  pl.h3 = M.upload(pl.nranks > 1 ? slice(hs.geo.h, 3) : hs.geo.h);
   pl.mask = M.upload(num.dirichlet_mask);
   pl.zero_mask = M.alloc<std::uint8_t>(pl.N);
   HXB_CUDA(cudaMemset(pl.zero_mask, 0, pl.N));
   pl.d_lumped = M.upload(hs.lumped);
+  {
+    std::vector<double> inv(hs.lumped.size());
+    for (std::size_t g = 0; g < inv.size(); ++g) inv[g] = 1.0 / hs.lumped[g];
+    pl.d_inv_lumped = M.upload(inv);
+  }
 
   // surface map [e][2][nsurf]: Dirichlet-encoded global ids and each copy's
   // position in the Ax surface CSR (copies of a node in ascending (e,l) order,
   // mesh.cpp:358-367) - producers write there, gathers stream contiguously
-  {
+  if (pl.nranks == 1) {
     std::vector<unsigned> off(static_cast<std::size_t>(pl.nsg) + 1, 0);
     for (gid g : num.l2g_surf) off[g + 1]++;
     for (int g = 0; g < pl.nsg; ++g) off[g + 1] += off[g];
@@ -693,8 +1050,11 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
       for (int q = 0; q < nsurf_raw; ++q)
         idx[smap[static_cast<std::size_t>(e) * 2 * pl.nsurf + pl.nsurf + q]] = e * pl.nsurf + q;
     pl.ax_idx = M.upload(idx);
+    pl.n_loc_surf = pl.n_grp0 = pl.nsg;
+  } else {
+    build_dist_ax(pl, hs, nsurf_raw);
   }
-  pl.rsurf = M.alloc<double>(static_cast<std::size_t>(ne) * pl.nsurf);
+  pl.rsurf = M.alloc<double>(static_cast<std::size_t>(pl.ne) * pl.nsurf);
 
   // fine: encoded sub_face and the subdomain gather CSR in (e, slot) order
   if (pl.do_fine) {
@@ -747,8 +1107,8 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.Z = M.alloc<double>(pl.nv);
     pl.rho = M.alloc<double>(pl.nv);
     pl.dZ = M.alloc<double>(pl.nv);
-    pl.psort = M.alloc<double>(pl.n_ax_entries);
-    pl.pint = M.alloc<double>(pl.N);
+    pl.Zc = M.alloc<double>(static_cast<std::size_t>(ne) * 8);
+    pl.esurf = M.alloc<double>(static_cast<std::size_t>(ne) * pl.nsurf);
     pl.coarse_n = hs.Kc.n;
     if (pl.use_amg) {
       pl.Kc = csr_to_device(pl, hs.Kc);
@@ -778,9 +1138,10 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
         pl.lv[l].b = M.alloc<double>(pl.lv[l].n);
         pl.lv[l].x = M.alloc<double>(pl.lv[l].n);
       }
-      dense_to_device(pl, amg.coarsest);
+      pl.dense = dense_to_device(pl, amg.coarsest);
+      pl.amg_cluster = (opt.reserved[0] & 1) == 0 && build_amg_cluster(pl, amg, hs.vmask);
     } else {
-      dense_to_device(pl, hs.Kc);
+      pl.dense = dense_to_device(pl, hs.Kc);
     }
   }
 
@@ -789,10 +1150,10 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     *v = M.alloc<double>(pl.N);
     HXB_CUDA(cudaMemset(*v, 0, sizeof(double) * pl.N));
   }
-  const int npart = ax_elem_grid(pl) + 8 * 148 * 4;
+  const int npart = ax_elem_grid(pl) + 64 * pl.num_sms;  // elem-kernel partials + any one-wave grid
   pl.partials = M.alloc<double>(npart);
   pl.ticket = M.alloc<unsigned>(1);
-  pl.cpartials = M.alloc<double>(8 * 148 * 4);
+  pl.cpartials = M.alloc<double>(64 * pl.num_sms);
   pl.cticket = M.alloc<unsigned>(1);
   HXB_CUDA(cudaMemset(pl.ticket, 0, sizeof(unsigned)));
   HXB_CUDA(cudaMemset(pl.cticket, 0, sizeof(unsigned)));
@@ -825,7 +1186,7 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
   cudaStream_t s = pl.s_main;
   const int n = pl.N;
   HXB_CUDA(cudaEventRecord(pl.ev_t0, s));
-  pcg_init_kernel<kVecBlock><<<vec_grid(n), kVecBlock, 0, s>>>(pl.b, pl.r, pl.u, n, dot_args(pl, pl.res2));
+  pcg_init_kernel<kVecBlock><<<fill_grid(pcg_init_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(pl.b, pl.r, pl.u, n, dot_args(pl, pl.res2));
   sqrt_store_kernel<<<1, 1, 0, s>>>(pl.res2, pl.res_hist);
   pl.launches += 2;
   HXB_CUDA(cudaMemcpyAsync(pl.h_status, pl.res_hist, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -835,12 +1196,12 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
   std::string diag;
   if (r0 != 0.0) {
     enqueue_precond(pl, nullptr);
-    copy_dot_kernel<kVecBlock><<<vec_grid(n), kVecBlock, 0, s>>>(pl.z, pl.r, pl.p, n, dot_args(pl, pl.zr_hist));
+    copy_dot_kernel<kVecBlock><<<fill_grid(copy_dot_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(pl.z, pl.r, pl.p, n, dot_args(pl, pl.zr_hist));
     pl.launches += 1;
     status = HXB_PCG_MAX_ITERATIONS;
     for (int k = 0; k < cfg.max_iterations; ++k) {
       enqueue_ax(pl, pl.p, pl.f, pl.pf_hist + k, s);
-      pcg_update_kernel<kVecBlock><<<vec_grid(n), kVecBlock, 0, s>>>(pl.f, pl.r, n, pl.zr_hist, pl.pf_hist, k,
+      pcg_update_kernel<kVecBlock><<<fill_grid(pcg_update_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(pl.f, pl.r, n, pl.zr_hist, pl.pf_hist, k,
                                                                      dot_args(pl, pl.res2));
       sqrt_store_kernel<<<1, 1, 0, s>>>(pl.res2, pl.res_hist + k + 1);
       pl.launches += 2;
@@ -860,18 +1221,18 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
       iterations = k + 1;
       if (rn / r0 <= cfg.rel_tolerance) {
         status = HXB_PCG_CONVERGED;
-        pcg_final_kernel<<<vec_grid(n), kVecBlock, 0, s>>>(pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
+        pcg_final_kernel<<<fill_grid(pcg_final_kernel, kVecBlock, n), kVecBlock, 0, s>>>(pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
         pl.launches += 1;
         break;
       }
       if (k + 1 == cfg.max_iterations) {
-        pcg_final_kernel<<<vec_grid(n), kVecBlock, 0, s>>>(pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
+        pcg_final_kernel<<<fill_grid(pcg_final_kernel, kVecBlock, n), kVecBlock, 0, s>>>(pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
         pl.launches += 1;
         diag = "not converged within " + std::to_string(cfg.max_iterations) + " iterations";
         break;
       }
       enqueue_precond(pl, pl.zr_hist + k + 1);
-      pcg_dir_kernel<<<vec_grid(n), kVecBlock, 0, s>>>(pl.z, pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
+      pcg_dir_kernel<<<fill_grid(pcg_dir_kernel, kVecBlock, n), kVecBlock, 0, s>>>(pl.z, pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
       pl.launches += 1;
     }
   }
@@ -959,6 +1320,7 @@ int hxb_apply_A_device(hxb_plan* plan, const double* d_u, double* d_r, void* str
 {
   return guarded([&] {
     Plan* pl = as_plan(plan);
+    if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use hxb_dist_apply_A_*");
     HXB_CUDA(cudaSetDevice(pl->device));
     cudaStream_t s = pl->s_main;
     if (stream) {
@@ -980,6 +1342,7 @@ int hxb_apply_A(hxb_plan* plan, const double* u, double* r)
 {
   return guarded([&] {
     Plan* pl = as_plan(plan);
+    if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use hxb_dist_apply_A_*");
     HXB_CUDA(cudaSetDevice(pl->device));
     const std::size_t bytes = sizeof(double) * pl->N;
     HXB_CUDA(cudaMemcpyAsync(pl->p, u, bytes, cudaMemcpyHostToDevice, pl->s_main));
@@ -1006,14 +1369,11 @@ static int apply_precond_host(hxb_plan* plan, const double* r, double* z, int mo
       // component-only applies (FinePreconditioner::apply / CoarsePreconditioner::apply):
       // run the requested branch and a combine without the mask/identity rows
       const bool f = mode == HXB_PRECOND_FINE_ONLY, c = mode == HXB_PRECOND_COARSE_ONLY;
-      if (c) {
-        HXB_CUDA(cudaEventRecord(pl->ev_fork, pl->s_main));
-        HXB_CUDA(cudaStreamWaitEvent(pl->s_coarse, pl->ev_fork, 0));
-        HXB_CUDA(cudaGraphLaunch(pl->coarse_exec, pl->s_coarse));
-        HXB_CUDA(cudaEventRecord(pl->ev_join, pl->s_coarse));
-        HXB_CUDA(cudaStreamWaitEvent(pl->s_main, pl->ev_join, 0));
-      }
       if (f) HXB_DISPATCH_NP(pl->np, launch_fdm, *pl, pl->s_main);
+      if (c) {
+        HXB_DISPATCH_NP(pl->np, launch_restrict, *pl, pl->s_main);
+        HXB_CUDA(cudaGraphLaunch(pl->coarse_exec, pl->s_main));
+      }
       // FinePreconditioner::apply / CoarsePreconditioner::apply have no mask
       // rows; emulate with a mask-free combine by temporarily pointing at a zero mask
       std::uint8_t* saved = pl->mask;
@@ -1071,6 +1431,7 @@ int hxb_solve(hxb_plan* plan, const double* b, const hxb_pcg_config* cfg, hxb_pc
 {
   return guarded([&] {
     Plan* pl = as_plan(plan);
+    if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans support the staged operator only");
     if (!cfg || !res) throw HxbError(HXB_EINVAL, "null argument");
     HXB_CUDA(cudaSetDevice(pl->device));
     if (b)
@@ -1085,6 +1446,7 @@ int hxb_solve_device(hxb_plan* plan, const double* d_b, const hxb_pcg_config* cf
 {
   return guarded([&] {
     Plan* pl = as_plan(plan);
+    if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans support the staged operator only");
     if (!cfg || !res) throw HxbError(HXB_EINVAL, "null argument");
     HXB_CUDA(cudaSetDevice(pl->device));
     if (d_b && d_b != pl->b)
@@ -1145,30 +1507,46 @@ int hxb_profile(hxb_plan* plan, int reps, double* out)
       HXB_CUDA(cudaEventElapsedTime(&ms, pl->ev_t0, pl->ev_t1));
       return static_cast<double>(ms) / reps;
     };
-    for (int q = 0; q < 12; ++q) out[q] = 0;
+    for (int q = 0; q < 16; ++q) out[q] = 0;
     ensure_hist(*pl, 4);
     out[0] = timeit([&] { HXB_DISPATCH_NP(pl->np, launch_ax_elem, *pl, pl->p, pl->f, DotArgs{}, s); });
     out[1] = timeit([&] { enqueue_ax(*pl, pl->p, pl->f, nullptr, s); }) - out[0];
     if (pl->do_fine) out[2] = timeit([&] { HXB_DISPATCH_NP(pl->np, launch_fdm, *pl, s); });
-    if (pl->do_coarse) out[3] = timeit([&] { HXB_CUDA(cudaGraphLaunch(pl->coarse_exec, s)); });
+    if (pl->do_coarse) out[3] = timeit([&] { HXB_CUDA(cudaGraphLaunch(pl->coarse_exec, s)); });  // after Rpart
     out[4] = timeit([&] { launch_combine(*pl, pl->zr_hist, s, pl->do_fine, pl->do_coarse); });
+    if (pl->do_fine) out[12] = timeit([&] { launch_combine(*pl, pl->zr_hist, s, true, false); });
+    if (pl->do_coarse) out[13] = timeit([&] { launch_combine(*pl, pl->zr_hist, s, false, true); });
     out[5] = timeit([&] { enqueue_precond(*pl, pl->zr_hist); });
     HXB_CUDA(cudaMemcpy(pl->pf_hist, pl->zr_hist, sizeof(double), cudaMemcpyDeviceToDevice));
     out[6] = timeit([&] {
-      pcg_update_kernel<kVecBlock><<<vec_grid(pl->N), kVecBlock, 0, s>>>(pl->f, pl->r, pl->N, pl->zr_hist, pl->pf_hist,
+      pcg_update_kernel<kVecBlock><<<fill_grid(pcg_update_kernel<kVecBlock>, kVecBlock, pl->N), kVecBlock, 0, s>>>(pl->f, pl->r, pl->N, pl->zr_hist, pl->pf_hist,
                                                                          0, dot_args(*pl, pl->res2));
     });
     out[7] = timeit([&] {
-      pcg_dir_kernel<<<vec_grid(pl->N), kVecBlock, 0, s>>>(pl->z, pl->p, pl->u, pl->N, pl->zr_hist, pl->pf_hist, 0);
+      pcg_dir_kernel<<<fill_grid(pcg_dir_kernel, kVecBlock, pl->N), kVecBlock, 0, s>>>(pl->z, pl->p, pl->u, pl->N, pl->zr_hist, pl->pf_hist, 0);
     });
     if (pl->do_coarse) {
-      out[8] = timeit([&] {
-        HXB_DISPATCH_NP(pl->np, launch_restrict, *pl, s);
-        vertex_gather_kernel<<<vec_grid(pl->nv), kVecBlock, 0, s>>>(pl->Rpart, pl->vtx_off, pl->vtx_idx, pl->vmask,
-                                                                     pl->R, pl->nv);
-      });
-      out[9] = timeit([&] { HXB_DISPATCH_NP(pl->np, launch_prolong, *pl, s); });
-      out[10] = out[3] - out[8] - out[9];
+      // standalone restriction (used without a fine branch; fused into FDM otherwise)
+      out[8] = timeit([&] { HXB_DISPATCH_NP(pl->np, launch_restrict, *pl, s); });
+      out[9] = timeit([&] { launch_prolong(*pl, s); });
+      out[10] = out[3] - out[9];  // vertex gather + AMG / dense solve
+      if (pl->amg_cluster) {       // one ksolve(1) cluster kernel alone
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(pl->cluster_size);
+        cfg.blockDim = dim3(kAmgClusterBlock);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = pl->cluster_size;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CLev& c1 = pl->cargs.lev[0];
+        out[11] = timeit([&] {
+          HXB_CUDA(cudaLaunchKernelEx(&cfg, amg_cluster_kernel, pl->cargs, static_cast<const double*>(c1.b), c1.x));
+        });
+      }
     }
     HXB_CUDA(cudaGetLastError());
   });
@@ -1198,6 +1576,98 @@ int hxb_bench_apply_A(hxb_plan* plan, int reps, double* ms_per_apply, double* ms
       *ms_elem_kernel = ms / reps;
     }
     HXB_CUDA(cudaGetLastError());
+  });
+}
+
+// ---- distributed Ax (element-slab partition) ---------------------------------
+static void dist_stream_in(Plan* pl, void* stream)
+{
+  if (stream) {
+    HXB_CUDA(cudaEventRecord(pl->ev_a, static_cast<cudaStream_t>(stream)));
+    HXB_CUDA(cudaStreamWaitEvent(pl->s_main, pl->ev_a, 0));
+  }
+}
+static void dist_stream_out(Plan* pl, void* stream)
+{
+  HXB_CUDA(cudaGetLastError());
+  if (stream) {
+    HXB_CUDA(cudaEventRecord(pl->ev_a, pl->s_main));
+    HXB_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), pl->ev_a, 0));
+  } else {
+    HXB_CUDA(cudaStreamSynchronize(pl->s_main));
+  }
+}
+
+int hxb_dist_info(hxb_plan* plan, int64_t* info)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (!info) throw HxbError(HXB_EINVAL, "null argument");
+    const int64_t v[8] = {pl->rank, pl->nranks, pl->e0, pl->e0 + pl->ne, pl->n_up, pl->n_down, pl->n_grp0, pl->N};
+    std::memcpy(info, v, sizeof(v));
+  });
+}
+
+int hxb_dist_lists(hxb_plan* plan, int32_t* up_nodes, int32_t* down_nodes)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    if (pl->nranks == 1) return;
+    if (up_nodes && pl->n_up)
+      HXB_CUDA(cudaMemcpy(up_nodes, pl->ax_nodes + pl->n_grp0, sizeof(int) * pl->n_up, cudaMemcpyDeviceToHost));
+    if (down_nodes && pl->n_down)
+      HXB_CUDA(cudaMemcpy(down_nodes, pl->ax_nodes + pl->n_grp0 + pl->n_up, sizeof(int) * pl->n_down,
+                          cudaMemcpyDeviceToHost));
+  });
+}
+
+int hxb_dist_apply_A_begin(hxb_plan* plan, const double* d_u, double* d_r, double* d_send_up, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    dist_stream_in(pl, stream);
+    enqueue_ax(*pl, d_u, d_r, nullptr, pl->s_main);  // owned elements + group-0 nodes
+    if (pl->n_up) {
+      dist_partial_kernel<<<vec_grid(pl->n_up), kVecBlock, 0, pl->s_main>>>(pl->ax_off + pl->n_grp0, pl->ax_idx, pl->rsurf,
+                                                                             pl->n_up, d_send_up);
+      pl->launches += 1;
+    }
+    dist_stream_out(pl, stream);
+  });
+}
+
+int hxb_dist_apply_A_continue(hxb_plan* plan, const double* d_u, double* d_r, const double* d_recv_down,
+                              double* d_send_down, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    dist_stream_in(pl, stream);
+    if (pl->n_down) {
+      const int t0 = pl->n_grp0 + pl->n_up;
+      dist_continue_kernel<<<vec_grid(pl->n_down), kVecBlock, 0, pl->s_main>>>(
+          pl->ax_off + t0, pl->ax_idx, pl->rsurf, pl->ax_nodes + t0, pl->n_down, d_u, pl->mask, d_recv_down, d_r,
+          d_send_down);
+      pl->launches += 1;
+    }
+    dist_stream_out(pl, stream);
+  });
+}
+
+int hxb_dist_apply_A_end(hxb_plan* plan, double* d_r, const double* d_recv_up, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    dist_stream_in(pl, stream);
+    if (pl->n_up) {
+      dist_finish_kernel<<<vec_grid(pl->n_up), kVecBlock, 0, pl->s_main>>>(pl->ax_nodes + pl->n_grp0, pl->n_up, d_recv_up,
+                                                                            d_r);
+      pl->launches += 1;
+    }
+    dist_stream_out(pl, stream);
   });
 }
 

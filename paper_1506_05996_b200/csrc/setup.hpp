@@ -187,6 +187,20 @@ struct HostSetup {
 };
 
 void build_host_setup(HostSetup& hs, int order, const SetupOptions& opt);  // hs.mesh, kappa, c pre-filled
+
+// Element-slab partition of the Ax assembly for rank `rank` of `nranks`
+// (SURVEY §8e): owned elements [e0, e1); local surface nodes ordered
+// [group 0 | up-interface | down-interface], each ascending global id;
+// local Ax CSR (copies in (e,l) order) and the [e][2][nsurfp] surface map.
+struct DistLists {
+  int e0 = 0, e1 = 0;
+  int n_grp0 = 0, n_up = 0, n_down = 0;
+  std::vector<int> nodes;
+  std::vector<unsigned> off;
+  std::vector<int> idx;
+  std::vector<int> smap;
+};
+DistLists dist_partition(const HostSetup& hs, int rank, int nranks, int nsurfp);
 HexMesh mesh_from_arrays(int nv, const double* xyz, int ne, const std::int32_t* conn, int nbf,
                          const std::int32_t* be, const std::int32_t* bf, const std::uint8_t* bt);
 // IndexMaps export in the reference layout (mesh.hpp:66-97); null pointers skipped.

@@ -100,12 +100,18 @@ SIGNATURES = {
     "hxb_kernel_timing": (C.c_int, [P, C.c_int, C.c_int]),
     "hxb_kernel_timing_read": (C.c_int, [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int)]),
     "hxb_launch_count": (C.c_int, [P, C.POINTER(C.c_int64)]),
+    "hxb_dist_info": (C.c_int, [P, P]),
+    "hxb_dist_lists": (C.c_int, [P, P, P]),
+    "hxb_dist_apply_A_begin": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hxb_dist_apply_A_continue": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hxb_dist_apply_A_end": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hxb_setup_create": (C.c_int, [C.POINTER(_Mesh), C.c_int, P, P, C.POINTER(_Options), C.POINTER(P)]),
     "hxb_setup_destroy": (None, [P]),
     "hxb_setup_info": (C.c_int, [P, C.POINTER(_PlanInfo)]),
     "hxb_setup_export_maps": (C.c_int, [P, P, P, P, P, P, P]),
     "hxb_setup_amg_level": (C.c_int, [P, C.c_int, P, P, P, P, P, P]),
     "hxb_setup_lumped_mass": (C.c_int, [P, P]),
+    "hxb_setup_dist_lists": (C.c_int, [P, C.c_int, C.c_int, P, P]),
     "hxb_gll": (C.c_int, [C.c_int, P, P, P]),
     "hxb_pencil": (C.c_int, [C.c_int, P, P, P, P, P]),
     "hxb_words_model": (C.c_uint64, [C.c_int64, C.c_int, C.c_int]),
@@ -259,7 +265,7 @@ class Plan:
 
     def __init__(self, mesh: HexMesh, order: int, kappa_e=None, c_e=None, *, precond: str = "two_scale",
                  coarse_solve: str = "automatic", direct_threshold: int = 64000, variant: str = "stored",
-                 device: int = 0):
+                 device: int = 0, amg_cluster: bool = True, rank: int = 0, nranks: int = 1):
         L = lib()
         ne = mesh.num_elements
         self.mesh = mesh
@@ -272,6 +278,9 @@ class Plan:
         opt.direct_threshold = direct_threshold
         opt.variant = VARIANTS[variant]
         opt.device = device
+        opt.reserved[0] = 0 if amg_cluster else 1
+        opt.reserved[1] = rank
+        opt.reserved[2] = nranks
         cm = mesh._c()
         h = C.c_void_p()
         _check(L.hxb_plan_create(C.byref(cm), order, _ptr(self.kappa_e), _ptr(self.c_e), C.byref(opt), C.byref(h)))
@@ -411,11 +420,37 @@ class Plan:
 
     def profile(self, reps: int = 10) -> dict:
         """Per-component device times in ms (CUDA events, warm caches)."""
-        out = np.zeros(12)
+        out = np.zeros(16)
         _check(lib().hxb_profile(self._h, reps, _ptr(out)))
         keys = ["ax_elem", "ax_gather", "fdm", "coarse", "combine", "precond", "pcg_update", "pcg_dir",
-                "restrict", "prolong", "amg"]
+                "restrict", "prolong", "amg", "amg_ksolve1_cluster", "combine_fine_only", "combine_coarse_only"]
         return dict(zip(keys, out.tolist()))
+
+    # --- distributed operator (element-slab partition, hxb_dist_*) -------------
+    def dist_info(self) -> dict:
+        v = np.zeros(8, dtype=np.int64)
+        _check(lib().hxb_dist_info(self._h, _ptr(v)))
+        keys = ["rank", "nranks", "e0", "e1", "n_up", "n_down", "n_group0", "N"]
+        return dict(zip(keys, (int(x) for x in v)))
+
+    def dist_lists(self):
+        info = self.dist_info()
+        up = np.zeros(max(1, info["n_up"]), dtype=np.int32)
+        down = np.zeros(max(1, info["n_down"]), dtype=np.int32)
+        _check(lib().hxb_dist_lists(self._h, _ptr(up), _ptr(down)))
+        return up[:info["n_up"]], down[:info["n_down"]]
+
+    def dist_apply_A_begin(self, d_u: int, d_r: int, d_send_up: int, stream: int = 0):
+        _check(lib().hxb_dist_apply_A_begin(self._h, C.c_void_p(d_u), C.c_void_p(d_r), C.c_void_p(d_send_up or None),
+                                            C.c_void_p(stream or None)))
+
+    def dist_apply_A_continue(self, d_u: int, d_r: int, d_recv_down: int, d_send_down: int, stream: int = 0):
+        _check(lib().hxb_dist_apply_A_continue(self._h, C.c_void_p(d_u), C.c_void_p(d_r), C.c_void_p(d_recv_down or None),
+                                               C.c_void_p(d_send_down or None), C.c_void_p(stream or None)))
+
+    def dist_apply_A_end(self, d_r: int, d_recv_up: int, stream: int = 0):
+        _check(lib().hxb_dist_apply_A_end(self._h, C.c_void_p(d_r), C.c_void_p(d_recv_up or None),
+                                          C.c_void_p(stream or None)))
 
     KT_TAGS = {"ax_elem": 0, "ax_gather": 1, "fdm": 2, "combine": 3}
 
@@ -515,6 +550,15 @@ class HostSetup:
         m = np.empty(self.N)
         _check(lib().hxb_setup_lumped_mass(self._h, _ptr(m)))
         return m
+
+    def dist_lists(self, rank: int, nranks: int) -> dict:
+        """Element-slab partition lists of one rank (hxb_setup_dist_lists)."""
+        cnt = np.zeros(6, dtype=np.int64)
+        _check(lib().hxb_setup_dist_lists(self._h, rank, nranks, _ptr(cnt), None))
+        nodes = np.zeros(max(1, int(cnt[5])), dtype=np.int32)
+        _check(lib().hxb_setup_dist_lists(self._h, rank, nranks, _ptr(cnt), _ptr(nodes)))
+        e0, e1, n0, nu, nd, nl = (int(x) for x in cnt)
+        return {"e0": e0, "e1": e1, "group0": nodes[:n0], "up": nodes[n0:n0 + nu], "down": nodes[n0 + nu:nl]}
 
 
 def gll(order: int):

@@ -39,3 +39,12 @@ def history_parity(ours: dict, ref: dict, tol=1e-10, iters_slack=1, per_rk=False
     if ours.get("u") is not None:
         assert rel(ours["u"], ref["u"]) <= tol, rel(ours["u"], ref["u"])
     return dr
+
+
+def rounding_noise(ref_result: dict, fma_result: dict) -> float:
+    """max_k |dr_k|/r_0 between the reference and its FMA-contracted
+    restatement on the same problem: how far rounding alone moves this
+    problem's residual history (SURVEY §8c parity study)."""
+    ra, rb = np.asarray(fma_result["residual_history"]), np.asarray(ref_result["residual_history"])
+    k = min(len(ra), len(rb))
+    return float(np.max(np.abs(ra[:k] - rb[:k])) / rb[0])

@@ -1,0 +1,32 @@
+"""Per-launch table of key ncu metrics from a .ncu-rep (run here, no GPU)."""
+import csv, subprocess, sys, io
+rep = sys.argv[1]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+h, u = rows[0], rows[1]
+keys = [("gpu__time_duration.sum", "us", 1e-3), ("dram__bytes_read.sum", "MB", None), ("dram__bytes_write.sum", "MB", None),
+        ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram%", 1), ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm%", 1),
+        ("l1tex__throughput.avg.pct_of_peak_sustained_active", "l1%", 1), ("sm__warps_active.avg.pct_of_peak_sustained_active", "occ%", 1),
+        ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64%", 1), ("launch__registers_per_thread", "regs", 1),
+        ("launch__grid_size", "grid", 1)]
+def conv(v, unit):
+    x = float(v.replace(",", ""))
+    if unit in ("Gbyte",): return x * 1e3
+    if unit in ("Kbyte",): return x * 1e-3
+    if unit in ("byte",): return x * 1e-6
+    if unit == "Mbyte": return x
+    if unit == "msecond": return x * 1e3
+    if unit == "usecond": return x
+    if unit == "nsecond": return x * 1e-3
+    return x
+idx = {k: h.index(k) for k, _, _ in keys if k in h}
+print(f"{'kernel':34s} " + " ".join(f"{lab:>8s}" for _, lab, _ in keys))
+for r in rows[2:]:
+    name = r[h.index("Kernel Name")].split("(")[0][:34]
+    vals = []
+    for k, lab, _ in keys:
+        if k in idx:
+            vals.append(f"{conv(r[idx[k]], u[idx[k]]):8.1f}")
+        else:
+            vals.append(f"{'-':>8s}")
+    print(f"{name:34s} " + " ".join(vals))
