@@ -317,13 +317,23 @@ def run_ours(args, rank, world, local_rank):
                "r0": float(res["residual_history"][0]), "r_final": float(res["residual_history"][-1]),
                "u_norm2": float(np.linalg.norm(res_e2e["u"]))}
         gold_path = os.path.join(ROOT, "tests", "golden", "cfg2_pcg.json")
+        exact_path = os.path.join(ROOT, "tests", "golden", "cfg2_oracle_exactdot.json")
         if (k, order) == (52, 7) and os.path.exists(gold_path):
             gold = json.load(open(gold_path))
             rh = np.asarray(res["residual_history"])
             gh = np.asarray(gold["residual_history"])
             m = min(len(rh), len(gh))
+            ex = None
+            if os.path.exists(exact_path):
+                eh = np.asarray(json.load(open(exact_path))["1"]["residual_history"])
+                me = min(len(rh), len(eh))
+                ex = {"max_abs_dr_over_rk_vs_exact_dot_oracle": float(np.max(np.abs(rh[:me] - eh[:me]) / eh[:me])),
+                      "reference_own_dot_rounding_floor": float(np.max(np.abs(eh[:min(len(eh), len(gh))] -
+                                                                             gh[:min(len(eh), len(gh))]) /
+                                                                      gh[:min(len(eh), len(gh))]))}
             pcg["parity_vs_reference"] = {
                 "ref_iterations": gold["iterations"],
+                "exact_dot": ex,
                 "max_abs_dr_over_r0": float(np.max(np.abs(rh[:m] - gh[:m])) / gh[0]),
                 "max_abs_dr_over_rk": float(np.max(np.abs(rh[:m] - gh[:m]) / gh[:m])),
                 "u_norm2_rel_diff": abs(pcg["u_norm2"] - gold["u_norm2"]) / gold["u_norm2"],

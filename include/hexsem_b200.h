@@ -80,7 +80,9 @@ typedef struct hxb_options {
   int variant;                 /* HXB_VARIANT_* (default stored) */
   int device;                  /* CUDA device ordinal for this plan */
   int reserved[7];             /* reserved[0] bit 0: run the AMG K-cycle as one kernel per step
-                                  instead of the default single cluster kernel (A/B checks);
+                                  instead of the default single cluster kernel; bit 2: persistent
+                                  TMA/cp.async-pipelined FDM kernel instead of one CTA per
+                                  subdomain (measured slower at cfg2, kept for A/B checks);
                                   reserved[1] = rank, reserved[2] = number of ranks: element-slab
                                   partition for the distributed operator (hxb_dist_*) */
 } hxb_options;

@@ -13,74 +13,6 @@ namespace hxb {
 
 constexpr double kJacobiOmega = 2.0 / 3.0;  // amg.cpp:44
 
-// Per element: Rpart[e*8+cb] = sum_l B[cb][l] * (r/m_N)[l] * m[l]
-// (restrict_residual, coarse.cpp:144-160; r masked, precond.cpp:35). Element
-// tile of NP x NP threads, each owning a k-column; the 8 corner sums are
-// reduced across the tile in a fixed tree.
-template <int NP, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) restrict_kernel(const double* __restrict__ r, const double* __restrict__ lumped,
-                                                         const int* __restrict__ smap, const double* __restrict__ mass,
-                                                         double* __restrict__ Rpart, int ne, int sstride, int nsg)
-{
-  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NW = BLOCK / 32;
-  const OrderTables& T = c_tab[NP];
-  __shared__ double red[NW][8];
-  __shared__ double hk0[NP], hk1[NP];
-  const int tid = threadIdx.x;
-  const int e = blockIdx.x;
-  const bool ok = tid < NP * NP;
-  const int i = (ok ? tid : 0) % NP, j = (ok ? tid : 0) / NP;
-  if (tid < NP) {
-    hk0[tid] = T.hat0[tid];
-    hk1[tid] = T.hat1[tid];
-  }
-  const double hi[2] = {T.hat0[i], T.hat1[i]}, hj[2] = {T.hat0[j], T.hat1[j]};
-  const int* surf = smap + (long long)e * sstride;
-  const long long ibase = (long long)nsg + (long long)e * NI;
-  const double* m0 = mass + (std::size_t)e * NP * NP * NP + j * NP + i;
-  double y[NP];
-#pragma unroll
-  for (int k = 0; k < NP; ++k) {
-    double v = 0.0;
-    if (ok) {
-      const int s = surface_slot(NP, i, j, k);
-      if (s < 0) {
-        const long long g = ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1);
-        v = __ldg(r + g) / __ldg(lumped + g);
-      } else {
-        const int code = __ldg(surf + s);
-        v = code >= 0 ? __ldg(r + code) / __ldg(lumped + code) : 0.0;
-      }
-    }
-    y[k] = v;
-  }
-  __syncthreads();
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (ok) {
-#pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const double ym = __ldg(m0 + k * NP * NP);
-      const double hk[2] = {hk0[k], hk1[k]};
-#pragma unroll
-      for (int cb = 0; cb < 8; ++cb) acc[cb] += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[cb >> 2] * y[k] * ym;
-    }
-  }
-  const int lane = tid & 31, warp = tid >> 5;
-#pragma unroll
-  for (int cb = 0; cb < 8; ++cb) {
-    double v = acc[cb];
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    if (lane == 0) red[warp][cb] = v;
-  }
-  __syncthreads();
-  if (tid < 8) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) s += red[w][tid];
-    Rpart[8 * e + tid] = s;
-  }
-}
-
 // Restriction, warp per element (restrict_residual, coarse.cpp:138-162, on
 // the masked residual, precond.cpp:35): R_cb(e) = sum_l B[cb][l] y_l m_l with
 // y = r / m_N. B is the tensor product of the two linear hats, so the sum is
@@ -178,37 +110,6 @@ __global__ void __launch_bounds__(256) restrict_warp_kernel(const double* __rest
   }
 }
 
-// Prolongation of every element-surface copy (coarse.cpp:170-181):
-// esurf[e][slot] = (sum_cb B[cb][l] Z[v_cb]) * m[e][l], element-major so the
-// writes are coalesced; the combine gathers them through the Ax CSR lists.
-template <int NP>
-__global__ void prolong_surface_kernel(const double* __restrict__ Z, const int* __restrict__ conn,
-                                       const double* __restrict__ mass, double* __restrict__ esurf, int ne)
-{
-  constexpr int NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2), NSP = (NS + 3) & ~3;
-  constexpr int kCorner[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // kHexCornerFromBits, mesh.hpp:33
-  __shared__ double h0[NP], h1[NP];
-  if (threadIdx.x < NP) {
-    h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
-    h1[threadIdx.x] = c_tab[NP].hat1[threadIdx.x];
-  }
-  __syncthreads();
-  const long long total = (long long)ne * NSP;
-  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < total; q += (long long)gridDim.x * blockDim.x) {
-    const long long e = q / NSP;
-    const int sl = static_cast<int>(q - e * NSP);
-    if (sl >= NS) continue;
-    int i, j, k;
-    surface_ijk<NP>(sl, i, j, k);
-    const double hi[2] = {h0[i], h1[i]}, hj[2] = {h0[j], h1[j]}, hk[2] = {h0[k], h1[k]};
-    double s = 0.0;
-#pragma unroll
-    for (int cb = 0; cb < 8; ++cb)
-      s += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[cb >> 2] * __ldg(Z + __ldg(conn + 8 * e + kCorner[cb]));
-    esurf[q] = s * __ldg(mass + e * NP * NP * NP + (k * NP + j) * NP + i);
-  }
-}
-
 // Zc[8e + cb] = Z[vertex of corner cb of e] (the 8 coarse values each element
 // prolongates, coarse.cpp:170-171), so the fused combine reads one 64-byte
 // block per element copy instead of 8 dependent gathers.
@@ -220,46 +121,6 @@ __global__ void corner_values_kernel(const double* __restrict__ Z, const int* __
     const long long e = q >> 3;
     const int cb = static_cast<int>(q & 7);
     Zc[q] = __ldg(Z + __ldg(conn + 8 * e + kCorner[cb]));
-  }
-}
-
-// Prolongation per element copy (coarse.cpp:164-182): p_l = (sum_cb B[cb][l]
-// Z[v_cb]) * m_l, stored like Ax outputs (element-interior nodes direct into
-// pint, element-surface copies at their CSR position in psort) for the
-// deterministic gather in combine_kernel. The 8 corner values are loaded once
-// per element.
-template <int NP, int EPB, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) prolong_elem_kernel(const double* __restrict__ Z, const int* __restrict__ conn,
-                                                             const double* __restrict__ mass, const int* __restrict__ smap,
-                                                             double* __restrict__ psort, double* __restrict__ pint, int ne,
-                                                             int nsurfp, int nsg)
-{
-  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1);
-  const OrderTables& T = c_tab[NP];
-  const int tid = threadIdx.x;
-  const int el = tid / (NP * NP), loc = tid % (NP * NP);
-  const int i = loc % NP, j = loc / NP;
-  const int e = blockIdx.x * EPB + el;
-  if (el >= EPB || e >= ne) return;
-  constexpr int kCorner[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // kHexCornerFromBits, mesh.hpp:33
-  double zc[8];
-#pragma unroll
-  for (int cb = 0; cb < 8; ++cb) zc[cb] = __ldg(Z + __ldg(conn + 8 * e + kCorner[cb]));
-  const double hi[2] = {T.hat0[i], T.hat1[i]}, hj[2] = {T.hat0[j], T.hat1[j]};
-  const long long ibase = (long long)nsg + (long long)e * NI;
-  const double* m0 = mass + (std::size_t)e * NP * NP * NP + j * NP + i;
-#pragma unroll
-  for (int k = 0; k < NP; ++k) {
-    const double hk[2] = {T.hat0[k], T.hat1[k]};
-    double s = 0.0;
-#pragma unroll
-    for (int cb = 0; cb < 8; ++cb) s += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[cb >> 2] * zc[cb];
-    const double v = s * __ldg(m0 + k * NP * NP);
-    const int sl = surface_slot(NP, i, j, k);
-    if (sl >= 0)
-      psort[__ldg(smap + (long long)e * 2 * nsurfp + nsurfp + sl)] = v;  // CSR position
-    else
-      pint[ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1)] = v;
   }
 }
 

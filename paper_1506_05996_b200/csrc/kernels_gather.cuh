@@ -17,34 +17,7 @@ namespace hxb {
 constexpr int kGatherBlock = 256;
 constexpr int kGatherCap = 320;  // staged values per warp (avg ~1.5-2.6 per node)
 
-// Sum vals[off[g] .. off[g+1]) left to right for the warp's 32 consecutive
-// nodes. The producers wrote each contribution at its CSR position, so the
-// warp's whole segment is contiguous: one coalesced sweep into the staging
-// buffer, then a sequential per-lane sum (reference order).
-__device__ __forceinline__ double warp_seg_sum(const unsigned* __restrict__ off, const double* __restrict__ vals, int g0,
-                                               int n, double* __restrict__ stage)
-{
-  const int lane = threadIdx.x & 31;
-  const int g = g0 + lane;
-  const unsigned my0 = __ldg(off + min(g, n));
-  const unsigned my1 = __ldg(off + min(g + 1, n));
-  const unsigned base = __shfl_sync(0xffffffffu, my0, 0);
-  const unsigned end = __shfl_sync(0xffffffffu, my1, 31);
-  const unsigned cnt = end - base;
-  double s = 0.0;
-  if (cnt <= static_cast<unsigned>(kGatherCap)) {
-#pragma unroll 4
-    for (unsigned c = lane; c < cnt; c += 32) stage[c] = __ldcs(vals + base + c);
-    __syncwarp();
-    for (unsigned q = my0 - base; q < my1 - base; ++q) s += stage[q];
-    __syncwarp();
-  } else {
-    for (unsigned q = my0; q < my1; ++q) s += __ldcs(vals + q);
-  }
-  return s;
-}
-
-// Same, for values scattered in an E-vector: src(idx[q]) gathered by the warp
+// Sums for a warp's 32 consecutive nodes of values scattered in an E-vector: src(idx[q]) gathered by the warp
 // (coalesced index segment, parallel value loads), then per-lane sequential sums.
 template <class Src>
 __device__ __forceinline__ double warp_csr_sum(const unsigned* __restrict__ off, const int* __restrict__ idx, Src&& src,
@@ -149,64 +122,6 @@ __global__ void dist_finish_kernel(const int* __restrict__ nodes, int n, const d
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) r[__ldg(nodes + t)] = __ldg(recv + t);
 }
 
-// ---------------------------------------------------------------------------
-// Two-scale combine (precond.cpp:57-66): z = mask ? r : (0 + zf) + zc, with
-//   zf = sum of the node's subdomain-slot values in ascending (e,slot) order
-//        (FinePreconditioner accumulation, fine.cpp:224-227)
-//   zc = (sum of the node's prolongated copies in (e,l) order) / m_N
-//        (CoarsePreconditioner::prolongate, coarse.cpp:164-186; the per-copy
-//        values come from prolong_elem_kernel)
-// plus the fused z.r partial.
-struct CombineArgs {
-  const double* r;
-  const std::uint8_t* mask;
-  const double* zsort;       // fine subdomain outputs in CSR order (fdm_kernel)
-  const unsigned* fine_off;  // N+1
-  const double* psort;       // prolongated surface copies in CSR order (prolong_elem_kernel)
-  const double* pint;        // prolongated element-interior nodes (N, [nsg,N) used)
-  const unsigned* ax_off;    // nsg+1
-  const double* lumped;      // m_N
-  double* z;
-  int N, nsg;
-  int do_fine, do_coarse;
-  DotArgs dot;
-};
-
-__global__ void __launch_bounds__(kGatherBlock, 4) combine_kernel(CombineArgs a)
-{
-  __shared__ double red[kGatherBlock / 32];
-  __shared__ double stage[kGatherBlock / 32][kGatherCap];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = gridDim.x * (kGatherBlock / 32);
-  double dot = 0.0;
-  for (int g0 = (blockIdx.x * (kGatherBlock / 32) + warp) * 32; g0 < a.N; g0 += nwarps * 32) {
-    const int g = g0 + lane;
-    double zf = 0.0, zc = 0.0;
-    if (a.do_fine)
-      zf = warp_seg_sum(a.fine_off, a.zsort, g0, a.N, stage[warp]);
-    if (a.do_coarse) {
-      if (g0 < a.nsg)
-        zc = warp_seg_sum(a.ax_off, a.psort, g0, a.nsg, stage[warp]);
-      if (g >= a.nsg && g < a.N) zc = __ldg(a.pint + g);
-    }
-    if (g < a.N) {
-      const double rg = __ldg(a.r + g);
-      double zg;
-      if (__ldg(a.mask + g)) {
-        zg = rg;
-      } else {
-        double s = 0.0;
-        if (a.do_fine) s += zf;
-        if (a.do_coarse) s += zc / __ldg(a.lumped + g);
-        zg = s;
-      }
-      a.z[g] = zg;
-      dot += zg * rg;
-    }
-  }
-  dot_commit<kGatherBlock>(a.dot, dot, red);
-}
-
 // Two-scale combine with the coarse prolongation fused in (precond.cpp:57-66,
 // prolongate coarse.cpp:164-186): per node g
 //   zf = sum of its subdomain contributions in (e, slot) order (fine.cpp:224-227)
@@ -226,7 +141,6 @@ struct CombineProlongArgs {
   const double* Zc;
   const double* mass;      // [e][nloc] (element-interior copies)
   const double* mass_csr;  // surface copies, Ax-CSR order
-  const double* esurf;     // [e][nsurfp] prolongated surface copies (prolong_surface_kernel)
   const double* lumped;
   double* z;
   int N, nsg;
@@ -318,131 +232,6 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(Combin
     dot += zg * rg;
   }
   dot_commit<kGatherBlock>(a.dot, dot, red);
-}
-
-// Tiled variant of the combine: a warp owns a tile of kTile consecutive nodes
-// (lane + 32 t). The tile's fine contributions and surface-copy lists are
-// contiguous in CSR order, so the warp first streams them into shared memory
-// with coalesced loads (every load of the tile in flight at once), then each
-// lane sums its nodes' segments left to right from shared memory. Segments
-// longer than the staging capacity fall back to direct loads.
-constexpr int kTile = 128;
-constexpr int kTileCapF = 512;  // staged fine contributions per warp (typ. 2.6 per node)
-constexpr int kTileCapC = 384;  // staged surface copies per warp (typ. 1.5-2 per surface node)
-constexpr int kCombBlock = 128;
-
-template <int NP>
-__global__ void __launch_bounds__(kCombBlock, 4) combine_tile_kernel(CombineProlongArgs a)
-{
-  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NLOC = NP * NP * NP;
-  constexpr int W = kCombBlock / 32, T = kTile / 32;
-  __shared__ double red[W];
-  __shared__ double h0[NP], h1[NP];
-  __shared__ double sf[W][kTileCapF];
-  __shared__ double sm[W][kTileCapC];
-  if (threadIdx.x < NP) {
-    h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
-    h1[threadIdx.x] = c_tab[NP].hat1[threadIdx.x];
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* stf = sf[warp];
-  double* stm = sm[warp];
-  auto pz = [&](long long e, int i, int j, int k) {  // sum_cb B[cb][l] Zc[e][cb] (coarse.cpp:176-179)
-    const double2* zc2 = reinterpret_cast<const double2*>(a.Zc + 8 * e);
-    const double2 c01 = __ldg(zc2), c23 = __ldg(zc2 + 1), c45 = __ldg(zc2 + 2), c67 = __ldg(zc2 + 3);
-    const double zc[8] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y};
-    const double hi[2] = {h0[i], h1[i]}, hj[2] = {h0[j], h1[j]}, hk[2] = {h0[k], h1[k]};
-    double s = 0.0;
-#pragma unroll
-    for (int cb = 0; cb < 8; ++cb) s += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[cb >> 2] * zc[cb];
-    return s;
-  };
-  double dot = 0.0;
-  const int nw = gridDim.x * W;
-  for (int g0 = (blockIdx.x * W + warp) * kTile; g0 < a.N; g0 += nw * kTile) {
-    // ---- first-level loads for the tile's nodes (coalesced) ----
-    unsigned f0[T], f1[T], c0[T], c1[T];
-    double rg[T];
-    bool msk[T];
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const int g = g0 + lane + 32 * t;
-      const bool in = g < a.N;
-      rg[t] = in ? __ldg(a.r + g) : 0.0;
-      msk[t] = in ? __ldg(a.mask + g) != 0 : true;
-      f0[t] = f1[t] = c0[t] = c1[t] = 0;
-      if (in && a.do_fine) {
-        f0[t] = __ldg(a.fine_off + g);
-        f1[t] = __ldg(a.fine_off + g + 1);
-      }
-      if (in && a.do_coarse && g < a.nsg) {
-        c0[t] = __ldg(a.ax_off + g);
-        c1[t] = __ldg(a.ax_off + g + 1);
-      }
-    }
-    // tile ranges (first lane holds the lowest node, last lane the highest)
-    const int glast = min(g0 + kTile, a.N) - 1;
-    unsigned fb = 0, fe = 0, cb0 = 0, ce = 0;
-    if (a.do_fine) {
-      fb = __shfl_sync(0xffffffffu, f0[0], 0);
-      fe = __ldg(a.fine_off + glast + 1);
-    }
-    const bool any_surf = a.do_coarse && g0 < a.nsg;
-    if (any_surf) {
-      cb0 = __shfl_sync(0xffffffffu, c0[0], 0);
-      ce = __ldg(a.ax_off + min(glast, a.nsg - 1) + 1);
-    }
-    const bool stage_f = a.do_fine && fe - fb <= (unsigned)kTileCapF;
-    const bool stage_c = any_surf && ce - cb0 <= (unsigned)kTileCapC;
-    // ---- stream the tile's segments into shared memory ----
-    if (stage_f)
-      for (unsigned q = lane; q < fe - fb; q += 32) stf[q] = __ldcs(a.zsort + fb + q);
-    if (stage_c)  // the tile's surface copies, gathered from the element-major E-vector
-      for (unsigned q = lane; q < ce - cb0; q += 32) stm[q] = __ldg(a.esurf + __ldg(a.ax_idx + cb0 + q));
-    __syncwarp();
-    // ---- per-lane sums in list order ----
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const int g = g0 + lane + 32 * t;
-      if (g >= a.N) continue;
-      double zg;
-      if (msk[t]) {
-        zg = rg[t];
-      } else {
-        double s = 0.0;
-        if (a.do_fine) {
-          double zf = 0.0;
-          if (stage_f)
-            for (unsigned q = f0[t] - fb; q < f1[t] - fb; ++q) zf += stf[q];
-          else
-            for (unsigned q = f0[t]; q < f1[t]; ++q) zf += __ldcs(a.zsort + q);
-          s += zf;
-        }
-        if (a.do_coarse) {
-          double zc = 0.0;
-          if (g >= a.nsg) {
-            if constexpr (NI > 0) {
-              const int u = g - a.nsg;
-              const long long e = u / NI;
-              const int l = u % NI;
-              const int i = 1 + l % (n - 1), j = 1 + (l / (n - 1)) % (n - 1), k = 1 + l / ((n - 1) * (n - 1));
-              zc = pz(e, i, j, k) * __ldg(a.mass + e * NLOC + (k * NP + j) * NP + i);  // coarse.cpp:180
-            }
-          } else {
-            for (unsigned q = c0[t]; q < c1[t]; ++q)  // copies in (e,l) order (coarse.cpp:181)
-              zc += stage_c ? stm[q - cb0] : __ldg(a.esurf + __ldg(a.ax_idx + q));
-          }
-          s += zc / __ldg(a.lumped + g);
-        }
-        zg = s;
-      }
-      a.z[g] = zg;
-      dot += zg * rg[t];
-    }
-    __syncwarp();  // staging buffers reused by the next tile
-  }
-  dot_commit<kCombBlock>(a.dot, dot, red);
 }
 
 // R[v] = vmask[v] ? 0 : sum of Rpart over (e,cb) incidences in ascending order

@@ -92,11 +92,6 @@ __global__ void sqrt_store_kernel(const double* __restrict__ src, double* __rest
   *dst = sqrt(*src);
 }
 
-__global__ void copy_kernel(const double* __restrict__ x, double* __restrict__ y, int n)
-{
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) y[i] = x[i];
-}
-
 // mode none: z = r, zr = z.r
 // (precond.cpp:30-33)
 

@@ -165,7 +165,6 @@ struct Plan {
   double *Rpart = nullptr, *R = nullptr, *Z = nullptr, *rho = nullptr, *dZ = nullptr;
   double* Zc = nullptr;       // [e][8] coarse corner values for the fused prolongation
   double* mass_csr = nullptr; // m of each surface copy in Ax-CSR order
-  double* esurf = nullptr;    // [e][nsurfp] prolongated surface copies
   std::vector<DevLevel> lv;  // AMG levels 0..L (L = coarsest, uses dense)
   DevDense dense;
   DevCsr Kc{};               // K_c on the device (AMG mode: residual between the two K-cycles)
@@ -202,6 +201,8 @@ struct Plan {
   int* ax_nodes = nullptr;    // local surface node -> global id (null: identity)
   int n_loc_surf = 0;         // local surface nodes = [group0 | up | down]
   int n_grp0 = 0, n_up = 0, n_down = 0;
+  int sfstride = 0;           // sub_face row stride (ints)
+  int fdm_grid = 0;           // persistent FDM grid (0: one CTA per element, fdm_kernel)
 
   // live kernel timing (bench roofline): event pairs around tagged launches on s_main
   bool kt_on = false;
@@ -319,6 +320,20 @@ void init_ax_grid(Plan& pl)
   pl.ax_grid = ax_persistent_grid<NP>(pl);
 }
 
+// persistent pipelined FDM grid (one wave of resident CTAs); 0 keeps fdm_kernel
+template <int NP>
+void init_fdm_grid(Plan& pl, bool enable)
+{
+  pl.fdm_grid = 0;
+  if (!enable || !pl.fdm_eo) return;
+  const int smem = static_cast<int>(FdmPipe<NP>::kSmemBytes);
+  HXB_CUDA(cudaFuncSetAttribute(fdm_pipe_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdm_pipe_kernel<NP>, FdmShape<NP>::kBlock, smem));
+  if (per_sm < 1) return;
+  pl.fdm_grid = std::max(1, std::min(pl.ne, per_sm * pl.num_sms));
+}
+
 int ax_elem_grid(const Plan& pl) { return pl.ax_grid; }
 
 // f = A u (+ optional u.f into *dot_result)
@@ -369,9 +384,12 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   a.inv_lumped = pl.d_inv_lumped;
   a.mass = pl.mass;
   a.Rpart = pl.do_coarse ? pl.Rpart : nullptr;
+  a.sfstride = pl.sfstride;
   KtScope kt(pl, HXB_KT_FDM, s);
   pl.launches += 1;
-  if (pl.fdm_eo)
+  if (pl.fdm_grid > 0)
+    fdm_pipe_kernel<NP><<<pl.fdm_grid, FdmShape<NP>::kBlock, FdmPipe<NP>::kSmemBytes, s>>>(a);
+  else if (pl.fdm_eo)
     fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
   else
     fdm_kernel<NP, false><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
@@ -390,7 +408,6 @@ void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine
   a.Zc = pl.Zc;
   a.mass = pl.mass;
   a.mass_csr = pl.mass_csr;
-  a.esurf = pl.esurf;
   a.lumped = pl.d_lumped;
   a.z = pl.z;
   a.N = pl.N;
@@ -398,8 +415,7 @@ void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine
   a.do_fine = do_fine ? 1 : 0;
   a.do_coarse = do_coarse ? 1 : 0;
   a.dot = zr_result ? dot_args(pl, zr_result) : DotArgs{};
-  const int grid = fill_grid(combine_tile_kernel<NP>, kCombBlock, (pl.N + kTile - 1) / kTile * 32);
-  combine_tile_kernel<NP><<<grid, kCombBlock, 0, s>>>(a);
+  combine_prolong_kernel<NP><<<fill_grid(combine_prolong_kernel<NP>, kGatherBlock, pl.N), kGatherBlock, 0, s>>>(a);
 }
 
 void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse)
@@ -411,14 +427,10 @@ void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, b
 
 // Zc = Z at each element's corners (interior copies, prolonged inside the
 // combine) and the prolongated surface copies (coarse.cpp:164-181)
-template <int NP>
-void launch_prolong_np(Plan& pl, cudaStream_t s)
+void launch_prolong(Plan& pl, cudaStream_t s)
 {
   corner_values_kernel<<<vec_grid(8LL * pl.ne), kVecBlock, 0, s>>>(pl.Z, pl.conn, pl.Zc, pl.ne);
-  prolong_surface_kernel<NP><<<fill_grid(prolong_surface_kernel<NP>, kVecBlock, (long long)pl.ne * pl.nsurf), kVecBlock, 0, s>>>(
-      pl.Z, pl.conn, pl.mass, pl.esurf, pl.ne);
 }
-void launch_prolong(Plan& pl, cudaStream_t s) { HXB_DISPATCH_NP(pl.np, launch_prolong_np, pl, s); }
 
 template <int NP>
 void launch_restrict(Plan& pl, cudaStream_t s)
@@ -988,6 +1000,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
 
   pl.fdm_eo = upload_tables(hs.basis, hs.pencil);
   HXB_DISPATCH_NP(pl.np, init_ax_grid, pl);
+  HXB_DISPATCH_NP(pl.np, init_fdm_grid, pl, (opt.reserved[0] & 4) != 0);
 
   HXB_CUDA(cudaStreamCreateWithFlags(&pl.s_main, cudaStreamNonBlocking));
   HXB_CUDA(cudaStreamCreateWithFlags(&pl.s_coarse, cudaStreamNonBlocking));
@@ -1051,6 +1064,19 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
         idx[smap[static_cast<std::size_t>(e) * 2 * pl.nsurf + pl.nsurf + q]] = e * pl.nsurf + q;
     pl.ax_idx = M.upload(idx);
     pl.n_loc_surf = pl.n_grp0 = pl.nsg;
+    if (pl.do_coarse) {  // mass of every surface copy in Ax-CSR order (streamed by the fused prolongation)
+      std::vector<int> slot_l(nsurf_raw);
+      for (int k = 0; k < pl.np; ++k)
+        for (int j = 0; j < pl.np; ++j)
+          for (int i = 0; i < pl.np; ++i) {
+            const int sl = surface_slot(pl.np, i, j, k);
+            if (sl >= 0) slot_l[sl] = (k * pl.np + j) * pl.np + i;
+          }
+      std::vector<double> mcsr(off[pl.nsg]);
+      for (std::size_t q = 0; q < mcsr.size(); ++q)
+        mcsr[q] = hs.geo.mass[static_cast<std::size_t>(idx[q] / pl.nsurf) * pl.nloc + slot_l[idx[q] % pl.nsurf]];
+      pl.mass_csr = M.upload(mcsr);
+    }
   } else {
     build_dist_ax(pl, hs, nsurf_raw);
   }
@@ -1058,11 +1084,14 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
 
   // fine: encoded sub_face and the subdomain gather CSR in (e, slot) order
   if (pl.do_fine) {
-    std::vector<int> enc(num.sub_face.size());
-    for (std::size_t q = 0; q < enc.size(); ++q) {
-      const gid g = num.sub_face[q];
-      enc[q] = g < 0 ? -1 : (num.dirichlet_mask[g] ? encode_dirichlet(g) : g);
-    }
+    const int nf = 6 * pl.np * pl.np, nfp = (nf + 3) & ~3;  // rows padded for 16-byte TMA copies
+    pl.sfstride = nfp;
+    std::vector<int> enc(static_cast<std::size_t>(ne) * nfp, -1);
+    for (int e = 0; e < ne; ++e)
+      for (int q = 0; q < nf; ++q) {
+        const gid g = num.sub_face[static_cast<std::size_t>(e) * nf + q];
+        enc[static_cast<std::size_t>(e) * nfp + q] = g < 0 ? -1 : (num.dirichlet_mask[g] ? encode_dirichlet(g) : g);
+      }
     pl.sub_face = M.upload(enc);
     const std::size_t nsub = static_cast<std::size_t>(pl.P) * pl.P * pl.P;
     std::vector<unsigned> cnt(static_cast<std::size_t>(pl.N) + 1, 0);
@@ -1108,7 +1137,6 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.rho = M.alloc<double>(pl.nv);
     pl.dZ = M.alloc<double>(pl.nv);
     pl.Zc = M.alloc<double>(static_cast<std::size_t>(ne) * 8);
-    pl.esurf = M.alloc<double>(static_cast<std::size_t>(ne) * pl.nsurf);
     pl.coarse_n = hs.Kc.n;
     if (pl.use_amg) {
       pl.Kc = csr_to_device(pl, hs.Kc);

@@ -36,7 +36,7 @@ def history_parity(ours: dict, ref: dict, tol=1e-10, iters_slack=1, per_rk=False
     else:
         dr = float(np.max(np.abs(ra[:k] - rb[:k])) / r0)
     assert dr <= tol, dr
-    if ours.get("u") is not None:
+    if ours.get("u") is not None and ref.get("u") is not None:
         assert rel(ours["u"], ref["u"]) <= tol, rel(ours["u"], ref["u"])
     return dr
 
