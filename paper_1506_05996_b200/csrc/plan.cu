@@ -1543,6 +1543,7 @@ int hxb_profile(hxb_plan* plan, int reps, double* out)
     if (pl->do_coarse) out[3] = timeit([&] { HXB_CUDA(cudaGraphLaunch(pl->coarse_exec, s)); });  // after Rpart
     out[4] = timeit([&] { launch_combine(*pl, pl->zr_hist, s, pl->do_fine, pl->do_coarse); });
     if (pl->do_fine) out[12] = timeit([&] { launch_combine(*pl, pl->zr_hist, s, true, false); });
+
     if (pl->do_coarse) out[13] = timeit([&] { launch_combine(*pl, pl->zr_hist, s, false, true); });
     out[5] = timeit([&] { enqueue_precond(*pl, pl->zr_hist); });
     HXB_CUDA(cudaMemcpy(pl->pf_hist, pl->zr_hist, sizeof(double), cudaMemcpyDeviceToDevice));

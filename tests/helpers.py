@@ -48,3 +48,28 @@ def rounding_noise(ref_result: dict, fma_result: dict) -> float:
     ra, rb = np.asarray(fma_result["residual_history"]), np.asarray(ref_result["residual_history"])
     k = min(len(ra), len(rb))
     return float(np.max(np.abs(ra[:k] - rb[:k])) / rb[0])
+
+
+def reference_noise(ref_result: dict, b, cfg, **mesh_kw) -> float:
+    """Rounding floor of one problem: the larger of two rounding-only
+    perturbations of the reference algorithm, measured against the reference
+    itself: (1) the restatement compiled with FMA contraction, (2) the
+    restatement with correctly rounded dot products. On ill-conditioned
+    cases (tiny high-order meshes, distorted geometry) either alone can move
+    r_k by 1e-8 of r_0 and even change the iteration count by one."""
+    import ctypes as C
+
+    from oracle import OracleFmaSystem, OracleSystem
+    from oracle.ctypes_oracle import _ORC_SO, _load
+
+    tol = 1e-8
+    n1 = rounding_noise(ref_result, OracleFmaSystem(cfg, **mesh_kw).pcg(b, tol=tol))
+    L = _load(_ORC_SO, "orc_")
+    L.orc_set_dot_mode.argtypes = [C.c_int]
+    L.orc_set_dot_mode.restype = None
+    L.orc_set_dot_mode(1)
+    try:
+        n2 = rounding_noise(ref_result, OracleSystem(cfg, **mesh_kw).pcg(b, tol=tol))
+    finally:
+        L.orc_set_dot_mode(0)
+    return max(n1, n2)

@@ -198,12 +198,10 @@ def test_cfg3_mixed_bc_variable_coefficients(coarse_solve):
         theirs = ref.pcg(b, tol=1e-8)
         # distorted meshes amplify rounding: the tolerance is calibrated
         # on this very problem by the reference's FMA-contracted restatement
-        from oracle import OracleFmaSystem
-        from helpers import rounding_noise
+        from helpers import reference_noise
 
-        fma = OracleFmaSystem(RefConfig(order=order, coarse_solve=coarse_solve), mesh=mesh.as_dict(), order=order,
-                              kappa_e=kappa, c_e=c)
-        noise = rounding_noise(theirs, fma.pcg(b, tol=1e-8))
+        noise = reference_noise(theirs, b, RefConfig(order=order, coarse_solve=coarse_solve), mesh=mesh.as_dict(),
+                                order=order, kappa_e=kappa, c_e=c)
         tol = max(1e-10, 10 * noise)
         print(f"cfg3 {coarse_solve}: reference FMA noise {noise:.2e}, tolerance {tol:.2e}")
         history_parity(plan.pcg(b, tol=1e-8), theirs, tol=tol)
@@ -219,10 +217,10 @@ def test_order_sweep_pcg(order):
     assert rel(plan.apply_P(u), ref.apply_P(u)) <= 1e-11
     b = ref.load_ones()
     theirs = ref.pcg(b, tol=1e-8)
-    from oracle import OracleFmaSystem
-    from helpers import rounding_noise
+    from helpers import reference_noise
 
-    noise = rounding_noise(theirs, OracleFmaSystem(RefConfig(k=k, order=order)).pcg(b, tol=1e-8))
+    noise = reference_noise(theirs, b, RefConfig(k=k, order=order))
+    print(f"order {order}: reference rounding floor {noise:.2e}")
     history_parity(plan.pcg(b, tol=1e-8), theirs, tol=max(1e-10, 10 * noise))
 
 

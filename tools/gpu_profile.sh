@@ -3,7 +3,7 @@
 # usage: tools/gpu_profile.sh "kernel_regex" [tag]
 rx=${1:-"fdm_kernel|combine_prolong|restrict_warp"}; tag=${2:-it}
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "not golden" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "not golden" > gpurun_out/pytest_quick.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_quick.log
 timeout 300 python - > gpurun_out/profile.log 2>&1 <<'PY'
 import sys, json
 sys.path.insert(0, ".")

@@ -26,7 +26,9 @@ for w in $what; do
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:ax_elem_kernel -s 3 -c 1 -o gpurun_out/prof_ax -f \
         python tools/prof_driver.py 52 7 > gpurun_out/ncu_full_ax.log 2>&1; echo "rc=$?" >> gpurun_out/ncu_full_ax.log
       timeout 900 ncu --set full --clock-control none --import-source on -k regex:fdm_kernel -s 1 -c 1 -o gpurun_out/prof_fdm -f \
-        python tools/prof_driver.py 52 7 > gpurun_out/ncu_full_fdm.log 2>&1; echo "rc=$?" >> gpurun_out/ncu_full_fdm.log ;;
+        python tools/prof_driver.py 52 7 > gpurun_out/ncu_full_fdm.log 2>&1; echo "rc=$?" >> gpurun_out/ncu_full_fdm.log
+      timeout 900 ncu --set full --clock-control none --import-source on -k "regex:combine_prolong|ax_gather|amg_cluster|pcg_dir|restrict_warp" -s 2 -c 6 -o gpurun_out/prof_rest -f \
+        python tools/prof_driver.py 52 7 > gpurun_out/ncu_full_rest.log 2>&1; echo "rc=$?" >> gpurun_out/ncu_full_rest.log ;;
   esac
 done
 exit 0

@@ -11,13 +11,13 @@ keys = [("gpu__time_duration.sum", "us", 1e-3), ("dram__bytes_read.sum", "MB", N
         ("launch__grid_size", "grid", 1)]
 def conv(v, unit):
     x = float(v.replace(",", ""))
-    if unit in ("Gbyte",): return x * 1e3
-    if unit in ("Kbyte",): return x * 1e-3
+    if unit in ("Gbyte", "GB"): return x * 1e3
+    if unit in ("Kbyte", "KB"): return x * 1e-3
     if unit in ("byte",): return x * 1e-6
     if unit == "Mbyte": return x
-    if unit == "msecond": return x * 1e3
-    if unit == "usecond": return x
-    if unit == "nsecond": return x * 1e-3
+    if unit in ("msecond", "ms"): return x * 1e3
+    if unit in ("usecond", "us"): return x
+    if unit in ("nsecond", "ns"): return x * 1e-3
     return x
 idx = {k: h.index(k) for k, _, _ in keys if k in h}
 print(f"{'kernel':34s} " + " ".join(f"{lab:>8s}" for _, lab, _ in keys))
