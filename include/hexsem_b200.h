@@ -224,6 +224,33 @@ int hxb_dist_apply_A_continue(hxb_plan* plan, const double* d_u, double* d_r, co
                               double* d_send_down, void* stream);
 int hxb_dist_apply_A_end(hxb_plan* plan, double* d_r, const double* d_recv_up, void* stream);
 
+/* Distributed two-scale PCG, staged (same slab plans, options.reserved[1..2];
+ * the caller carries the messages, see paper_1506_05996_b200/dist.py). Per
+ * iteration of krylov.cpp:20-71: vector updates over the rank's nodes
+ * (hxb_dist_vec: 0 r=b,u=0  1 u+=a p, r-=a f  2 p=z+a p  3 p=z), partial dots
+ * over its finalised nodes (hxb_dist_dot -> device scalar, then all-reduce),
+ * and the preconditioner:
+ *   ghost r exchange (pack/unpack which 0/1), hxb_dist_fine -> fsend
+ *   [to lower | to upper] + Rpart slab, exchange, hxb_dist_fine_recv,
+ *   Rpart slab out (hxb_dist_rpart 0) -> all-gather -> full in (1),
+ *   hxb_dist_coarse (replicated AMG), hxb_dist_combine (z on finalised
+ *   nodes + partial z.r), finals of the down-interface to the lower rank
+ *   (pack/unpack which 2).
+ * info[16] = ghost from lower/upper, ghost to lower/upper, fine send to
+ * lower/upper, fine recv from lower/upper, e0, e1, NE, has fine, has coarse,
+ * n_up, n_down, N. */
+int hxb_dist_pcg_info(hxb_plan* plan, int64_t* info);
+int hxb_dist_vec(hxb_plan* plan, int mode, double a, const double* x0, const double* x1, double* y0, double* y1,
+                 void* stream);
+int hxb_dist_dot(hxb_plan* plan, const double* x, const double* y, double* d_out, void* stream);
+int hxb_dist_pack(hxb_plan* plan, int which, const double* d_x, double* d_buf, void* stream);
+int hxb_dist_unpack(hxb_plan* plan, int which, const double* d_buf, double* d_x, void* stream);
+int hxb_dist_fine(hxb_plan* plan, const double* d_r, double* d_fsend, void* stream);
+int hxb_dist_fine_recv(hxb_plan* plan, const double* d_frecv, void* stream);
+int hxb_dist_rpart(hxb_plan* plan, int direction, double* d_buf, void* stream);
+int hxb_dist_coarse(hxb_plan* plan, void* stream);
+int hxb_dist_combine(hxb_plan* plan, const double* d_r, double* d_z, double* d_zr, void* stream);
+
 /* Live kernel timing for the bench roofline: while enabled, the plan brackets
  * each tagged launch on its main stream with a CUDA event pair (up to
  * max_launches launches). _read sums the durations of one tag. The reference

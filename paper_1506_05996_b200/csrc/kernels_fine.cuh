@@ -54,6 +54,7 @@ struct FdmArgs {
   const double* inv_lumped; // 1/m_N
   const double* mass;       // [e][nloc]
   double* Rpart;            // [e][8] corner partial sums
+  double* fsend = nullptr;  // distributed plans: contributions finalised by a neighbour (pos <= -2)
   int ne, sstride, num_surface_global;
   int sfstride;             // per-element stride of sub_face (6 np^2 padded to 4 ints: TMA rows)
 };
@@ -300,7 +301,10 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
 #pragma unroll
     for (int x = 0; x < P; ++x) {
       const int q = __ldg(ps + x);
-      if (q >= 0) a.zsort[q] = out[x];
+      if (q >= 0)
+        a.zsort[q] = out[x];
+      else if (q <= -2)  // finalised by a neighbour rank (distributed plans)
+        a.fsend[-2 - q] = out[x];
     }
   }
 }
@@ -529,7 +533,10 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_pipe_kernel(FdmArgs 
 #pragma unroll
       for (int x = 0; x < P; ++x) {
         const int q = __ldg(ps + x);
-        if (q >= 0) a.zsort[q] = out[x];
+        if (q >= 0)
+        a.zsort[q] = out[x];
+      else if (q <= -2)  // finalised by a neighbour rank (distributed plans)
+        a.fsend[-2 - q] = out[x];
       }
     }
     cp_async_wait_all();  // e' inputs landed (this thread's copies)

@@ -115,6 +115,64 @@ __global__ void dist_continue_kernel(const unsigned* __restrict__ off, const int
   }
 }
 
+// --- distributed preconditioned CG helpers ----------------------------------
+// x[list[t]] -> buf[t]
+__global__ void dist_pack_kernel(const int* __restrict__ list, int n, const double* __restrict__ x, double* __restrict__ buf)
+{
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) buf[t] = __ldg(x + __ldg(list + t));
+}
+// buf[t] -> x[list[t]]
+__global__ void dist_unpack_kernel(const int* __restrict__ list, int n, const double* __restrict__ buf, double* __restrict__ x)
+{
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) x[__ldg(list + t)] = __ldg(buf + t);
+}
+// local vector updates over the rank's nodes: surface list + interior range
+//   mode 0: r = b, u = 0              (krylov.cpp:29-30)
+//   mode 1: u += a p, r -= a f        (krylov.cpp:53-56)
+//   mode 2: p = z + a p               (krylov.cpp:64-66)
+//   mode 3: p = z                     (krylov.cpp:38)
+__global__ void dist_vec_kernel(int mode, const int* __restrict__ list, int nlist, int ib0, int ib1, double a,
+                                const double* __restrict__ x0, const double* __restrict__ x1, double* __restrict__ y0,
+                                double* __restrict__ y1)
+{
+  const int total = nlist + (ib1 - ib0);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const int g = t < nlist ? __ldg(list + t) : ib0 + (t - nlist);
+    if (mode == 0) {
+      y0[g] = x0[g];
+      y1[g] = 0.0;
+    } else if (mode == 1) {
+      y1[g] += a * x0[g];   // u (y1) += a p (x0)
+      y0[g] -= a * x1[g];   // r (y0) -= a f (x1)
+    } else if (mode == 2) {
+      y0[g] = x0[g] + a * y0[g];
+    } else {
+      y0[g] = x0[g];
+    }
+  }
+}
+// partial dot over the rank's finalised nodes (each global node counted once)
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) dist_dot_kernel(const int* __restrict__ list, int nlist, int ib0, int ib1,
+                                                        const double* __restrict__ x, const double* __restrict__ y,
+                                                        DotArgs d)
+{
+  __shared__ double red[BLOCK / 32];
+  const int total = nlist + (ib1 - ib0);
+  double s = 0.0;
+  for (int t = blockIdx.x * BLOCK + threadIdx.x; t < total; t += gridDim.x * BLOCK) {
+    const int g = t < nlist ? __ldg(list + t) : ib0 + (t - nlist);
+    s += __ldg(x + g) * __ldg(y + g);
+  }
+  dot_commit<BLOCK>(d, s, red);
+}
+// neighbours' fine contributions into their sum positions
+__global__ void dist_fine_scatter_kernel(const int* __restrict__ pos, int n, const double* __restrict__ recv,
+                                         double* __restrict__ zsort)
+{
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) zsort[__ldg(pos + t)] = __ldg(recv + t);
+}
+
 // up-interface node t: the final value computed by the upper rank
 __global__ void dist_finish_kernel(const int* __restrict__ nodes, int n, const double* __restrict__ recv,
                                    double* __restrict__ r)
@@ -146,6 +204,12 @@ struct CombineProlongArgs {
   int N, nsg;
   int do_fine, do_coarse;
   DotArgs dot;
+  // item t -> node: t < nsg: surface node (surf_nodes ? surf_nodes[t] : t),
+  // t >= nsg: interior node ibase + (t - nsg) of element (t - nsg)/NI + e0;
+  // the distributed plan runs over its finalised nodes only
+  const int* surf_nodes = nullptr;
+  int ibase = 0;    // global id of the first interior item
+  int e0 = 0;       // global id of the first element whose mass block is at `mass`
 };
 
 template <int NP>
@@ -172,7 +236,9 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(Combin
     return s;
   };
   double dot = 0.0;
-  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < a.N; g += gridDim.x * blockDim.x) {
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < a.N; it += gridDim.x * blockDim.x) {
+    const bool surf = it < a.nsg;
+    const int g = surf ? (a.surf_nodes ? __ldg(a.surf_nodes + it) : it) : a.ibase + (it - a.nsg);
     const double rg = __ldg(a.r + g);
     double zg;
     if (__ldg(a.mask + g)) {
@@ -181,7 +247,7 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(Combin
       double s = 0.0;
       if (a.do_fine) {
         // up to 8 contributions loaded at once (predicated), summed in list order
-        const unsigned q0 = __ldg(a.fine_off + g), q1 = __ldg(a.fine_off + g + 1);
+        const unsigned q0 = __ldg(a.fine_off + it), q1 = __ldg(a.fine_off + it + 1);
         double v[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) v[t] = q0 + t < q1 ? __ldcs(a.zsort + q0 + t) : 0.0;
@@ -194,18 +260,18 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(Combin
       }
       if (a.do_coarse) {
         double zc = 0.0;
-        if (g >= a.nsg) {
+        if (!surf) {
           if constexpr (NI > 0) {
-            const int t = g - a.nsg;
-            const long long e = t / NI;
+            const int t = it - a.nsg;  // interior ids are (e, local)-ordered (mesh.cpp:283)
+            const long long el = t / NI;          // element relative to e0
             const int l = t % NI;
             const int i = 1 + l % (n - 1), j = 1 + (l / (n - 1)) % (n - 1), k = 1 + l / ((n - 1) * (n - 1));
-            zc = pz(e, i, j, k) * __ldg(a.mass + e * NLOC + (k * NP + j) * NP + i);  // coarse.cpp:180
+            zc = pz(el + a.e0, i, j, k) * __ldg(a.mass + el * NLOC + (k * NP + j) * NP + i);  // coarse.cpp:180
           }
         } else {
           // face nodes (2 copies) dominate: the first two copies are evaluated
           // independently, the rest (edges 4, vertices 8+) in order after them
-          const unsigned c0 = __ldg(a.ax_off + g), c1 = __ldg(a.ax_off + g + 1);
+          const unsigned c0 = __ldg(a.ax_off + it), c1 = __ldg(a.ax_off + it + 1);
           const int x0 = __ldg(a.ax_idx + c0);
           const int x1 = c0 + 1 < c1 ? __ldg(a.ax_idx + c0 + 1) : x0;
           int i0, j0, k0, i1, j1, k1;

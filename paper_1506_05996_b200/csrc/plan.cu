@@ -202,6 +202,19 @@ struct Plan {
   int n_loc_surf = 0;         // local surface nodes = [group0 | up | down]
   int n_grp0 = 0, n_up = 0, n_down = 0;
   int sfstride = 0;           // sub_face row stride (ints)
+  int ne_total = 0;           // elements of the whole mesh
+  // distributed preconditioned CG (setup_dist.cpp)
+  int* fin_surf = nullptr;    // finalised surface nodes (group 0 + down)
+  int n_fin_surf = 0, ib0 = 0, ib1 = 0;
+  unsigned* pr_off = nullptr; // prolongation CSR of the finalised surface nodes (all copies)
+  int* pr_idx = nullptr;
+  double* pr_mass = nullptr;
+  int* frecv_pos = nullptr;   // [from down | from up] sum positions of the neighbours' contributions
+  int n_frecv_down = 0, n_frecv_up = 0, n_fsend_down = 0, n_fsend_up = 0;
+  int *g_from_down = nullptr, *g_from_up = nullptr, *g_to_down = nullptr, *g_to_up = nullptr;
+  int n_g_from_down = 0, n_g_from_up = 0, n_g_to_down = 0, n_g_to_up = 0;
+  int* loc_list = nullptr;    // local surface nodes (= ax_nodes) for vector updates
+  double* fsend = nullptr;    // FDM contributions for the neighbours (caller buffer, set per call)
   int fdm_grid = 0;           // persistent FDM grid (0: one CTA per element, fdm_kernel)
 
   // live kernel timing (bench roofline): event pairs around tagged launches on s_main
@@ -380,10 +393,11 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   a.zsort = pl.zsort;
   a.ne = pl.ne;
   a.sstride = 2 * pl.nsurf;
-  a.num_surface_global = pl.nsg;
+  a.num_surface_global = pl.nsg + pl.e0 * (pl.order - 1) * (pl.order - 1) * (pl.order - 1);  // first owned interior id
   a.inv_lumped = pl.d_inv_lumped;
   a.mass = pl.mass;
-  a.Rpart = pl.do_coarse ? pl.Rpart : nullptr;
+  a.Rpart = pl.do_coarse ? pl.Rpart + 8LL * pl.e0 : nullptr;  // owned slab of the full Rpart
+  a.fsend = pl.fsend;
   a.sfstride = pl.sfstride;
   KtScope kt(pl, HXB_KT_FDM, s);
   pl.launches += 1;
@@ -410,12 +424,25 @@ void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine
   a.mass_csr = pl.mass_csr;
   a.lumped = pl.d_lumped;
   a.z = pl.z;
-  a.N = pl.N;
-  a.nsg = pl.nsg;
+  if (pl.nranks > 1) {  // this rank's finalised nodes
+    a.N = pl.n_fin_surf + (pl.ib1 - pl.ib0);
+    a.nsg = pl.n_fin_surf;
+    a.surf_nodes = pl.fin_surf;
+    a.ibase = pl.ib0;
+    a.e0 = pl.e0;
+    a.ax_off = pl.pr_off;
+    a.ax_idx = pl.pr_idx;
+    a.mass_csr = pl.pr_mass;
+  } else {
+    a.N = pl.N;
+    a.nsg = pl.nsg;
+    a.ibase = pl.nsg;
+    a.e0 = 0;
+  }
   a.do_fine = do_fine ? 1 : 0;
   a.do_coarse = do_coarse ? 1 : 0;
   a.dot = zr_result ? dot_args(pl, zr_result) : DotArgs{};
-  combine_prolong_kernel<NP><<<fill_grid(combine_prolong_kernel<NP>, kGatherBlock, pl.N), kGatherBlock, 0, s>>>(a);
+  combine_prolong_kernel<NP><<<fill_grid(combine_prolong_kernel<NP>, kGatherBlock, a.N), kGatherBlock, 0, s>>>(a);
 }
 
 void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse)
@@ -429,7 +456,7 @@ void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, b
 // combine) and the prolongated surface copies (coarse.cpp:164-181)
 void launch_prolong(Plan& pl, cudaStream_t s)
 {
-  corner_values_kernel<<<vec_grid(8LL * pl.ne), kVecBlock, 0, s>>>(pl.Z, pl.conn, pl.Zc, pl.ne);
+  corner_values_kernel<<<vec_grid(8LL * pl.ne_total), kVecBlock, 0, s>>>(pl.Z, pl.conn, pl.Zc, pl.ne_total);
 }
 
 template <int NP>
@@ -862,70 +889,6 @@ DevCsr csr_to_device(Plan& pl, const Csr& A)
 //   down:    copies also in rank r-1's slab     -> continue the partial received
 // each group in ascending global id (the neighbour's matching list is the
 // same set in the same order). A node spanning three ranks is rejected.
-}  // namespace
-
-DistLists dist_partition(const HostSetup& hs, int rank, int nranks, int nsurfp)
-{
-  const Numbering& num = hs.num;
-  const int ne_all = hs.mesh.num_elements();
-  const int np = hs.order + 1;
-  const int nsurf_raw = surface_slot_count(np);
-  auto start = [&](int r) { return static_cast<int>(static_cast<long long>(ne_all) * r / nranks); };
-  const int e0 = start(rank), e1 = start(rank + 1);
-  const int e_lo = rank > 0 ? start(rank - 1) : 0, e_hi = rank + 1 < nranks ? start(rank + 2) : ne_all;
-  const int nsg = num.num_surface_global;
-  std::vector<int> minE(nsg, ne_all), maxE(nsg, -1);
-  for (int e = 0; e < ne_all; ++e)
-    for (int q = 0; q < nsurf_raw; ++q) {
-      const gid g = num.l2g_surf[static_cast<std::size_t>(e) * nsurf_raw + q];
-      minE[g] = std::min(minE[g], e);
-      maxE[g] = std::max(maxE[g], e);
-    }
-  std::vector<int> loc(nsg, -1);
-  std::vector<gid> grp[3];
-  for (int e = e0; e < e1; ++e)
-    for (int q = 0; q < nsurf_raw; ++q) {
-      const gid g = num.l2g_surf[static_cast<std::size_t>(e) * nsurf_raw + q];
-      if (loc[g] != -1) continue;
-      loc[g] = -2;
-      const bool up = maxE[g] >= e1, down = minE[g] < e0;
-      if ((up && down) || (up && maxE[g] >= e_hi) || (down && minE[g] < e_lo))
-        throw HxbError(HXB_EINVAL, "slab partition too thin: a node spans more than two ranks");
-      grp[up ? 1 : (down ? 2 : 0)].push_back(g);
-    }
-  DistLists d;
-  d.e0 = e0;
-  d.e1 = e1;
-  for (auto& v : grp) {
-    std::sort(v.begin(), v.end());
-    d.nodes.insert(d.nodes.end(), v.begin(), v.end());
-  }
-  d.n_grp0 = static_cast<int>(grp[0].size());
-  d.n_up = static_cast<int>(grp[1].size());
-  d.n_down = static_cast<int>(grp[2].size());
-  const int nl = static_cast<int>(d.nodes.size());
-  for (int t = 0; t < nl; ++t) loc[d.nodes[t]] = t;
-  d.off.assign(static_cast<std::size_t>(nl) + 1, 0);
-  for (int e = e0; e < e1; ++e)
-    for (int q = 0; q < nsurf_raw; ++q) d.off[loc[num.l2g_surf[static_cast<std::size_t>(e) * nsurf_raw + q]] + 1]++;
-  for (int t = 0; t < nl; ++t) d.off[t + 1] += d.off[t];
-  std::vector<unsigned> cur(d.off.begin(), d.off.end() - 1);
-  d.smap.assign(static_cast<std::size_t>(e1 - e0) * 2 * nsurfp, 0);
-  d.idx.assign(d.off[nl], 0);
-  for (int le = 0; le < e1 - e0; ++le)
-    for (int q = 0; q < nsurf_raw; ++q) {
-      const gid g = num.l2g_surf[static_cast<std::size_t>(e0 + le) * nsurf_raw + q];
-      int* row = &d.smap[static_cast<std::size_t>(le) * 2 * nsurfp];
-      row[q] = num.dirichlet_mask[g] ? -g - 2 : g;  // encode_dirichlet
-      const unsigned pos = cur[loc[g]]++;
-      row[nsurfp + q] = static_cast<int>(pos);
-      d.idx[pos] = le * nsurfp + q;
-    }
-  return d;
-}
-
-namespace {
-
 // Element-slab partition of the Ax gather, uploaded.
 void build_dist_ax(Plan& pl, const HostSetup& hs, int /*nsurf_raw*/)
 {
@@ -980,10 +943,11 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   pl.rank = opt.reserved[1];
   if (pl.nranks > 1) {
     if (pl.rank < 0 || pl.rank >= pl.nranks) throw HxbError(HXB_EINVAL, "rank out of range");
-    if (opt.precond_mode != HXB_PRECOND_NONE)
-      throw HxbError(HXB_EINVAL, "distributed plans carry the operator only (precond_mode none)");
+    if (opt.precond_mode != HXB_PRECOND_NONE && opt.precond_mode != HXB_PRECOND_TWO_SCALE)
+      throw HxbError(HXB_EINVAL, "distributed plans support precond_mode two_scale or none");
     if (pl.nranks > ne) throw HxbError(HXB_EINVAL, "more ranks than elements");
   }
+  pl.ne_total = ne;
   pl.e0 = static_cast<int>(static_cast<long long>(ne) * pl.rank / pl.nranks);
   pl.ne = static_cast<int>(static_cast<long long>(ne) * (pl.rank + 1) / pl.nranks) - pl.e0;
   pl.nv = mesh.num_vertices();
@@ -1086,13 +1050,43 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   if (pl.do_fine) {
     const int nf = 6 * pl.np * pl.np, nfp = (nf + 3) & ~3;  // rows padded for 16-byte TMA copies
     pl.sfstride = nfp;
-    std::vector<int> enc(static_cast<std::size_t>(ne) * nfp, -1);
-    for (int e = 0; e < ne; ++e)
+    std::vector<int> enc(static_cast<std::size_t>(pl.ne) * nfp, -1);
+    for (int le = 0; le < pl.ne; ++le)
       for (int q = 0; q < nf; ++q) {
-        const gid g = num.sub_face[static_cast<std::size_t>(e) * nf + q];
-        enc[static_cast<std::size_t>(e) * nfp + q] = g < 0 ? -1 : (num.dirichlet_mask[g] ? encode_dirichlet(g) : g);
+        const gid g = num.sub_face[static_cast<std::size_t>(pl.e0 + le) * nf + q];
+        enc[static_cast<std::size_t>(le) * nfp + q] = g < 0 ? -1 : (num.dirichlet_mask[g] ? encode_dirichlet(g) : g);
       }
     pl.sub_face = M.upload(enc);
+  }
+  if (pl.do_fine && pl.nranks > 1) {
+    const DistLists dl = dist_partition(hs, pl.rank, pl.nranks, pl.nsurf);
+    const DistPcgLists d = dist_pcg_setup(hs, dl, pl.rank, pl.nranks);
+    pl.fin_surf = M.upload(d.fin_surf);
+    pl.n_fin_surf = static_cast<int>(d.fin_surf.size());
+    pl.ib0 = d.ib0;
+    pl.ib1 = d.ib1;
+    pl.fine_off = M.upload(d.fine_off);
+    pl.fine_pos = M.upload(d.fine_pos);
+    pl.zsort = M.alloc<double>(std::max<std::size_t>(1, d.fine_off.back()));
+    pl.n_fsend_down = d.n_fsend_down;
+    pl.n_fsend_up = d.n_fsend_up;
+    std::vector<int> fr(d.frecv_down);
+    fr.insert(fr.end(), d.frecv_up.begin(), d.frecv_up.end());
+    pl.frecv_pos = M.upload(fr);
+    pl.n_frecv_down = static_cast<int>(d.frecv_down.size());
+    pl.n_frecv_up = static_cast<int>(d.frecv_up.size());
+    pl.g_from_down = M.upload(d.ghost_from_down);
+    pl.g_from_up = M.upload(d.ghost_from_up);
+    pl.g_to_down = M.upload(d.ghost_to_down);
+    pl.g_to_up = M.upload(d.ghost_to_up);
+    pl.n_g_from_down = static_cast<int>(d.ghost_from_down.size());
+    pl.n_g_from_up = static_cast<int>(d.ghost_from_up.size());
+    pl.n_g_to_down = static_cast<int>(d.ghost_to_down.size());
+    pl.n_g_to_up = static_cast<int>(d.ghost_to_up.size());
+    pl.pr_off = M.upload(d.pr_off);
+    pl.pr_idx = M.upload(d.pr_idx);
+    pl.pr_mass = M.upload(d.pr_mass);
+  } else if (pl.do_fine) {
     const std::size_t nsub = static_cast<std::size_t>(pl.P) * pl.P * pl.P;
     std::vector<unsigned> cnt(static_cast<std::size_t>(pl.N) + 1, 0);
     std::vector<gid> scratch(pl.nloc);
@@ -1112,6 +1106,20 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.fine_off = M.upload(cnt);
     pl.fine_pos = M.upload(pos);
     pl.zsort = M.alloc<double>(cnt[pl.N]);
+  }
+  if (pl.nranks > 1) {
+    std::vector<int> nodes_host(pl.n_loc_surf);
+    HXB_CUDA(cudaMemcpy(nodes_host.data(), pl.ax_nodes, sizeof(int) * pl.n_loc_surf, cudaMemcpyDeviceToHost));
+    pl.loc_list = pl.ax_nodes;
+    if (!pl.do_fine) {  // operator-only plan: finalised set still needed for dots
+      std::vector<int> fs(nodes_host.begin(), nodes_host.begin() + pl.n_grp0);
+      fs.insert(fs.end(), nodes_host.begin() + pl.n_grp0 + pl.n_up, nodes_host.end());
+      pl.fin_surf = M.upload(fs);
+      pl.n_fin_surf = static_cast<int>(fs.size());
+      const long long NI = static_cast<long long>(pl.order - 1) * (pl.order - 1) * (pl.order - 1);
+      pl.ib0 = static_cast<int>(pl.nsg + pl.e0 * NI);
+      pl.ib1 = static_cast<int>(pl.nsg + (pl.e0 + pl.ne) * NI);
+    }
   }
 
   // coarse: connectivity, vertex incidence CSR (e, cb) order, coarse matrix, AMG / dense
@@ -1696,6 +1704,180 @@ int hxb_dist_apply_A_end(hxb_plan* plan, double* d_r, const double* d_recv_up, v
                                                                             d_r);
       pl->launches += 1;
     }
+    dist_stream_out(pl, stream);
+  });
+}
+
+// ---- distributed preconditioned CG (staged; Python/NCCL carries the messages)
+int hxb_dist_pcg_info(hxb_plan* plan, int64_t* info)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (!info) throw HxbError(HXB_EINVAL, "null argument");
+    const int64_t v[16] = {pl->n_g_from_down, pl->n_g_from_up, pl->n_g_to_down, pl->n_g_to_up,
+                           pl->n_fsend_down,  pl->n_fsend_up,  pl->n_frecv_down, pl->n_frecv_up,
+                           pl->e0,           pl->e0 + pl->ne, pl->ne_total,    pl->do_fine ? 1 : 0,
+                           pl->do_coarse ? 1 : 0, pl->n_up, pl->n_down, pl->N};
+    std::memcpy(info, v, sizeof(v));
+  });
+}
+
+int hxb_dist_vec(hxb_plan* plan, int mode, double a, const double* x0, const double* x1, double* y0, double* y1,
+                 void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (mode < 0 || mode > 3) throw HxbError(HXB_EINVAL, "mode out of range");
+    HXB_CUDA(cudaSetDevice(pl->device));
+    dist_stream_in(pl, stream);
+    const int total = pl->n_loc_surf + (pl->ib1 - pl->ib0);
+    dist_vec_kernel<<<fill_grid(dist_vec_kernel, kVecBlock, total), kVecBlock, 0, pl->s_main>>>(
+        mode, pl->loc_list, pl->n_loc_surf, pl->ib0, pl->ib1, a, x0, x1, y0, y1);
+    pl->launches += 1;
+    dist_stream_out(pl, stream);
+  });
+}
+
+int hxb_dist_dot(hxb_plan* plan, const double* x, const double* y, double* d_out, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    dist_stream_in(pl, stream);
+    const int total = pl->n_fin_surf + (pl->ib1 - pl->ib0);
+    dist_dot_kernel<kVecBlock><<<fill_grid(dist_dot_kernel<kVecBlock>, kVecBlock, total), kVecBlock, 0, pl->s_main>>>(
+        pl->fin_surf, pl->n_fin_surf, pl->ib0, pl->ib1, x, y, dot_args(*pl, d_out));
+    pl->launches += 1;
+    dist_stream_out(pl, stream);
+  });
+}
+
+// which: 0 ghost r to the lower rank, 1 ghost r to the upper rank, 2 finals of the
+// down-interface nodes (to the lower rank); unpack: 0/1 ghosts from lower/upper,
+// 2 finals of the up-interface nodes (from the upper rank)
+static void dist_list(Plan* pl, int which, bool pack, const int** list, int* n)
+{
+  if (which == 0) {
+    *list = pack ? pl->g_to_down : pl->g_from_down;
+    *n = pack ? pl->n_g_to_down : pl->n_g_from_down;
+  } else if (which == 1) {
+    *list = pack ? pl->g_to_up : pl->g_from_up;
+    *n = pack ? pl->n_g_to_up : pl->n_g_from_up;
+  } else if (which == 2) {
+    *list = pack ? pl->ax_nodes + pl->n_grp0 + pl->n_up : pl->ax_nodes + pl->n_grp0;
+    *n = pack ? pl->n_down : pl->n_up;
+  } else {
+    throw HxbError(HXB_EINVAL, "which out of range");
+  }
+}
+
+int hxb_dist_pack(hxb_plan* plan, int which, const double* d_x, double* d_buf, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    const int* list;
+    int n;
+    dist_list(pl, which, true, &list, &n);
+    dist_stream_in(pl, stream);
+    if (n) dist_pack_kernel<<<vec_grid(n), kVecBlock, 0, pl->s_main>>>(list, n, d_x, d_buf), pl->launches += 1;
+    dist_stream_out(pl, stream);
+  });
+}
+
+int hxb_dist_unpack(hxb_plan* plan, int which, const double* d_buf, double* d_x, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    const int* list;
+    int n;
+    dist_list(pl, which, false, &list, &n);
+    dist_stream_in(pl, stream);
+    if (n) dist_unpack_kernel<<<vec_grid(n), kVecBlock, 0, pl->s_main>>>(list, n, d_buf, d_x), pl->launches += 1;
+    dist_stream_out(pl, stream);
+  });
+}
+
+// fine subdomain solves of the owned elements on residual d_r (ghosts filled):
+// local contributions to the sum buffer, the others to d_fsend [to lower | to
+// upper], and the owned slab of the coarse restriction partials
+int hxb_dist_fine(hxb_plan* plan, const double* d_r, double* d_fsend, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (!pl->do_fine) throw HxbError(HXB_EINVAL, "plan has no fine preconditioner");
+    HXB_CUDA(cudaSetDevice(pl->device));
+    dist_stream_in(pl, stream);
+    double* keep = pl->r;
+    pl->r = const_cast<double*>(d_r);
+    pl->fsend = d_fsend;
+    HXB_DISPATCH_NP(pl->np, launch_fdm, *pl, pl->s_main);
+    pl->r = keep;
+    pl->fsend = nullptr;
+    dist_stream_out(pl, stream);
+  });
+}
+
+int hxb_dist_fine_recv(hxb_plan* plan, const double* d_frecv, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    dist_stream_in(pl, stream);
+    const int n = pl->n_frecv_down + pl->n_frecv_up;
+    if (n) dist_fine_scatter_kernel<<<vec_grid(n), kVecBlock, 0, pl->s_main>>>(pl->frecv_pos, n, d_frecv, pl->zsort),
+        pl->launches += 1;
+    dist_stream_out(pl, stream);
+  });
+}
+
+// Rpart slab (direction 0: owned slab -> d_buf) or full array (1: d_buf -> plan)
+int hxb_dist_rpart(hxb_plan* plan, int direction, double* d_buf, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (!pl->do_coarse) throw HxbError(HXB_EINVAL, "plan has no coarse preconditioner");
+    HXB_CUDA(cudaSetDevice(pl->device));
+    dist_stream_in(pl, stream);
+    if (direction == 0)
+      HXB_CUDA(cudaMemcpyAsync(d_buf, pl->Rpart + 8LL * pl->e0, sizeof(double) * 8 * pl->ne, cudaMemcpyDeviceToDevice,
+                               pl->s_main));
+    else
+      HXB_CUDA(cudaMemcpyAsync(pl->Rpart, d_buf, sizeof(double) * 8 * pl->ne_total, cudaMemcpyDeviceToDevice,
+                               pl->s_main));
+    dist_stream_out(pl, stream);
+  });
+}
+
+// coarse solve over the full Rpart (replicated on every rank, identical results)
+int hxb_dist_coarse(hxb_plan* plan, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (!pl->do_coarse) throw HxbError(HXB_EINVAL, "plan has no coarse preconditioner");
+    HXB_CUDA(cudaSetDevice(pl->device));
+    dist_stream_in(pl, stream);
+    HXB_CUDA(cudaGraphLaunch(pl->coarse_exec, pl->s_main));
+    pl->launches += pl->coarse_graph_nodes;
+    dist_stream_out(pl, stream);
+  });
+}
+
+// z = P r on the finalised nodes (mask rows, fine + coarse sums); partial z.r -> d_zr
+int hxb_dist_combine(hxb_plan* plan, const double* d_r, double* d_z, double* d_zr, void* stream)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    HXB_CUDA(cudaSetDevice(pl->device));
+    dist_stream_in(pl, stream);
+    double* kr = pl->r;
+    double* kz = pl->z;
+    pl->r = const_cast<double*>(d_r);
+    pl->z = d_z;
+    launch_combine(*pl, d_zr, pl->s_main, pl->do_fine, pl->do_coarse);
+    pl->r = kr;
+    pl->z = kz;
     dist_stream_out(pl, stream);
   });
 }

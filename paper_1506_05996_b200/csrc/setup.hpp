@@ -201,6 +201,28 @@ struct DistLists {
   std::vector<int> smap;
 };
 DistLists dist_partition(const HostSetup& hs, int rank, int nranks, int nsurfp);
+
+// The preconditioner side of the distributed solve (setup_dist.cpp):
+//   finalised nodes = fin_surf (group 0 + down, local-list order) then the
+//   owned interior range [ib0, ib1); fine CSR over them in (e, slot) order;
+//   fine_pos[le][slot] >= 0 local sum position, -1 sentinel, <= -2 index
+//   -2-q into this rank's send buffer [to down | to up]; frecv_* positions
+//   for the neighbours' contributions in the order they send them;
+//   ghost_from_* nodes whose r this rank receives, ghost_to_* it sends;
+//   pr_* every copy (global e*nsurfp+slot, mass) of the finalised surface nodes.
+struct DistPcgLists {
+  int ib0 = 0, ib1 = 0;
+  std::vector<int> fin_surf;
+  std::vector<unsigned> fine_off;
+  std::vector<int> fine_pos;
+  int n_fsend_down = 0, n_fsend_up = 0;
+  std::vector<int> frecv_down, frecv_up;
+  std::vector<int> ghost_from_down, ghost_from_up, ghost_to_down, ghost_to_up;
+  std::vector<unsigned> pr_off;
+  std::vector<int> pr_idx;
+  std::vector<double> pr_mass;
+};
+DistPcgLists dist_pcg_setup(const HostSetup& hs, const DistLists& d, int rank, int nranks);
 HexMesh mesh_from_arrays(int nv, const double* xyz, int ne, const std::int32_t* conn, int nbf,
                          const std::int32_t* be, const std::int32_t* bf, const std::uint8_t* bt);
 // IndexMaps export in the reference layout (mesh.hpp:66-97); null pointers skipped.

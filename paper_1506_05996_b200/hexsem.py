@@ -105,6 +105,16 @@ SIGNATURES = {
     "hxb_dist_apply_A_begin": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hxb_dist_apply_A_continue": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hxb_dist_apply_A_end": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hxb_dist_pcg_info": (C.c_int, [P, P]),
+    "hxb_dist_vec": (C.c_int, [P, C.c_int, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hxb_dist_dot": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hxb_dist_pack": (C.c_int, [P, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hxb_dist_unpack": (C.c_int, [P, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hxb_dist_fine": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "hxb_dist_fine_recv": (C.c_int, [P, C.c_void_p, C.c_void_p]),
+    "hxb_dist_rpart": (C.c_int, [P, C.c_int, C.c_void_p, C.c_void_p]),
+    "hxb_dist_coarse": (C.c_int, [P, C.c_void_p]),
+    "hxb_dist_combine": (C.c_int, [P, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "hxb_setup_create": (C.c_int, [C.POINTER(_Mesh), C.c_int, P, P, C.POINTER(_Options), C.POINTER(P)]),
     "hxb_setup_destroy": (None, [P]),
     "hxb_setup_info": (C.c_int, [P, C.POINTER(_PlanInfo)]),
@@ -452,6 +462,18 @@ class Plan:
     def dist_apply_A_end(self, d_r: int, d_recv_up: int, stream: int = 0):
         _check(lib().hxb_dist_apply_A_end(self._h, C.c_void_p(d_r), C.c_void_p(d_recv_up or None),
                                           C.c_void_p(stream or None)))
+
+    def dist_pcg_info(self) -> dict:
+        v = np.zeros(16, dtype=np.int64)
+        _check(lib().hxb_dist_pcg_info(self._h, _ptr(v)))
+        keys = ["ghost_from_down", "ghost_from_up", "ghost_to_down", "ghost_to_up", "fsend_down", "fsend_up",
+                "frecv_down", "frecv_up", "e0", "e1", "ne_total", "has_fine", "has_coarse", "n_up", "n_down", "N"]
+        return dict(zip(keys, (int(x) for x in v)))
+
+    def dist_call(self, name: str, *args):
+        """Raw staged call hxb_dist_<name>(plan, *args) (device pointers as ints)."""
+        conv = [C.c_void_p(a) if isinstance(a, int) and not isinstance(a, bool) else a for a in args]
+        _check(getattr(lib(), "hxb_dist_" + name)(self._h, *conv))
 
     KT_TAGS = {"ax_elem": 0, "ax_gather": 1, "fdm": 2, "combine": 3}
 
