@@ -196,12 +196,17 @@ def run_ours(args, rank, world, local_rank):
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the B200 path has no CPU fallback)")
+    local_rank = local_rank % torch.cuda.device_count()  # --backend gloo tests: ranks may share a GPU
     torch.cuda.set_device(local_rank)
     dist = None
+    host_staging = args.backend == "gloo"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if host_staging:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     def barrier():
         if dist is not None:
@@ -211,7 +216,7 @@ def run_ours(args, rank, world, local_rank):
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        t = torch.tensor([x], device="cpu" if host_staging else "cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -221,10 +226,10 @@ def run_ours(args, rank, world, local_rank):
     distributed = world > 1 and not args.replicas
     if distributed:
         # element-slab partition of the one cfg2 mesh over the ranks (strong scaling)
-        plan = hx.Plan(mesh, order, precond="none", device=local_rank, rank=rank, nranks=world)
+        plan = hx.Plan(mesh, order, device=local_rank, rank=rank, nranks=world)
         from paper_1506_05996_b200.dist import DistOperator
 
-        dop = DistOperator(plan, torch, dist)
+        dop = DistOperator(plan, torch, dist, host_staging)
     else:
         plan = hx.Plan(mesh, order, device=local_rank)
     setup_s = time.time() - t0
@@ -272,7 +277,7 @@ def run_ours(args, rank, world, local_rank):
     r_dev = d_r.cpu().numpy()
     if distributed:
         return finish_distributed(args, rank, world, plan, value, ms_step, launches, elem_ms, elem_n, gath_ms,
-                                  gath_n, ms_total, bytes_ax, N, NE, setup_s, sampler, dist, torch)
+                                  gath_n, ms_total, bytes_ax, N, NE, setup_s, sampler, dist, torch, max_over_ranks)
 
     # ---- e2e through the C-ABI with pinned host buffers -------------------
     h_u = torch.from_numpy(u_host).pin_memory()
@@ -400,20 +405,40 @@ def run_ours(args, rank, world, local_rank):
 
 
 def finish_distributed(args, rank, world, plan, value, ms_step, launches, elem_ms, elem_n, gath_ms, gath_n,
-                       ms_total, bytes_ax, N, NE, setup_s, sampler, dist, torch):
+                       ms_total, bytes_ax, N, NE, setup_s, sampler, dist, torch, max_over_ranks):
     """JSON line of the element-slab distributed Ax (strong scaling of cfg2)."""
     clocks = sampler.stop()
     peak, peak_src = _peaks()
     elem_avg_ms = elem_ms / max(1, elem_n)
     achieved = bytes_ax / (elem_avg_ms * 1e-3) / 1e9 if elem_n else None
     info = plan.dist_info()
+    pcg = None
+    if not args.no_pcg:  # distributed two-scale PCG to 1e-8 (paper_1506_05996_b200/dist.py)
+        from paper_1506_05996_b200.dist import RankCtx, TorchComm, dist_pcg
+
+        ctx = RankCtx(plan, torch)
+        comm = TorchComm(dist, torch, host_staging=args.backend == "gloo")
+        ctx.b.copy_(torch.from_numpy(plan.load_ones()).cuda())
+        dist_pcg([ctx], comm, tol=1e-8)  # warm-up
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        res = dist_pcg([ctx], comm, tol=1e-8)
+        t1.record()
+        torch.cuda.synchronize()
+        solve_s = max_over_ranks(t0.elapsed_time(t1) / 1e3)
+        pcg = {"tol": 1e-8, "iterations": res["iterations"], "status": res["status"], "solve_s": solve_s,
+               "r0": res["residual_history"][0], "r_final": res["residual_history"][-1],
+               "orchestration": "Python loop over staged C-ABI calls, NCCL p2p + all-reduce (torch.distributed)"}
     line = {
         "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated mesh, splitmix64 u)",
         "config": {"workload": f"cfg2 Ax distributed: {args.k}^3 hexes N={args.order} split in {world} element slabs",
                    "k": args.k, "order": args.order, "N": N, "NE_per_rank": NE,
-                   "parallelism": f"element-slab partition x{world}, NCCL neighbour exchange (2 messages per Ax)",
+                   "parallelism": f"element-slab partition x{world}, {args.backend} neighbour exchange (2 messages per Ax)",
                    "interface_doubles_rank0": info["n_up"],
                    "l2": "inputs larger than L2; no flush"},
         "e2e": None, "gpu_launches": launches,
@@ -421,7 +446,7 @@ def finish_distributed(args, rank, world, plan, value, ms_step, launches, elem_m
                      "frac": achieved / peak if achieved else None, "traffic": None, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_ax, "avg_launch_ms": elem_avg_ms,
                      "share_of_step": elem_ms / ms_total if ms_total else None},
-        "pcg": None, "pcg_note": "distributed PCG (FDM halos, coarse allgather) is not built yet; see DESIGN.md",
+        "pcg": pcg,
         "clocks": clocks, "setup_s": setup_s, "cpu_baseline": None,
     }
     plan.close()
@@ -442,6 +467,8 @@ def main():
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent cfg2 replicas instead of a partition")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: host-staged messages, lets several ranks share one GPU (tests)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

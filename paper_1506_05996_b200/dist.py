@@ -16,13 +16,26 @@ hxb_dist_*). The assembled result equals the single-plan Ax bit for bit.
 from __future__ import annotations
 
 
-def exchange(dist, rank: int, world: int, send_to_upper, recv_from_lower, direction: str):
+def _staged(tensors, host: bool):
+    """Host copies of device tensors for a CPU-only backend (gloo tests)."""
+    if not host:
+        return tensors, None
+    return [None if t is None else t.cpu() for t in tensors], tensors
+
+
+def exchange(dist, rank: int, world: int, send_to_upper, recv_from_lower, direction: str, host_staging: bool = False):
     """One neighbour exchange along the slab chain.
 
     direction "up":   send_to_upper -> rank+1, recv_from_lower <- rank-1
     direction "down": send_to_upper is sent to rank-1, recv_from_lower filled from rank+1
     Empty tensors (no interface on that side) are skipped.
     """
+    if host_staging:
+        (s_h, r_h), _ = _staged([send_to_upper, recv_from_lower], True)
+        exchange(dist, rank, world, s_h, r_h, direction)
+        if recv_from_lower is not None and recv_from_lower.numel():
+            recv_from_lower.copy_(r_h)
+        return
     if direction == "up":
         dst, src = rank + 1, rank - 1
     else:
@@ -40,11 +53,12 @@ def exchange(dist, rank: int, world: int, send_to_upper, recv_from_lower, direct
 class DistOperator:
     """Staged distributed Ax of one rank with its exchange buffers."""
 
-    def __init__(self, plan, torch, dist=None):
+    def __init__(self, plan, torch, dist=None, host_staging: bool = False):
         self.plan = plan
         self.info = plan.dist_info()
         self.rank, self.world = self.info["rank"], self.info["nranks"]
         self.dist = dist
+        self.host_staging = host_staging
         dev = "cuda"
         f64 = torch.float64
         self.send_up = torch.empty(self.info["n_up"], dtype=f64, device=dev)
@@ -68,9 +82,9 @@ class DistOperator:
     def apply(self, d_u: int, d_r: int, stream: int = 0):
         """r = A u across all ranks (torch.distributed must be initialised)."""
         self.begin(d_u, d_r, stream)
-        exchange(self.dist, self.rank, self.world, self.send_up, self.recv_down, "up")
+        exchange(self.dist, self.rank, self.world, self.send_up, self.recv_down, "up", self.host_staging)
         self.cont(d_u, d_r, stream)
-        exchange(self.dist, self.rank, self.world, self.send_down, self.recv_up, "down")
+        exchange(self.dist, self.rank, self.world, self.send_down, self.recv_up, "down", self.host_staging)
         self.end(d_r, stream)
 
 
@@ -171,12 +185,21 @@ class InProcessComm:
 
 
 class TorchComm:
-    """One rank per process; torch.distributed (NCCL over NVLink) messages."""
+    """One rank per process; torch.distributed (NCCL over NVLink) messages.
+    host_staging=True routes device tensors through host copies for a
+    CPU-only backend (gloo), e.g. several ranks sharing one GPU in tests."""
 
-    def __init__(self, dist, torch):
-        self.dist, self.torch = dist, torch
+    def __init__(self, dist, torch, host_staging: bool = False):
+        self.dist, self.torch, self.host = dist, torch, host_staging
 
     def exchange(self, ctxs, to_lower, to_upper, from_lower, from_upper):
+        if self.host:
+            h = [[t.cpu() for t in lst] for lst in (to_lower, to_upper, from_lower, from_upper)]
+            TorchComm(self.dist, self.torch).exchange(ctxs, *h)
+            for dev, hst in ((from_lower, h[2]), (from_upper, h[3])):
+                if dev[0].numel():
+                    dev[0].copy_(hst[0])
+            return
         (c,) = ctxs
         d, r, R = self.dist, c.rank, c.world
         ops = []
@@ -194,7 +217,7 @@ class TorchComm:
 
     def allreduce(self, ctxs, vals):
         (v,) = vals
-        t = v.clone()
+        t = v.cpu() if self.host else v.clone()
         self.dist.all_reduce(t)
         return float(t.item())
 
@@ -204,9 +227,10 @@ class TorchComm:
         R = c.world
         ne = c.info["ne_total"]
         cap = 8 * (-(-ne // R))  # slabs differ by at most one element: pad to the largest
-        buf = torch.zeros(cap, dtype=c.rpart.dtype, device=c.rpart.device)
+        dev = "cpu" if self.host else c.rpart.device
+        buf = torch.zeros(cap, dtype=c.rpart.dtype, device=dev)
         buf[:c.rpart.numel()] = c.rpart
-        out = torch.empty(cap * R, dtype=buf.dtype, device=buf.device)
+        out = torch.empty(cap * R, dtype=buf.dtype, device=dev)
         d.all_gather_into_tensor(out, buf)
         parts = []
         for q in range(R):

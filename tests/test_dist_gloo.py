@@ -81,3 +81,56 @@ def test_slab_partition_and_exchange(world, k, order):
     assert np.array_equal(np.sort(fin), touched)
     nsg = touched.max() + 1
     assert np.array_equal(touched, np.arange(nsg))  # surface ids are exactly [0, nsg)
+
+
+class _FakeCtx:
+    def __init__(self, rank, world, ne):
+        self.rank, self.world = rank, world
+        e0, e1 = ne * rank // world, ne * (rank + 1) // world
+        self.info = {"ne_total": ne}
+        self.rpart = torch.arange(8 * e0, 8 * e1, dtype=torch.float64)
+        self.rpart_full = torch.empty(8 * ne, dtype=torch.float64)
+
+
+def _comm_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1506_05996_b200.dist import TorchComm
+
+        comm = TorchComm(dist, torch)
+        ne = 7 * world + 2  # uneven slabs exercise the padded all-gather
+        c = _FakeCtx(rank, world, ne)
+        comm.allgather_rpart([c])
+        ok_gather = torch.equal(c.rpart_full, torch.arange(8 * ne, dtype=torch.float64))
+        s = comm.allreduce([c], [torch.tensor([float(rank + 1)])])
+        ok_sum = s == world * (world + 1) / 2
+        to_lower = torch.full((3,), 10.0 * rank)
+        to_upper = torch.full((2,), 20.0 * rank)
+        from_lower = torch.empty(2 if rank > 0 else 0)
+        from_upper = torch.empty(3 if rank + 1 < world else 0)
+        comm.exchange([c], [to_lower], [to_upper], [from_lower], [from_upper])
+        ok_x = (rank == 0 or torch.all(from_lower == 20.0 * (rank - 1)).item()) and \
+               (rank + 1 == world or torch.all(from_upper == 10.0 * (rank + 1)).item())
+        q.put((rank, bool(ok_gather), bool(ok_sum), bool(ok_x)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_torch_comm_primitives(world):
+    """The collectives the distributed PCG uses (dist.TorchComm): padded Rpart
+    all-gather in rank order, scalar all-reduce, neighbour exchange."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_comm_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        assert r[1] and r[2] and r[3], r
