@@ -158,6 +158,34 @@ int hxb_apply_P_device(hxb_plan* plan, const double* d_r, double* d_z, void* str
 int hxb_solve(hxb_plan* plan, const double* b, const hxb_pcg_config* cfg, hxb_pcg_result* res);
 int hxb_solve_device(hxb_plan* plan, const double* d_b, const hxb_pcg_config* cfg, hxb_pcg_result* res);
 
+/* HeatConfig (problem.hpp:18-31): backward Euler on rho cp du/dt - div(kappa grad u) = Q
+ * inside a ball moving along a straight trajectory. */
+typedef struct hxb_heat_config {
+  double dt;                   /* > 0; the plan must carry c = 1/dt per element (problem.cpp:149) */
+  int steps;
+  double rho, cp, q_power, source_radius;
+  int has_source;
+  int auto_trajectory;         /* straight line along the longest bounding-box axis */
+  double source_start[3], source_end[3];
+  double initial_value;
+} hxb_heat_config;
+
+/* HeatStep (report.hpp:57-64) */
+typedef struct hxb_heat_step {
+  int step, iterations;
+  double residual, mean_temperature, l2_norm, source_integral;
+} hxb_heat_step;
+
+/* solve_heat (problem.cpp:145-255) on the device: per step the load, the
+ * warm-start residual b - A u, a PCG solve for the correction and the
+ * update all stay in HBM. steps_out holds cfg->steps records; final_u (may
+ * be NULL) receives N values. */
+int hxb_solve_heat(hxb_plan* plan, const hxb_heat_config* cfg, const hxb_pcg_config* pcg, hxb_heat_step* steps_out,
+                   int* num_steps, int* all_converged, double* final_u, double* solve_seconds);
+
+/* Physical coordinates of the global nodes, xyz[3N] (global_node_coords, mesh.cpp:477-492). */
+int hxb_node_coords(hxb_plan* plan, double* xyz);
+
 /* assemble_load(s = 1) and lumped_mass (problem.cpp:38-46, operator.hpp:60). */
 int hxb_load_ones(hxb_plan* plan, double* b);
 int hxb_lumped_mass(hxb_plan* plan, double* m);

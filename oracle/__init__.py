@@ -20,6 +20,7 @@ from .ctypes_oracle import (  # noqa: F401
     oracle_fma_available,
     RefConfig,
     ref_available,
+    ref_solve_heat,
     oracle_available,
     ref_gll,
     ref_pencil,

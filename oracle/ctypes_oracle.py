@@ -302,6 +302,47 @@ def oracle_fma_available() -> bool:
     return os.path.exists(_ORC_FMA_SO)
 
 
+class _CHeat(C.Structure):
+    _fields_ = [("dt", C.c_double), ("steps", C.c_int), ("rho", C.c_double), ("cp", C.c_double),
+                ("q_power", C.c_double), ("source_radius", C.c_double), ("has_source", C.c_int),
+                ("auto_trajectory", C.c_int), ("source_start", C.c_double * 3), ("source_end", C.c_double * 3),
+                ("initial_value", C.c_double)]
+
+
+def ref_solve_heat(config: RefConfig, heat: dict, tol: float = 1e-6, max_iterations: int = 500) -> dict:
+    """The reference's own solve_heat (problem.cpp:145-255) via oracle/_ref."""
+    L = C.CDLL(_REF_SO)
+    fn = L.ref_solve_heat
+    fn.restype = C.c_int
+    n = RefSystem(config).N
+    h = _CHeat()
+    h.dt, h.steps = float(heat.get("dt", 0.04)), int(heat.get("steps", 70))
+    h.rho, h.cp = float(heat.get("rho", 7000.0)), float(heat.get("cp", 0.8))
+    h.q_power, h.source_radius = float(heat.get("q_power", 1000.0)), float(heat.get("source_radius", 0.5))
+    h.has_source, h.auto_trajectory = int(heat.get("has_source", True)), int(heat.get("auto_trajectory", True))
+    for d in range(3):
+        h.source_start[d] = float(heat.get("source_start", (0, 0, 0))[d])
+        h.source_end[d] = float(heat.get("source_end", (0, 0, 0))[d])
+    h.initial_value = float(heat.get("initial_value", 0.0))
+    S = max(1, h.steps)
+    its = np.zeros(S, dtype=np.int32)
+    res, mean, l2, src = (np.zeros(S) for _ in range(4))
+    u = np.zeros(n)
+    ns, ok = C.c_int(), C.c_int()
+    nout = C.c_int64()
+    secs = C.c_double()
+    cc = config.to_c()
+    rc = fn(C.byref(cc), C.byref(h), C.c_double(tol), C.c_int(max_iterations), C.c_int64(n), C.byref(ns), C.byref(ok),
+            _ptr(its), _ptr(res), _ptr(mean), _ptr(l2), _ptr(src), _ptr(u), C.byref(nout), C.byref(secs))
+    if rc:
+        L.ref_last_error.restype = C.c_char_p
+        raise RuntimeError(L.ref_last_error().decode())
+    k = ns.value
+    rows = [{"step": q + 1, "iterations": int(its[q]), "residual": float(res[q]), "mean_temperature": float(mean[q]),
+             "l2_norm": float(l2[q]), "source_integral": float(src[q])} for q in range(k)]
+    return {"steps": rows, "all_converged": bool(ok.value), "final_field": u, "solve_seconds": secs.value}
+
+
 def ref_available() -> bool:
     return os.path.exists(_REF_SO)
 

@@ -382,6 +382,53 @@ int ref_element_h(void* hp, double* h3)
   });
 }
 
+// solve_heat (problem.cpp:145-255) through the reference's own driver.
+struct ref_heat {
+  double dt;
+  int steps;
+  double rho, cp, q_power, source_radius;
+  int has_source, auto_trajectory;
+  double source_start[3], source_end[3];
+  double initial_value;
+};
+
+int ref_solve_heat(const ref_config* c, const ref_heat* h, double tol, int max_iterations, int64_t n_cap,
+                   int* num_steps, int* all_converged, int* iterations, double* residual, double* mean,
+                   double* l2, double* source_integral, double* final_u, int64_t* n_out, double* seconds)
+{
+  return guard([&] {
+    ProblemConfig cfg = to_cfg(c);
+    cfg.pcg.rel_tolerance = tol;
+    cfg.pcg.max_iterations = max_iterations;
+    cfg.heat.dt = h->dt;
+    cfg.heat.steps = h->steps;
+    cfg.heat.rho = h->rho;
+    cfg.heat.cp = h->cp;
+    cfg.heat.q_power = h->q_power;
+    cfg.heat.source_radius = h->source_radius;
+    cfg.heat.has_source = h->has_source != 0;
+    cfg.heat.auto_trajectory = h->auto_trajectory != 0;
+    for (int d = 0; d < 3; ++d) {
+      cfg.heat.source_start[d] = h->source_start[d];
+      cfg.heat.source_end[d] = h->source_end[d];
+    }
+    cfg.heat.initial_value = h->initial_value;
+    const HeatReport rep = solve_heat(cfg);
+    *num_steps = static_cast<int>(rep.steps.size());
+    *all_converged = rep.all_converged ? 1 : 0;
+    for (std::size_t q = 0; q < rep.steps.size(); ++q) {
+      iterations[q] = rep.steps[q].iterations;
+      residual[q] = rep.steps[q].residual;
+      mean[q] = rep.steps[q].mean_temperature;
+      l2[q] = rep.steps[q].l2_norm;
+      source_integral[q] = rep.steps[q].source_integral;
+    }
+    *n_out = static_cast<int64_t>(rep.final_field.size());
+    if (final_u && n_cap >= *n_out) std::memcpy(final_u, rep.final_field.data(), rep.final_field.size() * sizeof(double));
+    if (seconds) *seconds = rep.base.timings.solve_seconds;
+  });
+}
+
 // Counter models (operator.cpp:20-37, fine.cpp:82-92)
 unsigned long long ref_words_model(long long ne, int n, int variant)
 {

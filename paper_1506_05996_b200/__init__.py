@@ -5,6 +5,9 @@ C-ABI in ``include/hexsem_b200.h``); this package is its Python host mirror.
 """
 from .hexsem import (  # noqa: F401
     HexMesh,
+    HeatConfig,
+    build_heat_system,
+    solve_heat,
     HostSetup,
     HxbError,
     Plan,
@@ -20,6 +23,7 @@ from .hexsem import (  # noqa: F401
     lib,
     make_mesh,
     mesh_info,
+    mms_convergence,
     pencil,
     refine_uniform,
     residual_flops_model,

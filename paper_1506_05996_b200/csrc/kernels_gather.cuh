@@ -200,6 +200,7 @@ struct CombineProlongArgs {
   const double* mass;      // [e][nloc] (element-interior copies)
   const double* mass_csr;  // surface copies, Ax-CSR order
   const double* lumped;
+  const double* inv_lumped;
   double* z;
   int N, nsg;
   int do_fine, do_coarse;
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(Combin
             zc += pz(c / NSP, i, j, k) * __ldcs(a.mass_csr + q);
           }
         }
-        s += zc / __ldg(a.lumped + g);
+        s += zc * __ldg(a.inv_lumped + g);  // /m_N (coarse.cpp:185) as a product with 1/m_N
       }
       zg = s;
     }

@@ -92,6 +92,55 @@ __global__ void sqrt_store_kernel(const double* __restrict__ src, double* __rest
   *dst = sqrt(*src);
 }
 
+// --- backward-Euler heat driver (problem.cpp:145-255) -------------------------
+// b = mask ? 0 : m (u/dt + q), q = Q/(rho cp) inside the moving ball;
+// source integral sum m q over free nodes -> dot
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) heat_rhs_kernel(const double* __restrict__ xyz, const double* __restrict__ m,
+                                                        const std::uint8_t* __restrict__ mask,
+                                                        const double* __restrict__ u, double* __restrict__ b, int n,
+                                                        double cx, double cy, double cz, double r2, double qd,
+                                                        double dt, int has_source, DotArgs d)
+{
+  __shared__ double red[BLOCK / 32];
+  double s = 0.0;
+  for (int g = blockIdx.x * BLOCK + threadIdx.x; g < n; g += gridDim.x * BLOCK) {
+    double dist2 = 0.0;
+    const double dx = xyz[3 * (long long)g] - cx, dy = xyz[3 * (long long)g + 1] - cy, dz = xyz[3 * (long long)g + 2] - cz;
+    dist2 += dx * dx;
+    dist2 += dy * dy;
+    dist2 += dz * dz;
+    const double q = (has_source && dist2 <= r2) ? qd : 0.0;
+    const bool fixed = mask[g] != 0;
+    b[g] = fixed ? 0.0 : m[g] * (u[g] / dt + q);
+    if (!fixed) s += m[g] * q;
+  }
+  dot_commit<BLOCK>(d, s, red);
+}
+
+// b -= A u (warm start residual, problem.cpp:211-212)
+__global__ void sub_kernel(double* __restrict__ b, const double* __restrict__ au, int n)
+{
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) b[g] -= au[g];
+}
+
+// u += du; partial sums of m u (slot 0) and m u^2 (slot 1) (problem.cpp:214-221)
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) heat_update_kernel(double* __restrict__ u, const double* __restrict__ du,
+                                                           const double* __restrict__ m, int n, DotArgs d0, DotArgs d1)
+{
+  __shared__ double red[BLOCK / 32];
+  double s0 = 0.0, s1 = 0.0;
+  for (int g = blockIdx.x * BLOCK + threadIdx.x; g < n; g += gridDim.x * BLOCK) {
+    const double v = u[g] + du[g];
+    u[g] = v;
+    s0 += m[g] * v;
+    s1 += m[g] * v * v;
+  }
+  dot_commit<BLOCK>(d0, s0, red);
+  dot_commit<BLOCK>(d1, s1, red);
+}
+
 // mode none: z = r, zr = z.r
 // (precond.cpp:30-33)
 

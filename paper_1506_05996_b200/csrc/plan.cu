@@ -215,6 +215,9 @@ struct Plan {
   int n_g_from_down = 0, n_g_from_up = 0, n_g_to_down = 0, n_g_to_up = 0;
   int* loc_list = nullptr;    // local surface nodes (= ax_nodes) for vector updates
   double* fsend = nullptr;    // FDM contributions for the neighbours (caller buffer, set per call)
+  std::vector<double> h_xyz;  // global node coordinates (heat driver), host copy
+  double* d_xyz = nullptr;
+  double* heat_u = nullptr;
   int fdm_grid = 0;           // persistent FDM grid (0: one CTA per element, fdm_kernel)
 
   // live kernel timing (bench roofline): event pairs around tagged launches on s_main
@@ -423,6 +426,7 @@ void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine
   a.mass = pl.mass;
   a.mass_csr = pl.mass_csr;
   a.lumped = pl.d_lumped;
+  a.inv_lumped = pl.d_inv_lumped;
   a.z = pl.z;
   if (pl.nranks > 1) {  // this rank's finalised nodes
     a.N = pl.n_fin_surf + (pl.ib1 - pl.ib0);
@@ -1490,6 +1494,114 @@ int hxb_solve_device(hxb_plan* plan, const double* d_b, const hxb_pcg_config* cf
     else if (!d_b)
       fill_default_b(*pl);
     run_pcg(*pl, *cfg, res);
+  });
+}
+
+static void ensure_coords(Plan& pl)
+{
+  if (pl.d_xyz) return;
+  pl.h_xyz = global_node_coords(pl.hs);
+  pl.d_xyz = pl.mem.upload(pl.h_xyz);
+}
+
+int hxb_node_coords(hxb_plan* plan, double* xyz)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (!xyz) throw HxbError(HXB_EINVAL, "null argument");
+    HXB_CUDA(cudaSetDevice(pl->device));
+    ensure_coords(*pl);
+    std::memcpy(xyz, pl->h_xyz.data(), sizeof(double) * pl->h_xyz.size());
+  });
+}
+
+int hxb_solve_heat(hxb_plan* plan, const hxb_heat_config* hc, const hxb_pcg_config* pc, hxb_heat_step* steps_out,
+                   int* num_steps, int* all_converged, double* final_u, double* solve_seconds)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    if (!hc || !pc || !steps_out || !num_steps || !all_converged) throw HxbError(HXB_EINVAL, "null argument");
+    if (!(hc->dt > 0)) throw HxbError(HXB_EINVAL, "heat: dt must be positive");
+    if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use the staged API");
+    HXB_CUDA(cudaSetDevice(pl->device));
+    Plan& P = *pl;
+    const int n = P.N;
+    ensure_coords(P);
+    const std::vector<double>& xyz = P.h_xyz;
+    // trajectory (problem.cpp:155-170)
+    double lo[3] = {xyz.empty() ? 0.0 : xyz[0], xyz.empty() ? 0.0 : xyz[1], xyz.empty() ? 0.0 : xyz[2]};
+    double hi[3] = {lo[0], lo[1], lo[2]};
+    for (int g = 0; g < n; ++g)
+      for (int d = 0; d < 3; ++d) {
+        lo[d] = std::min(lo[d], xyz[3 * static_cast<std::size_t>(g) + d]);
+        hi[d] = std::max(hi[d], xyz[3 * static_cast<std::size_t>(g) + d]);
+      }
+    double s0[3], s1[3];
+    for (int d = 0; d < 3; ++d) {
+      s0[d] = hc->source_start[d];
+      s1[d] = hc->source_end[d];
+    }
+    if (hc->auto_trajectory) {
+      int axis = 0;
+      for (int d = 1; d < 3; ++d)
+        if (hi[d] - lo[d] > hi[axis] - lo[axis]) axis = d;
+      for (int d = 0; d < 3; ++d) s0[d] = s1[d] = 0.5 * (lo[d] + hi[d]);
+      s0[axis] = lo[axis] + hc->source_radius;
+      s1[axis] = hi[axis] - hc->source_radius;
+    }
+    const double qd = hc->q_power / (hc->rho * hc->cp);
+    const double r2 = hc->source_radius * hc->source_radius;
+    const double total_time = hc->dt * hc->steps;
+    double mass_total = 0;
+    for (int g = 0; g < n; ++g) mass_total += P.hs.lumped[g];
+    if (!P.heat_u) P.heat_u = P.mem.alloc<double>(n);
+    {
+      std::vector<double> u0(n);
+      for (int g = 0; g < n; ++g) u0[g] = P.hs.num.dirichlet_mask[g] ? 0.0 : hc->initial_value;
+      HXB_CUDA(cudaMemcpy(P.heat_u, u0.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+    }
+    cudaStream_t s = P.s_main;
+    std::vector<double> hist(static_cast<std::size_t>(pc->max_iterations) + 2);
+    *all_converged = 1;
+    *num_steps = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int step = 1; step <= hc->steps; ++step) {
+      const double t = hc->dt * step;
+      const double frac = total_time > 0 ? std::min(1.0, t / total_time) : 0.0;
+      double c[3];
+      for (int d = 0; d < 3; ++d) c[d] = s0[d] + frac * (s1[d] - s0[d]);
+      heat_rhs_kernel<kVecBlock><<<fill_grid(heat_rhs_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(
+          P.d_xyz, P.d_lumped, P.mask, P.heat_u, P.b, n, c[0], c[1], c[2], r2, qd, hc->dt, hc->has_source,
+          dot_args(P, P.scratch + 2));
+      enqueue_ax(P, P.heat_u, P.f, nullptr, s);  // warm start: b -= A u_prev
+      sub_kernel<<<fill_grid(sub_kernel, kVecBlock, n), kVecBlock, 0, s>>>(P.b, P.f, n);
+      P.launches += 2;
+      hxb_pcg_result res{};
+      res.residual_history = hist.data();
+      hxb_pcg_config cfg = *pc;
+      cfg.record_history = 1;
+      run_pcg(P, cfg, &res);  // du in P.u
+      heat_update_kernel<kVecBlock><<<fill_grid(heat_update_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(
+          P.heat_u, P.u, P.d_lumped, n, dot_args(P, P.scratch + 3), cdot_args(P, P.scratch + 4));
+      P.launches += 1;
+      double sc[5];
+      HXB_CUDA(cudaMemcpyAsync(sc, P.scratch, sizeof(sc), cudaMemcpyDeviceToHost, s));
+      HXB_CUDA(cudaStreamSynchronize(s));
+      hxb_heat_step& rec = steps_out[step - 1];
+      rec.step = step;
+      rec.iterations = res.iterations;
+      rec.residual = res.num_residuals > 0 ? hist[res.num_residuals - 1] : 0.0;
+      rec.mean_temperature = sc[3] / mass_total;
+      rec.l2_norm = std::sqrt(sc[4]);
+      rec.source_integral = sc[2];
+      *num_steps = step;
+      if (res.status != HXB_PCG_CONVERGED) {
+        *all_converged = 0;
+        break;
+      }
+    }
+    if (solve_seconds) *solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (final_u) HXB_CUDA(cudaMemcpy(final_u, P.heat_u, sizeof(double) * n, cudaMemcpyDeviceToHost));
   });
 }
 

@@ -223,6 +223,9 @@ struct DistPcgLists {
   std::vector<double> pr_mass;
 };
 DistPcgLists dist_pcg_setup(const HostSetup& hs, const DistLists& d, int rank, int nranks);
+
+// Physical coordinates of every global node, xyz[3g+d] (mesh.cpp:477-492).
+std::vector<double> global_node_coords(const HostSetup& hs);
 HexMesh mesh_from_arrays(int nv, const double* xyz, int ne, const std::int32_t* conn, int nbf,
                          const std::int32_t* be, const std::int32_t* bf, const std::uint8_t* bt);
 // IndexMaps export in the reference layout (mesh.hpp:66-97); null pointers skipped.

@@ -237,4 +237,26 @@ DistPcgLists dist_pcg_setup(const HostSetup& hs, const DistLists& d, int rank, i
   return o;
 }
 
+// global_node_coords (mesh.cpp:477-492): every element's copy writes its
+// trilinear image in (e, l) order, so the last copy wins, as in the reference.
+std::vector<double> global_node_coords(const HostSetup& hs)
+{
+  const Numbering& num = hs.num;
+  const int ne = hs.mesh.num_elements();
+  const int np = hs.order + 1, nloc = np * np * np;
+  std::vector<double> xyz(3 * static_cast<std::size_t>(num.num_global));
+  std::vector<gid> l2g(nloc);
+  for (int e = 0; e < ne; ++e) {
+    element_l2g(num, ne, e, l2g.data());
+    int l = 0;
+    for (int k = 0; k < np; ++k)
+      for (int j = 0; j < np; ++j)
+        for (int i = 0; i < np; ++i, ++l) {
+          const auto p = trilinear_map(hs.mesh, e, hs.basis.nodes[i], hs.basis.nodes[j], hs.basis.nodes[k]);
+          for (int d = 0; d < 3; ++d) xyz[3 * static_cast<std::size_t>(l2g[l]) + d] = p[d];
+        }
+  }
+  return xyz;
+}
+
 }  // namespace hxb

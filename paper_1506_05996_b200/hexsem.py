@@ -63,6 +63,18 @@ class _PcgResult(C.Structure):
                 ("u", C.POINTER(C.c_double)), ("solve_seconds", C.c_double), ("diagnostic", C.c_char * 256)]
 
 
+class _HeatConfig(C.Structure):
+    _fields_ = [("dt", C.c_double), ("steps", C.c_int), ("rho", C.c_double), ("cp", C.c_double),
+                ("q_power", C.c_double), ("source_radius", C.c_double), ("has_source", C.c_int),
+                ("auto_trajectory", C.c_int), ("source_start", C.c_double * 3), ("source_end", C.c_double * 3),
+                ("initial_value", C.c_double)]
+
+
+class _HeatStep(C.Structure):
+    _fields_ = [("step", C.c_int), ("iterations", C.c_int), ("residual", C.c_double),
+                ("mean_temperature", C.c_double), ("l2_norm", C.c_double), ("source_integral", C.c_double)]
+
+
 class _PlanInfo(C.Structure):
     _fields_ = [("num_global", C.c_int64), ("num_elements", C.c_int64), ("num_vertices", C.c_int64),
                 ("order", C.c_int32), ("coarse_uses_amg", C.c_int32), ("coarse_n", C.c_int64),
@@ -92,6 +104,9 @@ SIGNATURES = {
     "hxb_solve": (C.c_int, [P, P, C.POINTER(_PcgConfig), C.POINTER(_PcgResult)]),
     "hxb_solve_device": (C.c_int, [P, C.c_void_p, C.POINTER(_PcgConfig), C.POINTER(_PcgResult)]),
     "hxb_load_ones": (C.c_int, [P, P]),
+    "hxb_solve_heat": (C.c_int, [P, C.POINTER(_HeatConfig), C.POINTER(_PcgConfig), C.POINTER(_HeatStep),
+                                 C.POINTER(C.c_int), C.POINTER(C.c_int), P, C.POINTER(C.c_double)]),
+    "hxb_node_coords": (C.c_int, [P, P]),
     "hxb_lumped_mass": (C.c_int, [P, P]),
     "hxb_export_maps": (C.c_int, [P, P, P, P, P, P, P]),
     "hxb_amg_level": (C.c_int, [P, C.c_int, P, P, P, P, P, P]),
@@ -392,6 +407,27 @@ class Plan:
     def pcg_device(self, d_b: int | None, tol: float = 1e-6, max_iterations: int = 500, want_u: bool = False):
         return self._solve(lib().hxb_solve_device, C.c_void_p(d_b) if d_b else None, tol, max_iterations, want_u)
 
+    def solve_heat(self, heat: "HeatConfig", tol: float = 1e-6, max_iterations: int = 500) -> dict:
+        """solve_heat's time loop (problem.cpp:145-255) on this plan, which must
+        carry c = 1/dt per element (build it with build_heat_system)."""
+        hc = heat._c()
+        cfg = _PcgConfig(float(tol), int(max_iterations), 1)
+        steps = (_HeatStep * max(1, heat.steps))()
+        ns, ok = C.c_int(), C.c_int()
+        u = np.zeros(self.N)
+        secs = C.c_double()
+        _check(lib().hxb_solve_heat(self._h, C.byref(hc), C.byref(cfg), steps, C.byref(ns), C.byref(ok), _ptr(u),
+                                    C.byref(secs)))
+        rows = [{"step": st.step, "iterations": st.iterations, "residual": st.residual,
+                 "mean_temperature": st.mean_temperature, "l2_norm": st.l2_norm,
+                 "source_integral": st.source_integral} for st in steps[:ns.value]]
+        return {"steps": rows, "all_converged": bool(ok.value), "final_field": u, "solve_seconds": secs.value}
+
+    def node_coords(self):
+        xyz = np.zeros(3 * self.N)
+        _check(lib().hxb_node_coords(self._h, _ptr(xyz)))
+        return xyz.reshape(self.N, 3)
+
     # --- data ---------------------------------------------------------------------
     def load_ones(self):
         b = np.empty(self.N)
@@ -657,6 +693,84 @@ def solve_poisson(**kw) -> dict:
         if res["diagnostic"]:
             report["diagnostic"] = res["diagnostic"]
         return {"report": report, "u": res["u"]}
+
+
+@dataclass
+class HeatConfig:
+    """HeatConfig (problem.hpp:18-31)."""
+    dt: float = 0.04
+    steps: int = 70
+    rho: float = 7000.0
+    cp: float = 0.8
+    q_power: float = 1000.0
+    source_radius: float = 0.5
+    has_source: bool = True
+    auto_trajectory: bool = True
+    source_start: tuple = (0.0, 0.0, 0.0)
+    source_end: tuple = (0.0, 0.0, 0.0)
+    initial_value: float = 0.0
+
+    def _c(self) -> _HeatConfig:
+        h = _HeatConfig()
+        h.dt, h.steps, h.rho, h.cp = float(self.dt), int(self.steps), float(self.rho), float(self.cp)
+        h.q_power, h.source_radius = float(self.q_power), float(self.source_radius)
+        h.has_source, h.auto_trajectory = int(bool(self.has_source)), int(bool(self.auto_trajectory))
+        for d in range(3):
+            h.source_start[d] = float(self.source_start[d])
+            h.source_end[d] = float(self.source_end[d])
+        h.initial_value = float(self.initial_value)
+        return h
+
+
+def build_heat_system(config: ProblemConfig, heat: HeatConfig) -> Plan:
+    """build_system with c = 1/dt enforced (problem.cpp:148-150)."""
+    if not heat.dt > 0:
+        raise ValueError("heat: dt must be positive")
+    mesh = make_mesh(config)
+    ne = mesh.num_elements
+    return Plan(mesh, config.order, np.full(ne, float(config.kappa)), np.full(ne, 1.0 / heat.dt),
+                precond=config.precond, coarse_solve=config.coarse_solve,
+                direct_threshold=config.coarse_direct_threshold, device=config.device)
+
+
+def solve_heat(**kw) -> dict:
+    """solve_heat (problem.cpp:145-255 / module.cpp:116-134) on the device."""
+    cfg = _config_from_kwargs(kw)
+    heat = HeatConfig()
+    for key, name in (("dt", "dt"), ("steps", "steps"), ("rho", "rho"), ("cp", "cp"), ("Q", "q_power"),
+                      ("q_power", "q_power"), ("source_radius", "source_radius"), ("has_source", "has_source"),
+                      ("initial_value", "initial_value"), ("auto_trajectory", "auto_trajectory"),
+                      ("source_start", "source_start"), ("source_end", "source_end")):
+        if key in kw:
+            setattr(heat, name, kw[key])
+    with build_heat_system(cfg, heat) as plan:
+        out = plan.solve_heat(heat, cfg.tol, cfg.max_iterations)
+        out["N"] = plan.N
+        return out
+
+
+def mms_convergence(min_order: int = 1, max_order: int = 6, **kw) -> dict:
+    """mms_convergence (problem.cpp:257-284 / module.cpp:129-133): u* = sin(pi x)
+    sin(pi y) sin(pi z), s = 3 pi^2 kappa u*, all-Dirichlet, c = 0; per order
+    the mass-weighted discrete L2 error of the device PCG solution."""
+    cfg = _config_from_kwargs(kw)
+    cfg.boundary = "dirichlet"
+    cfg.c = 0.0
+    rows = []
+    for n in range(min_order, max_order + 1):
+        cfg.order = n
+        with build_system(cfg) as plan:
+            x = plan.node_coords()
+            ustar = np.sin(np.pi * x[:, 0]) * np.sin(np.pi * x[:, 1]) * np.sin(np.pi * x[:, 2])
+            m = plan.lumped_mass()
+            mask = plan.maps(sub=False)["dirichlet_mask"].astype(bool)
+            s = 3 * np.pi * np.pi * cfg.kappa * ustar  # assemble_load (problem.cpp:38-46)
+            b = np.where(mask, 0.0, m * s)
+            res = plan.pcg(b, cfg.tol, cfg.max_iterations)
+            d = res["u"] - ustar
+            rows.append({"order": n, "num_global": plan.N, "error": float(np.sqrt(np.sum(m * d * d))),
+                         "iterations": res["iterations"]})
+    return {"rows": rows}
 
 
 def mesh_info(**kw) -> dict:
