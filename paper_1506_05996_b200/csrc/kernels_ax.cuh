@@ -73,8 +73,9 @@ struct AxArgs {
   const int* smap;          // [e][2][nsurfp]: row 0 Dirichlet-encoded global ids (TMA-staged)
   double* rsurf;            // [e][nsurfp] surface E-vector (output)
   double* r;                // N output (interior nodes written here)
-  int ne;
+  int ne;                   // one past the last element processed
   int num_surface_global;   // first element-interior global id
+  int e_begin = 0;          // first element processed (chunked host-pointer apply)
   DotArgs dot;              // optional: sum over interior nodes of u*r
 };
 
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
     code[k] = s >= 0 ? s : -1 - (((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1));
   }
 
-  int e = blockIdx.x;
+  int e = a.e_begin + blockIdx.x;
   for (int q = tid; q < NP * NP; q += Sh::kBlock) {
     sD[q] = c_tab[NP].D[q];
     sDT[q] = c_tab[NP].DT[q];

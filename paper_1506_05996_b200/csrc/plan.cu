@@ -203,6 +203,9 @@ struct Plan {
   int n_grp0 = 0, n_up = 0, n_down = 0;
   int sfstride = 0;           // sub_face row stride (ints)
   int ne_total = 0;           // elements of the whole mesh
+  // host-pointer Ax pipeline: copy streams and per-chunk events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> pipe_ev;
   // distributed preconditioned CG (setup_dist.cpp)
   int* fin_surf = nullptr;    // finalised surface nodes (group 0 + down)
   int n_fin_surf = 0, ib0 = 0, ib1 = 0;
@@ -237,6 +240,9 @@ struct Plan {
     if (s_coarse) cudaStreamDestroy(s_coarse);
     if (h_status) cudaFreeHost(h_status);
     for (cudaEvent_t e : kt_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
   }
 };
 
@@ -328,6 +334,27 @@ void launch_ax_elem(Plan& pl, const double* u, double* r, DotArgs dot, cudaStrea
   a.num_surface_global = pl.nsg + pl.e0 * (pl.order - 1) * (pl.order - 1) * (pl.order - 1);  // first owned interior id
   a.dot = dot;
   ax_elem_kernel<NP><<<pl.ax_grid, Sh::kBlock, Sh::kSmemBytes, s>>>(a);
+}
+
+// element range [e_begin, e_end) of the element kernel (host-pointer pipeline)
+template <int NP>
+void launch_ax_elem_range(Plan& pl, const double* u, double* r, int e_begin, int e_end, cudaStream_t s)
+{
+  using Sh = AxShape<NP>;
+  AxArgs a;
+  a.u = u;
+  a.wg = pl.wg;
+  a.mass = pl.mass;
+  a.c_e = pl.c_e;
+  a.smap = pl.smap;
+  a.rsurf = pl.rsurf;
+  a.r = r;
+  a.ne = e_end;
+  a.e_begin = e_begin;
+  a.num_surface_global = pl.nsg;
+  a.dot = DotArgs{};
+  const int grid = std::max(1, std::min(pl.ax_grid, e_end - e_begin));
+  ax_elem_kernel<NP><<<grid, Sh::kBlock, Sh::kSmemBytes, s>>>(a);
 }
 
 template <int NP>
@@ -1378,18 +1405,65 @@ int hxb_apply_A_device(hxb_plan* plan, const double* d_u, double* d_r, void* str
   });
 }
 
+// Host-pointer Ax (SemOperator::apply on host spans) as a copy/compute
+// pipeline: element-interior values belong to one element each and are
+// contiguous per element range, so after the surface part of u is on the
+// device, chunk c's interior u (H2D stream), chunk c's element kernel (main
+// stream) and chunk c-1's interior r (D2H stream) run concurrently; the
+// surface gather and its D2H close the apply. PCIe is full duplex, so the
+// in- and outbound copies overlap each other and the compute.
 int hxb_apply_A(hxb_plan* plan, const double* u, double* r)
 {
   return guarded([&] {
     Plan* pl = as_plan(plan);
     if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use hxb_dist_apply_A_*");
     HXB_CUDA(cudaSetDevice(pl->device));
-    const std::size_t bytes = sizeof(double) * pl->N;
-    HXB_CUDA(cudaMemcpyAsync(pl->p, u, bytes, cudaMemcpyHostToDevice, pl->s_main));
-    enqueue_ax(*pl, pl->p, pl->f, nullptr, pl->s_main);
+    Plan& P = *pl;
+    constexpr int C = 8;
+    if (!P.s_in) {
+      HXB_CUDA(cudaStreamCreateWithFlags(&P.s_in, cudaStreamNonBlocking));
+      HXB_CUDA(cudaStreamCreateWithFlags(&P.s_out, cudaStreamNonBlocking));
+      P.pipe_ev.resize(2 * C + 2);
+      for (cudaEvent_t& e : P.pipe_ev) HXB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const long long NI = static_cast<long long>(P.order - 1) * (P.order - 1) * (P.order - 1);
+    const std::size_t sbytes = sizeof(double) * P.nsg;
+    cudaEvent_t ev_surf = P.pipe_ev[2 * C], ev_done = P.pipe_ev[2 * C + 1];
+    HXB_CUDA(cudaEventRecord(ev_done, P.s_main));  // previous work on the plan's buffers is ordered first
+    HXB_CUDA(cudaStreamWaitEvent(P.s_in, ev_done, 0));
+    HXB_CUDA(cudaMemcpyAsync(P.p, u, sbytes, cudaMemcpyHostToDevice, P.s_in));
+    HXB_CUDA(cudaEventRecord(ev_surf, P.s_in));
+    for (int c = 0; c < C; ++c) {
+      const int e0 = static_cast<int>(static_cast<long long>(P.ne) * c / C);
+      const int e1 = static_cast<int>(static_cast<long long>(P.ne) * (c + 1) / C);
+      const long long g0 = P.nsg + e0 * NI, cnt = (e1 - e0) * NI;
+      if (cnt > 0)
+        HXB_CUDA(cudaMemcpyAsync(P.p + g0, u + g0, sizeof(double) * cnt, cudaMemcpyHostToDevice, P.s_in));
+      HXB_CUDA(cudaEventRecord(P.pipe_ev[2 * c], P.s_in));
+      HXB_CUDA(cudaStreamWaitEvent(P.s_main, P.pipe_ev[2 * c], 0));
+      if (e1 > e0) HXB_DISPATCH_NP(P.np, launch_ax_elem_range, P, P.p, P.f, e0, e1, P.s_main);
+      HXB_CUDA(cudaEventRecord(P.pipe_ev[2 * c + 1], P.s_main));
+      HXB_CUDA(cudaStreamWaitEvent(P.s_out, P.pipe_ev[2 * c + 1], 0));
+      if (cnt > 0)
+        HXB_CUDA(cudaMemcpyAsync(r + g0, P.f + g0, sizeof(double) * cnt, cudaMemcpyDeviceToHost, P.s_out));
+    }
+    AxGatherArgs g;  // surface assembly + Dirichlet rows (operator.cpp:278-280)
+    g.rsurf = P.rsurf;
+    g.off = P.ax_off;
+    g.idx = P.ax_idx;
+    g.u = P.p;
+    g.mask = P.mask;
+    g.r = P.f;
+    g.num_surface_global = P.nsg;
+    g.nodes = nullptr;
+    g.dot = DotArgs{};
+    ax_gather_kernel<<<fill_grid(ax_gather_kernel, kGatherBlock, P.nsg), kGatherBlock, 0, P.s_main>>>(g);
+    P.launches += C + 1;
     HXB_CUDA(cudaGetLastError());
-    HXB_CUDA(cudaMemcpyAsync(r, pl->f, bytes, cudaMemcpyDeviceToHost, pl->s_main));
-    HXB_CUDA(cudaStreamSynchronize(pl->s_main));
+    HXB_CUDA(cudaEventRecord(ev_done, P.s_main));
+    HXB_CUDA(cudaStreamWaitEvent(P.s_out, ev_done, 0));
+    HXB_CUDA(cudaMemcpyAsync(r, P.f, sbytes, cudaMemcpyDeviceToHost, P.s_out));
+    HXB_CUDA(cudaStreamSynchronize(P.s_out));
   });
 }
 
