@@ -124,6 +124,18 @@ __global__ void corner_values_kernel(const double* __restrict__ Z, const int* __
   }
 }
 
+// Dense coarse block on the device: scatter the CSR into a zeroed m x m array.
+__global__ void dense_scatter_kernel(const long long* __restrict__ ptr, const int* __restrict__ col,
+                                     const double* __restrict__ val, int m, double* __restrict__ A)
+{
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x)
+    for (long long k = ptr[r]; k < ptr[r + 1]; ++k) A[(std::size_t)r * m + col[k]] += val[k];
+}
+__global__ void dense_identity_kernel(double* __restrict__ A, int m)
+{
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) A[(std::size_t)r * m + r] = 1.0;
+}
+
 // ---------------------------------------------------------------------------
 // AMG level data (device pointers)
 struct DevCsr {

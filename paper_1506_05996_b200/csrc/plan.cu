@@ -720,36 +720,58 @@ DevDense dense_to_device(Plan& pl, const Csr& A)
     d.ainv = pl.mem.upload(dc.ainv);
     return d;
   }
-  // large coupled block: Cholesky + inverse on the device (cuSOLVER potrf/potri)
+  // large coupled block: Cholesky on the device (64-bit cuSOLVER API: m^2 may
+  // exceed 2^31) and the inverse from potrs against the identity; the
+  // inverse is symmetric, so its column-major columns are the row-major rows
+  const int m = d.m;
+  double* L = nullptr;
+  HXB_CUDA(cudaMalloc(&L, mm * sizeof(double)));
+  HXB_CUDA(cudaMemset(L, 0, mm * sizeof(double)));
+  {
+    long long* dptr = nullptr;
+    int* dcol = nullptr;
+    double* dval = nullptr;
+    HXB_CUDA(cudaMalloc(&dptr, dc.csr_ptr.size() * sizeof(long long)));
+    HXB_CUDA(cudaMalloc(&dcol, std::max<std::size_t>(1, dc.csr_col.size()) * sizeof(int)));
+    HXB_CUDA(cudaMalloc(&dval, std::max<std::size_t>(1, dc.csr_val.size()) * sizeof(double)));
+    HXB_CUDA(cudaMemcpy(dptr, dc.csr_ptr.data(), dc.csr_ptr.size() * sizeof(long long), cudaMemcpyHostToDevice));
+    HXB_CUDA(cudaMemcpy(dcol, dc.csr_col.data(), dc.csr_col.size() * sizeof(int), cudaMemcpyHostToDevice));
+    HXB_CUDA(cudaMemcpy(dval, dc.csr_val.data(), dc.csr_val.size() * sizeof(double), cudaMemcpyHostToDevice));
+    dense_scatter_kernel<<<vec_grid(m), kVecBlock>>>(dptr, dcol, dval, m, L);
+    HXB_CUDA(cudaDeviceSynchronize());
+    cudaFree(dptr);
+    cudaFree(dcol);
+    cudaFree(dval);
+  }
   d.ainv = pl.mem.alloc<double>(mm);
-  HXB_CUDA(cudaMemcpy(d.ainv, dc.coupled_a.data(), mm * sizeof(double), cudaMemcpyHostToDevice));
+  HXB_CUDA(cudaMemset(d.ainv, 0, mm * sizeof(double)));
+  dense_identity_kernel<<<vec_grid(m), kVecBlock>>>(d.ainv, m);
   cusolverDnHandle_t h;
-  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw HxbError(HXB_ECUDA, "cusolverDnCreate failed");
-  int lwork = 0, lwork2 = 0;
-  cusolverDnDpotrf_bufferSize(h, CUBLAS_FILL_MODE_LOWER, d.m, d.ainv, d.m, &lwork);
-  cusolverDnDpotri_bufferSize(h, CUBLAS_FILL_MODE_LOWER, d.m, d.ainv, d.m, &lwork2);
-  lwork = std::max(lwork, lwork2);
-  double* work = nullptr;
+  cusolverDnParams_t prm;
+  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS || cusolverDnCreateParams(&prm) != CUSOLVER_STATUS_SUCCESS)
+    throw HxbError(HXB_ECUDA, "cusolverDnCreate failed");
+  std::size_t wdev = 0, whost = 0;
+  cusolverDnXpotrf_bufferSize(h, prm, CUBLAS_FILL_MODE_LOWER, m, CUDA_R_64F, L, m, CUDA_R_64F, &wdev, &whost);
+  void* work = nullptr;
+  std::vector<unsigned char> hwork(std::max<std::size_t>(1, whost));
   int* info = nullptr;
-  HXB_CUDA(cudaMalloc(&work, sizeof(double) * std::max(1, lwork)));
+  HXB_CUDA(cudaMalloc(&work, std::max<std::size_t>(1, wdev)));
   HXB_CUDA(cudaMalloc(&info, sizeof(int)));
   int hinfo = 0;
-  cusolverDnDpotrf(h, CUBLAS_FILL_MODE_LOWER, d.m, d.ainv, d.m, work, lwork, info);
+  cusolverStatus_t st = cusolverDnXpotrf(h, prm, CUBLAS_FILL_MODE_LOWER, m, CUDA_R_64F, L, m, CUDA_R_64F, work, wdev,
+                                         hwork.data(), whost, info);
   HXB_CUDA(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
-  if (hinfo == 0) {
-    cusolverDnDpotri(h, CUBLAS_FILL_MODE_LOWER, d.m, d.ainv, d.m, work, lwork, info);
+  if (st == CUSOLVER_STATUS_SUCCESS && hinfo == 0) {
+    st = cusolverDnXpotrs(h, prm, CUBLAS_FILL_MODE_LOWER, m, m, CUDA_R_64F, L, m, CUDA_R_64F, d.ainv, m, info);
     HXB_CUDA(cudaMemcpy(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost));
   }
   cudaFree(work);
   cudaFree(info);
+  cudaFree(L);
+  cusolverDnDestroyParams(prm);
   cusolverDnDestroy(h);
-  if (hinfo != 0) throw HxbError(HXB_ENUMERIC, "coarse matrix Cholesky failed (matrix not SPD?)");
-  // potri fills one triangle (column-major lower == row-major upper); mirror it
-  std::vector<double> hinv(mm);
-  HXB_CUDA(cudaMemcpy(hinv.data(), d.ainv, mm * sizeof(double), cudaMemcpyDeviceToHost));
-  for (int i = 0; i < d.m; ++i)
-    for (int j = i + 1; j < d.m; ++j) hinv[static_cast<std::size_t>(j) * d.m + i] = hinv[static_cast<std::size_t>(i) * d.m + j];
-  HXB_CUDA(cudaMemcpy(d.ainv, hinv.data(), mm * sizeof(double), cudaMemcpyHostToDevice));
+  if (st != CUSOLVER_STATUS_SUCCESS || hinfo != 0)
+    throw HxbError(HXB_ENUMERIC, "coarse matrix Cholesky failed (matrix not SPD?)");
   return d;
 }
 

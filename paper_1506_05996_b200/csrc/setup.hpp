@@ -148,7 +148,11 @@ struct DenseCoarse {
   std::vector<gid> coupled;        // row ids of the coupled block, ascending
   std::vector<double> inv_diag;    // 1/a_ii for decoupled rows (0 for coupled)
   std::vector<double> ainv;        // coupled x coupled inverse, row-major (host-computed if small)
-  std::vector<double> coupled_a;   // coupled block (dense, row-major) for device factorization
+  std::vector<double> coupled_a;   // coupled block (dense, row-major), small blocks only
+  // large blocks: the coupled block as CSR (coupled numbering) for the device factorization
+  std::vector<std::int64_t> csr_ptr;
+  std::vector<gid> csr_col;
+  std::vector<double> csr_val;
 };
 DenseCoarse dense_coarse_setup(const Csr& A, int host_inverse_limit);
 

@@ -361,6 +361,21 @@ DenseCoarse dense_coarse_setup(const Csr& A, int host_inverse_limit)
     }
   }
   const std::size_t m = dc.coupled.size();
+  if (static_cast<long>(m) > host_inverse_limit) {
+    // large block: hand its sparse rows to the device factorization (no m^2 host array)
+    dc.csr_ptr.assign(1, 0);
+    for (std::size_t r = 0; r < m; ++r) {
+      const gid i = dc.coupled[r];
+      for (std::int64_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
+        const gid j = A.col[k];
+        if (pos[j] < 0) throw HxbError(3, "coarse matrix is not structurally symmetric");
+        dc.csr_col.push_back(pos[j]);
+        dc.csr_val.push_back(A.val[k]);
+      }
+      dc.csr_ptr.push_back(static_cast<std::int64_t>(dc.csr_col.size()));
+    }
+    return dc;
+  }
   dc.coupled_a.assign(m * m, 0.0);
   for (std::size_t r = 0; r < m; ++r) {
     const gid i = dc.coupled[r];

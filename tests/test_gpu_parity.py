@@ -302,3 +302,16 @@ def test_distributed_pcg(R, k, order, family):
         u[have] = part[have]
     u = np.nan_to_num(u)
     assert rel(u, one["u"]) <= 1e-9
+
+
+@pytest.mark.parametrize("k,order", [(16, 3), (12, 2)])
+def test_direct_coarse_device_factorization(k, order):
+    """Direct coarse solve (NV <= 64000, coarse.cpp:112-127) with a coupled
+    block too large for the host inverse (> 1500 rows): device Cholesky
+    (64-bit cuSOLVER) and inverse; PCG parity with the reference."""
+    ref, plan = _pair(k=k, order=order)
+    assert not plan.coarse_amg and plan.coarse_n == (k + 1) ** 3
+    r = splitmix_vector(plan.N, 8)
+    assert rel(plan.apply_P(r), ref.apply_P(r)) <= 1e-11
+    b = ref.load_ones()
+    history_parity(plan.pcg(b, tol=1e-8), ref.pcg(b, tol=1e-8), tol=1e-10)
