@@ -292,4 +292,87 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
   dot_commit<Sh::kBlock>(a.dot, dot, red);
 }
 
+// ---------------------------------------------------------------------------
+// Low orders (NP <= 3, nloc <= 27; dispatched by plan.cu): one thread per local node, EPB elements
+// per 256-thread CTA, persistent. Each CTA keeps EPB elements' u and fluxes in
+// shared memory; the per-node arithmetic is contraction_kernel's
+// (operator.cpp:124-163) with phase 2 in the reference's interleaved order.
+// The NP x NP-tile kernel above would leave most of every warp idle here.
+template <int NP>
+struct AxSmall {
+  static constexpr int kNL = NP * NP * NP;
+  static constexpr int kBlock = 256;
+  static constexpr int kEPB = kBlock / kNL;
+  static constexpr int kNlocP = (kNL + 1) & ~1;
+  static constexpr int kNS = kNL - (NP - 2) * (NP - 2) * (NP - 2);
+  static constexpr int kNSP = (kNS + 3) & ~3;
+};
+
+template <int NP>
+__global__ void __launch_bounds__(256) ax_small_kernel(AxArgs a)
+{
+  using S = AxSmall<NP>;
+  constexpr int NL = S::kNL, EPB = S::kEPB, n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1);
+  __shared__ double su[EPB][NL], fa[EPB][NL], fb[EPB][NL], fc[EPB][NL];
+  __shared__ double sD[NP * NP];
+  __shared__ double red[S::kBlock / 32];
+  const int tid = threadIdx.x;
+  for (int q = tid; q < NP * NP; q += S::kBlock) sD[q] = c_tab[NP].D[q];
+  const int el = tid / NL, l = tid % NL;
+  const int i = l % NP, j = (l / NP) % NP, k = l / (NP * NP);
+  const int slot = surface_slot(NP, i, j, k);
+  const int ioff = slot >= 0 ? 0 : ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1);
+  const bool lane_ok = el < EPB;
+  __syncthreads();
+  double dot = 0.0;
+  for (int eb = a.e_begin + blockIdx.x * EPB; eb < a.ne; eb += gridDim.x * EPB) {
+    const int e = eb + el;
+    const bool act = lane_ok && e < a.ne;
+    double u = 0.0, w[6] = {0, 0, 0, 0, 0, 0};
+    if (act) {
+      if (slot >= 0)
+        u = load_masked(a.u, __ldg(a.smap + (long long)e * 2 * S::kNSP + slot));  // masked (operator.cpp:264)
+      else
+        u = __ldg(a.u + (long long)a.num_surface_global + (long long)e * NI + ioff);
+      const double* wp = a.wg + (long long)e * 6 * S::kNlocP + l;
+#pragma unroll
+      for (int p = 0; p < 6; ++p) w[p] = __ldg(wp + p * S::kNlocP);
+      su[el][l] = u;
+    }
+    __syncthreads();
+    if (act) {  // derivatives and metric fluxes (operator.cpp:135-144)
+      double sx = 0, sy = 0, sz = 0;
+#pragma unroll
+      for (int m = 0; m < NP; ++m) {
+        sx += sD[m * NP + i] * su[el][(k * NP + j) * NP + m];
+        sy += sD[m * NP + j] * su[el][(k * NP + m) * NP + i];
+        sz += sD[m * NP + k] * su[el][(m * NP + j) * NP + i];
+      }
+      fa[el][l] = w[0] * sx + w[1] * sy + w[2] * sz;
+      fb[el][l] = w[1] * sx + w[3] * sy + w[4] * sz;
+      fc[el][l] = w[2] * sx + w[4] * sy + w[5] * sz;
+    }
+    __syncthreads();
+    if (act) {  // adjoint contractions, one accumulator (operator.cpp:152-157)
+      double s = 0;
+#pragma unroll
+      for (int m = 0; m < NP; ++m) {
+        s += sD[i * NP + m] * fa[el][(k * NP + j) * NP + m];
+        s += sD[j * NP + m] * fb[el][(k * NP + m) * NP + i];
+        s += sD[k * NP + m] * fc[el][(m * NP + j) * NP + i];
+      }
+      const double ce = __ldg(a.c_e + e);
+      if (ce != 0.0) s += (ce * u) * __ldg(a.mass + (std::size_t)e * NL + l);  // operator.cpp:159
+      if (slot >= 0) {
+        a.rsurf[(long long)e * S::kNSP + slot] = s;
+      } else {
+        a.r[(long long)a.num_surface_global + (long long)e * NI + ioff] = s;
+        dot += u * s;
+      }
+    }
+    __syncthreads();
+  }
+  dot_commit<S::kBlock>(a.dot, dot, red);
+}
+
 }  // namespace hxb

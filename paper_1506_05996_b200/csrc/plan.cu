@@ -308,6 +308,13 @@ DotArgs cdot_args(Plan& pl, double* result)
 template <int NP>
 int ax_persistent_grid(const Plan& pl)
 {
+  if constexpr (NP <= 3) {  // thread-per-node kernel for the low orders
+    int per_sm = 0;
+    HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ax_small_kernel<NP>, AxSmall<NP>::kBlock, 0));
+    per_sm = std::max(per_sm, 1);
+    const int need = (pl.ne + AxSmall<NP>::kEPB - 1) / AxSmall<NP>::kEPB;
+    return std::max(1, std::min(need, per_sm * pl.num_sms));
+  }
   using Sh = AxShape<NP>;
   HXB_CUDA(cudaFuncSetAttribute(ax_elem_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(Sh::kSmemBytes)));
@@ -333,7 +340,10 @@ void launch_ax_elem(Plan& pl, const double* u, double* r, DotArgs dot, cudaStrea
   a.ne = pl.ne;
   a.num_surface_global = pl.nsg + pl.e0 * (pl.order - 1) * (pl.order - 1) * (pl.order - 1);  // first owned interior id
   a.dot = dot;
-  ax_elem_kernel<NP><<<pl.ax_grid, Sh::kBlock, Sh::kSmemBytes, s>>>(a);
+  if constexpr (NP <= 3)
+    ax_small_kernel<NP><<<pl.ax_grid, AxSmall<NP>::kBlock, 0, s>>>(a);
+  else
+    ax_elem_kernel<NP><<<pl.ax_grid, Sh::kBlock, Sh::kSmemBytes, s>>>(a);
 }
 
 // element range [e_begin, e_end) of the element kernel (host-pointer pipeline)
@@ -353,8 +363,13 @@ void launch_ax_elem_range(Plan& pl, const double* u, double* r, int e_begin, int
   a.e_begin = e_begin;
   a.num_surface_global = pl.nsg;
   a.dot = DotArgs{};
-  const int grid = std::max(1, std::min(pl.ax_grid, e_end - e_begin));
-  ax_elem_kernel<NP><<<grid, Sh::kBlock, Sh::kSmemBytes, s>>>(a);
+  if constexpr (NP <= 3) {
+    const int grid = std::max(1, std::min(pl.ax_grid, (e_end - e_begin + AxSmall<NP>::kEPB - 1) / AxSmall<NP>::kEPB));
+    ax_small_kernel<NP><<<grid, AxSmall<NP>::kBlock, 0, s>>>(a);
+  } else {
+    const int grid = std::max(1, std::min(pl.ax_grid, e_end - e_begin));
+    ax_elem_kernel<NP><<<grid, Sh::kBlock, Sh::kSmemBytes, s>>>(a);
+  }
 }
 
 template <int NP>
