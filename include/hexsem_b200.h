@@ -36,7 +36,8 @@ enum {
   HXB_EMESH = 2,    /* std::runtime_error: inverted element (geometry.cpp:70-72), non-conforming (mesh.cpp:402-403) */
   HXB_ENUMERIC = 3, /* std::runtime_error: Cholesky / AMG diagonal / pencil failure (coarse.cpp:126, amg.cpp:145) */
   HXB_ECUDA = 4,    /* CUDA runtime failure or no sm_100 device */
-  HXB_ENCCL = 5     /* NCCL failure (multi-GPU plans) */
+  HXB_ENCCL = 5,    /* NCCL failure (multi-GPU plans) */
+  HXB_EIO = 6       /* std::runtime_error from the mesh readers/writers (mesh_io.cpp:53,112,127,190-193,214) */
 };
 
 /* PrecondMode (precond.hpp:12) */
@@ -135,6 +136,15 @@ int hxb_generate_cube_mesh(int k, int family, int boundary_tag, hxb_mesh_buf** o
 int hxb_generate_box_mesh(int kx, int ky, int kz, const double size[3], int boundary_tag, hxb_mesh_buf** out);
 int hxb_refine_uniform(const hxb_mesh* in, hxb_mesh_buf** out);
 void hxb_mesh_free(hxb_mesh_buf* m);
+
+/* Mesh files (mesh_io.hpp:14-31): Gmsh MSH 2.2 ASCII (read_msh/write_msh,
+ * mesh_io.cpp:49-145) and the native "HXSM0001" binary (read_native/
+ * write_native, mesh_io.cpp:147-218). HXB_MESHFILE_AUTO dispatches on the
+ * ".msh" extension like read_mesh_file/write_mesh_file (mesh_io.cpp:220-232).
+ * Readers check every element's Jacobian (HXB_EMESH on an inverted one). */
+enum { HXB_MESHFILE_AUTO = 0, HXB_MESHFILE_MSH = 1, HXB_MESHFILE_NATIVE = 2 };
+int hxb_read_mesh_file(const char* path, int format, hxb_mesh_buf** out);
+int hxb_write_mesh_file(const hxb_mesh* mesh, const char* path, int format);
 
 /* build_system (problem.cpp:73-108) on a caller mesh with per-element kappa/c
  * (operator.hpp:49-55). Uploads everything once; all vectors stay on the GPU. */

@@ -20,6 +20,8 @@ from .ctypes_oracle import (  # noqa: F401
     oracle_fma_available,
     RefConfig,
     ref_available,
+    ref_read_mesh,
+    ref_write_mesh,
     ref_solve_heat,
     oracle_available,
     ref_gll,

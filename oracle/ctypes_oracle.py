@@ -343,6 +343,57 @@ def ref_solve_heat(config: RefConfig, heat: dict, tol: float = 1e-6, max_iterati
     return {"steps": rows, "all_converged": bool(ok.value), "final_field": u, "solve_seconds": secs.value}
 
 
+_MESHFMT = {"auto": 0, "msh": 1, "native": 2}
+
+
+def _ref_mesh_lib():
+    lib = _load(RefSystem.PATH, RefSystem.PREFIX)
+    if not getattr(lib, "_mesh_bound", False):
+        P = C.c_void_p
+        lib.ref_write_mesh.restype = C.c_int
+        lib.ref_write_mesh.argtypes = [C.c_int, P, C.c_int, P, C.c_int, P, P, P, C.c_char_p, C.c_int]
+        lib.ref_read_mesh.restype = C.c_int
+        lib.ref_read_mesh.argtypes = [C.c_char_p, C.c_int, C.POINTER(P)]
+        lib.ref_mesh_counts.argtypes = [P, P]
+        lib.ref_mesh_export.argtypes = [P, P, P, P, P, P]
+        lib.ref_mesh_free.argtypes = [P]
+        lib._mesh_bound = True
+    return lib
+
+
+def ref_write_mesh(mesh: dict, path: str, fmt: str = "auto") -> None:
+    """The reference's write_mesh_file / write_msh / write_native (mesh_io.cpp)."""
+    lib = _ref_mesh_lib()
+    xyz = np.ascontiguousarray(mesh["xyz"], dtype=np.float64)
+    conn = np.ascontiguousarray(mesh["conn"], dtype=np.int32)
+    be = np.ascontiguousarray(mesh["bf_elem"], dtype=np.int32)
+    bf = np.ascontiguousarray(mesh["bf_face"], dtype=np.int32)
+    bt = np.ascontiguousarray(mesh["bf_tag"], dtype=np.uint8)
+    rc = lib.ref_write_mesh(xyz.shape[0], _ptr(xyz), conn.shape[0], _ptr(conn), be.size, _ptr(be), _ptr(bf),
+                            _ptr(bt), os.fsencode(path), _MESHFMT[fmt])
+    if rc:
+        raise RuntimeError(lib.ref_last_error().decode())
+
+
+def ref_read_mesh(path: str, fmt: str = "auto") -> dict:
+    """The reference's read_mesh_file / read_msh / read_native (mesh_io.cpp)."""
+    lib = _ref_mesh_lib()
+    h = C.c_void_p()
+    if lib.ref_read_mesh(os.fsencode(path), _MESHFMT[fmt], C.byref(h)):
+        raise RuntimeError(lib.ref_last_error().decode())
+    try:
+        c = np.zeros(3, dtype=np.int64)
+        lib.ref_mesh_counts(h, _ptr(c))
+        nv, ne, nb = (int(x) for x in c)
+        out = {"xyz": np.zeros((nv, 3)), "conn": np.zeros((ne, 8), dtype=np.int32),
+               "bf_elem": np.zeros(nb, dtype=np.int32), "bf_face": np.zeros(nb, dtype=np.int32),
+               "bf_tag": np.zeros(nb, dtype=np.uint8)}
+        lib.ref_mesh_export(h, *(_ptr(out[k]) for k in ("xyz", "conn", "bf_elem", "bf_face", "bf_tag")))
+        return out
+    finally:
+        lib.ref_mesh_free(h)
+
+
 def ref_available() -> bool:
     return os.path.exists(_REF_SO)
 

@@ -21,6 +21,7 @@
 #include <memory>
 #include <string>
 
+#include "hexsem/mesh_io.hpp"
 #include "hexsem/problem.hpp"
 
 using namespace hexsem;
@@ -437,5 +438,71 @@ unsigned long long ref_words_model(long long ne, int n, int variant)
 unsigned long long ref_flops_model(long long ne, int n) { return KernelCounters::contraction_flops_model(ne, n); }
 unsigned long long ref_fine_ops_model(long long ne, int n) { return FineCounters::ops_model(ne, n); }
 unsigned long long ref_fine_words_model(long long ne, int n) { return FineCounters::words_model(ne, n); }
+
+// Mesh files through the reference's own readers/writers (mesh_io.cpp): the
+// cross-implementation fixtures for the mesh-format row.
+static HexMesh mesh_of(int nv, const double* xyz, int ne, const int32_t* conn, int nbf, const int32_t* be,
+                       const int32_t* bf, const uint8_t* bt)
+{
+  HexMesh m;
+  m.vertices.resize(nv);
+  for (int v = 0; v < nv; ++v)
+    for (int d = 0; d < 3; ++d) m.vertices[v][d] = xyz[3 * v + d];
+  m.elements.resize(ne);
+  for (int e = 0; e < ne; ++e)
+    for (int q = 0; q < 8; ++q) m.elements[e][q] = conn[8 * e + q];
+  for (int b = 0; b < nbf; ++b) m.boundary_faces.push_back({be[b], bf[b], static_cast<BoundaryTag>(bt[b])});
+  return m;
+}
+
+// format: 0 = by extension (write_mesh_file), 1 = write_msh, 2 = write_native
+int ref_write_mesh(int nv, const double* xyz, int ne, const int32_t* conn, int nbf, const int32_t* be,
+                   const int32_t* bf, const uint8_t* bt, const char* path, int format)
+{
+  return guard([&] {
+    const HexMesh m = mesh_of(nv, xyz, ne, conn, nbf, be, bf, bt);
+    if (format == 1)
+      write_msh(m, path);
+    else if (format == 2)
+      write_native(m, path);
+    else
+      write_mesh_file(m, path);
+  });
+}
+
+// format: 0 = read_mesh_file, 1 = read_msh, 2 = read_native
+int ref_read_mesh(const char* path, int format, void** out)
+{
+  return guard([&] {
+    auto m = std::make_unique<HexMesh>(format == 1 ? read_msh(path)
+                                       : format == 2 ? read_native(path)
+                                                     : read_mesh_file(path));
+    *out = m.release();
+  });
+}
+
+void ref_mesh_counts(void* m, int64_t* c)
+{
+  const HexMesh& h = *static_cast<HexMesh*>(m);
+  c[0] = h.num_vertices();
+  c[1] = h.num_elements();
+  c[2] = static_cast<int64_t>(h.boundary_faces.size());
+}
+
+void ref_mesh_export(void* m, double* xyz, int32_t* conn, int32_t* be, int32_t* bf, uint8_t* bt)
+{
+  const HexMesh& h = *static_cast<HexMesh*>(m);
+  for (std::size_t v = 0; v < h.vertices.size(); ++v)
+    for (int d = 0; d < 3; ++d) xyz[3 * v + d] = h.vertices[v][d];
+  for (std::size_t e = 0; e < h.elements.size(); ++e)
+    for (int q = 0; q < 8; ++q) conn[8 * e + q] = h.elements[e][q];
+  for (std::size_t b = 0; b < h.boundary_faces.size(); ++b) {
+    be[b] = h.boundary_faces[b].element;
+    bf[b] = h.boundary_faces[b].face;
+    bt[b] = static_cast<uint8_t>(h.boundary_faces[b].tag);
+  }
+}
+
+void ref_mesh_free(void* m) { delete static_cast<HexMesh*>(m); }
 
 }  // extern "C"

@@ -129,6 +129,33 @@ int hxb_refine_uniform(const hxb_mesh* in, hxb_mesh_buf** out)
   return guarded([&] { *out = wrap_mesh(refine_uniform(view_to_mesh(in))); });
 }
 
+int hxb_read_mesh_file(const char* path, int format, hxb_mesh_buf** out)
+{
+  return guarded([&] {
+    if (!path || !out) throw HxbError(HXB_EINVAL, "null argument");
+    switch (format) {
+      case HXB_MESHFILE_AUTO: *out = wrap_mesh(read_mesh_file(path)); break;
+      case HXB_MESHFILE_MSH: *out = wrap_mesh(read_msh(path)); break;
+      case HXB_MESHFILE_NATIVE: *out = wrap_mesh(read_native(path)); break;
+      default: throw HxbError(HXB_EINVAL, "unknown mesh file format");
+    }
+  });
+}
+
+int hxb_write_mesh_file(const hxb_mesh* mesh, const char* path, int format)
+{
+  return guarded([&] {
+    if (!path) throw HxbError(HXB_EINVAL, "null argument");
+    const HexMesh m = view_to_mesh(mesh);
+    switch (format) {
+      case HXB_MESHFILE_AUTO: write_mesh_file(m, path); break;
+      case HXB_MESHFILE_MSH: write_msh(m, path); break;
+      case HXB_MESHFILE_NATIVE: write_native(m, path); break;
+      default: throw HxbError(HXB_EINVAL, "unknown mesh file format");
+    }
+  });
+}
+
 void hxb_mesh_free(hxb_mesh_buf* m)
 {
   if (!m) return;

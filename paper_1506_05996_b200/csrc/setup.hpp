@@ -46,6 +46,13 @@ HexMesh generate_cube_mesh(int k, MeshFamily family, std::uint8_t tag);
 HexMesh refine_uniform(const HexMesh& mesh);
 const std::array<int, 4>& face_corners(int face);
 void check_jacobians(const HexMesh& mesh);
+// mesh_io.hpp:14-31 (setup_mesh_io.cpp)
+HexMesh read_msh(const std::string& path);
+void write_msh(const HexMesh& mesh, const std::string& path);
+HexMesh read_native(const std::string& path);
+void write_native(const HexMesh& mesh, const std::string& path);
+HexMesh read_mesh_file(const std::string& path);
+void write_mesh_file(const HexMesh& mesh, const std::string& path);
 
 struct GllBasis {  // gll.hpp:17-31
   int order = 0;

@@ -92,6 +92,8 @@ SIGNATURES = {
                                         C.POINTER(C.POINTER(_MeshBuf))]),
     "hxb_refine_uniform": (C.c_int, [C.POINTER(_Mesh), C.POINTER(C.POINTER(_MeshBuf))]),
     "hxb_mesh_free": (None, [C.POINTER(_MeshBuf)]),
+    "hxb_read_mesh_file": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.POINTER(_MeshBuf))]),
+    "hxb_write_mesh_file": (C.c_int, [C.POINTER(_Mesh), C.c_char_p, C.c_int]),
     "hxb_plan_create": (C.c_int, [C.POINTER(_Mesh), C.c_int, P, P, C.POINTER(_Options), C.POINTER(P)]),
     "hxb_plan_destroy": (C.c_int, [P]),
     "hxb_plan_get_info": (C.c_int, [P, C.POINTER(_PlanInfo)]),
@@ -235,6 +237,38 @@ def generate_cube_mesh(k: int, family: str = "uniform", boundary: str = "dirichl
     return _take_mesh(out)
 
 
+_MESHFILE = {"auto": 0, "msh": 1, "native": 2}
+
+
+def read_mesh_file(path: str, fmt: str = "auto") -> HexMesh:
+    """read_mesh_file / read_msh / read_native (mesh_io.cpp:49-124, 188-225)."""
+    out = C.POINTER(_MeshBuf)()
+    _check(lib().hxb_read_mesh_file(os.fsencode(path), _MESHFILE[fmt], C.byref(out)))
+    return _take_mesh(out)
+
+
+def write_mesh_file(mesh: HexMesh, path: str, fmt: str = "auto") -> None:
+    """write_mesh_file / write_msh / write_native (mesh_io.cpp:126-186, 227-232)."""
+    view = mesh._c()
+    _check(lib().hxb_write_mesh_file(C.byref(view), os.fsencode(path), _MESHFILE[fmt]))
+
+
+def read_msh(path: str) -> HexMesh:
+    return read_mesh_file(path, "msh")
+
+
+def write_msh(mesh: HexMesh, path: str) -> None:
+    write_mesh_file(mesh, path, "msh")
+
+
+def read_native(path: str) -> HexMesh:
+    return read_mesh_file(path, "native")
+
+
+def write_native(mesh: HexMesh, path: str) -> None:
+    write_mesh_file(mesh, path, "native")
+
+
 def generate_box_mesh(kx: int, ky: int, kz: int, size=(1.0, 1.0, 1.0), boundary: str = "dirichlet") -> HexMesh:
     """generate_box_mesh (mesh.hpp:57-58, mesh.cpp:67-108)."""
     out = C.POINTER(_MeshBuf)()
@@ -255,6 +289,7 @@ def refine_uniform(mesh: HexMesh) -> HexMesh:
 class ProblemConfig:
     """Solver-path subset of hexsem::ProblemConfig (problem.hpp:35-62)."""
     label: str = "poisson"
+    mesh_file: str = ""
     family: str = "uniform"
     k: int = 8
     refine: int = 0
@@ -274,8 +309,10 @@ class ProblemConfig:
 
 
 def make_mesh(cfg: ProblemConfig) -> HexMesh:
-    """make_mesh (problem.cpp:13-26) for generated meshes."""
-    if cfg.bar[0] > 0:
+    """make_mesh (problem.cpp:13-26): mesh file, box bar, or generated cube."""
+    if cfg.mesh_file:
+        mesh = read_mesh_file(cfg.mesh_file)
+    elif cfg.bar[0] > 0:
         mesh = generate_box_mesh(cfg.bar[0], cfg.bar[1], cfg.bar[2], cfg.bar_size, cfg.boundary)
     else:
         mesh = generate_cube_mesh(cfg.k, cfg.family, cfg.boundary)
@@ -650,7 +687,7 @@ def pencil(order: int) -> dict:
 
 def _config_from_kwargs(kw) -> ProblemConfig:
     cfg = ProblemConfig()
-    for key in ("k", "refine", "order", "kappa", "c", "family", "precond", "variant", "boundary", "tol",
+    for key in ("mesh_file", "k", "refine", "order", "kappa", "c", "family", "precond", "variant", "boundary", "tol",
                 "max_iterations", "coarse_solve", "coarse_direct_threshold", "device", "label"):
         if key in kw:
             setattr(cfg, key, kw[key])
@@ -773,12 +810,20 @@ def mms_convergence(min_order: int = 1, max_order: int = 6, **kw) -> dict:
     return {"rows": rows}
 
 
+def write_mesh(path: str, **kw) -> None:
+    """module.cpp:102-105: write_mesh_file(make_mesh(config), path)."""
+    write_mesh_file(make_mesh(_config_from_kwargs(kw)), path)
+
+
 def mesh_info(**kw) -> dict:
     cfg = _config_from_kwargs(kw)
     mesh = make_mesh(cfg)
     n = cfg.order
-    with Plan(mesh, n, precond="none") as plan:
-        return {"num_elements": mesh.num_elements, "num_vertices": mesh.num_vertices, "num_nodes": plan.N}
+    hs = HostSetup(mesh, n, precond="none")  # build_index_maps only (module.cpp:91-101); no device needed
+    try:
+        return {"num_elements": mesh.num_elements, "num_vertices": mesh.num_vertices, "num_nodes": hs.N}
+    finally:
+        hs.close()
 
 
 def residual_flops_model(ne: int, n: int) -> int:
