@@ -84,6 +84,8 @@ typedef struct hxb_options {
                                   instead of the default single cluster kernel; bit 2: persistent
                                   TMA/cp.async-pipelined FDM kernel instead of one CTA per
                                   subdomain (measured slower at cfg2, kept for A/B checks);
+                                  bit 3: one fused combine after the coarse solve instead of
+                                  the fine half running concurrently with it;
                                   reserved[1] = rank, reserved[2] = number of ranks: element-slab
                                   partition for the distributed operator (hxb_dist_*) */
 } hxb_options;

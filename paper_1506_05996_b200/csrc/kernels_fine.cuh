@@ -209,13 +209,19 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
 #pragma unroll
       for (int ii = 0; ii <= n; ++ii) in[ii + 1] = gl[ii] >= 0 ? __ldg(a.r + gl[ii]) : 0.0;
       if (a.Rpart) {
-        // this line's share of the 8 corner sums R_cb = sum_l B[cb][l] (r/m_N)_l m_l
+        // this line's share of the 8 corner sums R_cb = sum_l B[cb][l] (r/m_N)_l m_l.
+        // An element-interior node has one copy, so m_N = m_l and its term is
+        // r itself (to rounding): only surface nodes read 1/m_N and m_l.
         const double* ml = a.mass + (std::size_t)e * NP * NP * NP + (kk * NP + jj) * NP;
+        const bool line_interior = jj > 0 && jj < n && kk > 0 && kk < n;
         double w0 = 0.0, w1 = 0.0;
 #pragma unroll
         for (int ii = 0; ii <= n; ++ii) {
-          const double y = gl[ii] >= 0 ? in[ii + 1] * __ldg(a.inv_lumped + gl[ii]) : 0.0;
-          const double w = y * __ldg(ml + ii);
+          double w;
+          if (line_interior && ii > 0 && ii < n)
+            w = in[ii + 1];
+          else
+            w = gl[ii] >= 0 ? (in[ii + 1] * __ldg(a.inv_lumped + gl[ii])) * __ldg(ml + ii) : 0.0;
           w0 += s_h0[ii] * w;
           w1 += s_h1[ii] * w;
         }
@@ -449,10 +455,11 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_pipe_kernel(FdmArgs 
       if (a.Rpart && jj >= 0 && jj <= n && kk >= 0 && kk <= n) {
         const double* ml = a.mass + (std::size_t)e * NLOC + (kk * NP + jj) * NP;
         const double* lr = ll + (kk * NP + jj) * NP;
+        const bool line_interior = jj > 0 && jj < n && kk > 0 && kk < n;
         double w0 = 0.0, w1 = 0.0;
 #pragma unroll
-        for (int ii = 0; ii <= n; ++ii) {
-          const double w = (in[ii + 1] * lr[ii]) * __ldg(ml + ii);
+        for (int ii = 0; ii <= n; ++ii) {  // element-interior nodes: r itself (see fdm_kernel)
+          const double w = line_interior && ii > 0 && ii < n ? in[ii + 1] : (in[ii + 1] * lr[ii]) * __ldg(ml + ii);
           w0 += s_h0[ii] * w;
           w1 += s_h1[ii] * w;
         }

@@ -204,6 +204,7 @@ struct CombineProlongArgs {
   double* z;
   int N, nsg;
   int do_fine, do_coarse;
+  int fine_in_z = 0;  // the fine sums are already in z (combine_fine_kernel ran concurrently with the coarse solve)
   DotArgs dot;
   // item t -> node: t < nsg: surface node (surf_nodes ? surf_nodes[t] : t),
   // t >= nsg: interior node ibase + (t - nsg) of element (t - nsg)/NI + e0;
@@ -216,7 +217,7 @@ struct CombineProlongArgs {
 template <int NP>
 __global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(CombineProlongArgs a)
 {
-  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NLOC = NP * NP * NP;
+  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1);
   constexpr int NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2), NSP = (NS + 3) & ~3;
   __shared__ double red[kGatherBlock / 32];
   __shared__ double h0[NP], h1[NP];
@@ -242,11 +243,13 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(Combin
     const int g = surf ? (a.surf_nodes ? __ldg(a.surf_nodes + it) : it) : a.ibase + (it - a.nsg);
     const double rg = __ldg(a.r + g);
     double zg;
-    if (__ldg(a.mask + g)) {
+    if (surf && __ldg(a.mask + g)) {  // Dirichlet nodes are element-surface nodes
       zg = rg;
     } else {
       double s = 0.0;
-      if (a.do_fine) {
+      if (a.fine_in_z) {
+        s = a.z[g];
+      } else if (a.do_fine) {
         // up to 8 contributions loaded at once (predicated), summed in list order
         const unsigned q0 = __ldg(a.fine_off + it), q1 = __ldg(a.fine_off + it + 1);
         double v[8];
@@ -267,7 +270,8 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(Combin
             const long long el = t / NI;          // element relative to e0
             const int l = t % NI;
             const int i = 1 + l % (n - 1), j = 1 + (l / (n - 1)) % (n - 1), k = 1 + l / ((n - 1) * (n - 1));
-            zc = pz(el + a.e0, i, j, k) * __ldg(a.mass + el * NLOC + (k * NP + j) * NP + i);  // coarse.cpp:180
+            // single copy: (B zc) m / m_N with m_N = m is B zc to rounding (coarse.cpp:180, 185)
+            zc = pz(el + a.e0, i, j, k);
           }
         } else {
           // face nodes (2 copies) dominate: the first two copies are evaluated
@@ -291,7 +295,7 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(Combin
             zc += pz(c / NSP, i, j, k) * __ldcs(a.mass_csr + q);
           }
         }
-        s += zc * __ldg(a.inv_lumped + g);  // /m_N (coarse.cpp:185) as a product with 1/m_N
+        s += surf ? zc * __ldg(a.inv_lumped + g) : zc;  // /m_N (coarse.cpp:185) as a product with 1/m_N
       }
       zg = s;
     }
@@ -299,6 +303,32 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(Combin
     dot += zg * rg;
   }
   dot_commit<kGatherBlock>(a.dot, dot, red);
+}
+
+// First half of the split combine: z[g] = sum of node g's fine contributions
+// in list order (the do_fine branch of combine_prolong_kernel, same
+// arithmetic). It runs while the coarse solve occupies a few SMs; the coarse
+// half then reads z back (fine_in_z), so the result is bit-identical to the
+// fused kernel. One item per thread, no persistent loop, so the coarse
+// kernels on the high-priority stream are scheduled as soon as CTAs retire.
+__global__ void __launch_bounds__(kGatherBlock) combine_fine_kernel(const double* __restrict__ zsort,
+                                                                    const unsigned* __restrict__ fine_off,
+                                                                    const int* __restrict__ surf_nodes, int nsg,
+                                                                    int ibase, int n_items, double* __restrict__ z)
+{
+  const int it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  const int g = it < nsg ? (surf_nodes ? __ldg(surf_nodes + it) : it) : ibase + (it - nsg);
+  const unsigned q0 = __ldg(fine_off + it), q1 = __ldg(fine_off + it + 1);
+  double v[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) v[t] = q0 + t < q1 ? __ldcs(zsort + q0 + t) : 0.0;
+  double zf = 0.0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+    if (q0 + t < q1) zf += v[t];
+  for (unsigned q = q0 + 8; q < q1; ++q) zf += __ldcs(zsort + q);
+  z[g] = zf;
 }
 
 // R[v] = vmask[v] ? 0 : sum of Rpart over (e,cb) incidences in ascending order

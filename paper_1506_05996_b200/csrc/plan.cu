@@ -125,7 +125,8 @@ struct DevDense {
 
 struct Plan {
   int device = 0;
-  cudaStream_t s_main = nullptr, s_coarse = nullptr;
+  cudaStream_t s_main = nullptr, s_coarse = nullptr;  // s_coarse: highest priority
+  bool split_combine = true;  // fine half of the combine concurrent with the coarse solve (options.reserved[0] bit 3 off)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_a = nullptr;
   cudaGraphExec_t coarse_exec = nullptr;
   DeviceArena mem;
@@ -455,7 +456,8 @@ void launch_fdm(Plan& pl, cudaStream_t s)
 }
 
 template <int NP>
-void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse)
+void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse,
+                       bool fine_in_z = false)
 {
   CombineProlongArgs a;
   a.r = pl.r;
@@ -487,15 +489,28 @@ void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine
   }
   a.do_fine = do_fine ? 1 : 0;
   a.do_coarse = do_coarse ? 1 : 0;
+  a.fine_in_z = fine_in_z ? 1 : 0;
   a.dot = zr_result ? dot_args(pl, zr_result) : DotArgs{};
   combine_prolong_kernel<NP><<<fill_grid(combine_prolong_kernel<NP>, kGatherBlock, a.N), kGatherBlock, 0, s>>>(a);
 }
 
-void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse)
+void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, bool do_coarse,
+                    bool fine_in_z = false)
 {
   KtScope kt(pl, HXB_KT_COMBINE, s);
   pl.launches += 1;
-  HXB_DISPATCH_NP(pl.np, launch_combine_np, pl, zr_result, s, do_fine, do_coarse);
+  HXB_DISPATCH_NP(pl.np, launch_combine_np, pl, zr_result, s, do_fine, do_coarse, fine_in_z);
+}
+
+void launch_combine_fine(Plan& pl, cudaStream_t s)
+{
+  const bool dist = pl.nranks > 1;
+  const int n_items = dist ? pl.n_fin_surf + (pl.ib1 - pl.ib0) : pl.N;
+  const int nsg = dist ? pl.n_fin_surf : pl.nsg;
+  const int ibase = dist ? pl.ib0 : pl.nsg;
+  combine_fine_kernel<<<(n_items + kGatherBlock - 1) / kGatherBlock, kGatherBlock, 0, s>>>(
+      pl.zsort, pl.fine_off, dist ? pl.fin_surf : nullptr, nsg, ibase, n_items, pl.z);
+  pl.launches += 1;
 }
 
 // Zc = Z at each element's corners (interior copies, prolonged inside the
@@ -648,6 +663,19 @@ void enqueue_precond(Plan& pl, double* zr_result)
   } else if (pl.do_coarse) {
     HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s);
     pl.launches += 1;
+  }
+  if (pl.do_fine && pl.do_coarse && pl.split_combine) {
+    // the coarse solve (a latency-bound chain on a few SMs) on the
+    // high-priority stream, concurrent with the fine half of the combine
+    HXB_CUDA(cudaEventRecord(pl.ev_fork, s));
+    HXB_CUDA(cudaStreamWaitEvent(pl.s_coarse, pl.ev_fork, 0));
+    HXB_CUDA(cudaGraphLaunch(pl.coarse_exec, pl.s_coarse));
+    pl.launches += pl.coarse_graph_nodes;
+    HXB_CUDA(cudaEventRecord(pl.ev_join, pl.s_coarse));
+    launch_combine_fine(pl, s);
+    HXB_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
+    launch_combine(pl, zr_result, s, false, true, true);
+    return;
   }
   if (pl.do_coarse) {
     HXB_CUDA(cudaGraphLaunch(pl.coarse_exec, s));
@@ -1033,9 +1061,14 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   pl.fdm_eo = upload_tables(hs.basis, hs.pencil);
   HXB_DISPATCH_NP(pl.np, init_ax_grid, pl);
   HXB_DISPATCH_NP(pl.np, init_fdm_grid, pl, (opt.reserved[0] & 4) != 0);
+  pl.split_combine = (opt.reserved[0] & 8) == 0;
 
   HXB_CUDA(cudaStreamCreateWithFlags(&pl.s_main, cudaStreamNonBlocking));
-  HXB_CUDA(cudaStreamCreateWithFlags(&pl.s_coarse, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;
+    HXB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    HXB_CUDA(cudaStreamCreateWithPriority(&pl.s_coarse, cudaStreamNonBlocking, hi));
+  }
   for (cudaEvent_t* e : {&pl.ev_fork, &pl.ev_join}) HXB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   for (cudaEvent_t* e : {&pl.ev_t0, &pl.ev_t1, &pl.ev_a}) HXB_CUDA(cudaEventCreate(e));
 
