@@ -54,6 +54,17 @@ def _env_int(name, default):
         return default
 
 
+def _ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed `ncu --set full` capture summary (profiles/ncu_traffic.json,
+    written by tools/ncu_table.py); None when absent."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(path))["kernels"][kernel]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -344,6 +355,33 @@ def run_ours(args, rank, world, local_rank):
                 "u_norm2_rel_diff": abs(pcg["u_norm2"] - gold["u_norm2"]) / gold["u_norm2"],
                 "ref_cpu_solve_s_build_host": gold["timing"]["solve_s"],
             }
+    # ---- operator variant on_the_fly (operator.cpp:174-253): same Ax, geometry from corners
+    otf = None
+    if not args.no_otf:
+        try:
+            plan_o = hx.Plan(mesh, order, device=local_rank, precond="none", variant="on_the_fly")
+            d_r2 = torch.empty_like(d_r)
+            for _ in range(args.warmup):
+                plan_o.apply_A_device(d_u.data_ptr(), d_r2.data_ptr(), stream)
+            plan_o.kernel_timing(True, max_launches=4 * args.steps + 16)
+            barrier()
+            ev0.record()
+            for _ in range(args.steps):
+                plan_o.apply_A_device(d_u.data_ptr(), d_r2.data_ptr(), stream)
+            ev1.record()
+            barrier()
+            ms_o = ev0.elapsed_time(ev1) / args.steps
+            oe_ms, oe_n = plan_o.kernel_time("ax_elem")
+            plan_o.kernel_timing(False)
+            d_r_t = torch.from_numpy(r_dev).to("cuda")
+            otf = {"ms_per_step": ms_o, "gdofs": N / (ms_o * 1e-3) / 1e9,
+                   "elem_kernel_ms": oe_ms / max(1, oe_n),
+                   "words_model_bytes": 8 * NE * (3 * np1 ** 3 + np1 ** 2 + 2),
+                   "rel_l2_vs_stored": float(torch.linalg.norm(d_r2 - d_r_t) / torch.linalg.norm(d_r_t)),
+                   "device_bytes_saved": 8 * NE * 6 * ((np1 ** 3 + 1) & ~1)}
+            plan_o.close()
+        except Exception as exc:  # noqa: BLE001
+            otf = {"error": str(exc)}
     clocks = sampler.stop()
 
     # ---- CPU baseline (rank 0, N=1 only) ----------------------------------
@@ -384,7 +422,7 @@ def run_ours(args, rank, world, local_rank):
                 "ms_per_step": e2e_s * 1e3, "max_abs_diff_vs_device_path": e2e_parity},
         "gpu_launches": launches,
         "roofline": {"kernel": "ax_elem_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": None,
+                     "frac": achieved / peak if achieved else None, "traffic": _ncu_traffic("ax_elem_kernel"),
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_ax,
                      "avg_launch_ms": elem_avg_ms, "launches_timed": elem_n,
                      "share_of_step": elem_ms / ms_total if ms_total else None,
@@ -392,6 +430,7 @@ def run_ours(args, rank, world, local_rank):
                      "whole_ax_gbs": bytes_ax / (ms_step * 1e-3) / 1e9},
         "fdm": fdm,
         "pcg": pcg,
+        "ax_on_the_fly": otf,
         "clocks": clocks,
         "setup_s": setup_s,
         "cpu_baseline": cpu,
@@ -443,7 +482,7 @@ def finish_distributed(args, rank, world, plan, value, ms_step, launches, elem_m
                    "l2": "inputs larger than L2; no flush"},
         "e2e": None, "gpu_launches": launches,
         "roofline": {"kernel": "ax_elem_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": None, "peak_source": peak_src,
+                     "frac": achieved / peak if achieved else None, "traffic": _ncu_traffic("ax_elem_kernel"), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": bytes_ax, "avg_launch_ms": elem_avg_ms,
                      "share_of_step": elem_ms / ms_total if ms_total else None},
         "pcg": pcg,
@@ -466,6 +505,7 @@ def main():
     ap.add_argument("--order", type=int, default=7)
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-otf", action="store_true", help="skip the on-the-fly operator variant measurement")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent cfg2 replicas instead of a partition")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: host-staged messages, lets several ranks share one GPU (tests)")

@@ -1059,6 +1059,7 @@ void subdomain_solve(const Pencil& P, const double* r, const std::array<double, 
 // The system (problem.cpp:73-108 build_system)
 struct System {
   int mode = 0;  // 0 two_scale, 1 fine_only, 2 coarse_only, 3 none
+  int variant = 0;  // OperatorVariant: 0 stored, 1 on_the_fly (operator.hpp:14)
   Mesh mesh;
   Basis basis;
   Maps maps;
@@ -1166,15 +1167,83 @@ void build(System& S, const int* ccfg_mode, int coarse_solve, int direct_thresho
   }
 }
 
-// SemOperator::apply, stored variant (operator.cpp:124-163, 255-287)
+// otf_element_kernel geometry (operator.cpp:174-251): per node, the Jacobian
+// from the 8 corners in (bk,bj,bi) order, its adjugate, det, and
+// kappa rho^3/det adj adj^T, m = rho^3 det. Writes element-local planes.
+void otf_geometry(const System& S, i32 e, std::array<Vec, 6>& wg, Vec& m)
+{
+  const int np = S.basis.np();
+  const Vec& t = S.basis.t;
+  const Vec& w = S.basis.w;
+  double xyz[8][3];
+  for (int cc = 0; cc < 8; ++cc)
+    for (int d = 0; d < 3; ++d) xyz[cc][d] = S.mesh.X[S.mesh.E[e][cc]][d];
+  const double kap = S.kappa[e];
+  for (int k = 0, node = 0; k < np; ++k)
+    for (int j = 0; j < np; ++j)
+      for (int i = 0; i < np; ++i, ++node) {
+        const double h[3][2] = {{0.5 * (1 - t[i]), 0.5 * (1 + t[i])},
+                                {0.5 * (1 - t[j]), 0.5 * (1 + t[j])},
+                                {0.5 * (1 - t[k]), 0.5 * (1 + t[k])}};
+        const double dh[2] = {-0.5, 0.5};
+        double J[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        for (int bk = 0; bk < 2; ++bk)
+          for (int bj = 0; bj < 2; ++bj)
+            for (int bi = 0; bi < 2; ++bi) {
+              const int cc = slot_of(bi, bj, bk);
+              const double wx = dh[bi] * h[1][bj] * h[2][bk];
+              const double wy = h[0][bi] * dh[bj] * h[2][bk];
+              const double wz = h[0][bi] * h[1][bj] * dh[bk];
+              for (int d = 0; d < 3; ++d) {
+                J[d * 3 + 0] += wx * xyz[cc][d];
+                J[d * 3 + 1] += wy * xyz[cc][d];
+                J[d * 3 + 2] += wz * xyz[cc][d];
+              }
+            }
+        double a[9];
+        a[0] = J[4] * J[8] - J[5] * J[7];
+        a[1] = J[2] * J[7] - J[1] * J[8];
+        a[2] = J[1] * J[5] - J[2] * J[4];
+        a[3] = J[5] * J[6] - J[3] * J[8];
+        a[4] = J[0] * J[8] - J[2] * J[6];
+        a[5] = J[2] * J[3] - J[0] * J[5];
+        a[6] = J[3] * J[7] - J[4] * J[6];
+        a[7] = J[1] * J[6] - J[0] * J[7];
+        a[8] = J[0] * J[4] - J[1] * J[3];
+        const double det = J[0] * a[0] + J[1] * a[3] + J[2] * a[6];
+        if (!(det > 0)) throw std::runtime_error("inverted element in on-the-fly kernel");
+        const double rho3 = w[i] * w[j] * w[k];
+        const double scale = kap * rho3 / det;
+        auto aat = [&](int r0, int c0) {
+          return a[r0 * 3 + 0] * a[c0 * 3 + 0] + a[r0 * 3 + 1] * a[c0 * 3 + 1] + a[r0 * 3 + 2] * a[c0 * 3 + 2];
+        };
+        wg[0][node] = scale * aat(0, 0);
+        wg[1][node] = scale * aat(0, 1);
+        wg[2][node] = scale * aat(0, 2);
+        wg[3][node] = scale * aat(1, 1);
+        wg[4][node] = scale * aat(1, 2);
+        wg[5][node] = scale * aat(2, 2);
+        m[node] = rho3 * det;
+      }
+}
+
+// SemOperator::apply (operator.cpp:124-163, 255-287), stored or on-the-fly geometry
 void apply_A(const System& S, const double* u, double* r)
 {
   const int np = S.basis.np(), nloc = np * np * np;
   const Maps& M = S.maps;
   const double* D = S.basis.D.data();
   Vec ul(nloc), fa(nloc), fb(nloc), fc(nloc), rl(static_cast<std::size_t>(S.mesh.ne()) * nloc);
+  std::array<Vec, 6> wotf;
+  Vec motf(S.variant ? nloc : 0);
+  for (auto& v : wotf) v.resize(S.variant ? nloc : 0);
   for (i32 e = 0; e < S.mesh.ne(); ++e) {
     const std::size_t eb = static_cast<std::size_t>(e) * nloc;
+    if (S.variant) otf_geometry(S, e, wotf, motf);
+    const std::size_t gb = S.variant ? 0 : eb;  // plane offset of this element
+    const std::array<const Vec*, 6> W = S.variant ? std::array<const Vec*, 6>{&wotf[0], &wotf[1], &wotf[2], &wotf[3], &wotf[4], &wotf[5]}
+                                                  : std::array<const Vec*, 6>{&S.wg[0], &S.wg[1], &S.wg[2], &S.wg[3], &S.wg[4], &S.wg[5]};
+    const double* mass = S.variant ? motf.data() : &S.mass[eb];
     for (int l = 0; l < nloc; ++l) {
       const i32 g = M.l2g[eb + l];
       ul[l] = M.mask[g] ? 0.0 : u[g];
@@ -1188,7 +1257,7 @@ void apply_A(const System& S, const double* u, double* r)
             sy += D[m * np + j] * ul[(k * np + m) * np + i];
             sz += D[m * np + k] * ul[(m * np + j) * np + i];
           }
-          const double* w[6] = {&S.wg[0][eb], &S.wg[1][eb], &S.wg[2][eb], &S.wg[3][eb], &S.wg[4][eb], &S.wg[5][eb]};
+          const double* w[6] = {&(*W[0])[gb], &(*W[1])[gb], &(*W[2])[gb], &(*W[3])[gb], &(*W[4])[gb], &(*W[5])[gb]};
           fa[l] = w[0][l] * sx + w[1][l] * sy + w[2][l] * sz;
           fb[l] = w[1][l] * sx + w[3][l] * sy + w[4][l] * sz;
           fc[l] = w[2][l] * sx + w[4][l] * sy + w[5][l] * sz;
@@ -1202,7 +1271,7 @@ void apply_A(const System& S, const double* u, double* r)
             s += D[j * np + m] * fb[(k * np + m) * np + i];
             s += D[k * np + m] * fc[(m * np + j) * np + i];
           }
-          rl[eb + l] = s + (S.c[e] * ul[l]) * S.mass[eb + l];
+          rl[eb + l] = s + (S.c[e] * ul[l]) * mass[l];
         }
   }
   Vec rg;
@@ -1438,8 +1507,9 @@ static void finish(System& S, const orc_config* c)
 int orc_create(const orc_config* c, void** out)
 {
   return guard([&] {
-    if (c->variant != 0) throw BadInput("oracle restates the stored operator variant only");
+    if (c->variant != 0 && c->variant != 1) throw BadInput("unknown operator variant");
     auto S = std::make_unique<System>();
+    S->variant = c->variant;
     const auto t0 = std::chrono::steady_clock::now();
     if (c->bar[0] > 0)
       S->mesh = box(c->bar[0], c->bar[1], c->bar[2], c->bar_size, c->boundary);
@@ -1461,6 +1531,7 @@ int orc_create_mesh(int nv, const double* xyz, int ne, const int32_t* conn, int 
 {
   return guard([&] {
     auto S = std::make_unique<System>();
+    S->variant = c->variant;
     S->mesh.X.resize(nv);
     for (int v = 0; v < nv; ++v)
       for (int d = 0; d < 3; ++d) S->mesh.X[v][d] = xyz[3 * v + d];

@@ -44,6 +44,14 @@ struct AxShape {
   static constexpr std::size_t kSmemBytes = kGBytes + (kBufA + kBufB + 2 * NP * NP) * sizeof(double) + kIdxBytes +
                                             2 * sizeof(unsigned long long);
   static constexpr int kMinBlocks = NP <= 8 ? 6 : 2;  // caps registers; shared memory sets the real limit
+  // on-the-fly geometry: the planes are replaced by the element record (8
+  // corners + kappa, TMA-staged) and two Jacobian-column tables
+  static constexpr int kRecD = 26;                      // doubles per element record (16-byte multiple)
+  static constexpr std::size_t kRecBytes = kRecD * sizeof(double);
+  static constexpr int kOtfHeadD = 32 + 6 * NP * NP;    // record (padded) + T0 + T1
+  static constexpr std::size_t kSmemOtfBytes = kOtfHeadD * sizeof(double) +
+                                               (kBufA + kBufB + 2 * NP * NP) * sizeof(double) + kIdxBytes +
+                                               2 * sizeof(unsigned long long);
 };
 
 // x-layout: owner (i,j | k) and x-line (j,k | m) accesses conflict free
@@ -68,6 +76,7 @@ __device__ __forceinline__ int lay_b(int k, int j, int i)
 struct AxArgs {
   const double* u;          // N, input (p in PCG)
   const double* wg;         // [e][6][nlocp]: kappa*m*Gt planes per element (TMA-staged)
+  const double* erec;       // on-the-fly variant: [e][26] = corner xyz in (bi,bj,bk)-bit order, kappa_e, 0
   const double* mass;       // NE * nloc
   const double* c_e;        // NE
   const int* smap;          // [e][2][nsurfp]: row 0 Dirichlet-encoded global ids (TMA-staged)
@@ -111,6 +120,84 @@ __device__ __forceinline__ void contract3(const double* __restrict__ M, FX&& in_
   }
 }
 
+// ---- on-the-fly geometry (SemOperator::otf_element_kernel, operator.cpp:174-253)
+// The trilinear map's Jacobian columns are bilinear in the other two
+// coordinates: dX/dxi depends on (eta_j, zeta_k) only, dX/deta on (xi_i,
+// zeta_k), dX/dzeta on (xi_i, eta_j), so each is an NP^2 table per element
+// instead of a 24-term sum per node. X[b*3+d] with b = bi + 2 bj + 4 bk.
+__device__ __forceinline__ double hatv(const OrderTables& T, int b, int q) { return b ? T.hat1[q] : T.hat0[q]; }
+
+// column c (0: d/dxi, 1: d/deta, 2: d/dzeta) at the two other coordinates' node indices (p, q)
+__device__ __forceinline__ void jac_column(const OrderTables& T, const double* __restrict__ X, int c, int p, int q,
+                                           double (&out)[3])
+{
+  const int sc = 1 << c, s1 = c == 0 ? 2 : 1, s2 = c == 2 ? 2 : 4;  // bit strides: varied axis, first/second other axis
+  out[0] = out[1] = out[2] = 0.0;
+#pragma unroll
+  for (int b2 = 0; b2 < 2; ++b2)
+#pragma unroll
+    for (int b1 = 0; b1 < 2; ++b1) {
+      const double h = hatv(T, b1, p) * hatv(T, b2, q);
+      const int lo = b1 * s1 + b2 * s2, hi = lo + sc;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) out[d] += h * (0.5 * (X[hi * 3 + d] - X[lo * 3 + d]));
+    }
+}
+
+// 1/x to full FP64 precision: MUFU reciprocal seed + two Newton steps
+// (5 FP64 instructions instead of the division sequence); within 1 ulp
+__device__ __forceinline__ double fast_rcp(double x)
+{
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Metric flux at one node straight from the adjugate A of its Jacobian:
+// kappa m Gt s = kappa rho^3/det A A^T s, evaluated as A (A^T s) (18 FMAs
+// instead of forming the six entries and applying them); m = rho^3 det.
+__device__ __forceinline__ void otf_flux(const double (&jx)[3], const double (&jy)[3], const double (&jz)[3],
+                                         double kap_rho3, double rho3, double sx, double sy, double sz,
+                                         double& fa, double& fb, double& fc, double& m)
+{
+  const double J0 = jx[0], J1 = jy[0], J2 = jz[0], J3 = jx[1], J4 = jy[1], J5 = jz[1], J6 = jx[2], J7 = jy[2],
+               J8 = jz[2];
+  const double a0 = J4 * J8 - J5 * J7, a1 = J2 * J7 - J1 * J8, a2 = J1 * J5 - J2 * J4;
+  const double a3 = J5 * J6 - J3 * J8, a4 = J0 * J8 - J2 * J6, a5 = J2 * J3 - J0 * J5;
+  const double a6 = J3 * J7 - J4 * J6, a7 = J1 * J6 - J0 * J7, a8 = J0 * J4 - J1 * J3;
+  const double det = J0 * a0 + J1 * a3 + J2 * a6;
+  const double scale = kap_rho3 * fast_rcp(det);
+  const double v0 = a0 * sx + a3 * sy + a6 * sz, v1 = a1 * sx + a4 * sy + a7 * sz, v2 = a2 * sx + a5 * sy + a8 * sz;
+  fa = scale * (a0 * v0 + a1 * v1 + a2 * v2);
+  fb = scale * (a3 * v0 + a4 * v1 + a5 * v2);
+  fc = scale * (a6 * v0 + a7 * v1 + a8 * v2);
+  m = rho3 * det;
+}
+
+// kappa*m*Gt (six symmetric entries) and m at one node from its Jacobian
+// columns: m Gt = rho^3/det adj adj^T, m = rho^3 det (operator.cpp:226-250)
+__device__ __forceinline__ void otf_metric(const double (&jx)[3], const double (&jy)[3], const double (&jz)[3],
+                                           double kap_rho3, double rho3, double (&w)[6], double& m)
+{
+  const double J0 = jx[0], J1 = jy[0], J2 = jz[0], J3 = jx[1], J4 = jy[1], J5 = jz[1], J6 = jx[2], J7 = jy[2],
+               J8 = jz[2];
+  const double a0 = J4 * J8 - J5 * J7, a1 = J2 * J7 - J1 * J8, a2 = J1 * J5 - J2 * J4;
+  const double a3 = J5 * J6 - J3 * J8, a4 = J0 * J8 - J2 * J6, a5 = J2 * J3 - J0 * J5;
+  const double a6 = J3 * J7 - J4 * J6, a7 = J1 * J6 - J0 * J7, a8 = J0 * J4 - J1 * J3;
+  const double det = J0 * a0 + J1 * a3 + J2 * a6;
+  const double scale = kap_rho3 / det;
+  w[0] = scale * (a0 * a0 + a1 * a1 + a2 * a2);
+  w[1] = scale * (a0 * a3 + a1 * a4 + a2 * a5);
+  w[2] = scale * (a0 * a6 + a1 * a7 + a2 * a8);
+  w[3] = scale * (a3 * a3 + a4 * a4 + a5 * a5);
+  w[4] = scale * (a3 * a6 + a4 * a7 + a5 * a8);
+  w[5] = scale * (a6 * a6 + a7 * a7 + a8 * a8);
+  m = rho3 * det;
+}
+
 // Persistent: CTA b processes elements b, b+grid, ... . The element's six
 // metric planes (6*nloc FP64, the bulk of Ax traffic) and its surface index
 // block are streamed into shared memory by TMA bulk copies issued one element
@@ -119,14 +206,23 @@ __device__ __forceinline__ void contract3(const double* __restrict__ M, FX&& in_
 // phase D of e, so HBM traffic overlaps the contractions. D and D^T live in
 // shared memory and are read as warp-uniform broadcasts, keeping registers
 // low enough for 6 CTAs per SM.
-template <int NP>
+//
+// OTF (operator variant on_the_fly): instead of the planes, a 208-byte element
+// record (corners + kappa) is staged the same way; phase B builds the
+// Jacobian-column tables, phase C forms kappa*m*Gt per node in registers.
+template <int NP, bool OTF = false>
 __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) ax_elem_kernel(AxArgs a)
 {
   using Sh = AxShape<NP>;
   constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NLP = Sh::kNlocP;
+  constexpr std::size_t kStage = OTF ? Sh::kRecBytes : Sh::kGBytes;  // bar[0] transaction per element
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* sG = reinterpret_cast<double*>(smem_raw);                  // [6][nlocp]
-  double* sa = sG + 6 * NLP;
+  double* sG = reinterpret_cast<double*>(smem_raw);                  // [6][nlocp] | OTF: record, T0, T1
+  double* sT0 = sG + 32;                                             // OTF: dX/dxi at (eta_j, zeta_k)
+  double* sT1 = sT0 + 3 * NP * NP;                                   // OTF: dX/deta at (xi_i, zeta_k)
+  const double* stage_src = OTF ? a.erec : a.wg;
+  constexpr int kStageD = OTF ? Sh::kRecD : 6 * NLP;
+  double* sa = sG + (OTF ? Sh::kOtfHeadD : 6 * NLP);
   double* sb = sa + Sh::kBufA;
   double* sD = sb + Sh::kBufB;                                       // D, then D^T
   double* sDT = sD + NP * NP;
@@ -160,8 +256,8 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
   if (tid == 0 && e < a.ne) {
     mbar_expect_tx(&bar[1], Sh::kIdxBytes);
     bulk_g2s(sidx, a.smap + (long long)e * 2 * Sh::kNsurfP, Sh::kIdxBytes, &bar[1]);
-    mbar_expect_tx(&bar[0], Sh::kGBytes);
-    bulk_g2s(sG, a.wg + (long long)e * 6 * NLP, Sh::kGBytes, &bar[0]);
+    mbar_expect_tx(&bar[0], kStage);
+    bulk_g2s(sG, stage_src + (long long)e * kStageD, kStage, &bar[0]);
   }
   // gather u for element ee (masked, operator.cpp:264-265) using the staged indices
   auto gather_u = [&](int ee, double (&dst)[NP]) {
@@ -201,6 +297,22 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
 
     // ---- B: derivatives (operator.cpp:136-138): x-line, y-line, owner z-column
     double fz[NP];
+    double jz[3] = {0.0, 0.0, 0.0}, kap = 0.0;
+    if constexpr (OTF) {  // Jacobian-column tables of element e (consumed in phase C)
+      mbar_wait(&bar[0], phase);
+      if (lane_ok) {
+        const OrderTables& T = c_tab[NP];
+        double t[3];
+        jac_column(T, sG, 0, i, j, t);  // entry (k'=j, j'=i)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) sT0[(j * NP + i) * 3 + d] = t[d];
+        jac_column(T, sG, 1, i, j, t);  // entry (k'=j, i'=i)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) sT1[(j * NP + i) * 3 + d] = t[d];
+        jac_column(T, sG, 2, i, j, jz);
+        kap = sG[24];
+      }
+    }
     {
       double ox[NP], oy[NP];
       contract3<NP>(sD, [&](int m) { return sa[lay_a<NP>(j, i, m)]; }, [&](int m) { return sb[lay_b<NP>(j, m, i)]; },
@@ -217,25 +329,38 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
     __syncthreads();
 
     // ---- C: metric fluxes (operator.cpp:142-144), planes from shared ----------
-    mbar_wait(&bar[0], phase);
+    double mk[OTF ? NP : 1];
+    if constexpr (!OTF) mbar_wait(&bar[0], phase);
     if (lane_ok) {
+      const double wij = OTF ? c_tab[NP].w[i] * c_tab[NP].w[j] : 0.0;
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
-        const int l = (k * NP + j) * NP + i;
-        const double w0 = sG[l], w1 = sG[NLP + l], w2 = sG[2 * NLP + l];
-        const double w3 = sG[3 * NLP + l], w4 = sG[4 * NLP + l], w5 = sG[5 * NLP + l];
         const int pa = lay_a<NP>(k, j, i), pb = lay_b<NP>(k, j, i);
         const double sx = sa[pa], sy = sb[pb], sz = fz[k];
-        sa[pa] = w0 * sx + w1 * sy + w2 * sz;
-        sb[pb] = w1 * sx + w3 * sy + w4 * sz;
-        fz[k] = w2 * sx + w4 * sy + w5 * sz;
+        if constexpr (OTF) {
+          const double jx[3] = {sT0[(k * NP + j) * 3], sT0[(k * NP + j) * 3 + 1], sT0[(k * NP + j) * 3 + 2]};
+          const double jy[3] = {sT1[(k * NP + i) * 3], sT1[(k * NP + i) * 3 + 1], sT1[(k * NP + i) * 3 + 2]};
+          const double rho3 = wij * c_tab[NP].w[k];
+          double f0, f1, f2;
+          otf_flux(jx, jy, jz, kap * rho3, rho3, sx, sy, sz, f0, f1, f2, mk[k]);
+          sa[pa] = f0;
+          sb[pb] = f1;
+          fz[k] = f2;
+        } else {
+          const int l = (k * NP + j) * NP + i;
+          const double w0 = sG[l], w1 = sG[NLP + l], w2 = sG[2 * NLP + l];
+          const double w3 = sG[3 * NLP + l], w4 = sG[4 * NLP + l], w5 = sG[5 * NLP + l];
+          sa[pa] = w0 * sx + w1 * sy + w2 * sz;
+          sb[pb] = w1 * sx + w3 * sy + w4 * sz;
+          fz[k] = w2 * sx + w4 * sy + w5 * sz;
+        }
       }
     }
     __syncthreads();  // sG consumed
     if (tid == 0 && en < a.ne) {
       fence_proxy_async_smem();
-      mbar_expect_tx(&bar[0], Sh::kGBytes);
-      bulk_g2s(sG, a.wg + (long long)en * 6 * NLP, Sh::kGBytes, &bar[0]);
+      mbar_expect_tx(&bar[0], kStage);
+      bulk_g2s(sG, stage_src + (long long)en * kStageD, kStage, &bar[0]);
     }
     // prefetch u(e') and c(e') while the adjoint contractions run
     double unext[NP];
@@ -275,7 +400,12 @@ __global__ void __launch_bounds__(AxShape<NP>::kBlock, AxShape<NP>::kMinBlocks) 
 #pragma unroll
       for (int k = 0; k < NP; ++k) {
         double r = (sa[lay_a<NP>(k, j, i)] + sb[lay_b<NP>(k, j, i)]) + tz[k];
-        if (ce != 0.0) r += (ce * ucol[k]) * __ldg(m0 + k * NP * NP);  // operator.cpp:159
+        if (ce != 0.0) {  // operator.cpp:159
+          if constexpr (OTF)
+            r += (ce * ucol[k]) * mk[k];
+          else
+            r += (ce * ucol[k]) * __ldg(m0 + k * NP * NP);
+        }
         if (code[k] >= 0) {
           rs[code[k]] = r;
         } else {
@@ -308,12 +438,14 @@ struct AxSmall {
   static constexpr int kNSP = (kNS + 3) & ~3;
 };
 
-template <int NP>
+template <int NP, bool OTF = false>
 __global__ void __launch_bounds__(256) ax_small_kernel(AxArgs a)
 {
   using S = AxSmall<NP>;
   constexpr int NL = S::kNL, EPB = S::kEPB, n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1);
+  constexpr int RD = AxShape<NP>::kRecD;
   __shared__ double su[EPB][NL], fa[EPB][NL], fb[EPB][NL], fc[EPB][NL];
+  __shared__ double srec[OTF ? EPB : 1][RD];
   __shared__ double sD[NP * NP];
   __shared__ double red[S::kBlock / 32];
   const int tid = threadIdx.x;
@@ -328,18 +460,37 @@ __global__ void __launch_bounds__(256) ax_small_kernel(AxArgs a)
   for (int eb = a.e_begin + blockIdx.x * EPB; eb < a.ne; eb += gridDim.x * EPB) {
     const int e = eb + el;
     const bool act = lane_ok && e < a.ne;
-    double u = 0.0, w[6] = {0, 0, 0, 0, 0, 0};
+    double u = 0.0, w[6] = {0, 0, 0, 0, 0, 0}, mo = 0.0;
+    if constexpr (OTF) {
+      for (int q = tid; q < EPB * RD; q += S::kBlock) {
+        const int qe = q / RD;
+        srec[qe][q % RD] = eb + qe < a.ne ? __ldg(a.erec + (long long)(eb + qe) * RD + q % RD) : 1.0;
+      }
+    }
     if (act) {
       if (slot >= 0)
         u = load_masked(a.u, __ldg(a.smap + (long long)e * 2 * S::kNSP + slot));  // masked (operator.cpp:264)
       else
         u = __ldg(a.u + (long long)a.num_surface_global + (long long)e * NI + ioff);
-      const double* wp = a.wg + (long long)e * 6 * S::kNlocP + l;
+      if constexpr (!OTF) {
+        const double* wp = a.wg + (long long)e * 6 * S::kNlocP + l;
 #pragma unroll
-      for (int p = 0; p < 6; ++p) w[p] = __ldg(wp + p * S::kNlocP);
+        for (int p = 0; p < 6; ++p) w[p] = __ldg(wp + p * S::kNlocP);
+      }
       su[el][l] = u;
     }
     __syncthreads();
+    if constexpr (OTF) {
+      if (act) {
+        const OrderTables& T = c_tab[NP];
+        double jx[3], jy[3], jz[3];
+        jac_column(T, srec[el], 0, j, k, jx);
+        jac_column(T, srec[el], 1, i, k, jy);
+        jac_column(T, srec[el], 2, i, j, jz);
+        const double rho3 = T.w[i] * T.w[j] * T.w[k];
+        otf_metric(jx, jy, jz, srec[el][24] * rho3, rho3, w, mo);
+      }
+    }
     if (act) {  // derivatives and metric fluxes (operator.cpp:135-144)
       double sx = 0, sy = 0, sz = 0;
 #pragma unroll
@@ -362,7 +513,7 @@ __global__ void __launch_bounds__(256) ax_small_kernel(AxArgs a)
         s += sD[k * NP + m] * fc[el][(m * NP + j) * NP + i];
       }
       const double ce = __ldg(a.c_e + e);
-      if (ce != 0.0) s += (ce * u) * __ldg(a.mass + (std::size_t)e * NL + l);  // operator.cpp:159
+      if (ce != 0.0) s += (ce * u) * (OTF ? mo : __ldg(a.mass + (std::size_t)e * NL + l));  // operator.cpp:159
       if (slot >= 0) {
         a.rsurf[(long long)e * S::kNSP + slot] = s;
       } else {

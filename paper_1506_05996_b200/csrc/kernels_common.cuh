@@ -30,6 +30,7 @@ struct OrderTables {
   double lam[kMaxP];           // pencil eigenvalues (fine.hpp:24)
   double hat0[kMaxNP];         // 0.5*(1-t_i)  coarse hats (gll.cpp:92)
   double hat1[kMaxNP];         // 0.5*(1+t_i)
+  double w[kMaxNP];            // GLL weights rho_i (gll.hpp:21), on-the-fly geometry
 };
 // Single translation unit (plan.cu) includes the kernels, so this is the definition.
 __device__ OrderTables c_tab[kMaxNP + 1];

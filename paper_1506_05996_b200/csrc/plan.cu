@@ -146,6 +146,7 @@ struct Plan {
 
   // device arrays
   double* wg = nullptr;
+  double* erec = nullptr;  // on-the-fly variant: [e][26] corners + kappa
   double* mass = nullptr;
   double* c_e = nullptr;
   double* kappa_e = nullptr;
@@ -306,24 +307,49 @@ DotArgs cdot_args(Plan& pl, double* result)
   return d;
 }
 
-template <int NP>
-int ax_persistent_grid(const Plan& pl)
+template <int NP, bool OTF>
+int ax_persistent_grid_v(const Plan& pl)
 {
   if constexpr (NP <= 3) {  // thread-per-node kernel for the low orders
     int per_sm = 0;
-    HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ax_small_kernel<NP>, AxSmall<NP>::kBlock, 0));
+    HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ax_small_kernel<NP, OTF>, AxSmall<NP>::kBlock, 0));
     per_sm = std::max(per_sm, 1);
     const int need = (pl.ne + AxSmall<NP>::kEPB - 1) / AxSmall<NP>::kEPB;
     return std::max(1, std::min(need, per_sm * pl.num_sms));
   }
   using Sh = AxShape<NP>;
-  HXB_CUDA(cudaFuncSetAttribute(ax_elem_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(Sh::kSmemBytes)));
-  HXB_CUDA(cudaFuncSetAttribute(ax_elem_kernel<NP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  const int smem = static_cast<int>(OTF ? Sh::kSmemOtfBytes : Sh::kSmemBytes);
+  HXB_CUDA(cudaFuncSetAttribute(ax_elem_kernel<NP, OTF>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  HXB_CUDA(cudaFuncSetAttribute(ax_elem_kernel<NP, OTF>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int per_sm = 0;
-  HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ax_elem_kernel<NP>, Sh::kBlock, Sh::kSmemBytes));
+  HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ax_elem_kernel<NP, OTF>, Sh::kBlock, smem));
   per_sm = std::max(per_sm, 1);
   return std::max(1, std::min(pl.ne, per_sm * pl.num_sms));
+}
+
+template <int NP>
+int ax_persistent_grid(const Plan& pl)
+{
+  return pl.variant == HXB_VARIANT_ON_THE_FLY ? ax_persistent_grid_v<NP, true>(pl) : ax_persistent_grid_v<NP, false>(pl);
+}
+
+template <int NP, bool OTF>
+void launch_ax_kernel(const Plan& pl, const AxArgs& a, int grid, cudaStream_t s)
+{
+  if constexpr (NP <= 3)
+    ax_small_kernel<NP, OTF><<<grid, AxSmall<NP>::kBlock, 0, s>>>(a);
+  else
+    ax_elem_kernel<NP, OTF><<<grid, AxShape<NP>::kBlock, OTF ? AxShape<NP>::kSmemOtfBytes : AxShape<NP>::kSmemBytes,
+                              s>>>(a);
+}
+
+template <int NP>
+void launch_ax_kernel(const Plan& pl, const AxArgs& a, int grid, cudaStream_t s)
+{
+  if (pl.variant == HXB_VARIANT_ON_THE_FLY)
+    launch_ax_kernel<NP, true>(pl, a, grid, s);
+  else
+    launch_ax_kernel<NP, false>(pl, a, grid, s);
 }
 
 template <int NP>
@@ -333,6 +359,7 @@ void launch_ax_elem(Plan& pl, const double* u, double* r, DotArgs dot, cudaStrea
   AxArgs a;
   a.u = u;
   a.wg = pl.wg;
+  a.erec = pl.erec;
   a.mass = pl.mass;
   a.c_e = pl.c_e;
   a.smap = pl.smap;
@@ -341,10 +368,7 @@ void launch_ax_elem(Plan& pl, const double* u, double* r, DotArgs dot, cudaStrea
   a.ne = pl.ne;
   a.num_surface_global = pl.nsg + pl.e0 * (pl.order - 1) * (pl.order - 1) * (pl.order - 1);  // first owned interior id
   a.dot = dot;
-  if constexpr (NP <= 3)
-    ax_small_kernel<NP><<<pl.ax_grid, AxSmall<NP>::kBlock, 0, s>>>(a);
-  else
-    ax_elem_kernel<NP><<<pl.ax_grid, Sh::kBlock, Sh::kSmemBytes, s>>>(a);
+  launch_ax_kernel<NP>(pl, a, pl.ax_grid, s);
 }
 
 // element range [e_begin, e_end) of the element kernel (host-pointer pipeline)
@@ -355,6 +379,7 @@ void launch_ax_elem_range(Plan& pl, const double* u, double* r, int e_begin, int
   AxArgs a;
   a.u = u;
   a.wg = pl.wg;
+  a.erec = pl.erec;
   a.mass = pl.mass;
   a.c_e = pl.c_e;
   a.smap = pl.smap;
@@ -364,13 +389,9 @@ void launch_ax_elem_range(Plan& pl, const double* u, double* r, int e_begin, int
   a.e_begin = e_begin;
   a.num_surface_global = pl.nsg;
   a.dot = DotArgs{};
-  if constexpr (NP <= 3) {
-    const int grid = std::max(1, std::min(pl.ax_grid, (e_end - e_begin + AxSmall<NP>::kEPB - 1) / AxSmall<NP>::kEPB));
-    ax_small_kernel<NP><<<grid, AxSmall<NP>::kBlock, 0, s>>>(a);
-  } else {
-    const int grid = std::max(1, std::min(pl.ax_grid, e_end - e_begin));
-    ax_elem_kernel<NP><<<grid, Sh::kBlock, Sh::kSmemBytes, s>>>(a);
-  }
+  const int grid = NP <= 3 ? std::max(1, std::min(pl.ax_grid, (e_end - e_begin + AxSmall<NP>::kEPB - 1) / AxSmall<NP>::kEPB))
+                           : std::max(1, std::min(pl.ax_grid, e_end - e_begin));
+  launch_ax_kernel<NP>(pl, a, grid, s);
 }
 
 template <int NP>
@@ -731,6 +752,7 @@ bool upload_tables(const GllBasis& basis, const Pencil& pencil)
   for (int i = 0; i < np; ++i) {
     t.hat0[i] = 0.5 * (1 - basis.nodes[i]);
     t.hat1[i] = 0.5 * (1 + basis.nodes[i]);
+    t.w[i] = basis.weights[i];
   }
   HXB_CUDA(cudaMemcpyToSymbol(c_tab, &t, sizeof(OrderTables), sizeof(OrderTables) * np));
   FdmConst fc{};
@@ -1005,7 +1027,8 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
 {
   const auto t0 = std::chrono::steady_clock::now();
   if (!m) throw HxbError(HXB_EINVAL, "mesh must be non-null");
-  if (opt.variant != HXB_VARIANT_STORED) throw HxbError(HXB_EINVAL, "only the stored operator variant is built");
+  if (opt.variant != HXB_VARIANT_STORED && opt.variant != HXB_VARIANT_ON_THE_FLY)
+    throw HxbError(HXB_EINVAL, "unknown operator variant");
   pl.device = opt.device;
   HXB_CUDA(cudaSetDevice(pl.device));
   {
@@ -1025,6 +1048,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   so.precond_mode = opt.precond_mode;
   so.coarse_solve = opt.coarse_solve;
   so.direct_threshold = opt.direct_threshold;
+  so.store_planes = opt.variant == HXB_VARIANT_STORED;
   build_host_setup(hs, order, so);
   const HexMesh& mesh = hs.mesh;
   const Numbering& num = hs.num;
@@ -1074,7 +1098,19 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
 
   DeviceArena& M = pl.mem;
   const int e0 = pl.e0, nel = pl.ne;  // owned elements [e0, e0 + nel)
-  {  // kappa*m*Gt planes regrouped per element: [e][6][nlocp] (one TMA stream per element)
+  if (pl.variant == HXB_VARIANT_ON_THE_FLY) {  // element records: corners in (bi,bj,bk)-bit order, kappa
+    constexpr int RD = 26;
+    std::vector<double> rec(static_cast<std::size_t>(nel) * RD, 0.0);
+    for (int le = 0; le < nel; ++le) {
+      double* q = &rec[static_cast<std::size_t>(le) * RD];
+      for (int b = 0; b < 8; ++b) {
+        const auto& v = mesh.vertices[mesh.elements[e0 + le][hex_corner(b & 1, (b >> 1) & 1, b >> 2)]];
+        for (int d = 0; d < 3; ++d) q[3 * b + d] = v[d];
+      }
+      q[24] = hs.kappa[e0 + le];
+    }
+    pl.erec = M.upload(rec);
+  } else {  // kappa*m*Gt planes regrouped per element: [e][6][nlocp] (one TMA stream per element)
     const int nlocp = (pl.nloc + 1) & ~1;
     const std::size_t total = static_cast<std::size_t>(ne) * pl.nloc;
     std::vector<double> wge(static_cast<std::size_t>(nel) * 6 * nlocp, 0.0);

@@ -180,6 +180,7 @@ struct SetupOptions {
   int precond_mode = 0;         // PrecondMode
   int coarse_solve = 0;         // CoarseSolve
   gid direct_threshold = 64000; // coarse.hpp:36
+  bool store_planes = true;     // false for the on-the-fly operator variant (no kappa*m*Gt planes)
 };
 
 struct HostSetup {

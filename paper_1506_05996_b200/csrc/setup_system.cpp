@@ -46,7 +46,7 @@ void build_host_setup(HostSetup& hs, int order, const SetupOptions& opt)
       if (!(hs.kappa[e] > 0)) throw HxbError(1, "need kappa > 0, c >= 0");
 
   hs.basis = make_gll_basis(order);
-  hs.geo = compute_geometry(hs.mesh, hs.basis, hs.kappa, true);  // throws on inverted elements
+  hs.geo = compute_geometry(hs.mesh, hs.basis, hs.kappa, opt.store_planes);  // throws on inverted elements
   hs.num = build_numbering(hs.mesh, order);
   const int nloc = hs.basis.npts() * hs.basis.npts() * hs.basis.npts();
   hs.lumped.assign(hs.num.num_global, 0.0);

@@ -16,14 +16,15 @@ pytestmark = pytest.mark.gpu
 
 
 def _pair(k=8, order=4, family="uniform", refine=0, precond="two_scale", coarse_solve="automatic", kappa=1.0, c=0.0,
-          boundary="dirichlet"):
+          boundary="dirichlet", variant="stored"):
     ref = checker(k=k, order=order, family=family, refine=refine, precond=precond, coarse_solve=coarse_solve,
-                  kappa=kappa, c=c, boundary=boundary)
+                  kappa=kappa, c=c, boundary=boundary, variant=variant)
     mesh = hx.generate_cube_mesh(k, family, boundary)
     for _ in range(refine):
         mesh = hx.refine_uniform(mesh)
     ne = mesh.num_elements
-    plan = hx.Plan(mesh, order, np.full(ne, kappa), np.full(ne, c), precond=precond, coarse_solve=coarse_solve)
+    plan = hx.Plan(mesh, order, np.full(ne, kappa), np.full(ne, c), precond=precond, coarse_solve=coarse_solve,
+                   variant=variant)
     return ref, plan
 
 
@@ -55,6 +56,48 @@ def test_apply_A_mass_term_and_distorted():
     ref, plan = _pair(k=3, order=5, family="distorted_elements", c=0.7, kappa=2.5)
     u = splitmix_vector(plan.N, 7)
     assert rel(plan.apply_A(u), ref.apply_A(u)) <= 1e-13
+
+
+@pytest.mark.parametrize("order", [1, 2, 3, 4, 7, 9])
+def test_apply_A_on_the_fly_matches_reference(order):
+    """Operator variant on_the_fly (operator.cpp:174-253): geometry from the 8
+    corners per node, no stored planes. Distorted elements, c != 0 (the mass
+    term uses the on-the-fly rho^3 det)."""
+    ref, plan = _pair(k=3, order=order, family="distorted_elements", kappa=2.5, c=0.7, precond="none",
+                      variant="on_the_fly")
+    u = splitmix_vector(plan.N, 11)
+    a, b = plan.apply_A(u), ref.apply_A(u)
+    assert rel(a, b) <= 1e-13, rel(a, b)
+
+
+@pytest.mark.parametrize("k,order", [(16, 7), (12, 5), (40, 2)])
+def test_on_the_fly_agrees_with_stored(k, order):
+    """test_operator.cpp:103-121 on meshes with many elements per CTA: the two
+    variants agree to 1e-12 and the on-the-fly path is bitwise repeatable."""
+    mesh = hx.generate_cube_mesh(k, "distorted_domain")
+    ne = mesh.num_elements
+    kap, cc = np.full(ne, 2.5), np.full(ne, 0.7)
+    a = hx.Plan(mesh, order, kap, cc, precond="none")
+    b = hx.Plan(mesh, order, kap, cc, precond="none", variant="on_the_fly")
+    u = splitmix_vector(a.N, 42)
+    ra, rb = a.apply_A(u), b.apply_A(u)
+    assert rel(rb, ra) <= 1e-12
+    assert np.array_equal(b.apply_A(u), rb)
+
+
+@pytest.mark.parametrize("family", ["uniform", "distorted_elements"])
+def test_pcg_on_the_fly_matches_reference(family):
+    """Two-scale PCG with the on-the-fly operator against the reference's;
+    distorted meshes amplify rounding, so the tolerance is this problem's own
+    rounding floor (helpers.reference_noise) when that exceeds 1e-10."""
+    from helpers import reference_noise
+
+    ref, plan = _pair(k=6, order=5, family=family, variant="on_the_fly")
+    b = ref.load_ones()
+    theirs = ref.pcg(b, tol=1e-8)
+    noise = reference_noise(theirs, b, RefConfig(k=6, order=5, family=family, variant="on_the_fly"))
+    print(f"on-the-fly {family}: reference rounding floor {noise:.2e}")
+    history_parity(plan.pcg(b, tol=1e-8), theirs, tol=max(1e-10, 10 * noise))
 
 
 @pytest.mark.parametrize("precond", ["two_scale", "fine_only", "coarse_only", "none"])

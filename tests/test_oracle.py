@@ -216,3 +216,24 @@ def test_restrict_prolong_match_reference():
     Z = splitmix_vector(a.NV, 10)
     assert np.array_equal(a.prolongate(Z), b.prolongate(Z))
     assert np.array_equal(a.element_h(), b.element_h())
+
+
+# --- on-the-fly operator variant (operator.cpp:174-253) ------------------------
+@pytest.mark.parametrize("family", ["distorted_domain", "distorted_elements"])
+def test_oracle_otf_agrees_with_stored(family):
+    """test_operator.cpp:103-121: stored and on-the-fly agree to 1e-12."""
+    kw = dict(k=2, order=3, family=family, kappa=2.5, c=0.7, precond="none")
+    a, b = orc(**kw), orc(variant="on_the_fly", **kw)
+    u = splitmix_vector(a.N, 42)
+    ra, rb = a.apply_A(u), b.apply_A(u)
+    assert np.linalg.norm(ra - rb) <= 1e-12 * np.linalg.norm(ra)
+
+
+@needs_ref
+@pytest.mark.parametrize("order", [1, 3, 6])
+def test_oracle_otf_matches_reference(order):
+    """The restated on-the-fly geometry is the reference's, bit for bit."""
+    kw = dict(k=3, order=order, family="distorted_elements", kappa=1.5, c=0.3, precond="none",
+              variant="on_the_fly")
+    u = splitmix_vector(orc(**kw).N, 3)
+    assert np.array_equal(orc(**kw).apply_A(u), RefSystem(RefConfig(**kw)).apply_A(u))

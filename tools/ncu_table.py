@@ -30,3 +30,20 @@ for r in rows[2:]:
         else:
             vals.append(f"{'-':>8s}")
     print(f"{name:34s} " + " ".join(vals))
+
+# --json PATH: merge {kernel: dram bytes per launch (first launch of each kernel)}
+# into PATH (profiles/ncu_traffic.json, read by bench.py for roofline.traffic)
+if "--json" in sys.argv:
+    import json, os
+    path = sys.argv[sys.argv.index("--json") + 1]
+    doc = json.load(open(path)) if os.path.exists(path) else {"source": "ncu --set full --clock-control none", "kernels": {}}
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")].split("(")[0].split("<")[0].replace("void ", "").strip()
+        if name in doc["kernels"] and doc["kernels"][name].get("rep") == os.path.basename(rep):
+            continue
+        rd = conv(r[idx["dram__bytes_read.sum"]], u[idx["dram__bytes_read.sum"]]) * 1e6
+        wr = conv(r[idx["dram__bytes_write.sum"]], u[idx["dram__bytes_write.sum"]]) * 1e6
+        doc["kernels"][name] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
+                                "us": conv(r[idx["gpu__time_duration.sum"]], u[idx["gpu__time_duration.sum"]]),
+                                "rep": os.path.basename(rep)}
+    json.dump(doc, open(path, "w"), indent=1)

@@ -9,7 +9,8 @@ from oracle import splitmix_vector
 
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 7
-plan = hx.Plan(hx.generate_cube_mesh(k), n)
+variant = sys.argv[3] if len(sys.argv) > 3 else "stored"
+plan = hx.Plan(hx.generate_cube_mesh(k), n, variant=variant)
 u = splitmix_vector(plan.N, 12345)
 for _ in range(2):
     plan.apply_A(u)
