@@ -201,6 +201,10 @@ int hxb_node_coords(hxb_plan* plan, double* xyz);
 /* assemble_load(s = 1) and lumped_mass (problem.cpp:38-46, operator.hpp:60). */
 int hxb_load_ones(hxb_plan* plan, double* b);
 int hxb_lumped_mass(hxb_plan* plan, double* m);
+/* Geometric factors of the plan's elements (compute_factors, geometry.cpp:105-151,
+ * computed on the device): mass[NE*nloc] = rho^3 det J and, stored variant
+ * only, wg[6][NE*nloc] = kappa*mass*Gt planes (operator.cpp:76-88). NULL skips. */
+int hxb_export_geometry(hxb_plan* plan, double* mass, double* wg);
 
 /* IndexMaps export for the bit-exact numbering check (mesh.hpp:66-97).
  * Any pointer may be NULL. Sizes: l2g/g2l_elem/g2l_local NE*(n+1)^3,
@@ -225,6 +229,7 @@ int hxb_setup_export_maps(const hxb_setup* setup, int32_t* l2g, int64_t* g2l_off
 int hxb_setup_amg_level(const hxb_setup* setup, int level, int64_t* rows, int64_t* nnz, int64_t* ptr,
                         int32_t* col, double* val, int32_t* aggregate);
 int hxb_setup_lumped_mass(const hxb_setup* setup, double* m);
+int hxb_setup_export_geometry(const hxb_setup* setup, double* mass, double* wg);  /* host restatement */
 /* GPU-free partition lists of the distributed operator (see hxb_dist_*):
  * counts[6] = e0, e1, n_group0, n_up, n_down, local surface nodes; nodes
  * (optional) = local node ids [group0 | up | down]. */

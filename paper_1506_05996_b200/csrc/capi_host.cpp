@@ -233,6 +233,16 @@ int hxb_setup_lumped_mass(const hxb_setup* s, double* m)
   });
 }
 
+int hxb_setup_export_geometry(const hxb_setup* s, double* mass, double* wg)
+{
+  return guarded([&] {
+    const HostSetup* hs = reinterpret_cast<const HostSetup*>(s);
+    if (!hs) throw HxbError(HXB_EINVAL, "null setup");
+    if (mass) std::memcpy(mass, hs->geo.mass.data(), hs->geo.mass.size() * sizeof(double));
+    if (wg) std::memcpy(wg, hs->geo.wg.data(), hs->geo.wg.size() * sizeof(double));
+  });
+}
+
 int hxb_gll(int order, double* nodes, double* weights, double* deriv)
 {
   return guarded([&] {

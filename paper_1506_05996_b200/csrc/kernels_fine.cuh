@@ -31,6 +31,9 @@ struct FdmLayout {  // (row stride S, plane stride PS) per pencil size
   static constexpr int PS = P == 4 ? 19 : P == 6 ? 54 : P == 8 ? 72 : P == 10 ? 170 : P == 12 ? 156 : P * S;
 };
 
+#ifndef FDM_MIN_BLOCKS
+#define FDM_MIN_BLOCKS 8
+#endif
 template <int NP>
 struct FdmShape {
   static constexpr int kP = NP + 2;
@@ -39,6 +42,7 @@ struct FdmShape {
   static constexpr int kS = FdmLayout<kP>::S;
   static constexpr int kPS = FdmLayout<kP>::PS;
   static constexpr int kBuf = kP * kPS;
+  static constexpr int kMinBlocks = FDM_MIN_BLOCKS;  // resident CTAs per SM the register budget is sized for
 };
 
 struct FdmArgs {
@@ -133,7 +137,7 @@ __device__ __forceinline__ void pencil_inv_eo(const double* __restrict__ IE, con
 }
 
 template <int NP, bool EO>
-__global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_kernel(FdmArgs a)
+__global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks) fdm_kernel(FdmArgs a)
 {
   using Sh = FdmShape<NP>;
   constexpr int P = Sh::kP, S = Sh::kS, PS = Sh::kPS, n = NP - 1;

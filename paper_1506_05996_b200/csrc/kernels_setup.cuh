@@ -1,0 +1,88 @@
+// Device-side setup: the geometric factors of the stored
+// operator, compute_factors (geometry.cpp:105-151) + the kappa*mass scaling
+// of the SemOperator constructor (operator.cpp:76-88), one thread per local
+// node. Every operation is an explicitly rounded IEEE intrinsic in the
+// reference's evaluation order (its Release build has no FMA contraction),
+// so the planes and the mass are bit-identical to the host restatement and
+// to the reference, while taking milliseconds instead of seconds.
+#pragma once
+
+#include "kernels_common.cuh"
+
+namespace hxb {
+
+struct GeoArgs {
+  double hat0[kMaxNP], hat1[kMaxNP], w[kMaxNP];  // 0.5(1 -+ t_i) and GLL weights, host-computed
+  const double* xyz;                             // nv*3
+  const int* conn;                               // ne*8, Gmsh corner order
+  const double* kappa;                           // ne
+  double* mass;                                  // [ne][nloc] (all elements)
+  double* wg;                                    // [e - e0][6][nlocp] for e in [e0, e0 + nel), or null
+  int ne, e0, nel, nlocp;
+  int* bad;                                      // min inverted element (init INT_MAX)
+};
+
+template <int NP>
+__global__ void __launch_bounds__(256) geometry_kernel(const __grid_constant__ GeoArgs a)
+{
+  constexpr int NL = NP * NP * NP;
+  constexpr int kSlot[8] = {0, 1, 3, 2, 4, 5, 7, 6};  // corner bits (bi,bj,bk) -> connectivity slot (mesh.hpp:31-33)
+  const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<long long>(a.ne) * NL) return;
+  const int e = static_cast<int>(t / NL), node = static_cast<int>(t % NL);
+  const int i = node % NP, j = (node / NP) % NP, k = node / (NP * NP);
+  const double h[3][2] = {{a.hat0[i], a.hat1[i]}, {a.hat0[j], a.hat1[j]}, {a.hat0[k], a.hat1[k]}};
+  const double dh[2] = {-0.5, 0.5};
+  double J[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int bk = 0; bk < 2; ++bk)  // jacobian (geometry.cpp:43-64)
+    for (int bj = 0; bj < 2; ++bj)
+      for (int bi = 0; bi < 2; ++bi) {
+        const int v = __ldg(a.conn + 8LL * e + kSlot[bi + 2 * bj + 4 * bk]);
+        const double wx = __dmul_rn(__dmul_rn(dh[bi], h[1][bj]), h[2][bk]);
+        const double wy = __dmul_rn(__dmul_rn(h[0][bi], dh[bj]), h[2][bk]);
+        const double wz = __dmul_rn(__dmul_rn(h[0][bi], h[1][bj]), dh[bk]);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double x = __ldg(a.xyz + 3LL * v + d);
+          J[d * 3 + 0] = __dadd_rn(J[d * 3 + 0], __dmul_rn(wx, x));
+          J[d * 3 + 1] = __dadd_rn(J[d * 3 + 1], __dmul_rn(wy, x));
+          J[d * 3 + 2] = __dadd_rn(J[d * 3 + 2], __dmul_rn(wz, x));
+        }
+      }
+  auto cof = [](double p, double q, double r, double s) { return __dsub_rn(__dmul_rn(p, q), __dmul_rn(r, s)); };
+  const double det = __dadd_rn(__dsub_rn(__dmul_rn(J[0], cof(J[4], J[8], J[5], J[7])),
+                                         __dmul_rn(J[1], cof(J[3], J[8], J[5], J[6]))),
+                               __dmul_rn(J[2], cof(J[3], J[7], J[4], J[6])));
+  if (!(det > 0)) {
+    atomicMin(a.bad, e);
+    return;
+  }
+  double inv[9];  // compute_factors (geometry.cpp:122-131)
+  inv[0] = __ddiv_rn(cof(J[4], J[8], J[5], J[7]), det);
+  inv[1] = __ddiv_rn(cof(J[2], J[7], J[1], J[8]), det);
+  inv[2] = __ddiv_rn(cof(J[1], J[5], J[2], J[4]), det);
+  inv[3] = __ddiv_rn(cof(J[5], J[6], J[3], J[8]), det);
+  inv[4] = __ddiv_rn(cof(J[0], J[8], J[2], J[6]), det);
+  inv[5] = __ddiv_rn(cof(J[2], J[3], J[0], J[5]), det);
+  inv[6] = __ddiv_rn(cof(J[3], J[7], J[4], J[6]), det);
+  inv[7] = __ddiv_rn(cof(J[1], J[6], J[0], J[7]), det);
+  inv[8] = __ddiv_rn(cof(J[0], J[4], J[1], J[3]), det);
+  const double m = __dmul_rn(__dmul_rn(__dmul_rn(a.w[i], a.w[j]), a.w[k]), det);
+  a.mass[static_cast<long long>(e) * NL + node] = m;
+  if (a.wg && e >= a.e0 && e < a.e0 + a.nel) {
+    auto gt = [&](int r, int c) {
+      return __dadd_rn(__dadd_rn(__dmul_rn(inv[r * 3], inv[c * 3]), __dmul_rn(inv[r * 3 + 1], inv[c * 3 + 1])),
+                       __dmul_rn(inv[r * 3 + 2], inv[c * 3 + 2]));
+    };
+    const double scale = __dmul_rn(__ldg(a.kappa + e), m);  // operator.cpp:83-87
+    double* o = a.wg + static_cast<long long>(e - a.e0) * 6 * a.nlocp + node;
+    o[0] = __dmul_rn(gt(0, 0), scale);
+    o[a.nlocp] = __dmul_rn(gt(0, 1), scale);
+    o[2 * a.nlocp] = __dmul_rn(gt(0, 2), scale);
+    o[3 * a.nlocp] = __dmul_rn(gt(1, 1), scale);
+    o[4 * a.nlocp] = __dmul_rn(gt(1, 2), scale);
+    o[5 * a.nlocp] = __dmul_rn(gt(2, 2), scale);
+  }
+}
+
+}  // namespace hxb

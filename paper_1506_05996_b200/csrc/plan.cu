@@ -22,6 +22,7 @@
 #include "kernels_amg.cuh"
 #include "kernels_ax.cuh"
 #include "kernels_coarse.cuh"
+#include "kernels_setup.cuh"
 #include "kernels_common.cuh"
 #include "kernels_fine.cuh"
 #include "kernels_gather.cuh"
@@ -1023,9 +1024,68 @@ void build_dist_ax(Plan& pl, const HostSetup& hs, int /*nsurf_raw*/)
   pl.n_ax_entries = d.off[pl.n_loc_surf];
 }
 
+template <int NP>
+void launch_geometry(const GeoArgs& a, long long n, cudaStream_t s)
+{
+  geometry_kernel<NP><<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(a);
+}
+
+// compute_factors + kappa*mass scaling on the device: the
+// stored planes go straight into their [e][6][nlocp] TMA layout, the mass is
+// kept on the device and copied back once for the host-side consumers
+// (lumped mass, coarse/prolongation lists).
+void device_geometry(Plan& pl, HostSetup& hs, const hxb_options& opt)
+{
+  const int np = hs.basis.npts(), nloc = np * np * np, ne = hs.mesh.num_elements();
+  const int nranks = std::max(1, opt.reserved[2]), rank = opt.reserved[2] > 1 ? opt.reserved[1] : 0;
+  const int e0 = static_cast<int>(static_cast<long long>(ne) * rank / nranks);
+  const int e1 = static_cast<int>(static_cast<long long>(ne) * (rank + 1) / nranks);
+  GeoArgs a{};
+  for (int i = 0; i < np; ++i) {
+    a.hat0[i] = 0.5 * (1 - hs.basis.nodes[i]);  // the jacobian's h (geometry.cpp:47-49)
+    a.hat1[i] = 0.5 * (1 + hs.basis.nodes[i]);
+    a.w[i] = hs.basis.weights[i];
+  }
+  std::vector<double> xyz(3 * static_cast<std::size_t>(hs.mesh.num_vertices()));
+  for (std::size_t v = 0; v < hs.mesh.vertices.size(); ++v)
+    for (int d = 0; d < 3; ++d) xyz[3 * v + d] = hs.mesh.vertices[v][d];
+  std::vector<int> conn(8 * static_cast<std::size_t>(ne));
+  for (int e = 0; e < ne; ++e)
+    for (int q = 0; q < 8; ++q) conn[8 * static_cast<std::size_t>(e) + q] = hs.mesh.elements[e][q];
+  DeviceArena tmp;
+  a.xyz = tmp.upload(xyz);
+  a.conn = tmp.upload(conn);
+  a.kappa = tmp.upload(hs.kappa);
+  a.ne = ne;
+  a.e0 = e0;
+  a.nel = e1 - e0;
+  a.nlocp = (nloc + 1) & ~1;
+  double* mass = (nranks == 1 ? pl.mem : tmp).alloc<double>(static_cast<std::size_t>(ne) * nloc);
+  a.mass = mass;
+  a.wg = opt.variant == HXB_VARIANT_STORED ? pl.mem.alloc<double>(static_cast<std::size_t>(e1 - e0) * 6 * a.nlocp)
+                                           : nullptr;
+  if (a.wg) HXB_CUDA(cudaMemset(a.wg, 0, static_cast<std::size_t>(e1 - e0) * 6 * a.nlocp * sizeof(double)));
+  int* bad = tmp.alloc<int>(1);
+  const int big = 0x7fffffff;
+  HXB_CUDA(cudaMemcpy(bad, &big, sizeof(int), cudaMemcpyHostToDevice));
+  a.bad = bad;
+  HXB_DISPATCH_NP(np, launch_geometry, a, static_cast<long long>(ne) * nloc, cudaStream_t{});
+  HXB_CUDA(cudaGetLastError());
+  int first_bad = big;
+  HXB_CUDA(cudaMemcpy(&first_bad, bad, sizeof(int), cudaMemcpyDeviceToHost));
+  if (first_bad != big)
+    throw HxbError(HXB_EMESH, "inverted element " + std::to_string(first_bad) +
+                                  ": non-positive Jacobian determinant at a GLL node");
+  hs.geo.mass.resize(static_cast<std::size_t>(ne) * nloc);
+  HXB_CUDA(cudaMemcpy(hs.geo.mass.data(), mass, hs.geo.mass.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  pl.wg = a.wg;
+  pl.mass = nranks == 1 ? mass : nullptr;
+}
+
 void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, const double* c_e, const hxb_options& opt)
 {
   const auto t0 = std::chrono::steady_clock::now();
+  setup_phase("device init");
   if (!m) throw HxbError(HXB_EINVAL, "mesh must be non-null");
   if (opt.variant != HXB_VARIANT_STORED && opt.variant != HXB_VARIANT_ON_THE_FLY)
     throw HxbError(HXB_EINVAL, "unknown operator variant");
@@ -1049,7 +1109,10 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   so.coarse_solve = opt.coarse_solve;
   so.direct_threshold = opt.direct_threshold;
   so.store_planes = opt.variant == HXB_VARIANT_STORED;
+  so.geometry_hook = [&pl, &opt](HostSetup& h) { device_geometry(pl, h, opt); };
+  setup_phase("mesh + checks");
   build_host_setup(hs, order, so);
+  setup_phase("device: streams, tables");
   const HexMesh& mesh = hs.mesh;
   const Numbering& num = hs.num;
 
@@ -1098,6 +1161,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
 
   DeviceArena& M = pl.mem;
   const int e0 = pl.e0, nel = pl.ne;  // owned elements [e0, e0 + nel)
+  setup_phase("upload geometry");
   if (pl.variant == HXB_VARIANT_ON_THE_FLY) {  // element records: corners in (bi,bj,bk)-bit order, kappa
     constexpr int RD = 26;
     std::vector<double> rec(static_cast<std::size_t>(nel) * RD, 0.0);
@@ -1110,7 +1174,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
       q[24] = hs.kappa[e0 + le];
     }
     pl.erec = M.upload(rec);
-  } else {  // kappa*m*Gt planes regrouped per element: [e][6][nlocp] (one TMA stream per element)
+  } else if (!pl.wg) {  // host planes regrouped per element: [e][6][nlocp] (one TMA stream per element)
     const int nlocp = (pl.nloc + 1) & ~1;
     const std::size_t total = static_cast<std::size_t>(ne) * pl.nloc;
     std::vector<double> wge(static_cast<std::size_t>(nel) * 6 * nlocp, 0.0);
@@ -1126,7 +1190,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     return std::vector<double>(v.begin() + static_cast<std::size_t>(e0) * per,
                                v.begin() + static_cast<std::size_t>(e0 + nel) * per);
   };
-  pl.mass = M.upload(pl.nranks > 1 ? slice(hs.geo.mass, pl.nloc) : hs.geo.mass);
+  if (!pl.mass) pl.mass = M.upload(pl.nranks > 1 ? slice(hs.geo.mass, pl.nloc) : hs.geo.mass);
   pl.c_e = M.upload(pl.nranks > 1 ? slice(hs.c, 1) : hs.c);
   pl.kappa_e = M.upload(pl.nranks > 1 ? slice(hs.kappa, 1) : hs.kappa);
   pl.h3 = M.upload(pl.nranks > 1 ? slice(hs.geo.h, 3) : hs.geo.h);
@@ -1140,6 +1204,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.d_inv_lumped = M.upload(inv);
   }
 
+  setup_phase("surface map + Ax CSR");
   // surface map [e][2][nsurf]: Dirichlet-encoded global ids and each copy's
   // position in the Ax surface CSR (copies of a node in ascending (e,l) order,
   // mesh.cpp:358-367) - producers write there, gathers stream contiguously
@@ -1183,6 +1248,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   }
   pl.rsurf = M.alloc<double>(static_cast<std::size_t>(pl.ne) * pl.nsurf);
 
+  setup_phase("fine lists");
   // fine: encoded sub_face and the subdomain gather CSR in (e, slot) order
   if (pl.do_fine) {
     const int nf = 6 * pl.np * pl.np, nfp = (nf + 3) & ~3;  // rows padded for 16-byte TMA copies
@@ -1259,6 +1325,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     }
   }
 
+  setup_phase("coarse device");
   // coarse: connectivity, vertex incidence CSR (e, cb) order, coarse matrix, AMG / dense
   if (pl.do_coarse) {
     std::vector<int> conn(static_cast<std::size_t>(ne) * 8);
@@ -1318,6 +1385,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     }
   }
 
+  setup_phase("vectors + graph");
   // PCG vectors and reduction scratch
   for (double** v : {&pl.u, &pl.r, &pl.z, &pl.p, &pl.f, &pl.b}) {
     *v = M.alloc<double>(pl.N);
@@ -1335,6 +1403,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   HXB_CUDA(cudaMallocHost(&pl.h_status, 64 * sizeof(double)));
   if (pl.do_coarse) capture_coarse_graph(pl);
   HXB_CUDA(cudaDeviceSynchronize());
+  setup_phase(nullptr);
   pl.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
@@ -1798,6 +1867,23 @@ int hxb_lumped_mass(hxb_plan* plan, double* m)
   return guarded([&] {
     Plan* pl = as_plan(plan);
     std::memcpy(m, pl->hs.lumped.data(), sizeof(double) * pl->N);
+  });
+}
+
+int hxb_export_geometry(hxb_plan* plan, double* mass, double* wg)
+{
+  return guarded([&] {
+    Plan* pl = as_plan(plan);
+    const std::size_t nloc = pl->nloc, nlocp = (nloc + 1) & ~std::size_t{1}, nel = pl->ne;
+    if (mass) HXB_CUDA(cudaMemcpy(mass, pl->mass, nel * nloc * sizeof(double), cudaMemcpyDeviceToHost));
+    if (wg) {
+      if (!pl->wg) throw HxbError(HXB_EINVAL, "plan holds no stored planes (on-the-fly variant)");
+      std::vector<double> blk(nel * 6 * nlocp);
+      HXB_CUDA(cudaMemcpy(blk.data(), pl->wg, blk.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      for (std::size_t e = 0; e < nel; ++e)
+        for (int p = 0; p < 6; ++p)
+          std::memcpy(wg + p * nel * nloc + e * nloc, &blk[(e * 6 + p) * nlocp], nloc * sizeof(double));
+    }
   });
 }
 

@@ -12,6 +12,7 @@
 #include <array>
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -110,6 +111,7 @@ struct Geometry {
 };
 Geometry compute_geometry(const HexMesh& mesh, const GllBasis& basis, const std::vector<double>& kappa,
                           bool store_planes);
+std::vector<double> element_dimensions_all(const HexMesh& mesh);  // NE*3
 
 struct Pencil {  // fine.hpp:18-26
   int p = 0;
@@ -163,6 +165,9 @@ struct DenseCoarse {
 };
 DenseCoarse dense_coarse_setup(const Csr& A, int host_inverse_limit);
 
+// Setup phase timer: HXB_SETUP_TIMING=1 prints each phase's wall time to stderr.
+void setup_phase(const char* name);  // closes the running phase, opens `name` (nullptr: close and print)
+
 struct HxbError : std::runtime_error {
   int code;
   HxbError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
@@ -176,11 +181,15 @@ namespace hxb {
 // (build_system, problem.cpp:73-108, minus the GPU upload). Separate from the
 // device plan so the bit-exact parts (numbering, aggregation) are testable
 // without a GPU.
+struct HostSetup;
 struct SetupOptions {
   int precond_mode = 0;         // PrecondMode
   int coarse_solve = 0;         // CoarseSolve
   gid direct_threshold = 64000; // coarse.hpp:36
   bool store_planes = true;     // false for the on-the-fly operator variant (no kappa*m*Gt planes)
+  // when set, replaces the host per-node geometry: must fill hs.geo.mass (all
+  // elements); hs.geo.h is computed on the host either way (device plans)
+  std::function<void(HostSetup&)> geometry_hook;
 };
 
 struct HostSetup {

@@ -403,6 +403,16 @@ void check_jacobians(const HexMesh& mesh)
           (void)jacobian(mesh, e, static_cast<double>(i), static_cast<double>(j), static_cast<double>(k));
 }
 
+std::vector<double> element_dimensions_all(const HexMesh& mesh)
+{
+  std::vector<double> h(static_cast<std::size_t>(mesh.num_elements()) * 3);
+  for (gid e = 0; e < mesh.num_elements(); ++e) {
+    const auto hh = element_dimensions(mesh, e);
+    for (int d = 0; d < 3; ++d) h[3 * static_cast<std::size_t>(e) + d] = hh[d];
+  }
+  return h;
+}
+
 Geometry compute_geometry(const HexMesh& mesh, const GllBasis& basis, const std::vector<double>& kappa,
                           bool store_planes)
 {

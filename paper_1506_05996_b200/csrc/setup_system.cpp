@@ -1,5 +1,8 @@
 // Host setup driver: the B200 plan's counterpart of build_system
 // (problem.cpp:73-108) up to, but excluding, the device upload.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "setup.hpp"
@@ -27,6 +30,23 @@ HexMesh mesh_from_arrays(int nv, const double* xyz, int ne, const std::int32_t* 
   return mesh;
 }
 
+void setup_phase(const char* name)
+{
+  static const bool on = [] {
+    const char* v = std::getenv("HXB_SETUP_TIMING");
+    return v && *v && *v != '0';
+  }();
+  if (!on) return;
+  using clk = std::chrono::steady_clock;
+  static thread_local clk::time_point t0;
+  static thread_local std::string cur;
+  const auto now = clk::now();
+  if (!cur.empty())
+    std::fprintf(stderr, "[hxb setup] %-28s %8.3f s\n", cur.c_str(), std::chrono::duration<double>(now - t0).count());
+  cur = name ? name : "";
+  t0 = now;
+}
+
 void build_host_setup(HostSetup& hs, int order, const SetupOptions& opt)
 {
   if (order < 1 || order > 10) throw HxbError(1, "order must lie in 1..10");
@@ -46,8 +66,17 @@ void build_host_setup(HostSetup& hs, int order, const SetupOptions& opt)
       if (!(hs.kappa[e] > 0)) throw HxbError(1, "need kappa > 0, c >= 0");
 
   hs.basis = make_gll_basis(order);
-  hs.geo = compute_geometry(hs.mesh, hs.basis, hs.kappa, opt.store_planes);  // throws on inverted elements
+  setup_phase("geometry");
+  if (opt.geometry_hook) {  // device plans: factors computed on the GPU (kernels_setup.cuh)
+    hs.geo = Geometry{};
+    hs.geo.h = element_dimensions_all(hs.mesh);
+    opt.geometry_hook(hs);
+  } else {
+    hs.geo = compute_geometry(hs.mesh, hs.basis, hs.kappa, opt.store_planes);  // throws on inverted elements
+  }
+  setup_phase("numbering");
   hs.num = build_numbering(hs.mesh, order);
+  setup_phase("lumped mass");
   const int nloc = hs.basis.npts() * hs.basis.npts() * hs.basis.npts();
   hs.lumped.assign(hs.num.num_global, 0.0);
   std::vector<gid> l2g(nloc);
@@ -57,11 +86,14 @@ void build_host_setup(HostSetup& hs, int order, const SetupOptions& opt)
   }
   hs.pencil = build_pencil(hs.basis);
   if (hs.do_coarse) {
+    setup_phase("coarse matrix");
     hs.vmask = coarse_dirichlet_mask(hs.mesh);
     hs.Kc = assemble_coarse_matrix(hs.mesh, hs.kappa, hs.c, hs.vmask);
     hs.use_amg = opt.coarse_solve == 2 || (opt.coarse_solve == 0 && hs.Kc.n > opt.direct_threshold);
+    setup_phase("amg setup");
     if (hs.use_amg) hs.amg = amg_setup(hs.Kc);
   }
+  setup_phase("after host setup");
 }
 
 void export_index_maps(const HostSetup& hs, std::int32_t* l2g, std::int64_t* g2l_offsets, std::int32_t* g2l_elem,

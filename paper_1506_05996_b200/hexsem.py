@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhexsem_b200.so")
+LIB_PATH = os.environ.get("HXB_LIB") or os.path.join(_HERE, "libhexsem_b200.so")  # HXB_LIB: A/B builds
 
 FAMILIES = {"uniform": 0, "distorted_domain": 1, "distorted_elements": 2}
 PRECONDS = {"two_scale": 0, "fine_only": 1, "coarse_only": 2, "none": 3}
@@ -110,6 +110,7 @@ SIGNATURES = {
                                  C.POINTER(C.c_int), C.POINTER(C.c_int), P, C.POINTER(C.c_double)]),
     "hxb_node_coords": (C.c_int, [P, P]),
     "hxb_lumped_mass": (C.c_int, [P, P]),
+    "hxb_export_geometry": (C.c_int, [P, P, P]),
     "hxb_export_maps": (C.c_int, [P, P, P, P, P, P, P]),
     "hxb_amg_level": (C.c_int, [P, C.c_int, P, P, P, P, P, P]),
     "hxb_bench_apply_A": (C.c_int, [P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
@@ -138,6 +139,7 @@ SIGNATURES = {
     "hxb_setup_export_maps": (C.c_int, [P, P, P, P, P, P, P]),
     "hxb_setup_amg_level": (C.c_int, [P, C.c_int, P, P, P, P, P, P]),
     "hxb_setup_lumped_mass": (C.c_int, [P, P]),
+    "hxb_setup_export_geometry": (C.c_int, [P, P, P]),
     "hxb_setup_dist_lists": (C.c_int, [P, C.c_int, C.c_int, P, P]),
     "hxb_gll": (C.c_int, [C.c_int, P, P, P]),
     "hxb_pencil": (C.c_int, [C.c_int, P, P, P, P, P]),
@@ -476,6 +478,15 @@ class Plan:
         _check(lib().hxb_lumped_mass(self._h, _ptr(m)))
         return m
 
+    def geometry(self, planes: bool = True) -> dict:
+        """Device-computed factors of this plan's elements: mass (NE, nloc) and
+        the six kappa*m*Gt planes (6, NE, nloc) (compute_factors, geometry.cpp:105-151)."""
+        nloc = (self.order + 1) ** 3
+        mass = np.empty(self.NE * nloc)
+        wg = np.empty(6 * self.NE * nloc) if planes else None
+        _check(lib().hxb_export_geometry(self._h, _ptr(mass), _ptr(wg)))
+        return {"mass": mass.reshape(self.NE, nloc), "wg": None if wg is None else wg.reshape(6, self.NE, nloc)}
+
     def maps(self, sub: bool = True) -> dict:
         n = self.order
         nloc, nsub = (n + 1) ** 3, (n + 3) ** 3
@@ -646,6 +657,13 @@ class HostSetup:
         m = np.empty(self.N)
         _check(lib().hxb_setup_lumped_mass(self._h, _ptr(m)))
         return m
+
+    def geometry(self) -> dict:
+        """Host restatement of compute_factors + kappa*mass scaling (setup_mesh.cpp)."""
+        nloc = (self.order + 1) ** 3
+        mass, wg = np.empty(self.NE * nloc), np.empty(6 * self.NE * nloc)
+        _check(lib().hxb_setup_export_geometry(self._h, _ptr(mass), _ptr(wg)))
+        return {"mass": mass.reshape(self.NE, nloc), "wg": wg.reshape(6, self.NE, nloc)}
 
     def dist_lists(self, rank: int, nranks: int) -> dict:
         """Element-slab partition lists of one rank (hxb_setup_dist_lists)."""

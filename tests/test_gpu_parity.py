@@ -100,6 +100,32 @@ def test_pcg_on_the_fly_matches_reference(family):
     history_parity(plan.pcg(b, tol=1e-8), theirs, tol=max(1e-10, 10 * noise))
 
 
+@pytest.mark.parametrize("k,order,family", [(3, 1, "distorted_elements"), (4, 4, "distorted_domain"),
+                                             (3, 7, "distorted_elements"), (2, 10, "uniform")])
+def test_device_geometry_bit_exact(k, order, family):
+    """GPU setup of the geometric factors (kernels_setup.cuh) equals the host
+    restatement of compute_factors bit for bit (which itself equals the
+    reference's, test_host_setup.py), with per-element kappa; and so does the
+    lumped mass built from it."""
+    mesh = hx.generate_cube_mesh(k, family)
+    ne = mesh.num_elements
+    kap = 0.5 + np.arange(ne) / ne
+    plan = hx.Plan(mesh, order, kap, np.zeros(ne), precond="none")
+    hs = hx.HostSetup(mesh, order, kap, np.zeros(ne), precond="none")
+    a, b = plan.geometry(), hs.geometry()
+    assert np.array_equal(a["mass"], b["mass"])
+    assert np.array_equal(a["wg"], b["wg"])
+    assert np.array_equal(plan.lumped_mass(), hs.lumped_mass())
+
+
+def test_device_geometry_rejects_inverted_element():
+    mesh = hx.generate_cube_mesh(2)
+    mesh.conn[3] = mesh.conn[3][[1, 0, 2, 3, 5, 4, 6, 7]]  # mirrored: det J < 0 everywhere
+    with pytest.raises(hx.HxbError) as ei:
+        hx.Plan(mesh, 3, precond="none")
+    assert ei.value.code == 2 and "inverted element 3" in str(ei.value)
+
+
 @pytest.mark.parametrize("precond", ["two_scale", "fine_only", "coarse_only", "none"])
 def test_apply_P_matches_reference(precond):
     ref, plan = _pair(k=8, order=4, precond=precond)
