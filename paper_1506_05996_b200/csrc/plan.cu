@@ -308,10 +308,13 @@ DotArgs cdot_args(Plan& pl, double* result)
   return d;
 }
 
+#ifndef AX_SMALL_MAX_NP
+#define AX_SMALL_MAX_NP 3  // thread-per-node Ax kernel up to this np (tile kernel above)
+#endif
 template <int NP, bool OTF>
 int ax_persistent_grid_v(const Plan& pl)
 {
-  if constexpr (NP <= 3) {  // thread-per-node kernel for the low orders
+  if constexpr (NP <= AX_SMALL_MAX_NP) {  // thread-per-node kernel for the low orders
     int per_sm = 0;
     HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ax_small_kernel<NP, OTF>, AxSmall<NP>::kBlock, 0));
     per_sm = std::max(per_sm, 1);
@@ -337,7 +340,7 @@ int ax_persistent_grid(const Plan& pl)
 template <int NP, bool OTF>
 void launch_ax_kernel(const Plan& pl, const AxArgs& a, int grid, cudaStream_t s)
 {
-  if constexpr (NP <= 3)
+  if constexpr (NP <= AX_SMALL_MAX_NP)
     ax_small_kernel<NP, OTF><<<grid, AxSmall<NP>::kBlock, 0, s>>>(a);
   else
     ax_elem_kernel<NP, OTF><<<grid, AxShape<NP>::kBlock, OTF ? AxShape<NP>::kSmemOtfBytes : AxShape<NP>::kSmemBytes,
@@ -390,8 +393,11 @@ void launch_ax_elem_range(Plan& pl, const double* u, double* r, int e_begin, int
   a.e_begin = e_begin;
   a.num_surface_global = pl.nsg;
   a.dot = DotArgs{};
-  const int grid = NP <= 3 ? std::max(1, std::min(pl.ax_grid, (e_end - e_begin + AxSmall<NP>::kEPB - 1) / AxSmall<NP>::kEPB))
-                           : std::max(1, std::min(pl.ax_grid, e_end - e_begin));
+  int grid;
+  if constexpr (NP <= AX_SMALL_MAX_NP)
+    grid = std::max(1, std::min(pl.ax_grid, (e_end - e_begin + AxSmall<NP>::kEPB - 1) / AxSmall<NP>::kEPB));
+  else
+    grid = std::max(1, std::min(pl.ax_grid, e_end - e_begin));
   launch_ax_kernel<NP>(pl, a, grid, s);
 }
 
