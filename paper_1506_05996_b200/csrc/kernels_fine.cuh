@@ -25,6 +25,33 @@
 
 namespace hxb {
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
+{
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem)
+{
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
+{
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// stage n ints (16-byte aligned source and destination when n4) with the CTA's threads
+template <bool V16>
+__device__ __forceinline__ void stage_ints(int* dst, const int* src, int n, int tid, int nthreads)
+{
+  if constexpr (V16) {
+    for (int q = tid; q < n / 4; q += nthreads) cp_async16(dst + 4 * q, src + 4 * q);
+  } else {
+    for (int q = tid; q < n; q += nthreads) cp_async4(dst + q, src + q);
+  }
+}
+
 template <int P>
 struct FdmLayout {  // (row stride S, plane stride PS) per pencil size
   static constexpr int S = P == 6 ? 9 : P == 8 ? 9 : P == 10 ? 17 : P == 12 ? 13 : P;
@@ -181,30 +208,43 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
     s_h0[q] = T.hat0[q];
     s_h1[q] = T.hat1[q];
   }
+  // the element's surface codes and face-neighbour ids (needed first) and its
+  // output positions (needed last) are staged by coalesced cp.async copies
+  constexpr int NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2), NSP = (NS + 3) & ~3;
+  constexpr int NF = (6 * NP * NP + 3) & ~3, P3 = P * P * P;
+  __shared__ __align__(16) int s_code[NSP];
+  __shared__ __align__(16) int s_sf[NF];
+  __shared__ __align__(16) int s_pos[(P3 + 3) & ~3];
+  stage_ints<true>(s_code, a.smap + (long long)e * a.sstride, NSP, tid, Sh::kBlock);
+  stage_ints<true>(s_sf, a.sub_face + (long long)e * a.sfstride, NF, tid, Sh::kBlock);
+  cp_async_commit();
+  stage_ints<(P3 % 4) == 0>(s_pos, a.pos + (long long)e * P3, P3, tid, Sh::kBlock);
+  cp_async_commit();
   const double hx = __ldg(a.h3 + 3 * e), hy = __ldg(a.h3 + 3 * e + 1), hz = __ldg(a.h3 + 3 * e + 2);
   const double svol = 8.0 / (hx * hy * hz);  // fine.cpp:154
   double in[P], out[P];
   double racc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cp_async_wait_1();
   __syncthreads();
 
   // ---- 1: gather + r' scaling + V along x (thread = x-line (y=la, z=lb)) -------
   if (lt) {
     const int y = la, z = lb, jj = y - 1, kk = z - 1;
     const bool iny = jj >= 0 && jj <= n, inz = kk >= 0 && kk <= n;
-    const int* surf = a.smap + (long long)e * a.sstride;
-    const int* sf = a.sub_face + (long long)e * a.sfstride;
+    const int* surf = s_code;
+    const int* sf = s_sf;
     const long long ibase = (long long)a.num_surface_global + (long long)e * (n - 1) * (n - 1) * (n - 1);
 #pragma unroll
     for (int x = 0; x < P; ++x) in[x] = 0.0;
     if (iny && inz) {
-      in[0] = load_masked(a.r, __ldg(sf + (0 * NP + kk) * NP + jj));      // face 0 slot (u=jj, w=kk)
-      in[P - 1] = load_masked(a.r, __ldg(sf + (1 * NP + kk) * NP + jj));  // face 1 slot
+      in[0] = load_masked(a.r, sf[(0 * NP + kk) * NP + jj]);      // face 0 slot (u=jj, w=kk)
+      in[P - 1] = load_masked(a.r, sf[(1 * NP + kk) * NP + jj]);  // face 1 slot
       int gl[NP];  // own-node ids of this x-line (-1: Dirichlet, reads as 0)
 #pragma unroll
       for (int ii = 0; ii <= n; ++ii) {
         const int s = surface_slot(NP, ii, jj, kk);
         if (s >= 0) {
-          const int code = __ldg(surf + s);
+          const int code = surf[s];
           gl[ii] = code >= 0 ? code : -1;
         } else {
           gl[ii] = static_cast<int>(ibase + ((kk - 1) * (n - 1) + (jj - 1)) * (n - 1) + (ii - 1));
@@ -236,11 +276,11 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
     } else if (inz && (y == 0 || y == P - 1)) {  // faces 2/3: u=kk, w=ii
       const int f = y == 0 ? 2 : 3;
 #pragma unroll
-      for (int ii = 0; ii <= n; ++ii) in[ii + 1] = load_masked(a.r, __ldg(sf + (f * NP + ii) * NP + kk));
+      for (int ii = 0; ii <= n; ++ii) in[ii + 1] = load_masked(a.r, sf[(f * NP + ii) * NP + kk]);
     } else if (iny && (z == 0 || z == P - 1)) {  // faces 4/5: u=ii, w=jj
       const int f = z == 0 ? 4 : 5;
 #pragma unroll
-      for (int ii = 0; ii <= n; ++ii) in[ii + 1] = load_masked(a.r, __ldg(sf + (f * NP + jj) * NP + ii));
+      for (int ii = 0; ii <= n; ++ii) in[ii + 1] = load_masked(a.r, sf[(f * NP + jj) * NP + ii]);
     }
     // r' = 8/(hx hy hz) r / (M_i M_j M_k) (fine.cpp:161-166), as products of reciprocals
     const double syz = svol * s_invM[y] * s_invM[z];
@@ -300,6 +340,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
 #pragma unroll
     for (int y = 0; y < P; ++y) buf[at(la, y, lb)] = out[y];
   }
+  cp_async_wait_all();  // output positions staged
   __syncthreads();
 
   // ---- 5: V^-1 along x, store --------------------------------------------------
@@ -307,10 +348,10 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
 #pragma unroll
     for (int x = 0; x < P; ++x) in[x] = buf[at(x, la, lb)];
     inv(in, out);
-    const int* ps = a.pos + (long long)e * P * P * P + (lb * P + la) * P;
+    const int* ps = s_pos + (lb * P + la) * P;
 #pragma unroll
     for (int x = 0; x < P; ++x) {
-      const int q = __ldg(ps + x);
+      const int q = ps[x];
       if (q >= 0)
         a.zsort[q] = out[x];
       else if (q <= -2)  // finalised by a neighbour rank (distributed plans)
@@ -341,12 +382,6 @@ struct FdmPipe {
       ((std::size_t)NSUB + NLOC + kBufE) * sizeof(double) + kIdxInts * sizeof(int) + 16;
 };
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem)
-{
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 template <int NP>
 __global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_pipe_kernel(FdmArgs a)
