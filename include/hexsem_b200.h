@@ -80,8 +80,9 @@ typedef struct hxb_options {
   int32_t direct_threshold;    /* vertices; default 64000 (coarse.hpp:36) */
   int variant;                 /* HXB_VARIANT_* (default stored) */
   int device;                  /* CUDA device ordinal for this plan */
-  int reserved[7];             /* reserved[0] bit 0: run the AMG K-cycle as one kernel per step
-                                  instead of the default single cluster kernel; bit 2: persistent
+  int reserved[7];             /* reserved[0] bit 0: run AMG levels >= 1 as one 16-CTA cluster
+                                  kernel instead of the default kernel per step (measured slower
+                                  inside the PCG at cfg2: 1.45 vs 0.82 ms per coarse solve); bit 2: persistent
                                   TMA/cp.async-pipelined FDM kernel instead of one CTA per
                                   subdomain (measured slower at cfg2, kept for A/B checks);
                                   bit 3: one fused combine after the coarse solve instead of
@@ -301,7 +302,8 @@ int hxb_dist_combine(hxb_plan* plan, const double* d_r, double* d_z, double* d_z
  * max_launches launches). _read sums the durations of one tag. The reference
  * equivalent is the wall-clock counter of SemOperator::apply
  * (operator.cpp:262,285-286), per kernel instead of per apply. */
-enum { HXB_KT_AX_ELEM = 0, HXB_KT_AX_GATHER = 1, HXB_KT_FDM = 2, HXB_KT_COMBINE = 3 };
+enum { HXB_KT_AX_ELEM = 0, HXB_KT_AX_GATHER = 1, HXB_KT_FDM = 2, HXB_KT_COMBINE = 3, HXB_KT_COARSE = 4,
+       HXB_KT_COMBINE_FINE = 5 };
 int hxb_kernel_timing(hxb_plan* plan, int enable, int max_launches);
 int hxb_kernel_timing_read(hxb_plan* plan, int tag, double* total_ms, int* count);
 /* Kernels the plan has enqueued since creation (coarse-graph nodes counted per launch). */

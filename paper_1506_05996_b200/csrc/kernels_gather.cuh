@@ -316,8 +316,7 @@ __global__ void __launch_bounds__(kGatherBlock) combine_fine_kernel(const double
                                                                     const int* __restrict__ surf_nodes, int nsg,
                                                                     int ibase, int n_items, double* __restrict__ z)
 {
-  const int it = blockIdx.x * blockDim.x + threadIdx.x;
-  if (it >= n_items) return;
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += gridDim.x * blockDim.x) {
   const int g = it < nsg ? (surf_nodes ? __ldg(surf_nodes + it) : it) : ibase + (it - nsg);
   const unsigned q0 = __ldg(fine_off + it), q1 = __ldg(fine_off + it + 1);
   double v[8];
@@ -329,6 +328,7 @@ __global__ void __launch_bounds__(kGatherBlock) combine_fine_kernel(const double
     if (q0 + t < q1) zf += v[t];
   for (unsigned q = q0 + 8; q < q1; ++q) zf += __ldcs(zsort + q);
   z[g] = zf;
+  }
 }
 
 // R[v] = vmask[v] ? 0 : sum of Rpart over (e,cb) incidences in ascending order

@@ -536,7 +536,13 @@ void launch_combine_fine(Plan& pl, cudaStream_t s)
   const int n_items = dist ? pl.n_fin_surf + (pl.ib1 - pl.ib0) : pl.N;
   const int nsg = dist ? pl.n_fin_surf : pl.nsg;
   const int ibase = dist ? pl.ib0 : pl.nsg;
-  combine_fine_kernel<<<(n_items + kGatherBlock - 1) / kGatherBlock, kGatherBlock, 0, s>>>(
+#ifndef COMBINE_FINE_CTAS_PER_SM
+#define COMBINE_FINE_CTAS_PER_SM 0  // 0: one item per thread; k: persistent, k CTAs per SM
+#endif
+  const int grid = COMBINE_FINE_CTAS_PER_SM > 0
+                       ? std::min((n_items + kGatherBlock - 1) / kGatherBlock, COMBINE_FINE_CTAS_PER_SM * pl.num_sms)
+                       : (n_items + kGatherBlock - 1) / kGatherBlock;
+  combine_fine_kernel<<<std::max(grid, 1), kGatherBlock, 0, s>>>(
       pl.zsort, pl.fine_off, dist ? pl.fin_surf : nullptr, nsg, ibase, n_items, pl.z);
   pl.launches += 1;
 }
@@ -697,15 +703,22 @@ void enqueue_precond(Plan& pl, double* zr_result)
     // high-priority stream, concurrent with the fine half of the combine
     HXB_CUDA(cudaEventRecord(pl.ev_fork, s));
     HXB_CUDA(cudaStreamWaitEvent(pl.s_coarse, pl.ev_fork, 0));
-    HXB_CUDA(cudaGraphLaunch(pl.coarse_exec, pl.s_coarse));
+    {
+      KtScope kt(pl, HXB_KT_COARSE, pl.s_coarse);
+      HXB_CUDA(cudaGraphLaunch(pl.coarse_exec, pl.s_coarse));
+    }
     pl.launches += pl.coarse_graph_nodes;
     HXB_CUDA(cudaEventRecord(pl.ev_join, pl.s_coarse));
-    launch_combine_fine(pl, s);
+    {
+      KtScope kt(pl, HXB_KT_COMBINE_FINE, s);
+      launch_combine_fine(pl, s);
+    }
     HXB_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
     launch_combine(pl, zr_result, s, false, true, true);
     return;
   }
   if (pl.do_coarse) {
+    KtScope kt(pl, HXB_KT_COARSE, s);
     HXB_CUDA(cudaGraphLaunch(pl.coarse_exec, s));
     pl.launches += pl.coarse_graph_nodes;
   }
@@ -1385,7 +1398,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
         pl.lv[l].x = M.alloc<double>(pl.lv[l].n);
       }
       pl.dense = dense_to_device(pl, amg.coarsest);
-      pl.amg_cluster = (opt.reserved[0] & 1) == 0 && build_amg_cluster(pl, amg, hs.vmask);
+      pl.amg_cluster = (opt.reserved[0] & 1) != 0 && build_amg_cluster(pl, amg, hs.vmask);
     } else {
       pl.dense = dense_to_device(pl, hs.Kc);
     }
@@ -1929,6 +1942,11 @@ int hxb_profile(hxb_plan* plan, int reps, double* out)
     };
     for (int q = 0; q < 16; ++q) out[q] = 0;
     ensure_hist(*pl, 4);
+    // realistic operands: r = p = m_N (the Poisson load before masking), so the
+    // AMG K-cycles do their full work (a zero right-hand side exits early)
+    HXB_CUDA(cudaMemcpyAsync(pl->r, pl->d_lumped, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice, s));
+    HXB_CUDA(cudaMemcpyAsync(pl->p, pl->d_lumped, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice, s));
+    if (pl->do_fine) HXB_DISPATCH_NP(pl->np, launch_fdm, *pl, s);
     out[0] = timeit([&] { HXB_DISPATCH_NP(pl->np, launch_ax_elem, *pl, pl->p, pl->f, DotArgs{}, s); });
     out[1] = timeit([&] { enqueue_ax(*pl, pl->p, pl->f, nullptr, s); }) - out[0];
     if (pl->do_fine) out[2] = timeit([&] { HXB_DISPATCH_NP(pl->np, launch_fdm, *pl, s); });

@@ -329,7 +329,7 @@ class Plan:
 
     def __init__(self, mesh: HexMesh, order: int, kappa_e=None, c_e=None, *, precond: str = "two_scale",
                  coarse_solve: str = "automatic", direct_threshold: int = 64000, variant: str = "stored",
-                 device: int = 0, amg_cluster: bool = True, rank: int = 0, nranks: int = 1,
+                 device: int = 0, amg_cluster: bool = False, rank: int = 0, nranks: int = 1,
                  fdm_pipeline: bool = False, split_combine: bool = True):
         L = lib()
         ne = mesh.num_elements
@@ -343,7 +343,7 @@ class Plan:
         opt.direct_threshold = direct_threshold
         opt.variant = VARIANTS[variant]
         opt.device = device
-        opt.reserved[0] = (0 if amg_cluster else 1) | (4 if fdm_pipeline else 0) | (0 if split_combine else 8)
+        opt.reserved[0] = (1 if amg_cluster else 0) | (4 if fdm_pipeline else 0) | (0 if split_combine else 8)
         opt.reserved[1] = rank
         opt.reserved[2] = nranks
         cm = mesh._c()
@@ -559,7 +559,7 @@ class Plan:
         conv = [C.c_void_p(a) if isinstance(a, int) and not isinstance(a, bool) else a for a in args]
         _check(getattr(lib(), "hxb_dist_" + name)(self._h, *conv))
 
-    KT_TAGS = {"ax_elem": 0, "ax_gather": 1, "fdm": 2, "combine": 3}
+    KT_TAGS = {"ax_elem": 0, "ax_gather": 1, "fdm": 2, "combine": 3, "coarse": 4, "combine_fine": 5}
 
     def kernel_timing(self, enable: bool, max_launches: int = 4096):
         """Bracket tagged launches with CUDA events (hxb_kernel_timing)."""

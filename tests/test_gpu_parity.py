@@ -166,8 +166,8 @@ def test_amg_cluster_matches_per_step_kernels():
     """The single-cluster K-cycle (kernels_amg.cuh) equals the kernel-per-step
     K-cycle up to dot-product reduction order."""
     mesh = hx.generate_cube_mesh(12, "distorted_elements" if False else "uniform")
-    a = hx.Plan(mesh, 3, coarse_solve="amg")
-    b = hx.Plan(mesh, 3, coarse_solve="amg", amg_cluster=False)
+    a = hx.Plan(mesh, 3, coarse_solve="amg", amg_cluster=True)
+    b = hx.Plan(mesh, 3, coarse_solve="amg")
     r = splitmix_vector(a.N, 11)
     za, zb = a.apply_coarse(r), b.apply_coarse(r)
     assert rel(za, zb) <= 1e-13, rel(za, zb)
