@@ -86,7 +86,9 @@ typedef struct hxb_options {
                                   TMA/cp.async-pipelined FDM kernel instead of one CTA per
                                   subdomain (measured slower at cfg2, kept for A/B checks);
                                   bit 3: one fused combine after the coarse solve instead of
-                                  the fine half running concurrently with it;
+                                  the fine half running concurrently with it; bit 5: ksolve(2)
+                                  on the compacted levels as one single-CTA kernel (measured
+                                  slower at cfg2: 1.23 vs 0.82 ms per coarse solve);
                                   reserved[1] = rank, reserved[2] = number of ranks: element-slab
                                   partition for the distributed operator (hxb_dist_*) */
 } hxb_options;

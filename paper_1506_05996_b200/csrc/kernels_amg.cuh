@@ -269,6 +269,18 @@ __global__ void __launch_bounds__(kAmgClusterBlock, 1) amg_cluster_kernel(const 
   amg_ksolve(c, a, 0, b, x);
 }
 
+// ksolve(l) of the compacted hierarchy by ONE CTA with block barriers: the
+// small levels (<= kAmgLocalRows kept rows) of the default per-step K-cycle,
+// where a kernel per step would be all launch latency (one launch instead of
+// ~21 at cfg2).
+__global__ void __launch_bounds__(kAmgClusterBlock, 1) amg_local_ksolve_kernel(const __grid_constant__ AmgClusterArgs a,
+                                                                               int l, const double* b, double* x)
+{
+  __shared__ double part[2], bcast, wred[32];
+  ClusterCtx c{cg::this_cluster(), true, (int)threadIdx.x, (int)blockDim.x, part, &bcast, wred, 0};
+  amg_ksolve(c, a, l, b, x);
+}
+
 // ---------------------------------------------------------------------------
 // Finest-level (level 0, full vertex numbering) glue kernels.
 

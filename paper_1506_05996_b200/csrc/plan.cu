@@ -127,6 +127,9 @@ struct DevDense {
 struct Plan {
   int device = 0;
   cudaStream_t s_main = nullptr, s_coarse = nullptr;  // s_coarse: highest priority
+  bool amg_local2 = false;  // per-step K-cycle with ksolve(2) as one single-CTA kernel (opt-in: slower at cfg2)
+  int *agg1c = nullptr, *mptr1 = nullptr, *mem1 = nullptr;
+  int n2 = 0;
   bool split_combine = true;  // fine half of the combine concurrent with the coarse solve (options.reserved[0] bit 3 off)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_a = nullptr;
   cudaGraphExec_t coarse_exec = nullptr;
@@ -587,6 +590,14 @@ void enqueue_cycle(Plan& pl, int l, const double* r, double* zout, cudaStream_t 
   const int g = vec_grid(v.n);
   amg_jacobi2_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA);
   amg_resid_kernel<<<g, kVecBlock, 0, s>>>(v.A, r, v.zA, v.kf);  // kf is free during the cycle
+  if (l == 1 && pl.amg_local2) {  // ksolve(2) on the compacted levels by one CTA
+    CLev& c2 = pl.cargs.lev[1];
+    amg_agg_sum_compact_kernel<<<vec_grid(pl.n2), kVecBlock, 0, s>>>(v.kf, pl.mptr1, pl.mem1, c2.b, pl.n2);
+    amg_local_ksolve_kernel<<<1, kAmgClusterBlock, 0, s>>>(pl.cargs, 1, c2.b, c2.x);
+    amg_prolong_smooth_compact_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c2.x, pl.agg1c, v.zB);
+    amg_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout);
+    return;
+  }
   amg_agg_sum_kernel<<<vec_grid(v.nc), kVecBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
   enqueue_ksolve(pl, l + 1, c.b, c.x, s);
   amg_prolong_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
@@ -976,6 +987,23 @@ bool build_amg_cluster(Plan& pl, const AmgSetup& amg, const std::vector<std::uin
     pl.mptr0 = M.upload(mptr);
     pl.mem0 = M.upload(mem);
     pl.n1 = ncomp[1];
+  }
+  if (Lh >= 3) {  // level 1 (full numbering) -> compact level 2: glue of the one-CTA ksolve(2)
+    const AmgLevel& l1 = amg.levels[1];
+    std::vector<int> agg1c(l1.A.n), mptr(ncomp[2] + 1, 0), mem;
+    for (gid i = 0; i < l1.A.n; ++i) {
+      agg1c[i] = cidx[2][l1.aggregate[i]];
+      if (agg1c[i] >= 0) mptr[agg1c[i] + 1]++;
+    }
+    for (int k = 0; k < ncomp[2]; ++k) mptr[k + 1] += mptr[k];
+    mem.assign(mptr[ncomp[2]], 0);
+    std::vector<int> cur(mptr.begin(), mptr.end() - 1);
+    for (gid i = 0; i < l1.A.n; ++i)
+      if (agg1c[i] >= 0) mem[cur[agg1c[i]]++] = i;
+    pl.agg1c = M.upload(agg1c);
+    pl.mptr1 = M.upload(mptr);
+    pl.mem1 = M.upload(mem);
+    pl.n2 = ncomp[2];
   }
   // the K-cycle recursion (ksolve -> cycle -> ksolve ...) needs a per-thread
   // stack deeper than the 1 KB default for hierarchies of many levels
@@ -1398,7 +1426,12 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
         pl.lv[l].x = M.alloc<double>(pl.lv[l].n);
       }
       pl.dense = dense_to_device(pl, amg.coarsest);
-      pl.amg_cluster = (opt.reserved[0] & 1) != 0 && build_amg_cluster(pl, amg, hs.vmask);
+      const bool want_cluster = (opt.reserved[0] & 1) != 0;
+      const bool compact = (opt.reserved[0] & 32) != 0 || want_cluster;
+      const bool built = compact && build_amg_cluster(pl, amg, hs.vmask);
+      pl.amg_cluster = want_cluster && built;
+      pl.amg_local2 = !pl.amg_cluster && built && pl.cargs.L >= 2 && pl.agg1c &&
+                      pl.cargs.lev[1].n <= kAmgLocalRows;
     } else {
       pl.dense = dense_to_device(pl, hs.Kc);
     }
