@@ -151,10 +151,24 @@ __device__ __forceinline__ double csr_row_dot(const DevCsr& A, int i, const doub
 }
 
 // z = z1 + w d (r - A z1), z1 = w d r computed on the fly (amg.cpp:212-213)
+struct KScalars {
+  double zr, pf, zr_next;
+  int stopped;
+  int pad;
+};
+
+// init (the K-solve's first cycle): also r_copy = r, x = 0, stopped = 0 (the
+// K-solve's initialisation, folded into its first kernel)
 __global__ void amg_jacobi2_kernel(DevCsr A, const double* __restrict__ dinv, const double* __restrict__ r,
-                                   double* __restrict__ z)
+                                   double* __restrict__ z, double* __restrict__ r_copy = nullptr,
+                                   double* __restrict__ x_zero = nullptr, KScalars* ks_init = nullptr)
 {
+  if (ks_init && blockIdx.x == 0 && threadIdx.x == 0) ks_init->stopped = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < A.n; i += gridDim.x * blockDim.x) {
+    if (r_copy) {
+      r_copy[i] = __ldg(r + i);
+      x_zero[i] = 0.0;
+    }
     const double s = csr_row_sum(A.ptr, A.col, A.val, i,
                                  [&](int c) { return kJacobiOmega * __ldg(dinv + c) * __ldg(r + c); });
     const double z1 = kJacobiOmega * __ldg(dinv + i) * __ldg(r + i);
@@ -197,39 +211,30 @@ __global__ void amg_smooth_kernel(DevCsr A, const double* __restrict__ dinv, con
   }
 }
 
-// ---------------------------------------------------------------------------
-// K-cycle inner PCG (amg.cpp:230-263). Scalars of one ksolve invocation:
-struct KScalars {
-  double zr, pf, zr_next;
-  int stopped;
-  int pad;
-};
-
-// r = b; x = 0; stopped = 0
-__global__ void amg_kinit_kernel(const double* __restrict__ b, double* __restrict__ r, double* __restrict__ x, int n,
-                                 KScalars* ks)
-{
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    r[i] = b[i];
-    x[i] = 0.0;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) ks->stopped = 0;
-}
-
-// result = z.r, optionally p = z
+// the same smoothing step with the K-solve's following z.r (and optional
+// p = z) fused in: identical grid, loop and reduction as amg_dot_kernel, so
+// the dot is bitwise the separate kernel's
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) amg_dot_kernel(const double* __restrict__ z, const double* __restrict__ r,
-                                                       double* __restrict__ p, int n, DotArgs d)
+__global__ void __launch_bounds__(BLOCK) amg_smooth_dot_kernel(DevCsr A, const double* __restrict__ dinv,
+                                                              const double* __restrict__ r,
+                                                              const double* __restrict__ zin, double* __restrict__ zout,
+                                                              double* __restrict__ p, DotArgs d)
 {
   __shared__ double red[BLOCK / 32];
-  double s = 0.0;
-  for (int i = blockIdx.x * BLOCK + threadIdx.x; i < n; i += gridDim.x * BLOCK) {
-    const double zi = z[i];
-    s += zi * r[i];
+  double acc = 0.0;
+  for (int i = blockIdx.x * BLOCK + threadIdx.x; i < A.n; i += gridDim.x * BLOCK) {
+    const double s = csr_row_dot(A, i, zin);
+    const double ri = __ldg(r + i);
+    const double zi = __ldg(zin + i) + kJacobiOmega * __ldg(dinv + i) * (ri - s);
+    zout[i] = zi;
     if (p) p[i] = zi;
+    acc += zi * ri;
   }
-  dot_commit<BLOCK>(d, s, red);
+  dot_commit<BLOCK>(d, acc, red);
 }
+
+// ---------------------------------------------------------------------------
+// K-cycle inner PCG (amg.cpp:230-263). Scalars of one ksolve invocation:
 
 // f = A p; result = p.f
 template <int BLOCK>
@@ -246,11 +251,13 @@ __global__ void __launch_bounds__(BLOCK) amg_spmv_dot_kernel(DevCsr A, const dou
   dot_commit<BLOCK>(d, s, red);
 }
 
-// if (!(pf > 0) || !(|zr| > 0)) stop; else x += a p, r -= a f  (amg.cpp:244-253)
+// if (!(pf > 0) || !(|zr| > 0)) stop; else x += a p, r -= a f  (amg.cpp:244-253).
+// zr_is_next: the second step reads zr from zr_next (the value the separate
+// shift kernel used to copy into zr after amg_kdir_kernel)
 __global__ void amg_kupdate_kernel(const double* __restrict__ p, const double* __restrict__ f, double* __restrict__ x,
-                                   double* __restrict__ r, int n, KScalars* ks)
+                                   double* __restrict__ r, int n, KScalars* ks, int zr_is_next)
 {
-  const double pf = ks->pf, zr = ks->zr;
+  const double pf = ks->pf, zr = zr_is_next ? ks->zr_next : ks->zr;
   const bool stop = ks->stopped || !(pf > 0) || !(fabs(zr) > 0);
   if (stop) {
     __syncthreads();
@@ -270,12 +277,6 @@ __global__ void amg_kdir_kernel(const double* __restrict__ z, double* __restrict
   if (ks->stopped) return;
   const double beta = ks->zr_next / ks->zr;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = z[i] + beta * p[i];
-}
-
-// after kdir: zr <- zr_next (separate tiny kernel keeps kdir free of a grid-wide race)
-__global__ void amg_kshift_kernel(KScalars* ks)
-{
-  if (!ks->stopped) ks->zr = ks->zr_next;
 }
 
 // rho = R - K Z

@@ -578,7 +578,17 @@ void enqueue_dense(Plan& pl, const double* b, double* x, cudaStream_t s)
 
 void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s);
 
-void enqueue_cycle(Plan& pl, int l, const double* r, double* zout, cudaStream_t s)
+// Fusions used when the cycle runs inside ksolve(l): the K-solve's init
+// (r_copy = r, x = 0) in the first kernel, its z.r (and p = z) in the last.
+struct CycleFuse {
+  double* r_copy = nullptr;
+  double* x_zero = nullptr;
+  KScalars* ks_init = nullptr;
+  double* p_copy = nullptr;
+  const DotArgs* dot = nullptr;
+};
+
+void enqueue_cycle(Plan& pl, int l, const double* r, double* zout, cudaStream_t s, const CycleFuse& fu = {})
 {
   const int L = static_cast<int>(pl.lv.size()) - 1;
   if (l == L) {
@@ -588,20 +598,22 @@ void enqueue_cycle(Plan& pl, int l, const double* r, double* zout, cudaStream_t 
   DevLevel& v = pl.lv[l];
   DevLevel& c = pl.lv[l + 1];
   const int g = vec_grid(v.n);
-  amg_jacobi2_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA);
+  amg_jacobi2_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, fu.r_copy, fu.x_zero, fu.ks_init);
   amg_resid_kernel<<<g, kVecBlock, 0, s>>>(v.A, r, v.zA, v.kf);  // kf is free during the cycle
   if (l == 1 && pl.amg_local2) {  // ksolve(2) on the compacted levels by one CTA
     CLev& c2 = pl.cargs.lev[1];
     amg_agg_sum_compact_kernel<<<vec_grid(pl.n2), kVecBlock, 0, s>>>(v.kf, pl.mptr1, pl.mem1, c2.b, pl.n2);
     amg_local_ksolve_kernel<<<1, kAmgClusterBlock, 0, s>>>(pl.cargs, 1, c2.b, c2.x);
     amg_prolong_smooth_compact_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c2.x, pl.agg1c, v.zB);
-    amg_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout);
-    return;
+  } else {
+    amg_agg_sum_kernel<<<vec_grid(v.nc), kVecBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
+    enqueue_ksolve(pl, l + 1, c.b, c.x, s);
+    amg_prolong_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
   }
-  amg_agg_sum_kernel<<<vec_grid(v.nc), kVecBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
-  enqueue_ksolve(pl, l + 1, c.b, c.x, s);
-  amg_prolong_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
-  amg_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout);
+  if (fu.dot)
+    amg_smooth_dot_kernel<kVecBlock><<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout, fu.p_copy, *fu.dot);
+  else
+    amg_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout);
 }
 
 void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
@@ -613,17 +625,26 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
   }
   DevLevel& v = pl.lv[l];
   const int g = vec_grid(v.n);
-  amg_kinit_kernel<<<g, kVecBlock, 0, s>>>(b, v.kr, x, v.n, v.ks);
-  enqueue_cycle(pl, l, v.kr, v.kz, s);
-  amg_dot_kernel<kVecBlock><<<g, kVecBlock, 0, s>>>(v.kz, v.kr, v.kp, v.n, cdot_args(pl, &v.ks->zr));
+  {  // init fused into the first cycle's Jacobi kernel, z.r and p = z into its last smoother
+    const DotArgs d0 = cdot_args(pl, &v.ks->zr);
+    CycleFuse fu;
+    fu.r_copy = v.kr;
+    fu.x_zero = x;
+    fu.ks_init = v.ks;
+    fu.p_copy = v.kp;
+    fu.dot = &d0;
+    enqueue_cycle(pl, l, b, v.kz, s, fu);
+  }
   for (int it = 0; it < 2; ++it) {
     amg_spmv_dot_kernel<kVecBlock><<<g, kVecBlock, 0, s>>>(v.A, v.kp, v.kf, cdot_args(pl, &v.ks->pf));
-    amg_kupdate_kernel<<<g, kVecBlock, 0, s>>>(v.kp, v.kf, x, v.kr, v.n, v.ks);
+    // amg.cpp:244-253; the second step reads zr from zr_next (the shift after kdir is folded in)
+    amg_kupdate_kernel<<<g, kVecBlock, 0, s>>>(v.kp, v.kf, x, v.kr, v.n, v.ks, it);
     if (it == 1) break;
-    enqueue_cycle(pl, l, v.kr, v.kz, s);
-    amg_dot_kernel<kVecBlock><<<g, kVecBlock, 0, s>>>(v.kz, v.kr, nullptr, v.n, cdot_args(pl, &v.ks->zr_next));
+    const DotArgs d1 = cdot_args(pl, &v.ks->zr_next);
+    CycleFuse fu;
+    fu.dot = &d1;
+    enqueue_cycle(pl, l, v.kr, v.kz, s, fu);
     amg_kdir_kernel<<<g, kVecBlock, 0, s>>>(v.kz, v.kp, v.n, v.ks);
-    amg_kshift_kernel<<<1, 1, 0, s>>>(v.ks);
   }
 }
 
