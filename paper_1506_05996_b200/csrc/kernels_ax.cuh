@@ -44,9 +44,10 @@ struct AxShape {
   static constexpr std::size_t kSmemBytes = kGBytes + (kBufA + kBufB + 2 * NP * NP) * sizeof(double) + kIdxBytes +
                                             2 * sizeof(unsigned long long);
   // register cap per resident-CTA target (cfg4 sweep, element kernel / HBM):
-  // np = 9: 2 CTAs/SM 0.67, 3 0.84, 4 0.87; np = 10: 2 0.69, 3 0.77 (4 spills);
+  // np = 6: 6 CTAs/SM 0.72, 8 0.76, 10 0.72; np = 7: 6 0.87, 8 0.88, 10 0.56;
+  // np = 9: 2 0.67, 3 0.84, 4 0.87; np = 10: 2 0.69, 3 0.77 (4 spills);
   // np = 11: 2 0.86, 3 0.76
-  static constexpr int kMinBlocks = NP <= 8 ? 6 : NP == 9 ? 4 : NP == 10 ? 3 : 2;
+  static constexpr int kMinBlocks = NP <= 7 ? 8 : NP == 8 ? 6 : NP == 9 ? 4 : NP == 10 ? 3 : 2;
   // on-the-fly geometry: the planes are replaced by the element record (8
   // corners + kappa, TMA-staged) and two Jacobian-column tables
   static constexpr int kRecD = 26;                      // doubles per element record (16-byte multiple)
