@@ -314,4 +314,101 @@ __global__ void dense_solve_kernel(const double* __restrict__ ainv, const int* _
   }
 }
 
+// ---------------------------------------------------------------------------
+// Large direct coarse solve (coupled block m > 1500): the inverse is symmetric,
+// so only its lower-triangle 64x64 tiles are stored (m^2/2 doubles: 12 GB
+// instead of 24 GB at m = 54,872) and applied as y_I = sum_{J<=I} A_IJ x_J +
+// sum_{I'>I} A_I'I^T x_I'. Each tile is read once; its row and column partial
+// sums go to per-tile slots and a second kernel adds them in a fixed order
+// (deterministic, no atomics).
+constexpr int kDenseTile = 64;
+
+__device__ __forceinline__ void tile_of(long long t, int& I, int& J)
+{
+  I = static_cast<int>((sqrt(8.0 * static_cast<double>(t) + 1.0) - 1.0) * 0.5);
+  while (static_cast<long long>(I + 1) * (I + 2) / 2 <= t) ++I;
+  while (static_cast<long long>(I) * (I + 1) / 2 > t) --I;
+  J = static_cast<int>(t - static_cast<long long>(I) * (I + 1) / 2);
+}
+
+// tiles[t][64][64] from the full row-major inverse (zero padded past m)
+__global__ void dense_pack_kernel(const double* __restrict__ full, int m, double* __restrict__ tiles, long long ntiles)
+{
+  constexpr int T = kDenseTile;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int I, J;
+    tile_of(t, I, J);
+    double* dst = tiles + t * T * T;
+    for (int q = threadIdx.x; q < T * T; q += blockDim.x) {
+      const int r = I * T + q / T, c = J * T + q % T;
+      dst[q] = (r < m && c < m) ? full[static_cast<std::size_t>(r) * m + c] : 0.0;
+    }
+  }
+}
+
+// xg[c] = b[coupled[c]] (zero padded to nt*64)
+__global__ void dense_gather_x_kernel(const double* __restrict__ b, const int* __restrict__ coupled, int m, int mp,
+                                      double* __restrict__ xg)
+{
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < mp; c += gridDim.x * blockDim.x)
+    xg[c] = c < m ? __ldg(b + __ldg(coupled + c)) : 0.0;
+}
+
+// one 256-thread CTA per tile: coalesced tile load into padded shared memory,
+// then 64 threads form the row sums and 64 the column sums (off-diagonal tiles)
+__global__ void __launch_bounds__(256) dense_tile_gemv_kernel(const double* __restrict__ tiles,
+                                                              const double* __restrict__ xg, long long ntiles,
+                                                              double* __restrict__ rowpart, double* __restrict__ colpart)
+{
+  constexpr int T = kDenseTile, S = T + 1;
+  __shared__ double a[T * S];
+  __shared__ double xi[T], xj[T];
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int I, J;
+    tile_of(t, I, J);
+    const double* src = tiles + t * T * T;
+#pragma unroll 4
+    for (int q = threadIdx.x; q < T * T; q += 256) a[(q / T) * S + q % T] = __ldcs(src + q);
+    if (threadIdx.x < T) {
+      xj[threadIdx.x] = __ldg(xg + J * T + threadIdx.x);
+      xi[threadIdx.x] = __ldg(xg + I * T + threadIdx.x);
+    }
+    __syncthreads();
+    if (threadIdx.x < T) {  // row sums
+      const int r = threadIdx.x;
+      double s = 0.0;
+#pragma unroll 8
+      for (int c = 0; c < T; ++c) s += a[r * S + c] * xj[c];
+      rowpart[t * T + r] = s;
+    } else if (threadIdx.x < 2 * T && I != J) {  // column sums (transpose part)
+      const int c = threadIdx.x - T;
+      double s = 0.0;
+#pragma unroll 8
+      for (int r = 0; r < T; ++r) s += a[r * S + c] * xi[r];
+      colpart[t * T + c] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// z[coupled[i]] = sum_{J<=I} rowpart(I,J)[i] + sum_{I'>I} colpart(I',I)[i]; decoupled rows b/a_ii
+__global__ void dense_tile_reduce_kernel(const double* __restrict__ rowpart, const double* __restrict__ colpart, int m,
+                                         int nt, const int* __restrict__ coupled, const double* __restrict__ inv_diag,
+                                         const double* __restrict__ b, double* __restrict__ z, int n)
+{
+  constexpr int T = kDenseTile;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int I = i / T, il = i % T;
+    const long long base = static_cast<long long>(I) * (I + 1) / 2;
+    double s = 0.0;
+    for (int J = 0; J <= I; ++J) s += __ldg(rowpart + (base + J) * T + il);
+    for (int I2 = I + 1; I2 < nt; ++I2) s += __ldg(colpart + (static_cast<long long>(I2) * (I2 + 1) / 2 + I) * T + il);
+    z[__ldg(coupled + i)] = s;
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double di = __ldg(inv_diag + i);
+    if (di != 0.0) z[i] = __ldg(b + i) * di;
+  }
+}
+
 }  // namespace hxb

@@ -117,9 +117,14 @@ struct DevLevel {
 
 struct DevDense {
   int n = 0, m = 0;
-  double* ainv = nullptr;
+  double* ainv = nullptr;  // full row-major inverse (small blocks)
   int* coupled = nullptr;
   double* inv_diag = nullptr;
+  // large blocks: lower-triangle 64x64 tiles of the inverse + partial-sum slots
+  double* tiles = nullptr;
+  long long ntiles = 0;
+  int nt = 0;
+  double *xg = nullptr, *rowpart = nullptr, *colpart = nullptr;
 };
 
 }  // namespace
@@ -569,6 +574,15 @@ void launch_restrict(Plan& pl, cudaStream_t s)
 void enqueue_dense(Plan& pl, const double* b, double* x, cudaStream_t s)
 {
   const DevDense& d = pl.dense;
+  if (d.tiles) {  // packed symmetric tiles (large coupled block)
+    const int mp = d.nt * kDenseTile;
+    dense_gather_x_kernel<<<vec_grid(mp), kVecBlock, 0, s>>>(b, d.coupled, d.m, mp, d.xg);
+    const unsigned grid = static_cast<unsigned>(std::min<long long>(d.ntiles, 8LL * pl.num_sms));
+    dense_tile_gemv_kernel<<<grid, 256, 0, s>>>(d.tiles, d.xg, d.ntiles, d.rowpart, d.colpart);
+    dense_tile_reduce_kernel<<<vec_grid(std::max(d.m, d.n)), kVecBlock, 0, s>>>(d.rowpart, d.colpart, d.m, d.nt,
+                                                                                   d.coupled, d.inv_diag, b, x, d.n);
+    return;
+  }
   const int threads = 256;
   const int rows_per_block = threads / 32;
   int grid = std::max((d.m + rows_per_block - 1) / rows_per_block, (d.n + threads - 1) / threads);
@@ -860,7 +874,9 @@ DevDense dense_to_device(Plan& pl, const Csr& A)
     cudaFree(dcol);
     cudaFree(dval);
   }
-  d.ainv = pl.mem.alloc<double>(mm);
+  double* full = nullptr;  // the full inverse, packed into tiles below
+  HXB_CUDA(cudaMalloc(&full, mm * sizeof(double)));
+  d.ainv = full;
   HXB_CUDA(cudaMemset(d.ainv, 0, mm * sizeof(double)));
   dense_identity_kernel<<<vec_grid(m), kVecBlock>>>(d.ainv, m);
   cusolverDnHandle_t h;
@@ -887,8 +903,21 @@ DevDense dense_to_device(Plan& pl, const Csr& A)
   cudaFree(L);
   cusolverDnDestroyParams(prm);
   cusolverDnDestroy(h);
-  if (st != CUSOLVER_STATUS_SUCCESS || hinfo != 0)
+  if (st != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
+    cudaFree(full);
     throw HxbError(HXB_ENUMERIC, "coarse matrix Cholesky failed (matrix not SPD?)");
+  }
+  d.nt = (m + kDenseTile - 1) / kDenseTile;
+  d.ntiles = static_cast<long long>(d.nt) * (d.nt + 1) / 2;
+  d.tiles = pl.mem.alloc<double>(static_cast<std::size_t>(d.ntiles) * kDenseTile * kDenseTile);
+  dense_pack_kernel<<<static_cast<unsigned>(std::min<long long>(d.ntiles, 65535LL * 16)), 256>>>(full, m, d.tiles,
+                                                                                                d.ntiles);
+  HXB_CUDA(cudaDeviceSynchronize());
+  cudaFree(full);
+  d.ainv = nullptr;
+  d.xg = pl.mem.alloc<double>(static_cast<std::size_t>(d.nt) * kDenseTile);
+  d.rowpart = pl.mem.alloc<double>(static_cast<std::size_t>(d.ntiles) * kDenseTile);
+  d.colpart = pl.mem.alloc<double>(static_cast<std::size_t>(d.ntiles) * kDenseTile);
   return d;
 }
 
@@ -985,6 +1014,7 @@ bool build_amg_cluster(Plan& pl, const AmgSetup& amg, const std::vector<std::uin
       Ac.ptr.push_back(static_cast<std::int64_t>(Ac.col.size()));
     }
     pl.cdense = dense_to_device(pl, Ac);
+    if (pl.cdense.tiles) return false;  // the cluster kernel applies a full inverse only
     ca.ainv = pl.cdense.ainv;
     ca.coupled = pl.cdense.coupled;
     ca.inv_diag = pl.cdense.inv_diag;
