@@ -311,11 +311,21 @@ __global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(Combin
 // half then reads z back (fine_in_z), so the result is bit-identical to the
 // fused kernel. One item per thread, no persistent loop, so the coarse
 // kernels on the high-priority stream are scheduled as soon as CTAs retire.
+struct PcgUArgs {  // optional u += alpha_k p_k of the PCG (krylov.cpp:54) riding along
+  double* u = nullptr;
+  const double* p = nullptr;
+  const double* zr = nullptr;
+  const double* pf = nullptr;
+  int k = 0;
+};
+
 __global__ void __launch_bounds__(kGatherBlock) combine_fine_kernel(const double* __restrict__ zsort,
                                                                     const unsigned* __restrict__ fine_off,
                                                                     const int* __restrict__ surf_nodes, int nsg,
-                                                                    int ibase, int n_items, double* __restrict__ z)
+                                                                    int ibase, int n_items, double* __restrict__ z,
+                                                                    PcgUArgs ua)
 {
+  const double alpha = ua.u ? ua.zr[ua.k] / ua.pf[ua.k] : 0.0;
   for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += gridDim.x * blockDim.x) {
   const int g = it < nsg ? (surf_nodes ? __ldg(surf_nodes + it) : it) : ibase + (it - nsg);
   const unsigned q0 = __ldg(fine_off + it), q1 = __ldg(fine_off + it + 1);
@@ -328,6 +338,7 @@ __global__ void __launch_bounds__(kGatherBlock) combine_fine_kernel(const double
     if (q0 + t < q1) zf += v[t];
   for (unsigned q = q0 + 8; q < q1; ++q) zf += __ldcs(zsort + q);
   z[g] = zf;
+  if (ua.u) ua.u[g] += alpha * ua.p[g];
   }
 }
 

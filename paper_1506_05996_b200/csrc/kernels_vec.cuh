@@ -78,6 +78,15 @@ __global__ void pcg_dir_kernel(const double* __restrict__ z, double* __restrict_
   }
 }
 
+// p_{k+1} = z + beta_k p_k alone: u += alpha_k p_k already ran inside the
+// fine half of the combine (in the shadow of the coarse solve)
+__global__ void pcg_dir_p_kernel(const double* __restrict__ z, double* __restrict__ p, int n,
+                                 const double* __restrict__ zr, int k)
+{
+  const double beta = zr[k + 1] / zr[k];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = z[i] + beta * p[i];
+}
+
 // final u += alpha_k p_k
 __global__ void pcg_final_kernel(const double* __restrict__ p, double* __restrict__ u, int n,
                                  const double* __restrict__ zr, const double* __restrict__ pf, int k)

@@ -538,20 +538,15 @@ void launch_combine(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine, b
   HXB_DISPATCH_NP(pl.np, launch_combine_np, pl, zr_result, s, do_fine, do_coarse, fine_in_z);
 }
 
-void launch_combine_fine(Plan& pl, cudaStream_t s)
+void launch_combine_fine(Plan& pl, cudaStream_t s, const PcgUArgs& ua = {})
 {
   const bool dist = pl.nranks > 1;
   const int n_items = dist ? pl.n_fin_surf + (pl.ib1 - pl.ib0) : pl.N;
   const int nsg = dist ? pl.n_fin_surf : pl.nsg;
   const int ibase = dist ? pl.ib0 : pl.nsg;
-#ifndef COMBINE_FINE_CTAS_PER_SM
-#define COMBINE_FINE_CTAS_PER_SM 0  // 0: one item per thread; k: persistent, k CTAs per SM
-#endif
-  const int grid = COMBINE_FINE_CTAS_PER_SM > 0
-                       ? std::min((n_items + kGatherBlock - 1) / kGatherBlock, COMBINE_FINE_CTAS_PER_SM * pl.num_sms)
-                       : (n_items + kGatherBlock - 1) / kGatherBlock;
-  combine_fine_kernel<<<std::max(grid, 1), kGatherBlock, 0, s>>>(
-      pl.zsort, pl.fine_off, dist ? pl.fin_surf : nullptr, nsg, ibase, n_items, pl.z);
+  // one item per thread (a persistent grid leaves the coarse kernels no room: measured slower)
+  combine_fine_kernel<<<std::max((n_items + kGatherBlock - 1) / kGatherBlock, 1), kGatherBlock, 0, s>>>(
+      pl.zsort, pl.fine_off, dist ? pl.fin_surf : nullptr, nsg, ibase, n_items, pl.z, ua);
   pl.launches += 1;
 }
 
@@ -726,15 +721,17 @@ void capture_coarse_graph(Plan& pl)
   cudaGraphDestroy(graph);
 }
 
-// z = P r (reads pl.r, writes pl.z); optional z.r into *zr_result
-void enqueue_precond(Plan& pl, double* zr_result)
+// z = P r (reads pl.r, writes pl.z); optional z.r into *zr_result. With ua,
+// the PCG's u += alpha_k p_k runs inside the fine half of the combine (in the
+// shadow of the coarse solve); returns whether it did.
+bool enqueue_precond(Plan& pl, double* zr_result, const PcgUArgs* ua = nullptr)
 {
   cudaStream_t s = pl.s_main;
   if (pl.precond_mode == HXB_PRECOND_NONE) {
     copy_dot_kernel<kVecBlock><<<fill_grid(copy_dot_kernel<kVecBlock>, kVecBlock, pl.N), kVecBlock, 0, s>>>(pl.r, pl.r, pl.z, pl.N,
                                                                      zr_result ? dot_args(pl, zr_result) : DotArgs{});
     pl.launches += 1;
-    return;
+    return false;
   }
   // fine FDM solves with the coarse restriction fused in (one pass over r),
   // then the coarse graph; the combine sums both and applies the mask
@@ -755,13 +752,14 @@ void enqueue_precond(Plan& pl, double* zr_result)
     }
     pl.launches += pl.coarse_graph_nodes;
     HXB_CUDA(cudaEventRecord(pl.ev_join, pl.s_coarse));
+    const bool with_u = ua && pl.nranks == 1;
     {
       KtScope kt(pl, HXB_KT_COMBINE_FINE, s);
-      launch_combine_fine(pl, s);
+      launch_combine_fine(pl, s, with_u ? *ua : PcgUArgs{});
     }
     HXB_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
     launch_combine(pl, zr_result, s, false, true, true);
-    return;
+    return with_u;
   }
   if (pl.do_coarse) {
     KtScope kt(pl, HXB_KT_COARSE, s);
@@ -769,6 +767,7 @@ void enqueue_precond(Plan& pl, double* zr_result)
     pl.launches += pl.coarse_graph_nodes;
   }
   launch_combine(pl, zr_result, s, pl.do_fine, pl.do_coarse);
+  return false;
 }
 
 // ---------------------------------------------------------------------------
@@ -1576,8 +1575,17 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
         diag = "not converged within " + std::to_string(cfg.max_iterations) + " iterations";
         break;
       }
-      enqueue_precond(pl, pl.zr_hist + k + 1);
-      pcg_dir_kernel<<<fill_grid(pcg_dir_kernel, kVecBlock, n), kVecBlock, 0, s>>>(pl.z, pl.p, pl.u, n, pl.zr_hist, pl.pf_hist, k);
+      PcgUArgs ua;
+      ua.u = pl.u;
+      ua.p = pl.p;
+      ua.zr = pl.zr_hist;
+      ua.pf = pl.pf_hist;
+      ua.k = k;
+      if (enqueue_precond(pl, pl.zr_hist + k + 1, &ua))
+        pcg_dir_p_kernel<<<fill_grid(pcg_dir_p_kernel, kVecBlock, n), kVecBlock, 0, s>>>(pl.z, pl.p, n, pl.zr_hist, k);
+      else
+        pcg_dir_kernel<<<fill_grid(pcg_dir_kernel, kVecBlock, n), kVecBlock, 0, s>>>(pl.z, pl.p, pl.u, n, pl.zr_hist,
+                                                                                      pl.pf_hist, k);
       pl.launches += 1;
     }
   }
