@@ -85,4 +85,93 @@ __global__ void __launch_bounds__(256) geometry_kernel(const __grid_constant__ G
   }
 }
 
+// Subdomain slot -> global node of every element's (n+3)^3 FDM subdomain
+// (sub_l2g, mesh.cpp:385-451; for_each_sub_slot order): own nodes from the
+// surface codes / closed-form interior ids, face slots from the face-neighbour
+// table, edge and corner slots -1. Dirichlet codes (-g-2) decode to g.
+template <int NP>
+__global__ void sub_keys_kernel(const int* __restrict__ smap, int sstride, const int* __restrict__ sub_face,
+                                int sfstride, int ne, int nsg, int* __restrict__ keys)
+{
+  constexpr int n = NP - 1, P = NP + 2, P3 = P * P * P, NI = (n - 1) * (n - 1) * (n - 1);
+  auto dec = [](int c) { return c >= 0 ? c : (c <= -2 ? -c - 2 : -1); };
+  const long long total = static_cast<long long>(ne) * P3;
+  for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int e = static_cast<int>(t / P3), slot = static_cast<int>(t % P3);
+    const int x = slot % P, y = (slot / P) % P, z = slot / (P * P);
+    const int ii = x - 1, jj = y - 1, kk = z - 1;
+    const bool ox = ii < 0 || ii > n, oy = jj < 0 || jj > n, oz = kk < 0 || kk > n;
+    const int nout = ox + oy + oz;
+    int g = -1;
+    if (nout == 0) {
+      const int s = surface_slot(NP, ii, jj, kk);
+      g = s >= 0 ? dec(__ldg(smap + static_cast<long long>(e) * sstride + s))
+                 : nsg + e * NI + ((kk - 1) * (n - 1) + (jj - 1)) * (n - 1) + (ii - 1);
+    } else if (nout == 1) {
+      int f, u, w;
+      if (ox) {
+        f = ii < 0 ? 0 : 1, u = jj, w = kk;
+      } else if (oy) {
+        f = jj < 0 ? 2 : 3, u = kk, w = ii;
+      } else {
+        f = kk < 0 ? 4 : 5, u = ii, w = jj;
+      }
+      g = dec(__ldg(sub_face + static_cast<long long>(e) * sfstride + (f * NP + w) * NP + u));
+    }
+    keys[t] = g;
+  }
+}
+
+// Surface map rows and the Ax gather CSR from the sorted surface copies:
+// smap[e][0][q] = Dirichlet-encoded global id, smap[e][1][q] = the copy's CSR
+// position; ax_idx[pos] = e*nsurfp + q (copies ascending in (e, q)).
+__global__ void surface_map_kernel(const int* __restrict__ l2g_surf, const int* __restrict__ pos,
+                                   const std::uint8_t* __restrict__ mask, int ne, int nsurf, int nsurfp,
+                                   int* __restrict__ smap, int* __restrict__ ax_idx)
+{
+  const long long total = static_cast<long long>(ne) * nsurf;
+  for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int e = static_cast<int>(t / nsurf), q = static_cast<int>(t % nsurf);
+    const int g = l2g_surf[t], p = pos[t];
+    int* row = smap + static_cast<long long>(e) * 2 * nsurfp;
+    row[q] = mask[g] ? encode_dirichlet(g) : g;
+    row[nsurfp + q] = p;
+    ax_idx[p] = e * nsurfp + q;
+  }
+}
+
+// mass of every surface copy in Ax-CSR order (the fused prolongation streams it)
+__global__ void mass_csr_kernel(const int* __restrict__ ax_idx, long long n, const double* __restrict__ mass, int nloc,
+                                int nsurfp, const int* __restrict__ slot_l, double* __restrict__ mcsr)
+{
+  for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+       p += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int x = ax_idx[p];
+    mcsr[p] = mass[static_cast<long long>(x / nsurfp) * nloc + slot_l[x % nsurfp]];
+  }
+}
+
+// stable counting sort of a flat source stream by destination (see device_csr_by_key)
+__global__ void iota_key_kernel(const int* __restrict__ keys, long long n, int nkeys, int* __restrict__ k2,
+                                int* __restrict__ vals, unsigned* __restrict__ counts)
+{
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int k = keys[i];
+    k2[i] = k < 0 ? nkeys : k;
+    vals[i] = static_cast<int>(i);
+    if (k >= 0) atomicAdd(counts + k, 1u);
+  }
+}
+
+__global__ void scatter_pos_kernel(const int* __restrict__ sorted_vals, long long n_valid, long long n,
+                                   int* __restrict__ pos)
+{
+  for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+       p += static_cast<long long>(gridDim.x) * blockDim.x)
+    pos[sorted_vals[p]] = p < n_valid ? static_cast<int>(p) : -1;
+}
+
 }  // namespace hxb

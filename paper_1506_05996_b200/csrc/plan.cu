@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -135,7 +137,8 @@ struct Plan {
   bool amg_local2 = false;  // per-step K-cycle with ksolve(2) as one single-CTA kernel (opt-in: slower at cfg2)
   int *agg1c = nullptr, *mptr1 = nullptr, *mem1 = nullptr;
   int n2 = 0;
-  bool split_combine = true;  // fine half of the combine concurrent with the coarse solve (options.reserved[0] bit 3 off)
+  bool split_combine = true;
+  bool host_lists = false;  // build the fine gather lists on the host (A/B checks of the device sort)  // fine half of the combine concurrent with the coarse solve (options.reserved[0] bit 3 off)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_a = nullptr;
   cudaGraphExec_t coarse_exec = nullptr;
   DeviceArena mem;
@@ -1121,6 +1124,52 @@ void build_dist_ax(Plan& pl, const HostSetup& hs, int /*nsurf_raw*/)
   pl.n_ax_entries = d.off[pl.n_loc_surf];
 }
 
+// Stable counting sort of a flat source stream by destination on the device:
+// keys[i] in [0, nkeys) or -1 (no destination). off = CSR offsets over the
+// destinations; pos[i] = position of source i in its destination's list, in
+// ascending i (the reference's accumulation order), -1 when skipped. Returns
+// the number of entries. (The host equivalent is the two-pass counting sort.)
+long long device_csr_by_key(const int* d_keys, long long n, int nkeys, unsigned* d_off, int* d_pos)
+{
+  if (n > 0x7fffffffLL) throw HxbError(HXB_EINVAL, "device_csr_by_key: too many entries");
+  const int nn = static_cast<int>(n);
+  int *k2 = nullptr, *vals = nullptr, *k2s = nullptr, *valss = nullptr;
+  unsigned* counts = nullptr;
+  HXB_CUDA(cudaMalloc(&k2, sizeof(int) * std::max(nn, 1)));
+  HXB_CUDA(cudaMalloc(&vals, sizeof(int) * std::max(nn, 1)));
+  HXB_CUDA(cudaMalloc(&k2s, sizeof(int) * std::max(nn, 1)));
+  HXB_CUDA(cudaMalloc(&valss, sizeof(int) * std::max(nn, 1)));
+  HXB_CUDA(cudaMalloc(&counts, sizeof(unsigned) * (static_cast<std::size_t>(nkeys) + 1)));
+  HXB_CUDA(cudaMemset(counts, 0, sizeof(unsigned) * (static_cast<std::size_t>(nkeys) + 1)));
+  iota_key_kernel<<<vec_grid(n), kVecBlock>>>(d_keys, n, nkeys, k2, vals, counts);
+  HXB_CUDA(cudaGetLastError());
+  std::size_t b1 = 0, b2 = 0;
+  int bits = 1;
+  while ((1LL << bits) <= nkeys) ++bits;
+  HXB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b1, counts, d_off, nkeys + 1));
+  HXB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b2, k2, k2s, vals, valss, nn, 0, bits));
+  void* tmp = nullptr;
+  HXB_CUDA(cudaMalloc(&tmp, std::max<std::size_t>({b1, b2, 1})));
+  HXB_CUDA(cub::DeviceScan::ExclusiveSum(tmp, b1, counts, d_off, nkeys + 1));
+  HXB_CUDA(cub::DeviceRadixSort::SortPairs(tmp, b2, k2, k2s, vals, valss, nn, 0, bits));  // stable
+  unsigned total = 0;
+  HXB_CUDA(cudaMemcpy(&total, d_off + nkeys, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  scatter_pos_kernel<<<vec_grid(n), kVecBlock>>>(valss, total, n, d_pos);
+  HXB_CUDA(cudaGetLastError());
+  HXB_CUDA(cudaDeviceSynchronize());
+  for (void* q : {static_cast<void*>(k2), static_cast<void*>(vals), static_cast<void*>(k2s), static_cast<void*>(valss),
+                  static_cast<void*>(counts), tmp})
+    cudaFree(q);
+  return total;
+}
+
+template <int NP>
+void launch_sub_keys(const Plan& pl, int* keys)
+{
+  sub_keys_kernel<NP><<<vec_grid(static_cast<long long>(pl.ne) * pl.P * pl.P * pl.P), kVecBlock>>>(
+      pl.smap, 2 * pl.nsurf, pl.sub_face, pl.sfstride, pl.ne, pl.nsg, keys);
+}
+
 template <int NP>
 void launch_geometry(const GeoArgs& a, long long n, cudaStream_t s)
 {
@@ -1246,6 +1295,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   HXB_DISPATCH_NP(pl.np, init_ax_grid, pl);
   HXB_DISPATCH_NP(pl.np, init_fdm_grid, pl, (opt.reserved[0] & 4) != 0);
   pl.split_combine = (opt.reserved[0] & 8) == 0;
+  pl.host_lists = (opt.reserved[0] & 64) != 0;
 
   HXB_CUDA(cudaStreamCreateWithFlags(&pl.s_main, cudaStreamNonBlocking));
   {
@@ -1305,7 +1355,41 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   // surface map [e][2][nsurf]: Dirichlet-encoded global ids and each copy's
   // position in the Ax surface CSR (copies of a node in ascending (e,l) order,
   // mesh.cpp:358-367) - producers write there, gathers stream contiguously
-  if (pl.nranks == 1) {
+  if (pl.nranks == 1 && !pl.host_lists) {  // device sort of the surface copies by node
+    const long long ncopy = static_cast<long long>(ne) * nsurf_raw;
+    int* keys = nullptr;
+    int* pos = nullptr;
+    HXB_CUDA(cudaMalloc(&keys, sizeof(int) * std::max<long long>(1, ncopy)));
+    HXB_CUDA(cudaMalloc(&pos, sizeof(int) * std::max<long long>(1, ncopy)));
+    HXB_CUDA(cudaMemcpy(keys, num.l2g_surf.data(), sizeof(int) * ncopy, cudaMemcpyHostToDevice));
+    pl.ax_off = M.alloc<unsigned>(static_cast<std::size_t>(pl.nsg) + 1);
+    const long long total = device_csr_by_key(keys, ncopy, pl.nsg, pl.ax_off, pos);
+    pl.n_ax_entries = static_cast<unsigned>(total);
+    pl.smap = M.alloc<int>(static_cast<std::size_t>(ne) * 2 * pl.nsurf);
+    HXB_CUDA(cudaMemset(pl.smap, 0, sizeof(int) * static_cast<std::size_t>(ne) * 2 * pl.nsurf));
+    pl.ax_idx = M.alloc<int>(static_cast<std::size_t>(std::max<long long>(total, 1)));
+    surface_map_kernel<<<vec_grid(ncopy), kVecBlock>>>(keys, pos, pl.mask, ne, nsurf_raw, pl.nsurf, pl.smap,
+                                                        pl.ax_idx);
+    HXB_CUDA(cudaGetLastError());
+    pl.n_loc_surf = pl.n_grp0 = pl.nsg;
+    if (pl.do_coarse) {
+      std::vector<int> slot_l(nsurf_raw);
+      for (int k = 0; k < pl.np; ++k)
+        for (int j = 0; j < pl.np; ++j)
+          for (int i = 0; i < pl.np; ++i) {
+            const int sl = surface_slot(pl.np, i, j, k);
+            if (sl >= 0) slot_l[sl] = (k * pl.np + j) * pl.np + i;
+          }
+      int* d_slot = pl.mem.upload(slot_l);
+      pl.mass_csr = M.alloc<double>(static_cast<std::size_t>(std::max<long long>(total, 1)));
+      mass_csr_kernel<<<vec_grid(total), kVecBlock>>>(pl.ax_idx, total, pl.mass, pl.nloc, pl.nsurf, d_slot,
+                                                       pl.mass_csr);
+      HXB_CUDA(cudaGetLastError());
+    }
+    HXB_CUDA(cudaDeviceSynchronize());
+    cudaFree(keys);
+    cudaFree(pos);
+  } else if (pl.nranks == 1) {
     std::vector<unsigned> off(static_cast<std::size_t>(pl.nsg) + 1, 0);
     for (gid g : num.l2g_surf) off[g + 1]++;
     for (int g = 0; g < pl.nsg; ++g) off[g + 1] += off[g];
@@ -1386,6 +1470,18 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.pr_off = M.upload(d.pr_off);
     pl.pr_idx = M.upload(d.pr_idx);
     pl.pr_mass = M.upload(d.pr_mass);
+  } else if (pl.do_fine && !pl.host_lists) {
+    // subdomain contributions' (e, slot)-ordered positions by a device sort
+    const std::size_t nsub = static_cast<std::size_t>(pl.P) * pl.P * pl.P;
+    int* keys = nullptr;
+    HXB_CUDA(cudaMalloc(&keys, sizeof(int) * std::max<std::size_t>(1, ne * nsub)));
+    HXB_DISPATCH_NP(pl.np, launch_sub_keys, pl, keys);
+    HXB_CUDA(cudaGetLastError());
+    pl.fine_off = M.alloc<unsigned>(static_cast<std::size_t>(pl.N) + 1);
+    pl.fine_pos = M.alloc<int>(ne * nsub);
+    const long long total = device_csr_by_key(keys, static_cast<long long>(ne * nsub), pl.N, pl.fine_off, pl.fine_pos);
+    cudaFree(keys);
+    pl.zsort = M.alloc<double>(static_cast<std::size_t>(std::max<long long>(total, 1)));
   } else if (pl.do_fine) {
     const std::size_t nsub = static_cast<std::size_t>(pl.P) * pl.P * pl.P;
     std::vector<unsigned> cnt(static_cast<std::size_t>(pl.N) + 1, 0);
