@@ -53,9 +53,10 @@ struct AxGatherArgs {
   const double* u;
   const std::uint8_t* mask;
   double* r;
-  int num_surface_global;  // nodes gathered (off has one more entry)
+  int num_surface_global;  // one past the last node gathered (off has one more entry)
   const int* nodes;        // null: node t is global id t; else global id of local node t
   DotArgs dot;
+  int t_begin = 0;         // first node gathered (a sub-range of the surface nodes)
 };
 
 __global__ void __launch_bounds__(kGatherBlock) ax_gather_kernel(AxGatherArgs a)
@@ -65,7 +66,8 @@ __global__ void __launch_bounds__(kGatherBlock) ax_gather_kernel(AxGatherArgs a)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = gridDim.x * (kGatherBlock / 32);
   double dot = 0.0;
-  for (int g0 = (blockIdx.x * (kGatherBlock / 32) + warp) * 32; g0 < a.num_surface_global; g0 += nwarps * 32) {
+  for (int g0 = a.t_begin + (blockIdx.x * (kGatherBlock / 32) + warp) * 32; g0 < a.num_surface_global;
+       g0 += nwarps * 32) {
     const double s = warp_csr_sum(a.off, a.idx, [&](int q) { return __ldg(a.rsurf + q); }, g0,
                                   a.num_surface_global, stage[warp]);
     const int t = g0 + lane;

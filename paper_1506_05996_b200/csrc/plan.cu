@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -220,6 +221,13 @@ struct Plan {
   // host-pointer Ax pipeline: copy streams and per-chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> pipe_ev;
+  // host-pointer Ax pipeline: surface-node id runs by the element chunk that
+  // first needs them (H2D) and the chunk after which they are complete (D2H)
+  struct IdRun {
+    int g0, g1, chunk;
+  };
+  std::vector<IdRun> runs_in, runs_out;
+  bool runs_ready = false;
   // distributed preconditioned CG (setup_dist.cpp)
   int* fin_surf = nullptr;    // finalised surface nodes (group 0 + down)
   int n_fin_surf = 0, ib0 = 0, ib1 = 0;
@@ -1801,7 +1809,7 @@ int hxb_apply_A(hxb_plan* plan, const double* u, double* r)
     if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use hxb_dist_apply_A_*");
     HXB_CUDA(cudaSetDevice(pl->device));
     Plan& P = *pl;
-    constexpr int C = 8;
+    constexpr int C = 8;  // measured at cfg2: 8 chunks 10.5 ms, 16 10.8 ms, 32 11.1 ms
     if (!P.s_in) {
       HXB_CUDA(cudaStreamCreateWithFlags(&P.s_in, cudaStreamNonBlocking));
       HXB_CUDA(cudaStreamCreateWithFlags(&P.s_out, cudaStreamNonBlocking));
@@ -1811,6 +1819,104 @@ int hxb_apply_A(hxb_plan* plan, const double* u, double* r)
     const long long NI = static_cast<long long>(P.order - 1) * (P.order - 1) * (P.order - 1);
     const std::size_t sbytes = sizeof(double) * P.nsg;
     cudaEvent_t ev_surf = P.pipe_ev[2 * C], ev_done = P.pipe_ev[2 * C + 1];
+    if (!P.runs_ready) {  // surface nodes as id runs of equal first/last element chunk
+      P.runs_ready = true;
+      const int nsr = surface_slot_count(P.np);
+      std::vector<int> lo(P.nsg, C), hi(P.nsg, -1);
+      const auto& l2s = P.hs.num.l2g_surf;
+      for (long long e = 0; e < P.ne; ++e) {
+        int c = 0;
+        while (c + 1 < C && static_cast<long long>(P.ne) * (c + 1) / C <= e) ++c;
+        for (int q = 0; q < nsr; ++q) {
+          const int g = l2s[e * nsr + q];
+          lo[g] = std::min(lo[g], c);
+          hi[g] = std::max(hi[g], c);
+        }
+      }
+      // within each numbering class (vertices, edge nodes, face nodes: each
+      // ordered roughly along the element order) send u by the suffix minimum
+      // of the first-use chunk and r by the prefix maximum of the completion
+      // chunk: both are monotone, so each class splits into <= C id runs
+      const long long b1 = P.hs.num.num_vertex_nodes;
+      const long long b2 = b1 + static_cast<long long>(P.hs.num.num_edges) * (P.order - 1);
+      const long long bounds[4] = {0, b1, b2, P.nsg};
+      for (int k = 0; k < 3; ++k) {
+        const int s0 = static_cast<int>(bounds[k]), s1 = static_cast<int>(bounds[k + 1]);
+        if (s1 <= s0) continue;
+        std::vector<int> sm(s1 - s0), pm(s1 - s0);
+        int m = C;
+        for (int g = s1 - 1; g >= s0; --g) sm[g - s0] = m = std::min(m, lo[g]);
+        m = -1;
+        for (int g = s0; g < s1; ++g) pm[g - s0] = m = std::max(m, hi[g]);
+        auto runs = [&](const std::vector<int>& key, std::vector<Plan::IdRun>& out) {
+          for (int g = s0; g < s1;) {
+            int h = g + 1;
+            while (h < s1 && key[h - s0] == key[g - s0]) ++h;
+            out.push_back({g, h, std::max(0, std::min(C - 1, key[g - s0]))});
+            g = h;
+          }
+        };
+        runs(sm, P.runs_in);
+        runs(pm, P.runs_out);
+      }
+      auto by_chunk = [](const Plan::IdRun& a, const Plan::IdRun& b) { return a.chunk < b.chunk; };
+      std::stable_sort(P.runs_in.begin(), P.runs_in.end(), by_chunk);
+      std::stable_sort(P.runs_out.begin(), P.runs_out.end(), by_chunk);
+    }
+    if (!P.runs_in.empty()) {
+      // surface u by first use, interior u per chunk (H2D); element kernel per chunk;
+      // surface r gathered and sent as soon as every copy's element chunk is done (D2H)
+      HXB_CUDA(cudaEventRecord(ev_done, P.s_main));
+      HXB_CUDA(cudaStreamWaitEvent(P.s_in, ev_done, 0));
+      std::size_t ri = 0, ro = 0;
+      for (int c = 0; c < C; ++c) {
+        for (; ri < P.runs_in.size() && P.runs_in[ri].chunk <= c; ++ri) {
+          const auto& R = P.runs_in[ri];
+          HXB_CUDA(cudaMemcpyAsync(P.p + R.g0, u + R.g0, sizeof(double) * (R.g1 - R.g0), cudaMemcpyHostToDevice,
+                                   P.s_in));
+        }
+        const int e0 = static_cast<int>(static_cast<long long>(P.ne) * c / C);
+        const int e1 = static_cast<int>(static_cast<long long>(P.ne) * (c + 1) / C);
+        const long long g0 = P.nsg + e0 * NI, cnt = (e1 - e0) * NI;
+        if (cnt > 0)
+          HXB_CUDA(cudaMemcpyAsync(P.p + g0, u + g0, sizeof(double) * cnt, cudaMemcpyHostToDevice, P.s_in));
+        HXB_CUDA(cudaEventRecord(P.pipe_ev[2 * c], P.s_in));
+        HXB_CUDA(cudaStreamWaitEvent(P.s_main, P.pipe_ev[2 * c], 0));
+        if (e1 > e0) HXB_DISPATCH_NP(P.np, launch_ax_elem_range, P, P.p, P.f, e0, e1, P.s_main);
+        const std::size_t ro0 = ro;
+        for (; ro < P.runs_out.size() && P.runs_out[ro].chunk <= c; ++ro) {
+          AxGatherArgs g;  // surface assembly + Dirichlet rows (operator.cpp:278-280) of this run
+          g.rsurf = P.rsurf;
+          g.off = P.ax_off;
+          g.idx = P.ax_idx;
+          g.u = P.p;
+          g.mask = P.mask;
+          g.r = P.f;
+          g.t_begin = P.runs_out[ro].g0;
+          g.num_surface_global = P.runs_out[ro].g1;
+          g.nodes = nullptr;
+          g.dot = DotArgs{};
+          const int n = P.runs_out[ro].g1 - P.runs_out[ro].g0;
+          ax_gather_kernel<<<std::max(1, std::min(fill_grid(ax_gather_kernel, kGatherBlock, P.nsg),
+                                                  (n + kGatherBlock - 1) / kGatherBlock)),
+                             kGatherBlock, 0, P.s_main>>>(g);
+          P.launches += 1;
+        }
+        HXB_CUDA(cudaEventRecord(P.pipe_ev[2 * c + 1], P.s_main));
+        HXB_CUDA(cudaStreamWaitEvent(P.s_out, P.pipe_ev[2 * c + 1], 0));
+        if (cnt > 0)
+          HXB_CUDA(cudaMemcpyAsync(r + g0, P.f + g0, sizeof(double) * cnt, cudaMemcpyDeviceToHost, P.s_out));
+        for (std::size_t q = ro0; q < ro; ++q) {
+          const auto& R = P.runs_out[q];
+          HXB_CUDA(cudaMemcpyAsync(r + R.g0, P.f + R.g0, sizeof(double) * (R.g1 - R.g0), cudaMemcpyDeviceToHost,
+                                   P.s_out));
+        }
+        P.launches += 1;
+      }
+      HXB_CUDA(cudaGetLastError());
+      HXB_CUDA(cudaStreamSynchronize(P.s_out));
+      return;
+    }
     HXB_CUDA(cudaEventRecord(ev_done, P.s_main));  // previous work on the plan's buffers is ordered first
     HXB_CUDA(cudaStreamWaitEvent(P.s_in, ev_done, 0));
     HXB_CUDA(cudaMemcpyAsync(P.p, u, sbytes, cudaMemcpyHostToDevice, P.s_in));
