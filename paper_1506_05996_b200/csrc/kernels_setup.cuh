@@ -153,6 +153,34 @@ __global__ void mass_csr_kernel(const int* __restrict__ ax_idx, long long n, con
   }
 }
 
+// Lumped mass m_N = gather of the local masses (SemOperator ctor,
+// operator.cpp:90-91): surface nodes sum their copies in the CSR's (e, l)
+// order from 0, interior nodes have one copy (0 + m = m); and 1/m_N. Same
+// additions in the same order as the host loop, so bitwise equal.
+template <int NP>
+__global__ void lumped_mass_kernel(const unsigned* __restrict__ off, const int* __restrict__ ax_idx,
+                                   const double* __restrict__ mass, const int* __restrict__ slot_l, int nsurfp,
+                                   int nsg, int n, double* __restrict__ lumped, double* __restrict__ inv_lumped)
+{
+  constexpr int nn = NP - 1, NI = (nn - 1) * (nn - 1) * (nn - 1), NL = NP * NP * NP;
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    if (g < nsg) {
+      for (unsigned q = __ldg(off + g); q < __ldg(off + g + 1); ++q) {
+        const int x = __ldg(ax_idx + q);
+        s += __ldg(mass + static_cast<long long>(x / nsurfp) * NL + __ldg(slot_l + x % nsurfp));
+      }
+    } else if constexpr (NI > 0) {
+      const int t = g - nsg, l = t % NI;
+      const long long e = t / NI;
+      const int i = 1 + l % (nn - 1), j = 1 + (l / (nn - 1)) % (nn - 1), k = 1 + l / ((nn - 1) * (nn - 1));
+      s += __ldg(mass + e * NL + (k * NP + j) * NP + i);
+    }
+    lumped[g] = s;
+    inv_lumped[g] = 1.0 / s;
+  }
+}
+
 // stable counting sort of a flat source stream by destination (see device_csr_by_key)
 __global__ void iota_key_kernel(const int* __restrict__ keys, long long n, int nkeys, int* __restrict__ k2,
                                 int* __restrict__ vals, unsigned* __restrict__ counts)

@@ -1172,6 +1172,13 @@ long long device_csr_by_key(const int* d_keys, long long n, int nkeys, unsigned*
 }
 
 template <int NP>
+void launch_lumped(Plan& pl, const int* d_slot)
+{
+  lumped_mass_kernel<NP><<<vec_grid(pl.N), kVecBlock>>>(pl.ax_off, pl.ax_idx, pl.mass, d_slot, pl.nsurf, pl.nsg,
+                                                          pl.N, pl.d_lumped, pl.d_inv_lumped);
+}
+
+template <int NP>
 void launch_sub_keys(const Plan& pl, int* keys)
 {
   sub_keys_kernel<NP><<<vec_grid(static_cast<long long>(pl.ne) * pl.P * pl.P * pl.P), kVecBlock>>>(
@@ -1230,8 +1237,11 @@ void device_geometry(Plan& pl, HostSetup& hs, const hxb_options& opt)
   if (first_bad != big)
     throw HxbError(HXB_EMESH, "inverted element " + std::to_string(first_bad) +
                                   ": non-positive Jacobian determinant at a GLL node");
-  hs.geo.mass.resize(static_cast<std::size_t>(ne) * nloc);
-  HXB_CUDA(cudaMemcpy(hs.geo.mass.data(), mass, hs.geo.mass.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  const bool device_lumped = std::max(1, opt.reserved[2]) == 1 && (opt.reserved[0] & 64) == 0;
+  if (!device_lumped) {  // host consumers: lumped mass, host gather lists, distributed setup
+    hs.geo.mass.resize(static_cast<std::size_t>(ne) * nloc);
+    HXB_CUDA(cudaMemcpy(hs.geo.mass.data(), mass, hs.geo.mass.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  }
   pl.wg = a.wg;
   pl.mass = nranks == 1 ? mass : nullptr;
 }
@@ -1264,6 +1274,9 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   so.direct_threshold = opt.direct_threshold;
   so.store_planes = opt.variant == HXB_VARIANT_STORED;
   so.geometry_hook = [&pl, &opt](HostSetup& h) { device_geometry(pl, h, opt); };
+  // single-device plan with device lists: the lumped mass is assembled on the
+  // device after the surface CSR exists, so the masses never go back to the host
+  so.device_lumped = std::max(1, opt.reserved[2]) == 1 && (opt.reserved[0] & 64) == 0;
   setup_phase("mesh + checks");
   build_host_setup(hs, order, so);
   setup_phase("device: streams, tables");
@@ -1352,8 +1365,8 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   pl.mask = M.upload(num.dirichlet_mask);
   pl.zero_mask = M.alloc<std::uint8_t>(pl.N);
   HXB_CUDA(cudaMemset(pl.zero_mask, 0, pl.N));
-  pl.d_lumped = M.upload(hs.lumped);
-  {
+  if (!hs.lumped.empty()) {  // else assembled on the device once the surface CSR exists
+    pl.d_lumped = M.upload(hs.lumped);
     std::vector<double> inv(hs.lumped.size());
     for (std::size_t g = 0; g < inv.size(); ++g) inv[g] = 1.0 / hs.lumped[g];
     pl.d_inv_lumped = M.upload(inv);
@@ -1393,6 +1406,22 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
       mass_csr_kernel<<<vec_grid(total), kVecBlock>>>(pl.ax_idx, total, pl.mass, pl.nloc, pl.nsurf, d_slot,
                                                        pl.mass_csr);
       HXB_CUDA(cudaGetLastError());
+    }
+    if (hs.lumped.empty()) {  // lumped mass and 1/m_N from the device masses in CSR order
+      std::vector<int> slot_l(nsurf_raw);
+      for (int k = 0; k < pl.np; ++k)
+        for (int j = 0; j < pl.np; ++j)
+          for (int i = 0; i < pl.np; ++i) {
+            const int sl = surface_slot(pl.np, i, j, k);
+            if (sl >= 0) slot_l[sl] = (k * pl.np + j) * pl.np + i;
+          }
+      int* d_slot = M.upload(slot_l);
+      pl.d_lumped = M.alloc<double>(pl.N);
+      pl.d_inv_lumped = M.alloc<double>(pl.N);
+      HXB_DISPATCH_NP(pl.np, launch_lumped, pl, d_slot);
+      HXB_CUDA(cudaGetLastError());
+      hs.lumped.resize(pl.N);  // host copy for the load vector and exports
+      HXB_CUDA(cudaMemcpy(hs.lumped.data(), pl.d_lumped, sizeof(double) * pl.N, cudaMemcpyDeviceToHost));
     }
     HXB_CUDA(cudaDeviceSynchronize());
     cudaFree(keys);

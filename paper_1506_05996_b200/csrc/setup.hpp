@@ -190,6 +190,7 @@ struct SetupOptions {
   // when set, replaces the host per-node geometry: must fill hs.geo.mass (all
   // elements); hs.geo.h is computed on the host either way (device plans)
   std::function<void(HostSetup&)> geometry_hook;
+  bool device_lumped = false;  // the plan assembles the lumped mass on the device (hs.lumped filled later)
 };
 
 struct HostSetup {

@@ -78,11 +78,13 @@ void build_host_setup(HostSetup& hs, int order, const SetupOptions& opt)
   hs.num = build_numbering(hs.mesh, order);
   setup_phase("lumped mass");
   const int nloc = hs.basis.npts() * hs.basis.npts() * hs.basis.npts();
-  hs.lumped.assign(hs.num.num_global, 0.0);
-  std::vector<gid> l2g(nloc);
-  for (int e = 0; e < ne; ++e) {
-    element_l2g(hs.num, ne, e, l2g.data());
-    for (int l = 0; l < nloc; ++l) hs.lumped[l2g[l]] += hs.geo.mass[static_cast<std::size_t>(e) * nloc + l];
+  if (!opt.device_lumped) {
+    hs.lumped.assign(hs.num.num_global, 0.0);
+    std::vector<gid> l2g(nloc);
+    for (int e = 0; e < ne; ++e) {
+      element_l2g(hs.num, ne, e, l2g.data());
+      for (int l = 0; l < nloc; ++l) hs.lumped[l2g[l]] += hs.geo.mass[static_cast<std::size_t>(e) * nloc + l];
+    }
   }
   hs.pencil = build_pencil(hs.basis);
   if (hs.do_coarse) {

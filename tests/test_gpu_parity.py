@@ -128,6 +128,7 @@ def test_device_fine_lists_match_host(k, order, family):
     mesh = hx.generate_cube_mesh(k, family)
     a = hx.Plan(mesh, order)
     b = hx.Plan(mesh, order, host_lists=True)
+    assert np.array_equal(a.lumped_mass(), b.lumped_mass())  # device assembly of m_N
     r = splitmix_vector(a.N, 17)
     assert np.array_equal(a.apply_A(r), b.apply_A(r))
     assert np.array_equal(a.apply_fine(r), b.apply_fine(r))
