@@ -88,7 +88,8 @@ typedef struct hxb_options {
                                   bit 3: one fused combine after the coarse solve instead of
                                   the fine half running concurrently with it; bit 5: ksolve(2)
                                   on the compacted levels as one single-CTA kernel (measured
-                                  slower at cfg2: 1.23 vs 0.82 ms per coarse solve); bit 6:
+                                  slower at cfg2: 1.23 vs 0.82 ms per coarse solve); bit 8: FDM
+                                  subdomains in element order instead of Morton order; bit 6:
                                   build the fine-solve gather lists with the host counting sort
                                   instead of the device radix sort (A/B checks);
                                   reserved[1] = rank, reserved[2] = number of ranks: element-slab

@@ -88,6 +88,7 @@ struct FdmArgs {
   double* fsend = nullptr;  // distributed plans: contributions finalised by a neighbour (pos <= -2)
   int ne, sstride, num_surface_global;
   int sfstride;             // per-element stride of sub_face (6 np^2 padded to 4 ints: TMA rows)
+  const int* order = nullptr;  // optional CTA -> element map (L2-friendly traversal); results do not depend on it
 };
 
 // out[q] = sum_m MT[m*P+q] in[m] (dense, m ascending = tensor_pass order)
@@ -173,7 +174,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
   __shared__ double tab[kTab];  // dense fallback only: V^T, V^-T as warp-uniform broadcasts
   const OrderTables& T = c_tab[NP];
   const FdmConst& C = c_fdm[NP];  // even/odd tables, lambda, 1/M: constant bank
-  const int e = blockIdx.x;
+  const int e = a.order ? __ldg(a.order + blockIdx.x) : static_cast<int>(blockIdx.x);
   const int tid = threadIdx.x;
   const bool lt = tid < Sh::kLines;
   const int la = tid % P, lb = tid / P;

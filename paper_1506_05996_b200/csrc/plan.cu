@@ -139,6 +139,7 @@ struct Plan {
   int *agg1c = nullptr, *mptr1 = nullptr, *mem1 = nullptr;
   int n2 = 0;
   bool split_combine = true;
+  int* fdm_order = nullptr;  // FDM CTA -> element: Morton order of element centroids (neighbours close in time)
   bool host_lists = false;  // build the fine gather lists on the host (A/B checks of the device sort)  // fine half of the combine concurrent with the coarse solve (options.reserved[0] bit 3 off)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_a = nullptr;
   cudaGraphExec_t coarse_exec = nullptr;
@@ -492,6 +493,7 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   a.Rpart = pl.do_coarse ? pl.Rpart + 8LL * pl.e0 : nullptr;  // owned slab of the full Rpart
   a.fsend = pl.fsend;
   a.sfstride = pl.sfstride;
+  a.order = pl.fdm_order;
   KtScope kt(pl, HXB_KT_FDM, s);
   pl.launches += 1;
   if (pl.fdm_grid > 0)
@@ -1555,6 +1557,42 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     }
   }
 
+  if (pl.do_fine && pl.nranks == 1 && (opt.reserved[0] & 256) == 0) {
+    // Morton (z-order) traversal of the element centroids for the FDM: the
+    // face neighbours whose first layers a subdomain reads are processed
+    // close in time, so their r values are still in L2
+    double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+    std::vector<std::array<double, 3>> cen(ne);
+    for (int e = 0; e < ne; ++e) {
+      std::array<double, 3> c{0, 0, 0};
+      for (int q = 0; q < 8; ++q)
+        for (int d = 0; d < 3; ++d) c[d] += 0.125 * mesh.vertices[mesh.elements[e][q]][d];
+      cen[e] = c;
+      for (int d = 0; d < 3; ++d) lo[d] = std::min(lo[d], c[d]), hi[d] = std::max(hi[d], c[d]);
+    }
+    auto spread = [](std::uint64_t v) {  // 21 bits -> every third bit
+      v &= 0x1fffff;
+      v = (v | v << 32) & 0x1f00000000ffffULL;
+      v = (v | v << 16) & 0x1f0000ff0000ffULL;
+      v = (v | v << 8) & 0x100f00f00f00f00fULL;
+      v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+      v = (v | v << 2) & 0x1249249249249249ULL;
+      return v;
+    };
+    std::vector<std::pair<std::uint64_t, int>> key(ne);
+    for (int e = 0; e < ne; ++e) {
+      std::uint64_t m = 0;
+      for (int d = 0; d < 3; ++d) {
+        const double t = hi[d] > lo[d] ? (cen[e][d] - lo[d]) / (hi[d] - lo[d]) : 0.0;
+        m |= spread(static_cast<std::uint64_t>(t * 2097151.0)) << d;
+      }
+      key[e] = {m, e};
+    }
+    std::sort(key.begin(), key.end());
+    std::vector<int> ord(ne);
+    for (int e = 0; e < ne; ++e) ord[e] = key[e].second;
+    pl.fdm_order = M.upload(ord);
+  }
   setup_phase("coarse device");
   // coarse: connectivity, vertex incidence CSR (e, cb) order, coarse matrix, AMG / dense
   if (pl.do_coarse) {

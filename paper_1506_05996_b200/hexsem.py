@@ -331,7 +331,8 @@ class Plan:
                  coarse_solve: str = "automatic", direct_threshold: int = 64000, variant: str = "stored",
                  device: int = 0, amg_cluster: bool = False, rank: int = 0, nranks: int = 1,
                  fdm_pipeline: bool = False, split_combine: bool = True,
-                 amg_local_small: bool = False, host_lists: bool = False):
+                 amg_local_small: bool = False, host_lists: bool = False,
+                 fdm_morton: bool = True):
         L = lib()
         ne = mesh.num_elements
         self.mesh = mesh
@@ -344,7 +345,7 @@ class Plan:
         opt.direct_threshold = direct_threshold
         opt.variant = VARIANTS[variant]
         opt.device = device
-        opt.reserved[0] = (1 if amg_cluster else 0) | (4 if fdm_pipeline else 0) | (0 if split_combine else 8) | (32 if amg_local_small else 0) | (64 if host_lists else 0)
+        opt.reserved[0] = (1 if amg_cluster else 0) | (4 if fdm_pipeline else 0) | (0 if split_combine else 8) | (32 if amg_local_small else 0) | (64 if host_lists else 0) | (0 if fdm_morton else 256)
         opt.reserved[1] = rank
         opt.reserved[2] = nranks
         cm = mesh._c()

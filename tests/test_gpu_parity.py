@@ -137,6 +137,18 @@ def test_device_fine_lists_match_host(k, order, family):
     assert np.array_equal(ra["residual_history"], rb["residual_history"]) and np.array_equal(ra["u"], rb["u"])
 
 
+@pytest.mark.parametrize("k,order", [(12, 7), (7, 3)])
+def test_fdm_morton_order_is_bitwise_neutral(k, order):
+    """The FDM's CTA -> element traversal (Morton order of the centroids, for
+    L2 reuse of the neighbours' layers) does not change any result."""
+    mesh = hx.generate_cube_mesh(k, "distorted_domain")
+    a = hx.Plan(mesh, order)
+    b = hx.Plan(mesh, order, fdm_morton=False)
+    r = splitmix_vector(a.N, 23)
+    assert np.array_equal(a.apply_fine(r), b.apply_fine(r))
+    assert np.array_equal(a.apply_P(r), b.apply_P(r))
+
+
 def test_device_geometry_rejects_inverted_element():
     mesh = hx.generate_cube_mesh(2)
     mesh.conn[3] = mesh.conn[3][[1, 0, 2, 3, 5, 4, 6, 7]]  # mirrored: det J < 0 everywhere
