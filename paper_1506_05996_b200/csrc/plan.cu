@@ -1619,7 +1619,6 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.Zc = M.alloc<double>(static_cast<std::size_t>(ne) * 8);
     pl.coarse_n = hs.Kc.n;
     if (pl.use_amg) {
-      pl.Kc = csr_to_device(pl, hs.Kc);
       const AmgSetup& amg = hs.amg;
       const int L = static_cast<int>(amg.levels.size());
       pl.lv.resize(L + 1);
@@ -1647,6 +1646,12 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
         pl.lv[l].x = M.alloc<double>(pl.lv[l].n);
       }
       pl.dense = dense_to_device(pl, amg.coarsest);
+      // rho = R - K_c Z reads the same matrix as AMG level 0 (amg.cpp:151-160): share it
+      const Csr& A0 = amg.levels.empty() ? hs.Kc : amg.levels[0].A;
+      if (!amg.levels.empty() && A0.n == hs.Kc.n && A0.ptr == hs.Kc.ptr && A0.col == hs.Kc.col && A0.val == hs.Kc.val)
+        pl.Kc = pl.lv[0].A;
+      else
+        pl.Kc = csr_to_device(pl, hs.Kc);
       const bool want_cluster = (opt.reserved[0] & 1) != 0;
       const bool compact = (opt.reserved[0] & 32) != 0 || want_cluster;
       const bool built = compact && build_amg_cluster(pl, amg, hs.vmask);
