@@ -1253,6 +1253,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   const auto t0 = std::chrono::steady_clock::now();
   setup_phase("device init");
   if (!m) throw HxbError(HXB_EINVAL, "mesh must be non-null");
+  if (m->num_elements <= 0) throw HxbError(HXB_EINVAL, "mesh has no hexahedra");  // cf. mesh_io.cpp:118
   if (opt.variant != HXB_VARIANT_STORED && opt.variant != HXB_VARIANT_ON_THE_FLY)
     throw HxbError(HXB_EINVAL, "unknown operator variant");
   pl.device = opt.device;

@@ -100,3 +100,15 @@ def test_plan_create_fails_loudly_without_gpu():
     with pytest.raises(hx.HxbError) as ei:
         hx.Plan(mesh, 2)
     assert ei.value.code == 4
+
+
+def test_plan_rejects_empty_mesh():
+    """An empty mesh is an argument error (HXB_EINVAL), raised before any
+    device work, like the reference readers' "no hexahedra" (mesh_io.cpp:118)."""
+    import numpy as np
+
+    empty = hx.HexMesh(np.zeros((0, 3)), np.zeros((0, 8), dtype=np.int32), np.zeros(0, dtype=np.int32),
+                       np.zeros(0, dtype=np.int32), np.zeros(0, dtype=np.uint8))
+    with pytest.raises(hx.HxbError) as ei:
+        hx.Plan(empty, 3)
+    assert ei.value.code == 1 and "no hexahedra" in str(ei.value)
