@@ -322,9 +322,12 @@ def run_ours(args, rank, world, local_rank):
         res = plan.pcg_device(None, tol=1e-8, max_iterations=500, want_u=False)
         pcg_launches = plan.launch_count() - l0
         solve_s = max_over_ranks(res["solve_seconds"])
-        b_host = plan.load_ones()
+        # host b in and host u out through pinned buffers (the contract's e2e leg)
+        b_pin = torch.empty(N, dtype=torch.float64).pin_memory().numpy()
+        u_pin = torch.empty(N, dtype=torch.float64).pin_memory().numpy()
+        b_pin[:] = plan.load_ones()
         t = time.perf_counter()
-        res_e2e = plan.pcg(b_host, tol=1e-8, max_iterations=500, want_u=True)
+        res_e2e = plan.pcg(b_pin, tol=1e-8, max_iterations=500, u_out=u_pin)
         e2e_solve = max_over_ranks(time.perf_counter() - t)
         pcg = {"tol": 1e-8, "iterations": res["iterations"], "status": res["status"],
                "solve_s": solve_s, "ms_per_iteration": solve_s * 1e3 / max(1, res["iterations"]),

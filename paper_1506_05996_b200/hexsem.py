@@ -423,11 +423,15 @@ class Plan:
         _check(lib().hxb_apply_P_device(self._h, C.c_void_p(d_r), C.c_void_p(d_z), C.c_void_p(stream or None)))
 
     # --- solve ------------------------------------------------------------------
-    def _solve(self, fn, bptr, tol, max_iterations, want_u=True):
+    def _solve(self, fn, bptr, tol, max_iterations, want_u=True, u_out=None):
         cfg = _PcgConfig(float(tol), int(max_iterations), 1)
         rh = np.zeros(max_iterations + 1)
         zh = np.zeros(max_iterations + 1)
-        u = np.zeros(self.N) if want_u else None
+        if u_out is not None:  # caller-owned (e.g. pinned) output buffer
+            if u_out.dtype != np.float64 or u_out.shape != (self.N,) or not u_out.flags.c_contiguous:
+                raise ValueError("pcg: u_out must be a contiguous float64 array of length N")
+            want_u = True
+        u = (u_out if u_out is not None else np.zeros(self.N)) if want_u else None
         res = _PcgResult()
         res.residual_history = rh.ctypes.data_as(C.POINTER(C.c_double))
         res.zr_history = zh.ctypes.data_as(C.POINTER(C.c_double))
@@ -437,13 +441,14 @@ class Plan:
                 "residual_history": rh[:res.num_residuals].copy(), "zr_history": zh[:res.num_zr].copy(),
                 "u": u, "solve_seconds": float(res.solve_seconds), "diagnostic": res.diagnostic.decode()}
 
-    def pcg(self, b=None, tol: float = 1e-6, max_iterations: int = 500, want_u: bool = True) -> dict:
+    def pcg(self, b=None, tol: float = 1e-6, max_iterations: int = 500, want_u: bool = True, u_out=None) -> dict:
         """pcg(operator_fn, preconditioner_fn, b, cfg) (krylov.cpp:20-71) on the device.
-        b=None uses the Poisson load m_N*1 masked (problem.cpp:129)."""
+        b=None uses the Poisson load m_N*1 masked (problem.cpp:129). u_out: optional
+        caller-owned output array (pinned host memory makes the copies DMA-speed)."""
         bb = None if b is None else np.ascontiguousarray(b, dtype=np.float64)
         if bb is not None and bb.shape != (self.N,):
             raise ValueError("pcg: vector length mismatch")
-        return self._solve(lib().hxb_solve, _ptr(bb), tol, max_iterations, want_u)
+        return self._solve(lib().hxb_solve, _ptr(bb), tol, max_iterations, want_u, u_out)
 
     def pcg_device(self, d_b: int | None, tol: float = 1e-6, max_iterations: int = 500, want_u: bool = False):
         return self._solve(lib().hxb_solve_device, C.c_void_p(d_b) if d_b else None, tol, max_iterations, want_u)
