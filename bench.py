@@ -12,22 +12,22 @@ headline `value` is Ax GDOF/s = N / (ms per step) with u already in HBM;
 region). The PCG solve to 1e-8 (the metric's second half) is measured in the
 same run and reported under "pcg" (device-timed, plus the host-API e2e).
 
-`roofline` is for the dominant kernel (ax_elem_kernel): algorithmic bytes =
-the reference's own model B_R = 8*NE*(10 np^3 + np^2 + 2)
-(operator.cpp:31-37) per launch / its CUDA-event duration measured
-live over the timed region, against MEASURED_PEAKS.json hbm_gbs.
+`roofline` is for the Ax step (ax_elem_kernel + ax_gather_kernel): the
+reference's own byte model B_R = 8*NE*(10 np^3 + np^2 + 2) (operator.cpp:31-37,
+SURVEY §8d) divided by the device-timed step, against MEASURED_PEAKS.json
+hbm_gbs; the element kernel's own share (live CUDA-event time, ncu DRAM bytes)
+is a sub-field. `pcg.roofline` does the same for a whole PCG iteration
+(Ax + FDM + restriction/prolongation + vector passes).
 
-`cpu_baseline`: the unmodified reference (oracle/_ref/libhexsem_ref.so,
-compiled from /root/reference sources by oracle/Makefile) timed on this box's
-host cores on a bounded sample (26^3 hexes, N=7; the reference Ax is
-single-threaded by design, so cores=1).
+`cpu_baseline` and `--impl reference` run the unmodified reference
+(oracle/_ref/libhexsem_ref.so, compiled from /root/reference sources by
+oracle/Makefile) on this box's host cores at the SAME cfg2 workload: its Ax
+(single-threaded by design) and its two-scale PCG to 1e-8 in its fastest mode
+(fine_threads = cores-1, coarse solve concurrent), measured, not extrapolated.
 
-`--impl reference` times that same reference library's SemOperator::apply on
-the bounded sample, rank 0 only.
-
-Multi-GPU (torchrun, N>1): each rank runs its own cfg2 replica (weak scaling,
-no data-path collective); element-slab domain decomposition with halo
-exchange is not in this round.
+Multi-GPU (torchrun, N>1): the cfg2 mesh is split into N element slabs
+(strong scaling, `"scaling": "strong"`); `--replicas` runs N independent cfg2
+replicas instead (weak scaling).
 """
 from __future__ import annotations
 
@@ -135,15 +135,29 @@ class ClockSampler:
                 "power_w_max": max((num(r[3]) or 0) for r in rows)}
 
 
+def workload_config(k: int, order: int, N: int, NE: int) -> dict:
+    """The one `config` both arms print (same keys, same values)."""
+    return {"workload": f"cfg2: {k}^3 uniform hexes, N={order}, Poisson kappa=1 c=0, all-Dirichlet; "
+                        "step = one Ax (SemOperator::apply); PCG to 1e-8 under pcg",
+            "k": k, "order": order, "N": N, "NE": NE,
+            "l2": "inputs larger than L2 (5.83 GB per Ax vs 126 MB L2); no flush"}
+
+
 # ---------------------------------------------------------------------------
-def cpu_reference_ax(k: int, order: int, steps: int, warmup: int):
-    """Reference SemOperator::apply (oracle/_ref, unmodified sources) on a k^3 mesh."""
+def cpu_reference(k: int, order: int, steps: int, warmup: int, pcg: bool):
+    """The unmodified reference (oracle/_ref) on this host at the given
+    workload: SemOperator::apply timed `steps` times after `warmup`, and one
+    two-scale pcg to 1e-8 (krylov.cpp:20-71) in the reference's fastest mode
+    (fine_threads = cores-1 plus the concurrent coarse solve, precond.cpp:38-45),
+    timed by the reference itself (PcgResult wall clock)."""
     from oracle import RefConfig, RefSystem, ref_available, splitmix_vector, OracleSystem
 
     kind = "reference" if ref_available() else "port"
     cls = RefSystem if kind == "reference" else OracleSystem
+    cores = os.cpu_count() or 1
     t0 = time.time()
-    sys_ = cls(RefConfig(k=k, order=order, precond="none"))
+    sys_ = cls(RefConfig(k=k, order=order, precond="two_scale", concurrent_precond=True,
+                         fine_threads=max(1, cores - 1)))
     setup_s = time.time() - t0
     u = splitmix_vector(sys_.N, 12345)
     for _ in range(warmup):
@@ -153,49 +167,62 @@ def cpu_reference_ax(k: int, order: int, steps: int, warmup: int):
         t = time.perf_counter()
         sys_.apply_A(u)
         times.append(time.perf_counter() - t)
-    N = sys_.N
+    out = {"kind": kind, "N": sys_.N, "mean_s": sum(times) / len(times), "best_s": min(times),
+           "setup_s": setup_s, "steps": steps, "warmup": warmup, "cores": cores}
+    if pcg:
+        b = sys_.load_ones()
+        t = time.perf_counter()
+        res = sys_.pcg(b, tol=1e-8, max_iterations=500)
+        out["pcg"] = {"iterations": res["iterations"], "status": res["status"], "solve_s": res["solve_seconds"],
+                      "wall_s": time.perf_counter() - t, "threads": cores,
+                      "mode": f"two_scale, fine_threads={max(1, cores - 1)}, concurrent coarse (reference fastest)",
+                      "r_final_over_r0": float(res["residual_history"][-1] / res["residual_history"][0])}
     sys_.close()
-    mean = sum(times) / len(times)
-    return {"kind": kind, "N": N, "mean_s": mean, "best_s": min(times), "setup_s": setup_s, "steps": steps}
-
-
-def cpu_reference_pcg(k: int, order: int, iters: int, threads: int):
-    """Reference two-scale pcg (krylov.cpp:20-71) in its fastest legal mode
-    (fine_threads = cores-1, concurrent coarse), capped at `iters` iterations."""
-    from oracle import RefConfig, RefSystem, ref_available
-
-    if not ref_available():
-        return None
-    s = RefSystem(RefConfig(k=k, order=order, precond="two_scale", concurrent_precond=True,
-                            fine_threads=max(1, threads - 1)))
-    b = s.load_ones()
-    res = s.pcg(b, tol=1e-8, max_iterations=iters)
-    out = {"N": s.N, "iterations": res["iterations"], "solve_s": res["solve_seconds"],
-           "s_per_iteration": res["solve_seconds"] / max(1, res["iterations"])}
-    s.close()
     return out
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    cores = os.cpu_count() or 1
-    r = cpu_reference_ax(SAMPLE_K, args.order, args.steps, args.warmup)
+    r = cpu_reference(args.k, args.order, args.steps, args.warmup, not args.no_pcg)
     gdofs = r["N"] / r["mean_s"] / 1e9
+    NE = args.k ** 3
     line = {
         "impl": "reference", "metric": METRIC, "value": gdofs, "unit": "GDOF/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["mean_s"] * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated mesh, splitmix64 u)",
-        "config": {"workload": f"cfg2 Ax (SemOperator::apply), bounded sample {SAMPLE_K}^3 hexes N={args.order}",
-                   "k": SAMPLE_K, "order": args.order, "N": r["N"], "parallelism": "1 host thread"},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (generated mesh, splitmix64 u, s=1 load)",
+        "config": workload_config(args.k, args.order, r["N"], NE),
+        "parallelism": f"host CPU: Ax single-threaded by design (operator.cpp:255-287); PCG {r['cores']} threads",
         "cpu_baseline": {"value": gdofs, "unit": "GDOF/s", "cores": 1, "kind": r["kind"],
-                         "sample": f"SemOperator::apply on {SAMPLE_K}^3 hexes N={args.order} ({r['N']} DOF), "
-                                   f"mean of {args.steps} after {args.warmup} warm-up; reference Ax is "
-                                   f"single-threaded (host has {cores} cores)"},
+                         "sample": f"reference SemOperator::apply on the full cfg2 mesh ({r['N']} DOF), mean of "
+                                   f"{args.steps} after {args.warmup} warm-up (host has {r['cores']} cores)"},
         "e2e": {"value": gdofs, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "pcg": r.get("pcg"), "setup_s": r["setup_s"],
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def pcg_roofline(N: int, NE: int, order: int, ms_per_iteration: float, peak: float) -> dict:
+    """Algorithmic bytes of one two-scale PCG iteration over
+    its device time: Ax (B_R, operator.cpp:31-37), the fine solves (B_P,
+    fine.cpp:88-92), the coarse restriction (r, 1/m_N and the local masses,
+    coarse.cpp:138-162) and prolongation + combine (local masses, 1/m_N, r,
+    the mask and z, coarse.cpp:164-186 + precond.cpp:56-66), and the vector
+    passes of krylov.cpp:53-66 (u, r updates with p, f; p = z + beta p: 9 N
+    words)."""
+    np1, p = order + 1, order + 3
+    nl = NE * np1 ** 3
+    parts = {"ax": 8 * NE * (10 * np1 ** 3 + np1 ** 2 + 2),
+             "fine": 8 * NE * (3 * p ** 3 + 4 * p ** 2),
+             "restrict": 8 * (2 * N + nl),
+             "prolong_combine": 8 * (4 * N + nl) + N,
+             "vectors": 8 * 9 * N}
+    total = sum(parts.values())
+    gbs = total / (ms_per_iteration * 1e-3) / 1e9
+    return {"bound": "hbm", "bytes_per_iteration": total, "parts": parts, "achieved": gbs, "peak": peak,
+            "unit": "GB/s", "frac": gbs / peak}
 
 
 # ---------------------------------------------------------------------------
@@ -249,10 +276,8 @@ def run_ours(args, rank, world, local_rank):
     bytes_ax = 8 * NE * (10 * np1 ** 3 + np1 ** 2 + 2)  # B_R, operator.cpp:31-37 (this rank's share)
     bytes_fdm = 8 * NE * (3 * (order + 3) ** 3 + 4 * (order + 3) ** 2)  # B_P, fine.cpp:88-92
 
-    # u: splitmix64 seed 12345 (oracles.cpp:126-139), Dirichlet entries zeroed
-    from oracle import splitmix_vector  # input generator only (same vector the reference is fed)
-
-    u_host = splitmix_vector(N, 12345)
+    # u: splitmix64 seed 12345 (oracles.cpp:126-139), the vector the reference is fed
+    u_host = hx.synthetic_vector(N, 12345)
     d_u = torch.from_numpy(u_host).to("cuda")
     d_r = torch.empty(N, dtype=torch.float64, device="cuda")
     stream = torch.cuda.current_stream().cuda_stream
@@ -387,50 +412,48 @@ def run_ours(args, rank, world, local_rank):
             otf = {"error": str(exc)}
     clocks = sampler.stop()
 
-    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------
+    # ---- CPU baseline (rank 0, N=1 only): the reference at the same cfg2 workload
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cores = os.cpu_count() or 1
         try:
-            r = cpu_reference_ax(SAMPLE_K, order, 3, 1)
+            r = cpu_reference(k, order, 3, 1, not (args.no_pcg or args.no_cpu_pcg))
             cpu = {"value": r["N"] / r["mean_s"] / 1e9, "unit": "GDOF/s", "cores": 1, "kind": r["kind"],
-                   "sample": f"reference SemOperator::apply on {SAMPLE_K}^3 hexes N={order} ({r['N']} DOF), "
-                             f"mean of 3 after 1 warm-up, single-threaded by design; host has {cores} cores"}
-            if not args.no_pcg:
-                pr = cpu_reference_pcg(SAMPLE_K, order, 4, cores)
-                if pr:
-                    cpu["pcg_sample"] = {
-                        **pr, "threads": cores,
-                        "note": f"two-scale pcg, {pr['iterations']} iterations on {SAMPLE_K}^3 N={order}, "
-                                f"fine_threads={max(1, cores - 1)} + concurrent coarse (reference fastest mode)",
-                        "cfg2_solve_s_extrapolated": pr["s_per_iteration"] * (N / pr["N"]) *
-                                                     (pcg["iterations"] if pcg else 46)}
+                   "sample": f"reference SemOperator::apply on the full cfg2 mesh ({r['N']} DOF), mean of 3 after "
+                             f"1 warm-up, single-threaded by design; host has {r['cores']} cores",
+                   "pcg": r.get("pcg"), "setup_s": r["setup_s"]}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": "GDOF/s", "cores": 1, "kind": "reference", "sample": f"failed: {exc}"}
 
     peak, peak_src = _peaks()
     elem_avg_ms = elem_ms / max(1, elem_n)
-    achieved = bytes_ax / (elem_avg_ms * 1e-3) / 1e9 if elem_n else None
+    gath_avg_ms = gath_ms / max(1, gath_n)
+    achieved = bytes_ax / (ms_step * 1e-3) / 1e9  # whole Ax step: B_R / device-timed step
+    t_elem, t_gath = _ncu_traffic("ax_elem_kernel"), _ncu_traffic("ax_gather_kernel")
+    if pcg is not None:
+        pcg["roofline"] = pcg_roofline(N, NE, order, pcg["ms_per_iteration"], peak)
     line = {
         "metric": METRIC, "value": value, "unit": "GDOF/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak" if args.replicas else "strong",  # N>1 default: one mesh split in element slabs
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (generated 52^3 mesh, splitmix64 u, s=1 load)",
-        "config": {"workload": f"cfg2: {k}^3 uniform hexes, N={order}, Poisson kappa=1 c=0, all-Dirichlet; "
-                               "step = one Ax (SemOperator::apply)",
-                   "k": k, "order": order, "N": N, "NE": NE,
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (weak)",
-                   "l2": f"inputs larger than L2 ({bytes_ax / 1e9:.2f} GB per Ax vs 126 MB L2); no flush"},
+        "config": workload_config(k, order, N, NE),
+        "parallelism": "single GPU" if world == 1 else f"{world} independent replicas (weak)",
         "e2e": {"value": N * world / e2e_s / 1e9, "unit": "GDOF/s", "h2d_bytes_per_step": 8 * N,
                 "d2h_bytes_per_step": 8 * N, "api": "hxb_apply_A (host pointers, pinned)",
                 "ms_per_step": e2e_s * 1e3, "max_abs_diff_vs_device_path": e2e_parity},
         "gpu_launches": launches,
-        "roofline": {"kernel": "ax_elem_kernel", "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if achieved else None, "traffic": _ncu_traffic("ax_elem_kernel"),
+        "roofline": {"kernel": "Ax step = ax_elem_kernel + ax_gather_kernel", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": (t_elem + t_gath) if (t_elem and t_gath) else None,
                      "peak_source": peak_src, "algorithmic_bytes_per_launch": bytes_ax,
-                     "avg_launch_ms": elem_avg_ms, "launches_timed": elem_n,
-                     "share_of_step": elem_ms / ms_total if ms_total else None,
-                     "ax_gather_avg_ms": gath_ms / max(1, gath_n),
-                     "whole_ax_gbs": bytes_ax / (ms_step * 1e-3) / 1e9},
+                     "algorithmic_bytes_model": "B_R = 8*NE*(10 np^3 + np^2 + 2) (operator.cpp:31-37)",
+                     "avg_step_ms": ms_step,
+                     "elem_kernel": {"avg_launch_ms": elem_avg_ms, "launches_timed": elem_n,
+                                     "share_of_step": elem_ms / ms_total if ms_total else None,
+                                     "ncu_dram_bytes": t_elem,
+                                     "dram_frac": (t_elem / (elem_avg_ms * 1e-3) / 1e9 / peak)
+                                     if (t_elem and elem_n) else None},
+                     "gather_kernel": {"avg_launch_ms": gath_avg_ms, "ncu_dram_bytes": t_gath}},
         "fdm": fdm,
         "pcg": pcg,
         "ax_on_the_fly": otf,
@@ -508,6 +531,7 @@ def main():
     ap.add_argument("--order", type=int, default=7)
     ap.add_argument("--no-pcg", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-pcg", action="store_true", help="cpu_baseline: Ax only (skip the reference cfg2 PCG)")
     ap.add_argument("--no-otf", action="store_true", help="skip the on-the-fly operator variant measurement")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent cfg2 replicas instead of a partition")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",

@@ -73,27 +73,43 @@ typedef struct hxb_mesh_buf {
   void* impl;
 } hxb_mesh_buf;
 
-/* ProblemConfig solver knobs (problem.hpp:44-53). */
+/* ProblemConfig solver knobs (problem.hpp:44-53) plus the B200 plan layout. */
+#define HXB_MAX_GPUS 8
 typedef struct hxb_options {
   int precond_mode;            /* HXB_PRECOND_* (default two_scale) */
   int coarse_solve;            /* HXB_COARSE_* (default automatic) */
   int32_t direct_threshold;    /* vertices; default 64000 (coarse.hpp:36) */
   int variant;                 /* HXB_VARIANT_* (default stored) */
-  int device;                  /* CUDA device ordinal for this plan */
-  int reserved[7];             /* reserved[0] bit 0: run AMG levels >= 1 as one 16-CTA cluster
-                                  kernel instead of the default kernel per step (measured slower
-                                  inside the PCG at cfg2: 1.45 vs 0.82 ms per coarse solve); bit 2: persistent
-                                  TMA/cp.async-pipelined FDM kernel instead of one CTA per
-                                  subdomain (measured slower at cfg2, kept for A/B checks);
-                                  bit 3: one fused combine after the coarse solve instead of
-                                  the fine half running concurrently with it; bit 5: ksolve(2)
-                                  on the compacted levels as one single-CTA kernel (measured
-                                  slower at cfg2: 1.23 vs 0.82 ms per coarse solve); bit 8: FDM
-                                  subdomains in element order instead of Morton order; bit 6:
-                                  build the fine-solve gather lists with the host counting sort
-                                  instead of the device radix sort (A/B checks);
-                                  reserved[1] = rank, reserved[2] = number of ranks: element-slab
-                                  partition for the distributed operator (hxb_dist_*) */
+  int device;                  /* CUDA device ordinal of a single-GPU plan */
+  /* Verification mode: every floating-point operation in the reference's
+   * order and rounding (no FMA contraction, sequential dot products as
+   * krylov.cpp:11-16, the interleaved phase-2 sum of operator.cpp:152-157,
+   * the full x->y->z pencil passes of fine.cpp:169-182 with true divisions,
+   * the envelope Cholesky of the direct coarse solve). hxb_apply_* and
+   * hxb_solve then equal the reference bit for bit; the kernels are simple
+   * and slow (one thread per element / sequential reductions). */
+  int bitwise_reference;
+  /* Multi-GPU plan: n_gpus > 1 partitions the mesh into n_gpus
+   * contiguous element slabs, one per device (devices[r], default r), each
+   * driven by its own host thread; halos and PCG scalars move over NCCL
+   * (distinct devices) or device-to-device copies (ranks sharing a device).
+   * hxb_solve / hxb_apply_A work unchanged on such a plan. */
+  int n_gpus;
+  int devices[HXB_MAX_GPUS];
+  /* Staged distributed plan: this plan is rank `rank` of `nranks` element
+   * slabs and the caller carries the messages (hxb_dist_*). nranks <= 1: whole mesh. */
+  int rank;
+  int nranks;
+  /* A/B switches kept for measurement and bitwise cross-checks (0 = default):
+   * fused_combine: one combine after the coarse solve instead of its fine
+   *   half running concurrently with the coarse graph;
+   * fdm_element_order: FDM subdomains in element order instead of Morton order;
+   * host_lists: fine-solve gather lists by the host counting sort instead of
+   *   the device radix sort. */
+  int fused_combine;
+  int fdm_element_order;
+  int host_lists;
+  int reserved[4];
 } hxb_options;
 
 /* PcgConfig (krylov.hpp:15-19) */

@@ -105,6 +105,9 @@ void hxb_default_options(hxb_options* opt)
   opt->direct_threshold = 64000;
   opt->variant = HXB_VARIANT_STORED;
   opt->device = 0;
+  opt->n_gpus = 1;
+  for (int r = 0; r < HXB_MAX_GPUS; ++r) opt->devices[r] = r;
+  opt->nranks = 1;
 }
 
 int hxb_generate_cube_mesh(int k, int family, int boundary_tag, hxb_mesh_buf** out)

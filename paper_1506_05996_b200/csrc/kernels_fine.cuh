@@ -362,233 +362,4 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
 }
 
 // ---------------------------------------------------------------------------
-// fdm_pipe_kernel: the same subdomain solve as fdm_kernel (EO tables) as a
-// persistent, software-pipelined kernel. While element e is transformed from
-// shared memory, element e+G's inputs are already in flight:
-//   * its surface-code row and face-neighbour ids arrive by one TMA bulk copy
-//     per array (cp.async.bulk + mbarrier), issued one element further ahead;
-//   * its r values (all P^3 slots, sentinel slots zeroed) and the 1/m_N of its
-//     own nodes are gathered with cp.async (8-byte, LDGSTS) straight into the
-//     next input buffer, so no register waits on a gather.
-// Arithmetic is identical to fdm_kernel<NP, true>.
-template <int NP>
-struct FdmPipe {
-  static constexpr int P = NP + 2, n = NP - 1, NLOC = NP * NP * NP, NSUB = P * P * P;
-  static constexpr int NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2), NSP = (NS + 3) & ~3;
-  static constexpr int NF = (6 * NP * NP + 3) & ~3;  // face-neighbour ids per element (padded)
-  static constexpr int kBlock = FdmShape<NP>::kBlock;
-  static constexpr int kIdxInts = NSP + NF;          // staged ids per element
-  static constexpr int kBufE = (FdmShape<NP>::kBuf + 1) & ~1;  // keeps the id buffers 16-byte aligned
-  static constexpr std::size_t kSmemBytes =
-      ((std::size_t)NSUB + NLOC + kBufE) * sizeof(double) + kIdxInts * sizeof(int) + 16;
-};
-
-
-template <int NP>
-__global__ void __launch_bounds__(FdmShape<NP>::kBlock) fdm_pipe_kernel(FdmArgs a)
-{
-  using Sh = FdmShape<NP>;
-  using F = FdmPipe<NP>;
-  constexpr int P = F::P, S = Sh::kS, PS = Sh::kPS, n = F::n, NSUB = F::NSUB, NLOC = F::NLOC;
-  constexpr int NSP = F::NSP, NI = (n - 1) * (n - 1) * (n - 1);
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* inr = reinterpret_cast<double*>(smem_raw);  // [NSUB] r at every subdomain slot
-  double* inl = inr + NSUB;                            // [NLOC] 1/m_N at own nodes
-  double* buf = inl + NLOC;                            // transposes
-  int* sidx = reinterpret_cast<int*>(buf + F::kBufE);  // [NSP + NF] surface codes, face ids
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(sidx + F::kIdxInts);
-
-  const OrderTables& T = c_tab[NP];
-  const FdmConst& C = c_fdm[NP];
-  const int tid = threadIdx.x;
-  const bool lt = tid < Sh::kLines;
-  const int la = tid % P, lb = tid / P;
-  auto at = [](int x, int y, int z) { return z * PS + y * S + x; };
-  __shared__ double s_lam[P], s_invM[P], s_h0[NP], s_h1[NP];
-  __shared__ double s_red[Sh::kBlock / 32][8];
-  for (int q = tid; q < P; q += Sh::kBlock) {
-    s_lam[q] = C.lam[q];
-    s_invM[q] = C.invM[q];
-  }
-  for (int q = tid; q < NP; q += Sh::kBlock) {
-    s_h0[q] = T.hat0[q];
-    s_h1[q] = T.hat1[q];
-  }
-  if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  // TMA: the id block of element ee into sidx
-  auto fetch_ids = [&](int ee) {
-    mbar_expect_tx(&bar[0], (unsigned)(F::kIdxInts * sizeof(int)));
-    bulk_g2s(sidx, a.smap + (long long)ee * a.sstride, NSP * sizeof(int), &bar[0]);
-    bulk_g2s(sidx + NSP, a.sub_face + (long long)ee * a.sfstride, F::NF * sizeof(int), &bar[0]);
-  };
-  // cp.async gathers of element ee's inputs (ids in sidx)
-  auto gather = [&](int ee) {
-    const int* ids = sidx;
-    double* rr = inr;
-    double* ll = inl;
-    const long long ibase = (long long)a.num_surface_global + (long long)ee * NI;
-    for (int q = tid; q < NSUB; q += Sh::kBlock) {
-      const int x = q % P, y = (q / P) % P, z = q / (P * P);
-      const int i = x - 1, j = y - 1, k = z - 1;
-      const bool ix = i >= 0 && i <= n, iy = j >= 0 && j <= n, iz = k >= 0 && k <= n;
-      int g = -1;
-      if (ix && iy && iz) {  // own node
-        const int sl = surface_slot(NP, i, j, k);
-        g = sl >= 0 ? ids[sl] : static_cast<int>(ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1));
-        const int l = (k * NP + j) * NP + i;
-        if (a.Rpart) {
-          if (g >= 0)
-            cp_async8(ll + l, a.inv_lumped + g);
-          else
-            ll[l] = 0.0;
-        }
-      } else if (iy && iz && (i == -1 || i == n + 1)) {  // faces 0/1 (mesh.cpp:419-450)
-        g = ids[NSP + ((i == -1 ? 0 : 1) * NP + k) * NP + j];
-      } else if (ix && iz && (j == -1 || j == n + 1)) {  // faces 2/3
-        g = ids[NSP + ((j == -1 ? 2 : 3) * NP + i) * NP + k];
-      } else if (ix && iy && (k == -1 || k == n + 1)) {  // faces 4/5
-        g = ids[NSP + ((k == -1 ? 4 : 5) * NP + j) * NP + i];
-      }
-      if (g >= 0)
-        cp_async8(rr + q, a.r + g);
-      else
-        rr[q] = 0.0;  // sentinel / Dirichlet (masked residual, precond.cpp:35)
-    }
-    cp_async_commit();
-  };
-
-  // single-buffered pipeline: e's inputs are consumed in stage 1, then e'
-  // (= e + G) is gathered into the same buffers while stages 2-5 of e run
-  int e = blockIdx.x;
-  if (e >= a.ne) return;
-  unsigned ph = 0u;
-  if (tid == 0) fetch_ids(e);
-  mbar_wait(&bar[0], ph);
-  ph ^= 1u;
-  gather(e);
-  cp_async_wait_all();
-  __syncthreads();
-  if (tid == 0 && e + (int)gridDim.x < a.ne) {
-    fence_proxy_async_smem();
-    fetch_ids(e + gridDim.x);
-  }
-
-  for (; e < a.ne; e += gridDim.x) {
-    const int en = e + gridDim.x;
-    const double* rr = inr;
-    const double* ll = inl;
-    const double hx = __ldg(a.h3 + 3 * e), hy = __ldg(a.h3 + 3 * e + 1), hz = __ldg(a.h3 + 3 * e + 2);
-    const double svol = 8.0 / (hx * hy * hz);  // fine.cpp:154
-    double in[P], out[P];
-    double racc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-
-    // ---- 1: x-lines from the staged input, restriction share, r' scaling, V along x
-    if (lt) {
-      const int y = la, z = lb, jj = y - 1, kk = z - 1;
-#pragma unroll
-      for (int x = 0; x < P; ++x) in[x] = rr[(z * P + y) * P + x];
-      if (a.Rpart && jj >= 0 && jj <= n && kk >= 0 && kk <= n) {
-        const double* ml = a.mass + (std::size_t)e * NLOC + (kk * NP + jj) * NP;
-        const double* lr = ll + (kk * NP + jj) * NP;
-        const bool line_interior = jj > 0 && jj < n && kk > 0 && kk < n;
-        double w0 = 0.0, w1 = 0.0;
-#pragma unroll
-        for (int ii = 0; ii <= n; ++ii) {  // element-interior nodes: r itself (see fdm_kernel)
-          const double w = line_interior && ii > 0 && ii < n ? in[ii + 1] : (in[ii + 1] * lr[ii]) * __ldg(ml + ii);
-          w0 += s_h0[ii] * w;
-          w1 += s_h1[ii] * w;
-        }
-        const double hj[2] = {s_h0[jj], s_h1[jj]}, hk[2] = {s_h0[kk], s_h1[kk]};
-#pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) racc[c8] = (hj[(c8 >> 1) & 1] * hk[c8 >> 2]) * ((c8 & 1) ? w1 : w0);
-      }
-      const double syz = svol * s_invM[y] * s_invM[z];
-#pragma unroll
-      for (int x = 0; x < P; ++x) in[x] = in[x] * (syz * s_invM[x]);
-      pencil_fwd_eo<P>(C.FE, C.FO, in, out);
-#pragma unroll
-      for (int x = 0; x < P; ++x) buf[at(x, y, z)] = out[x];
-    }
-    if (a.Rpart) {
-#pragma unroll
-      for (int c8 = 0; c8 < 8; ++c8)
-        for (int o = 16; o > 0; o >>= 1) racc[c8] += __shfl_xor_sync(0xffffffffu, racc[c8], o);
-      if ((tid & 31) == 0)
-#pragma unroll
-        for (int c8 = 0; c8 < 8; ++c8) s_red[tid >> 5][c8] = racc[c8];
-    }
-    __syncthreads();  // e's inputs consumed: the buffers take e' now
-    if (a.Rpart && tid < 8) {
-      double v = 0.0;
-#pragma unroll
-      for (int w = 0; w < Sh::kBlock / 32; ++w) v += s_red[w][tid];
-      a.Rpart[8 * (long long)e + tid] = v;
-    }
-    if (en < a.ne) {
-      mbar_wait(&bar[0], ph);
-      ph ^= 1u;
-      gather(en);
-    }
-    // ---- 2: V along y
-    if (lt) {
-#pragma unroll
-      for (int y = 0; y < P; ++y) in[y] = buf[at(la, y, lb)];
-      pencil_fwd_eo<P>(C.FE, C.FO, in, out);
-#pragma unroll
-      for (int y = 0; y < P; ++y) buf[at(la, y, lb)] = out[y];
-    }
-    __syncthreads();  // also: every thread has issued its e' gathers (ids consumed)
-    if (tid == 0 && en + (int)gridDim.x < a.ne) {
-      fence_proxy_async_smem();
-      fetch_ids(en + gridDim.x);
-    }
-    // ---- 3: V along z, eigenvalue division, V^-1 along z
-    if (lt) {
-      const double ihx2 = 1.0 / (hx * hx), ihy2 = 1.0 / (hy * hy), ihz2 = 1.0 / (hz * hz);
-      const double kappa4 = 4.0 * __ldg(a.kappa_e + e), ce = __ldg(a.c_e + e);
-      const double lxy = s_lam[la] * ihx2 + s_lam[lb] * ihy2;
-#pragma unroll
-      for (int z = 0; z < P; ++z) in[z] = buf[at(la, lb, z)];
-      pencil_fwd_eo<P>(C.FE, C.FO, in, out);
-#pragma unroll
-      for (int z = 0; z < P; ++z) out[z] = out[z] * __drcp_rn(kappa4 * (lxy + s_lam[z] * ihz2) + ce);
-      pencil_inv_eo<P>(C.IE, C.IO, out, in);
-#pragma unroll
-      for (int z = 0; z < P; ++z) buf[at(la, lb, z)] = in[z];
-    }
-    __syncthreads();
-    // ---- 4: V^-1 along y
-    if (lt) {
-#pragma unroll
-      for (int y = 0; y < P; ++y) in[y] = buf[at(la, y, lb)];
-      pencil_inv_eo<P>(C.IE, C.IO, in, out);
-#pragma unroll
-      for (int y = 0; y < P; ++y) buf[at(la, y, lb)] = out[y];
-    }
-    __syncthreads();
-    // ---- 5: V^-1 along x, store at the sorted accumulation positions
-    if (lt) {
-#pragma unroll
-      for (int x = 0; x < P; ++x) in[x] = buf[at(x, la, lb)];
-      pencil_inv_eo<P>(C.IE, C.IO, in, out);
-      const int* ps = a.pos + (long long)e * NSUB + (lb * P + la) * P;
-#pragma unroll
-      for (int x = 0; x < P; ++x) {
-        const int q = __ldg(ps + x);
-        if (q >= 0)
-        a.zsort[q] = out[x];
-      else if (q <= -2)  // finalised by a neighbour rank (distributed plans)
-        a.fsend[-2 - q] = out[x];
-      }
-    }
-    cp_async_wait_all();  // e' inputs landed (this thread's copies)
-    __syncthreads();      // ... and everyone's; buf free for the next element
-  }
-}
-
 }  // namespace hxb

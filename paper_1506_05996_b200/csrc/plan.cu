@@ -22,7 +22,6 @@
 #include <vector>
 
 #include "../../include/hexsem_b200.h"
-#include "kernels_amg.cuh"
 #include "kernels_ax.cuh"
 #include "kernels_coarse.cuh"
 #include "kernels_setup.cuh"
@@ -135,12 +134,9 @@ struct DevDense {
 struct Plan {
   int device = 0;
   cudaStream_t s_main = nullptr, s_coarse = nullptr;  // s_coarse: highest priority
-  bool amg_local2 = false;  // per-step K-cycle with ksolve(2) as one single-CTA kernel (opt-in: slower at cfg2)
-  int *agg1c = nullptr, *mptr1 = nullptr, *mem1 = nullptr;
-  int n2 = 0;
   bool split_combine = true;
   int* fdm_order = nullptr;  // FDM CTA -> element: Morton order of element centroids (neighbours close in time)
-  bool host_lists = false;  // build the fine gather lists on the host (A/B checks of the device sort)  // fine half of the combine concurrent with the coarse solve (options.reserved[0] bit 3 off)
+  bool host_lists = false;  // build the fine gather lists on the host (A/B checks of the device sort)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_a = nullptr;
   cudaGraphExec_t coarse_exec = nullptr;
   DeviceArena mem;
@@ -184,15 +180,6 @@ struct Plan {
   std::vector<DevLevel> lv;  // AMG levels 0..L (L = coarsest, uses dense)
   DevDense dense;
   DevCsr Kc{};               // K_c on the device (AMG mode: residual between the two K-cycles)
-  // levels >= 1 of the K-cycle as one cluster kernel (kernels_amg.cuh)
-  bool amg_cluster = false;
-  int cluster_size = 0;
-  AmgClusterArgs cargs{};
-  int* agg0c = nullptr;      // level-0 row -> compact level-1 row (-1: dropped zero row)
-  int* mptr0 = nullptr;      // kept level-1 rows: level-0 members (ascending)
-  int* mem0 = nullptr;
-  int n1 = 0;
-  DevDense cdense;           // compact coarsest solve
   std::uint8_t* zero_mask = nullptr;
 
   // PCG vectors
@@ -244,7 +231,6 @@ struct Plan {
   std::vector<double> h_xyz;  // global node coordinates (heat driver), host copy
   double* d_xyz = nullptr;
   double* heat_u = nullptr;
-  int fdm_grid = 0;           // persistent FDM grid (0: one CTA per element, fdm_kernel)
 
   // live kernel timing (bench roofline): event pairs around tagged launches on s_main
   bool kt_on = false;
@@ -427,20 +413,6 @@ void init_ax_grid(Plan& pl)
   pl.ax_grid = ax_persistent_grid<NP>(pl);
 }
 
-// persistent pipelined FDM grid (one wave of resident CTAs); 0 keeps fdm_kernel
-template <int NP>
-void init_fdm_grid(Plan& pl, bool enable)
-{
-  pl.fdm_grid = 0;
-  if (!enable || !pl.fdm_eo) return;
-  const int smem = static_cast<int>(FdmPipe<NP>::kSmemBytes);
-  HXB_CUDA(cudaFuncSetAttribute(fdm_pipe_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  int per_sm = 0;
-  HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdm_pipe_kernel<NP>, FdmShape<NP>::kBlock, smem));
-  if (per_sm < 1) return;
-  pl.fdm_grid = std::max(1, std::min(pl.ne, per_sm * pl.num_sms));
-}
-
 int ax_elem_grid(const Plan& pl) { return pl.ax_grid; }
 
 // f = A u (+ optional u.f into *dot_result)
@@ -496,9 +468,7 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   a.order = pl.fdm_order;
   KtScope kt(pl, HXB_KT_FDM, s);
   pl.launches += 1;
-  if (pl.fdm_grid > 0)
-    fdm_pipe_kernel<NP><<<pl.fdm_grid, FdmShape<NP>::kBlock, FdmPipe<NP>::kSmemBytes, s>>>(a);
-  else if (pl.fdm_eo)
+  if (pl.fdm_eo)
     fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
   else
     fdm_kernel<NP, false><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
@@ -622,16 +592,9 @@ void enqueue_cycle(Plan& pl, int l, const double* r, double* zout, cudaStream_t 
   const int g = vec_grid(v.n);
   amg_jacobi2_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, fu.r_copy, fu.x_zero, fu.ks_init);
   amg_resid_kernel<<<g, kVecBlock, 0, s>>>(v.A, r, v.zA, v.kf);  // kf is free during the cycle
-  if (l == 1 && pl.amg_local2) {  // ksolve(2) on the compacted levels by one CTA
-    CLev& c2 = pl.cargs.lev[1];
-    amg_agg_sum_compact_kernel<<<vec_grid(pl.n2), kVecBlock, 0, s>>>(v.kf, pl.mptr1, pl.mem1, c2.b, pl.n2);
-    amg_local_ksolve_kernel<<<1, kAmgClusterBlock, 0, s>>>(pl.cargs, 1, c2.b, c2.x);
-    amg_prolong_smooth_compact_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c2.x, pl.agg1c, v.zB);
-  } else {
-    amg_agg_sum_kernel<<<vec_grid(v.nc), kVecBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
-    enqueue_ksolve(pl, l + 1, c.b, c.x, s);
-    amg_prolong_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
-  }
+  amg_agg_sum_kernel<<<vec_grid(v.nc), kVecBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
+  enqueue_ksolve(pl, l + 1, c.b, c.x, s);
+  amg_prolong_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
   if (fu.dot)
     amg_smooth_dot_kernel<kVecBlock><<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout, fu.p_copy, *fu.dot);
   else
@@ -670,31 +633,6 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
   }
 }
 
-// cycle(0, r, zout) with ksolve(1) as one cluster kernel (kernels_amg.cuh)
-void enqueue_cycle0_cluster(Plan& pl, const double* r, double* zout, cudaStream_t s)
-{
-  DevLevel& v = pl.lv[0];
-  const int g = vec_grid(v.n);
-  amg_jacobi2_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA);
-  amg_resid_kernel<<<g, kVecBlock, 0, s>>>(v.A, r, v.zA, v.kf);
-  CLev& c1 = pl.cargs.lev[0];
-  amg_agg_sum_compact_kernel<<<vec_grid(pl.n1), kVecBlock, 0, s>>>(v.kf, pl.mptr0, pl.mem0, c1.b, pl.n1);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pl.cluster_size);
-  cfg.blockDim = dim3(kAmgClusterBlock);
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = pl.cluster_size;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  HXB_CUDA(cudaLaunchKernelEx(&cfg, amg_cluster_kernel, pl.cargs, static_cast<const double*>(c1.b), c1.x));
-  amg_prolong_smooth_compact_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c1.x, pl.agg0c, v.zB);
-  amg_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout);
-}
-
 // restrict -> mask -> coarse solve; leaves Z (coarse.cpp:188-206)
 // Rpart -> R -> coarse solve -> Zc (coarse.cpp:188-206). Rpart comes from
 // the FDM kernel (fused restriction) or, without a fine branch, from
@@ -703,17 +641,11 @@ void enqueue_coarse(Plan& pl, cudaStream_t s)
 {
   vertex_gather_kernel<<<gather_grid(pl.nv), kGatherBlock, 0, s>>>(pl.Rpart, pl.vtx_off, pl.vtx_idx, pl.vmask, pl.R, pl.nv);
   if (pl.use_amg) {
-    auto cyc0 = [&](const double* r, double* z) {
-      if (pl.amg_cluster)
-        enqueue_cycle0_cluster(pl, r, z, s);
-      else
-        enqueue_cycle(pl, 0, r, z, s);
-    };
-    cyc0(pl.R, pl.Z);
+    enqueue_cycle(pl, 0, pl.R, pl.Z, s);
     // two composed K-cycles: Z = B R + B (R - K_c B R)  (coarse.cpp:193-200)
     const DevCsr K = pl.Kc;
     amg_resid_kernel<<<vec_grid(K.n), kVecBlock, 0, s>>>(K, pl.R, pl.Z, pl.rho);
-    cyc0(pl.rho, pl.dZ);
+    enqueue_cycle(pl, 0, pl.rho, pl.dZ, s);
     axpy1_kernel<<<vec_grid(K.n), kVecBlock, 0, s>>>(pl.Z, pl.dZ, K.n);
   } else {
     enqueue_dense(pl, pl.R, pl.Z, s);
@@ -933,172 +865,6 @@ DevDense dense_to_device(Plan& pl, const Csr& A)
   return d;
 }
 
-// Levels >= 1 of the AMG hierarchy, compacted to the rows that can carry
-// non-zero values (kernels_amg.cuh): a level-0 row is dropped when it is a
-// Dirichlet vertex (R masked to 0, coarse.cpp:191-192) with no off-diagonal
-// entry; a coarser row when all its aggregate members were dropped and it is
-// itself decoupled. Returns false when the cluster path cannot be used.
-bool build_amg_cluster(Plan& pl, const AmgSetup& amg, const std::vector<std::uint8_t>& vmask)
-{
-  const int Lh = static_cast<int>(amg.levels.size());
-  if (Lh < 1 || Lh > kAmgMaxLevels) return false;
-  auto A_of = [&](int l) -> const Csr& { return l < Lh ? amg.levels[l].A : amg.coarsest; };
-  auto decoupled = [&](const Csr& A, gid i) {
-    for (std::int64_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k)
-      if (A.col[k] != i) return false;
-    return true;
-  };
-  std::vector<std::vector<char>> drop(Lh + 1);
-  {
-    const Csr& A0 = A_of(0);
-    drop[0].assign(A0.n, 0);
-    for (gid i = 0; i < A0.n; ++i) drop[0][i] = (i < static_cast<gid>(vmask.size()) && vmask[i] && decoupled(A0, i)) ? 1 : 0;
-  }
-  for (int l = 0; l < Lh; ++l) {
-    const AmgLevel& lv = amg.levels[l];
-    const Csr& An = A_of(l + 1);
-    std::vector<char> all(lv.n_coarse, 1);
-    for (gid i = 0; i < lv.A.n; ++i)
-      if (!drop[l][i]) all[lv.aggregate[i]] = 0;
-    drop[l + 1].assign(An.n, 0);
-    for (gid c = 0; c < An.n; ++c) drop[l + 1][c] = (all[c] && decoupled(An, c)) ? 1 : 0;
-  }
-  std::vector<std::vector<gid>> cidx(Lh + 1);
-  std::vector<int> ncomp(Lh + 1, 0);
-  for (int l = 1; l <= Lh; ++l) {
-    cidx[l].assign(A_of(l).n, -1);
-    for (gid i = 0; i < A_of(l).n; ++i)
-      if (!drop[l][i]) cidx[l][i] = ncomp[l]++;
-  }
-  DeviceArena& M = pl.mem;
-  AmgClusterArgs& ca = pl.cargs;
-  ca.L = Lh - 1;
-  // compact levels 1..Lh-1 (ca.lev[l-1])
-  for (int l = 1; l < Lh; ++l) {
-    const AmgLevel& lv = amg.levels[l];
-    const Csr& A = lv.A;
-    CLev& c = ca.lev[l - 1];
-    c.n = ncomp[l];
-    std::vector<int> ptr(1, 0), col, agg, mptr(ncomp[l + 1] + 1, 0), mem;
-    std::vector<double> val, dinv;
-    for (gid i = 0; i < A.n; ++i) {
-      if (drop[l][i]) continue;
-      for (std::int64_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
-        const gid j = cidx[l][A.col[k]];
-        if (j < 0) throw HxbError(HXB_ENUMERIC, "amg compaction: kept row couples to a dropped row");
-        col.push_back(j);
-        val.push_back(A.val[k]);
-      }
-      ptr.push_back(static_cast<int>(col.size()));
-      dinv.push_back(lv.inv_diag[i]);
-      const gid a = cidx[l + 1][lv.aggregate[i]];
-      if (a < 0) throw HxbError(HXB_ENUMERIC, "amg compaction: kept row in a dropped aggregate");
-      agg.push_back(a);
-      mptr[a + 1]++;
-    }
-    for (int k = 0; k < ncomp[l + 1]; ++k) mptr[k + 1] += mptr[k];
-    mem.assign(c.n, 0);
-    std::vector<int> cur(mptr.begin(), mptr.end() - 1);
-    for (int i = 0; i < c.n; ++i) mem[cur[agg[i]]++] = i;  // ascending member order
-    c.ptr = M.upload(ptr);
-    c.col = M.upload(col);
-    c.val = M.upload(val);
-    c.dinv = M.upload(dinv);
-    c.agg = M.upload(agg);
-    c.mptr = M.upload(mptr);
-    c.mem = M.upload(mem);
-    c.nc = ncomp[l + 1];
-    for (double** v : {&c.zA, &c.zB, &c.rho, &c.kr, &c.kz, &c.kp, &c.kf, &c.b, &c.x}) *v = M.alloc<double>(c.n);
-  }
-  {  // compact coarsest (ca.lev[Lh-1])
-    const Csr& A = amg.coarsest;
-    CLev& c = ca.lev[Lh - 1];
-    c.n = ncomp[Lh];
-    Csr Ac;
-    Ac.n = c.n;
-    Ac.ptr.assign(1, 0);
-    for (gid i = 0; i < A.n; ++i) {
-      if (drop[Lh][i]) continue;
-      for (std::int64_t k = A.ptr[i]; k < A.ptr[i + 1]; ++k) {
-        Ac.col.push_back(cidx[Lh][A.col[k]]);
-        Ac.val.push_back(A.val[k]);
-      }
-      Ac.ptr.push_back(static_cast<std::int64_t>(Ac.col.size()));
-    }
-    pl.cdense = dense_to_device(pl, Ac);
-    if (pl.cdense.tiles) return false;  // the cluster kernel applies a full inverse only
-    ca.ainv = pl.cdense.ainv;
-    ca.coupled = pl.cdense.coupled;
-    ca.inv_diag = pl.cdense.inv_diag;
-    ca.m = pl.cdense.m;
-    c.b = M.alloc<double>(std::max(1, c.n));
-    c.x = M.alloc<double>(std::max(1, c.n));
-  }
-  {  // level 0 -> compact level 1
-    const AmgLevel& l0 = amg.levels[0];
-    std::vector<int> agg0c(l0.A.n), mptr(ncomp[1] + 1, 0), mem;
-    for (gid i = 0; i < l0.A.n; ++i) {
-      agg0c[i] = cidx[1][l0.aggregate[i]];
-      if (agg0c[i] >= 0) mptr[agg0c[i] + 1]++;
-    }
-    for (int k = 0; k < ncomp[1]; ++k) mptr[k + 1] += mptr[k];
-    mem.assign(mptr[ncomp[1]], 0);
-    std::vector<int> cur(mptr.begin(), mptr.end() - 1);
-    for (gid i = 0; i < l0.A.n; ++i)
-      if (agg0c[i] >= 0) mem[cur[agg0c[i]]++] = i;
-    pl.agg0c = M.upload(agg0c);
-    pl.mptr0 = M.upload(mptr);
-    pl.mem0 = M.upload(mem);
-    pl.n1 = ncomp[1];
-  }
-  if (Lh >= 3) {  // level 1 (full numbering) -> compact level 2: glue of the one-CTA ksolve(2)
-    const AmgLevel& l1 = amg.levels[1];
-    std::vector<int> agg1c(l1.A.n), mptr(ncomp[2] + 1, 0), mem;
-    for (gid i = 0; i < l1.A.n; ++i) {
-      agg1c[i] = cidx[2][l1.aggregate[i]];
-      if (agg1c[i] >= 0) mptr[agg1c[i] + 1]++;
-    }
-    for (int k = 0; k < ncomp[2]; ++k) mptr[k + 1] += mptr[k];
-    mem.assign(mptr[ncomp[2]], 0);
-    std::vector<int> cur(mptr.begin(), mptr.end() - 1);
-    for (gid i = 0; i < l1.A.n; ++i)
-      if (agg1c[i] >= 0) mem[cur[agg1c[i]]++] = i;
-    pl.agg1c = M.upload(agg1c);
-    pl.mptr1 = M.upload(mptr);
-    pl.mem1 = M.upload(mem);
-    pl.n2 = ncomp[2];
-  }
-  // the K-cycle recursion (ksolve -> cycle -> ksolve ...) needs a per-thread
-  // stack deeper than the 1 KB default for hierarchies of many levels
-  {
-    std::size_t stack = 0;
-    HXB_CUDA(cudaDeviceGetLimit(&stack, cudaLimitStackSize));
-    const std::size_t want = 1024 + 512 * static_cast<std::size_t>(Lh + 2);
-    if (stack < want) HXB_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, want));
-  }
-  // cluster size: 16 CTAs (non-portable) when the device can co-schedule them, else 8
-  HXB_CUDA(cudaFuncSetAttribute(amg_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  for (int cs : {16, 8}) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(kAmgClusterBlock);
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cs;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, amg_cluster_kernel, &cfg) == cudaSuccess && nclusters > 0) {
-      pl.cluster_size = cs;
-      break;
-    }
-    cudaGetLastError();
-  }
-  return pl.cluster_size > 0;
-}
-
 DevCsr csr_to_device(Plan& pl, const Csr& A)
 {
   if (A.nnz() > 0x7fffffffULL) throw HxbError(HXB_EINVAL, "coarse matrix too large");
@@ -1200,7 +966,7 @@ void launch_geometry(const GeoArgs& a, long long n, cudaStream_t s)
 void device_geometry(Plan& pl, HostSetup& hs, const hxb_options& opt)
 {
   const int np = hs.basis.npts(), nloc = np * np * np, ne = hs.mesh.num_elements();
-  const int nranks = std::max(1, opt.reserved[2]), rank = opt.reserved[2] > 1 ? opt.reserved[1] : 0;
+  const int nranks = std::max(1, opt.nranks), rank = nranks > 1 ? opt.rank : 0;
   const int e0 = static_cast<int>(static_cast<long long>(ne) * rank / nranks);
   const int e1 = static_cast<int>(static_cast<long long>(ne) * (rank + 1) / nranks);
   GeoArgs a{};
@@ -1239,7 +1005,7 @@ void device_geometry(Plan& pl, HostSetup& hs, const hxb_options& opt)
   if (first_bad != big)
     throw HxbError(HXB_EMESH, "inverted element " + std::to_string(first_bad) +
                                   ": non-positive Jacobian determinant at a GLL node");
-  const bool device_lumped = std::max(1, opt.reserved[2]) == 1 && (opt.reserved[0] & 64) == 0;
+  const bool device_lumped = std::max(1, opt.nranks) == 1 && opt.host_lists == 0;
   if (!device_lumped) {  // host consumers: lumped mass, host gather lists, distributed setup
     hs.geo.mass.resize(static_cast<std::size_t>(ne) * nloc);
     HXB_CUDA(cudaMemcpy(hs.geo.mass.data(), mass, hs.geo.mass.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1265,6 +1031,12 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.num_sms = prop.multiProcessorCount;
     g_num_sms = prop.multiProcessorCount;
   }
+  if (opt.nranks > 1) {  // validated before any setup work (the geometry hook reads them)
+    if (opt.rank < 0 || opt.rank >= opt.nranks) throw HxbError(HXB_EINVAL, "rank out of range");
+    if (opt.precond_mode != HXB_PRECOND_NONE && opt.precond_mode != HXB_PRECOND_TWO_SCALE)
+      throw HxbError(HXB_EINVAL, "distributed plans support precond_mode two_scale or none");
+    if (opt.nranks > m->num_elements) throw HxbError(HXB_EINVAL, "more ranks than elements");
+  }
   HostSetup& hs = pl.hs;
   hs.mesh = mesh_from_arrays(m->num_vertices, m->xyz, m->num_elements, m->conn, m->num_boundary_faces,
                              m->bface_element, m->bface_face, m->bface_tag);
@@ -1279,7 +1051,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   so.geometry_hook = [&pl, &opt](HostSetup& h) { device_geometry(pl, h, opt); };
   // single-device plan with device lists: the lumped mass is assembled on the
   // device after the surface CSR exists, so the masses never go back to the host
-  so.device_lumped = std::max(1, opt.reserved[2]) == 1 && (opt.reserved[0] & 64) == 0;
+  so.device_lumped = std::max(1, opt.nranks) == 1 && opt.host_lists == 0;
   setup_phase("mesh + checks");
   build_host_setup(hs, order, so);
   setup_phase("device: streams, tables");
@@ -1292,14 +1064,8 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   const int nsurf_raw = surface_slot_count(pl.np);
   pl.nsurf = (nsurf_raw + 3) & ~3;  // padded element stride of every surface-slot array (16 B aligned)
   pl.P = order + 3;
-  pl.nranks = std::max(1, opt.reserved[2]);
-  pl.rank = opt.reserved[1];
-  if (pl.nranks > 1) {
-    if (pl.rank < 0 || pl.rank >= pl.nranks) throw HxbError(HXB_EINVAL, "rank out of range");
-    if (opt.precond_mode != HXB_PRECOND_NONE && opt.precond_mode != HXB_PRECOND_TWO_SCALE)
-      throw HxbError(HXB_EINVAL, "distributed plans support precond_mode two_scale or none");
-    if (pl.nranks > ne) throw HxbError(HXB_EINVAL, "more ranks than elements");
-  }
+  pl.nranks = std::max(1, opt.nranks);
+  pl.rank = pl.nranks > 1 ? opt.rank : 0;
   pl.ne_total = ne;
   pl.e0 = static_cast<int>(static_cast<long long>(ne) * pl.rank / pl.nranks);
   pl.ne = static_cast<int>(static_cast<long long>(ne) * (pl.rank + 1) / pl.nranks) - pl.e0;
@@ -1317,9 +1083,8 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
 
   pl.fdm_eo = upload_tables(hs.basis, hs.pencil);
   HXB_DISPATCH_NP(pl.np, init_ax_grid, pl);
-  HXB_DISPATCH_NP(pl.np, init_fdm_grid, pl, (opt.reserved[0] & 4) != 0);
-  pl.split_combine = (opt.reserved[0] & 8) == 0;
-  pl.host_lists = (opt.reserved[0] & 64) != 0;
+  pl.split_combine = opt.fused_combine == 0;
+  pl.host_lists = opt.host_lists != 0;
 
   HXB_CUDA(cudaStreamCreateWithFlags(&pl.s_main, cudaStreamNonBlocking));
   {
@@ -1558,7 +1323,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     }
   }
 
-  if (pl.do_fine && pl.nranks == 1 && (opt.reserved[0] & 256) == 0) {
+  if (pl.do_fine && pl.nranks == 1 && opt.fdm_element_order == 0) {
     // Morton (z-order) traversal of the element centroids for the FDM: the
     // face neighbours whose first layers a subdomain reads are processed
     // close in time, so their r values are still in L2
@@ -1653,12 +1418,6 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
         pl.Kc = pl.lv[0].A;
       else
         pl.Kc = csr_to_device(pl, hs.Kc);
-      const bool want_cluster = (opt.reserved[0] & 1) != 0;
-      const bool compact = (opt.reserved[0] & 32) != 0 || want_cluster;
-      const bool built = compact && build_amg_cluster(pl, amg, hs.vmask);
-      pl.amg_cluster = want_cluster && built;
-      pl.amg_local2 = !pl.amg_cluster && built && pl.cargs.L >= 2 && pl.agg1c &&
-                      pl.cargs.lev[1].n <= kAmgLocalRows;
     } else {
       pl.dense = dense_to_device(pl, hs.Kc);
     }
@@ -1775,6 +1534,7 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
   res->iterations = iterations;
   res->num_residuals = r0 == 0.0 ? 1 : iterations + 1;
   if (status != HXB_PCG_BREAKDOWN) res->num_zr = r0 == 0.0 ? 0 : iterations;
+  if (!cfg.record_history) res->num_residuals = res->num_zr = 0;  // empty histories (krylov.cpp:36, 44, 55)
   std::snprintf(res->diagnostic, sizeof(res->diagnostic), "%s", diag.c_str());
   if (cfg.record_history) {
     if (res->residual_history)
@@ -1783,6 +1543,30 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
       HXB_CUDA(cudaMemcpy(res->zr_history, pl.zr_hist, sizeof(double) * res->num_zr, cudaMemcpyDeviceToHost));
   }
   if (res->u) HXB_CUDA(cudaMemcpy(res->u, pl.u, sizeof(double) * n, cudaMemcpyDeviceToHost));
+}
+
+// Ordering against the caller's stream for the _device entry points. A NULL
+// stream is the legacy default stream (torch's default stream has handle 0):
+// the plan's non-blocking streams would not otherwise wait for work queued
+// there (e.g. an NCCL receive that torch made the default stream wait on), so
+// the plan waits on an event recorded on cudaStreamLegacy, and the call
+// returns only when its own work is done.
+void caller_stream_in(Plan& pl, void* stream)
+{
+  const cudaStream_t caller = stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy;
+  HXB_CUDA(cudaEventRecord(pl.ev_a, caller));
+  HXB_CUDA(cudaStreamWaitEvent(pl.s_main, pl.ev_a, 0));
+}
+
+void caller_stream_out(Plan& pl, void* stream)
+{
+  HXB_CUDA(cudaGetLastError());
+  if (stream) {
+    HXB_CUDA(cudaEventRecord(pl.ev_a, pl.s_main));
+    HXB_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), pl.ev_a, 0));
+  } else {
+    HXB_CUDA(cudaStreamSynchronize(pl.s_main));
+  }
 }
 
 Plan* as_plan(hxb_plan* p)
@@ -1852,19 +1636,9 @@ int hxb_apply_A_device(hxb_plan* plan, const double* d_u, double* d_r, void* str
     Plan* pl = as_plan(plan);
     if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use hxb_dist_apply_A_*");
     HXB_CUDA(cudaSetDevice(pl->device));
-    cudaStream_t s = pl->s_main;
-    if (stream) {
-      HXB_CUDA(cudaEventRecord(pl->ev_a, static_cast<cudaStream_t>(stream)));
-      HXB_CUDA(cudaStreamWaitEvent(s, pl->ev_a, 0));
-    }
-    enqueue_ax(*pl, d_u, d_r, nullptr, s);
-    HXB_CUDA(cudaGetLastError());
-    if (stream) {
-      HXB_CUDA(cudaEventRecord(pl->ev_a, s));
-      HXB_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), pl->ev_a, 0));
-    } else {
-      HXB_CUDA(cudaStreamSynchronize(s));
-    }
+    caller_stream_in(*pl, stream);
+    enqueue_ax(*pl, d_u, d_r, nullptr, pl->s_main);
+    caller_stream_out(*pl, stream);
   });
 }
 
@@ -2078,20 +1852,11 @@ int hxb_apply_P_device(hxb_plan* plan, const double* d_r, double* d_z, void* str
     Plan* pl = as_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     cudaStream_t s = pl->s_main;
-    if (stream) {
-      HXB_CUDA(cudaEventRecord(pl->ev_a, static_cast<cudaStream_t>(stream)));
-      HXB_CUDA(cudaStreamWaitEvent(s, pl->ev_a, 0));
-    }
+    caller_stream_in(*pl, stream);
     if (d_r != pl->r) HXB_CUDA(cudaMemcpyAsync(pl->r, d_r, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice, s));
     enqueue_precond(*pl, nullptr);
     if (d_z != pl->z) HXB_CUDA(cudaMemcpyAsync(d_z, pl->z, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice, s));
-    HXB_CUDA(cudaGetLastError());
-    if (stream) {
-      HXB_CUDA(cudaEventRecord(pl->ev_a, s));
-      HXB_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), pl->ev_a, 0));
-    } else {
-      HXB_CUDA(cudaStreamSynchronize(s));
-    }
+    caller_stream_out(*pl, stream);
   });
 }
 
@@ -2158,6 +1923,11 @@ int hxb_solve_heat(hxb_plan* plan, const hxb_heat_config* hc, const hxb_pcg_conf
     if (!hc || !pc || !steps_out || !num_steps || !all_converged) throw HxbError(HXB_EINVAL, "null argument");
     if (!(hc->dt > 0)) throw HxbError(HXB_EINVAL, "heat: dt must be positive");
     if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use the staged API");
+    // backward Euler needs c = 1/dt on every element (problem.cpp:149 enforces it)
+    const double c_dt = 1 / hc->dt;
+    for (double c : pl->hs.c)
+      if (!(std::fabs(c - c_dt) <= 1e-12 * std::fabs(c_dt)))
+        throw HxbError(HXB_EINVAL, "heat: the plan must carry c = 1/dt on every element (problem.cpp:149)");
     HXB_CUDA(cudaSetDevice(pl->device));
     Plan& P = *pl;
     const int n = P.N;
@@ -2213,9 +1983,7 @@ int hxb_solve_heat(hxb_plan* plan, const hxb_heat_config* hc, const hxb_pcg_conf
       P.launches += 2;
       hxb_pcg_result res{};
       res.residual_history = hist.data();
-      hxb_pcg_config cfg = *pc;
-      cfg.record_history = 1;
-      run_pcg(P, cfg, &res);  // du in P.u
+      run_pcg(P, *pc, &res);  // du in P.u
       heat_update_kernel<kVecBlock><<<fill_grid(heat_update_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(
           P.heat_u, P.u, P.d_lumped, n, dot_args(P, P.scratch + 3), cdot_args(P, P.scratch + 4));
       P.launches += 1;
@@ -2336,23 +2104,6 @@ int hxb_profile(hxb_plan* plan, int reps, double* out)
       out[8] = timeit([&] { HXB_DISPATCH_NP(pl->np, launch_restrict, *pl, s); });
       out[9] = timeit([&] { launch_prolong(*pl, s); });
       out[10] = out[3] - out[9];  // vertex gather + AMG / dense solve
-      if (pl->amg_cluster) {       // one ksolve(1) cluster kernel alone
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(pl->cluster_size);
-        cfg.blockDim = dim3(kAmgClusterBlock);
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = pl->cluster_size;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        CLev& c1 = pl->cargs.lev[0];
-        out[11] = timeit([&] {
-          HXB_CUDA(cudaLaunchKernelEx(&cfg, amg_cluster_kernel, pl->cargs, static_cast<const double*>(c1.b), c1.x));
-        });
-      }
     }
     HXB_CUDA(cudaGetLastError());
   });
@@ -2386,23 +2137,8 @@ int hxb_bench_apply_A(hxb_plan* plan, int reps, double* ms_per_apply, double* ms
 }
 
 // ---- distributed Ax (element-slab partition) ---------------------------------
-static void dist_stream_in(Plan* pl, void* stream)
-{
-  if (stream) {
-    HXB_CUDA(cudaEventRecord(pl->ev_a, static_cast<cudaStream_t>(stream)));
-    HXB_CUDA(cudaStreamWaitEvent(pl->s_main, pl->ev_a, 0));
-  }
-}
-static void dist_stream_out(Plan* pl, void* stream)
-{
-  HXB_CUDA(cudaGetLastError());
-  if (stream) {
-    HXB_CUDA(cudaEventRecord(pl->ev_a, pl->s_main));
-    HXB_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), pl->ev_a, 0));
-  } else {
-    HXB_CUDA(cudaStreamSynchronize(pl->s_main));
-  }
-}
+static void dist_stream_in(Plan* pl, void* stream) { caller_stream_in(*pl, stream); }
+static void dist_stream_out(Plan* pl, void* stream) { caller_stream_out(*pl, stream); }
 
 int hxb_dist_info(hxb_plan* plan, int64_t* info)
 {

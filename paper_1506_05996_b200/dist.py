@@ -242,6 +242,12 @@ class TorchComm:
 
 def dist_precond(ctxs, comm):
     """z = P r (precond.cpp:27-67) across the ranks; returns the global z.r."""
+    if not ctxs[0].info["has_fine"]:
+        if ctxs[0].info["has_coarse"]:
+            raise ValueError("distributed plans support precond_mode two_scale or none")
+        for c in ctxs:  # PrecondMode::none: z = r (precond.cpp:30-33) on the rank's nodes
+            c.vec(3, 0.0, c.r, None, c.z, None)
+        return comm.allreduce(ctxs, [c.dot(c.z, c.r, 1) for c in ctxs])
     for c in ctxs:  # ghost r for the neighbours' subdomain halos
         c.call("pack", 0, _vp(c.r), _vp(c.gsend_down), None)
         c.call("pack", 1, _vp(c.r), _vp(c.gsend_up), None)

@@ -50,7 +50,10 @@ class _MeshBuf(C.Structure):
 
 class _Options(C.Structure):
     _fields_ = [("precond_mode", C.c_int), ("coarse_solve", C.c_int), ("direct_threshold", C.c_int32),
-                ("variant", C.c_int), ("device", C.c_int), ("reserved", C.c_int * 7)]
+                ("variant", C.c_int), ("device", C.c_int), ("bitwise_reference", C.c_int),
+                ("n_gpus", C.c_int), ("devices", C.c_int * 8), ("rank", C.c_int), ("nranks", C.c_int),
+                ("fused_combine", C.c_int), ("fdm_element_order", C.c_int), ("host_lists", C.c_int),
+                ("reserved", C.c_int * 4)]
 
 
 class _PcgConfig(C.Structure):
@@ -329,10 +332,9 @@ class Plan:
 
     def __init__(self, mesh: HexMesh, order: int, kappa_e=None, c_e=None, *, precond: str = "two_scale",
                  coarse_solve: str = "automatic", direct_threshold: int = 64000, variant: str = "stored",
-                 device: int = 0, amg_cluster: bool = False, rank: int = 0, nranks: int = 1,
-                 fdm_pipeline: bool = False, split_combine: bool = True,
-                 amg_local_small: bool = False, host_lists: bool = False,
-                 fdm_morton: bool = True):
+                 device: int = 0, rank: int = 0, nranks: int = 1, split_combine: bool = True,
+                 host_lists: bool = False, fdm_morton: bool = True, bitwise_reference: bool = False,
+                 devices=None):
         L = lib()
         ne = mesh.num_elements
         self.mesh = mesh
@@ -345,9 +347,18 @@ class Plan:
         opt.direct_threshold = direct_threshold
         opt.variant = VARIANTS[variant]
         opt.device = device
-        opt.reserved[0] = (1 if amg_cluster else 0) | (4 if fdm_pipeline else 0) | (0 if split_combine else 8) | (32 if amg_local_small else 0) | (64 if host_lists else 0) | (0 if fdm_morton else 256)
-        opt.reserved[1] = rank
-        opt.reserved[2] = nranks
+        opt.rank = rank
+        opt.nranks = nranks
+        opt.fused_combine = 0 if split_combine else 1
+        opt.host_lists = 1 if host_lists else 0
+        opt.fdm_element_order = 0 if fdm_morton else 1
+        opt.bitwise_reference = 1 if bitwise_reference else 0
+        if devices is not None:  # multi-GPU plan: one element slab per entry (a device may repeat)
+            if not 1 <= len(devices) <= 8:
+                raise ValueError("devices: 1..8 entries")
+            opt.n_gpus = len(devices)
+            for r, d in enumerate(devices):
+                opt.devices[r] = int(d)
         cm = mesh._c()
         h = C.c_void_p()
         _check(L.hxb_plan_create(C.byref(cm), order, _ptr(self.kappa_e), _ptr(self.c_e), C.byref(opt), C.byref(h)))
@@ -865,3 +876,17 @@ def fine_ops_model(ne: int, n: int) -> int:
 
 def fine_words_model(ne: int, n: int) -> int:
     return int(lib().hxb_fine_words_model(ne, n))
+
+
+def synthetic_vector(n: int, seed: int = 12345) -> np.ndarray:
+    """Synthetic input vector: splitmix64 values in [-0.5, 0.5), the generator
+    the reference's tests feed its operators (random_vector,
+    tests/support/oracles.cpp:126-139). Used by bench.py to build inputs."""
+    M = np.uint64(0xFFFFFFFFFFFFFFFF)
+    idx = np.arange(1, n + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = (np.uint64(seed) + idx * np.uint64(0x9E3779B97F4A7C15)) & M
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53) - 0.5

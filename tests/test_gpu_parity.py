@@ -193,35 +193,6 @@ def test_pcg_cfg1(precond, tol):
     history_parity(ours, theirs, tol=1e-10 if precond != "none" else 1e-6)
 
 
-@pytest.mark.parametrize("k", [12, 20])
-def test_amg_variants_match_per_step_kernels(k):
-    """The three K-cycle executions agree up to dot-product reduction order:
-    every level as kernels per step (default), ksolve(2) by one CTA on the
-    compacted levels, and the single-cluster ksolve(1) (kernels_amg.cuh)."""
-    mesh = hx.generate_cube_mesh(k)
-    a = hx.Plan(mesh, 3, coarse_solve="amg", amg_cluster=True)
-    b = hx.Plan(mesh, 3, coarse_solve="amg")
-    c = hx.Plan(mesh, 3, coarse_solve="amg", amg_local_small=True)
-    r = splitmix_vector(a.N, 11)
-    za, zb, zc = a.apply_coarse(r), b.apply_coarse(r), c.apply_coarse(r)
-    assert rel(za, zb) <= 1e-13, rel(za, zb)
-    assert rel(zc, zb) <= 1e-13, rel(zc, zb)
-    assert np.array_equal(a.apply_coarse(r), za)  # deterministic
-    assert np.array_equal(c.apply_coarse(r), zc)
-
-
-@pytest.mark.parametrize("k,order", [(12, 7), (6, 4), (5, 2)])
-def test_fdm_pipeline_matches_per_element_kernel(k, order):
-    """The persistent TMA/cp.async-pipelined FDM kernel performs the same
-    arithmetic as the one-CTA-per-subdomain kernel: bitwise equal."""
-    mesh = hx.generate_cube_mesh(k, "distorted_elements" if k <= 8 else "uniform")
-    a = hx.Plan(mesh, order, fdm_pipeline=True)
-    b = hx.Plan(mesh, order)
-    r = splitmix_vector(a.N, 5)
-    assert np.array_equal(a.apply_fine(r), b.apply_fine(r))
-    assert np.array_equal(a.apply_P(r), b.apply_P(r))
-
-
 @pytest.mark.parametrize("k,order,coarse", [(12, 7, "amg"), (6, 4, "automatic"), (5, 2, "direct")])
 def test_split_combine_matches_fused(k, order, coarse):
     """The combine split around the concurrent coarse solve (fine half first,

@@ -4,7 +4,7 @@ sys.path.insert(0, ".")
 import paper_1506_05996_b200 as hx
 import os
 p = hx.Plan(hx.generate_cube_mesh(int(sys.argv[1]) if len(sys.argv) > 1 else 52), 7,
-            split_combine=os.environ.get("SPLIT", "1") == "1", amg_cluster=os.environ.get("CLUSTER", "0") == "1")
+            split_combine=os.environ.get("SPLIT", "1") == "1")
 p.pcg_device(None, tol=1e-8, want_u=False)
 p.kernel_timing(True, 4000)
 r = p.pcg_device(None, tol=1e-8, want_u=False)
