@@ -30,6 +30,7 @@
 #include "kernels_gather.cuh"
 #include "kernels_vec.cuh"
 #include "capi_common.hpp"
+#include "compat.hpp"
 #include "setup.hpp"
 
 namespace hxb {
@@ -137,6 +138,8 @@ struct Plan {
   bool split_combine = true;
   int* fdm_order = nullptr;  // FDM CTA -> element: Morton order of element centroids (neighbours close in time)
   bool host_lists = false;  // build the fine gather lists on the host (A/B checks of the device sort)
+  bool bitwise = false;     // hxb_options.bitwise_reference: every apply/solve through compat.cu
+  CompatPlan cx;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_a = nullptr;
   cudaGraphExec_t coarse_exec = nullptr;
   DeviceArena mem;
@@ -1031,6 +1034,10 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.num_sms = prop.multiProcessorCount;
     g_num_sms = prop.multiProcessorCount;
   }
+  if (opt.bitwise_reference && (opt.nranks > 1 || opt.n_gpus > 1))
+    throw HxbError(HXB_EINVAL, "bitwise_reference plans are single-device, single-rank");
+  if (opt.bitwise_reference && opt.host_lists)
+    throw HxbError(HXB_EINVAL, "bitwise_reference plans use the device fine lists");
   if (opt.nranks > 1) {  // validated before any setup work (the geometry hook reads them)
     if (opt.rank < 0 || opt.rank >= opt.nranks) throw HxbError(HXB_EINVAL, "rank out of range");
     if (opt.precond_mode != HXB_PRECOND_NONE && opt.precond_mode != HXB_PRECOND_TWO_SCALE)
@@ -1441,6 +1448,28 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   HXB_CUDA(cudaMallocHost(&pl.h_status, 64 * sizeof(double)));
   if (pl.do_coarse) capture_coarse_graph(pl);
   HXB_CUDA(cudaDeviceSynchronize());
+  if (opt.bitwise_reference) {  // reference-order arithmetic (compat.cu) over the same device data
+    setup_phase("bitwise-reference tables");
+    CompatPlan& c = pl.cx;
+    c.variant = pl.variant;
+    c.wg = pl.wg;
+    c.erec = pl.erec;
+    c.mass = pl.mass;
+    c.c_e = pl.c_e;
+    c.kappa_e = pl.kappa_e;
+    c.h3 = pl.h3;
+    c.mask = pl.mask;
+    c.lumped = pl.d_lumped;
+    c.fine_pos = pl.fine_pos;
+    c.fine_off = pl.fine_off;
+    c.zsort = pl.zsort;
+    c.conn = pl.conn;
+    c.vtx_off = pl.vtx_off;
+    c.vtx_idx = pl.vtx_idx;
+    c.vmask = pl.vmask;
+    compat_init(c, hs);
+    pl.bitwise = true;
+  }
   setup_phase(nullptr);
   pl.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -1637,7 +1666,10 @@ int hxb_apply_A_device(hxb_plan* plan, const double* d_u, double* d_r, void* str
     if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use hxb_dist_apply_A_*");
     HXB_CUDA(cudaSetDevice(pl->device));
     caller_stream_in(*pl, stream);
-    enqueue_ax(*pl, d_u, d_r, nullptr, pl->s_main);
+    if (pl->bitwise)
+      compat_apply_A(pl->cx, d_u, d_r, pl->s_main);
+    else
+      enqueue_ax(*pl, d_u, d_r, nullptr, pl->s_main);
     caller_stream_out(*pl, stream);
   });
 }
@@ -1656,6 +1688,13 @@ int hxb_apply_A(hxb_plan* plan, const double* u, double* r)
     if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use hxb_dist_apply_A_*");
     HXB_CUDA(cudaSetDevice(pl->device));
     Plan& P = *pl;
+    if (P.bitwise) {  // verification mode: plain copies around the reference-order operator
+      HXB_CUDA(cudaMemcpyAsync(P.p, u, sizeof(double) * P.N, cudaMemcpyHostToDevice, P.s_main));
+      compat_apply_A(P.cx, P.p, P.f, P.s_main);
+      HXB_CUDA(cudaMemcpyAsync(r, P.f, sizeof(double) * P.N, cudaMemcpyDeviceToHost, P.s_main));
+      HXB_CUDA(cudaStreamSynchronize(P.s_main));
+      return;
+    }
     constexpr int C = 8;  // measured at cfg2: 8 chunks 10.5 ms, 16 10.8 ms, 32 11.1 ms
     if (!P.s_in) {
       HXB_CUDA(cudaStreamCreateWithFlags(&P.s_in, cudaStreamNonBlocking));
@@ -1812,7 +1851,9 @@ static int apply_precond_host(hxb_plan* plan, const double* r, double* z, int mo
       throw HxbError(HXB_EINVAL, "system has no coarse preconditioner");
     const std::size_t bytes = sizeof(double) * pl->N;
     HXB_CUDA(cudaMemcpyAsync(pl->r, r, bytes, cudaMemcpyHostToDevice, pl->s_main));
-    if (mode < 0) {
+    if (pl->bitwise) {
+      compat_apply_P(pl->cx, pl->precond_mode, mode, pl->r, pl->z, pl->s_main);
+    } else if (mode < 0) {
       enqueue_precond(*pl, nullptr);
     } else {
       // component-only applies (FinePreconditioner::apply / CoarsePreconditioner::apply):
@@ -1853,11 +1894,31 @@ int hxb_apply_P_device(hxb_plan* plan, const double* d_r, double* d_z, void* str
     HXB_CUDA(cudaSetDevice(pl->device));
     cudaStream_t s = pl->s_main;
     caller_stream_in(*pl, stream);
-    if (d_r != pl->r) HXB_CUDA(cudaMemcpyAsync(pl->r, d_r, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice, s));
-    enqueue_precond(*pl, nullptr);
-    if (d_z != pl->z) HXB_CUDA(cudaMemcpyAsync(d_z, pl->z, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice, s));
+    if (pl->bitwise) {
+      compat_apply_P(pl->cx, pl->precond_mode, -1, d_r, d_z, s);
+    } else {
+      if (d_r != pl->r) HXB_CUDA(cudaMemcpyAsync(pl->r, d_r, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice, s));
+      enqueue_precond(*pl, nullptr);
+      if (d_z != pl->z) HXB_CUDA(cudaMemcpyAsync(d_z, pl->z, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice, s));
+    }
     caller_stream_out(*pl, stream);
   });
+}
+
+static void solve_dispatch(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
+{
+  if (!pl.bitwise) {
+    run_pcg(pl, cfg, res);
+    return;
+  }
+  HXB_CUDA(cudaEventRecord(pl.ev_t0, pl.s_main));
+  compat_pcg(pl.cx, pl.precond_mode, pl.b, cfg, res, pl.s_main);
+  HXB_CUDA(cudaEventRecord(pl.ev_t1, pl.s_main));
+  HXB_CUDA(cudaEventSynchronize(pl.ev_t1));
+  float ms = 0;
+  HXB_CUDA(cudaEventElapsedTime(&ms, pl.ev_t0, pl.ev_t1));
+  res->solve_seconds = ms / 1000.0;
+  if (res->u) HXB_CUDA(cudaMemcpy(res->u, pl.cx.u, sizeof(double) * pl.N, cudaMemcpyDeviceToHost));
 }
 
 static void fill_default_b(Plan& pl)
@@ -1878,7 +1939,7 @@ int hxb_solve(hxb_plan* plan, const double* b, const hxb_pcg_config* cfg, hxb_pc
       HXB_CUDA(cudaMemcpy(pl->b, b, sizeof(double) * pl->N, cudaMemcpyHostToDevice));
     else
       fill_default_b(*pl);
-    run_pcg(*pl, *cfg, res);
+    solve_dispatch(*pl, *cfg, res);
   });
 }
 
@@ -1893,7 +1954,7 @@ int hxb_solve_device(hxb_plan* plan, const double* d_b, const hxb_pcg_config* cf
       HXB_CUDA(cudaMemcpy(pl->b, d_b, sizeof(double) * pl->N, cudaMemcpyDeviceToDevice));
     else if (!d_b)
       fill_default_b(*pl);
-    run_pcg(*pl, *cfg, res);
+    solve_dispatch(*pl, *cfg, res);
   });
 }
 

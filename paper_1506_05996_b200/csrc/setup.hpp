@@ -164,6 +164,16 @@ struct DenseCoarse {
   std::vector<double> csr_val;
 };
 DenseCoarse dense_coarse_setup(const Csr& A, int host_inverse_limit);
+// Profile Cholesky of an SPD matrix after reverse Cuthill-McKee (SimplicialLLT
+// as built for the reference here, coarse.cpp:117-127): row i of L holds
+// columns [first[i], i] at env[start[i] ..]; P A P^T = L L^T with row i of the
+// permuted matrix = row perm[i] of A.
+struct EnvelopeFactor {
+  gid n = 0;
+  std::vector<std::int64_t> perm, first, start;
+  std::vector<double> env;
+};
+EnvelopeFactor envelope_cholesky(const Csr& A);
 
 // Setup phase timer: HXB_SETUP_TIMING=1 prints each phase's wall time to stderr.
 void setup_phase(const char* name);  // closes the running phase, opens `name` (nullptr: close and print)

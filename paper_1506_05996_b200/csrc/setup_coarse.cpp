@@ -421,4 +421,92 @@ DenseCoarse dense_coarse_setup(const Csr& A, int host_inverse_limit)
   return dc;
 }
 
+// ---------------------------------------------------------------------------
+// Envelope (profile) Cholesky after a reverse Cuthill-McKee ordering: the
+// factorisation behind the reference's SimplicialLLT direct coarse solves
+// (coarse.cpp:117-127, amg.cpp:176-194) as built in this environment (Eigen is
+// absent from the image and unpinned by the reference; the test build of the
+// reference, oracle/_ref, links the profile-Cholesky SimplicialLLT of
+// oracle/eigen_shim). Used by the bitwise-reference plans, whose device solve
+// replays the same row-bordering recurrences in the same order.
+EnvelopeFactor envelope_cholesky(const Csr& A)
+{
+  const std::int64_t n = A.n;
+  EnvelopeFactor f;
+  f.n = A.n;
+  // graph of the strictly lower entries, both directions, sorted and unique
+  std::vector<std::vector<std::int64_t>> nbr(static_cast<std::size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i)
+    for (std::int64_t q = A.ptr[i]; q < A.ptr[i + 1]; ++q)
+      if (A.col[q] < i) {
+        nbr[i].push_back(A.col[q]);
+        nbr[A.col[q]].push_back(i);
+      }
+  for (auto& l : nbr) {
+    std::sort(l.begin(), l.end());
+    l.erase(std::unique(l.begin(), l.end()), l.end());
+  }
+  auto deg_less = [&](std::int64_t x, std::int64_t y) { return nbr[x].size() < nbr[y].size(); };
+  // Cuthill-McKee from min-degree seeds (ties in index order), reversed
+  std::vector<std::int64_t> seeds(static_cast<std::size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i) seeds[i] = i;
+  std::stable_sort(seeds.begin(), seeds.end(), deg_less);
+  std::vector<char> seen(static_cast<std::size_t>(n), 0);
+  f.perm.clear();
+  f.perm.reserve(static_cast<std::size_t>(n));
+  for (std::int64_t seed : seeds) {
+    if (seen[seed]) continue;
+    seen[seed] = 1;
+    std::size_t head = f.perm.size();
+    f.perm.push_back(seed);
+    while (head < f.perm.size()) {
+      const std::int64_t v = f.perm[head++];
+      std::vector<std::int64_t> fresh;
+      for (std::int64_t w : nbr[v])
+        if (!seen[w]) {
+          seen[w] = 1;
+          fresh.push_back(w);
+        }
+      std::stable_sort(fresh.begin(), fresh.end(), deg_less);
+      f.perm.insert(f.perm.end(), fresh.begin(), fresh.end());
+    }
+  }
+  std::reverse(f.perm.begin(), f.perm.end());
+  std::vector<std::int64_t> inv(static_cast<std::size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i) inv[f.perm[i]] = i;
+  // profile of the permuted lower triangle, then its values
+  f.first.resize(static_cast<std::size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i) f.first[i] = i;
+  for (std::int64_t i = 0; i < n; ++i)
+    for (std::int64_t q = A.ptr[i]; q < A.ptr[i + 1]; ++q)
+      if (A.col[q] <= i) {
+        const std::int64_t a = inv[i], b = inv[A.col[q]];
+        const std::int64_t row = std::max(a, b);
+        f.first[row] = std::min(f.first[row], std::min(a, b));
+      }
+  f.start.assign(static_cast<std::size_t>(n) + 1, 0);
+  for (std::int64_t i = 0; i < n; ++i) f.start[i + 1] = f.start[i] + (i - f.first[i] + 1);
+  f.env.assign(static_cast<std::size_t>(f.start[n]), 0.0);
+  auto L = [&](std::int64_t i, std::int64_t j) -> double& { return f.env[f.start[i] + (j - f.first[i])]; };
+  for (std::int64_t i = 0; i < n; ++i)
+    for (std::int64_t q = A.ptr[i]; q < A.ptr[i + 1]; ++q)
+      if (A.col[q] <= i) {
+        const std::int64_t a = inv[i], b = inv[A.col[q]];
+        L(std::max(a, b), std::min(a, b)) += A.val[q];
+      }
+  // row-bordering factorisation: L_ij = (a_ij - sum_k L_ik L_jk) / L_jj
+  for (std::int64_t i = 0; i < n; ++i) {
+    for (std::int64_t j = f.first[i]; j < i; ++j) {
+      double s = L(i, j);
+      for (std::int64_t k = std::max(f.first[i], f.first[j]); k < j; ++k) s -= L(i, k) * L(j, k);
+      L(i, j) = s / L(j, j);
+    }
+    double d = L(i, i);
+    for (std::int64_t k = f.first[i]; k < i; ++k) d -= L(i, k) * L(i, k);
+    if (!(d > 0)) throw HxbError(3, "coarse matrix Cholesky failed (matrix not SPD?)");
+    L(i, i) = std::sqrt(d);
+  }
+  return f;
+}
+
 }  // namespace hxb

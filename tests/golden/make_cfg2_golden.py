@@ -1,7 +1,9 @@
 """Generate the cfg2 golden fixture (52^3 hexes, N=7, two-scale PCG to 1e-8)
 with the compiled reference (oracle/_ref). Run in the build container:
     python tests/golden/make_cfg2_golden.py
-Writes tests/golden/cfg2_pcg.json (residual/zr histories, ||u||, Ax checksum)."""
+Writes tests/golden/cfg2_pcg.json (residual/zr histories, ||u||, Ax checksum,
+and, for the solution-vector and Ax-vector checks, a strided sample of 4096
+entries plus 64 contiguous block 2-norms of u and of r = A u)."""
 import json
 import os
 import sys
@@ -37,6 +39,18 @@ out = {
     "timing": {"setup_s": setup_s, "ax_s": ax_s, "solve_s": res["solve_seconds"]},
     "generator": "oracle/_ref (unmodified reference + Eigen shim), tests/golden/make_cfg2_golden.py",
 }
+def vector_digest(x):
+    """4096 strided entries (index g = q * (N // 4096)) and the 2-norms of 64
+    contiguous blocks [b*N//64, (b+1)*N//64)."""
+    n = x.size
+    stride = max(1, n // 4096)
+    idx = np.arange(0, min(n, 4096 * stride), stride)[:4096]
+    blocks = [float(np.linalg.norm(x[b * n // 64:(b + 1) * n // 64])) for b in range(64)]
+    return {"stride": int(stride), "sample": [float(v) for v in x[idx]], "block_norms": blocks}
+
+
+out["u_digest"] = vector_digest(res["u"])
+out["ax_digest_seed12345"] = vector_digest(r)
 name = "cfg2_pcg.json" if (k, n) == (52, 7) else f"pcg_k{k}_n{n}.json"
 with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), name), "w") as f:
     json.dump(out, f, indent=1)

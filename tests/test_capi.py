@@ -112,3 +112,17 @@ def test_plan_rejects_empty_mesh():
     with pytest.raises(hx.HxbError) as ei:
         hx.Plan(empty, 3)
     assert ei.value.code == 1 and "no hexahedra" in str(ei.value)
+
+
+def test_pencil_bitwise_vs_reference():
+    """build_pencil (fine.cpp:15-80): the product's pencil (K, M, V, V^-1,
+    lambda) equals the compiled reference's bit for bit for every order, so
+    the bitwise-reference FDM (compat.cu) can reproduce solve_subdomain."""
+    from oracle import ref_available, ref_pencil
+
+    if not ref_available():
+        pytest.skip("reference not built")
+    for n in range(1, 11):
+        P, R = hx.pencil(n), ref_pencil(n)
+        for key in ("K", "M", "V", "V_inv", "lambda"):
+            assert np.array_equal(P[key], R[key]), (n, key)
