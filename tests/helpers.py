@@ -51,25 +51,44 @@ def rounding_noise(ref_result: dict, fma_result: dict) -> float:
 
 
 def reference_noise(ref_result: dict, b, cfg, **mesh_kw) -> float:
-    """Rounding floor of one problem: the larger of two rounding-only
-    perturbations of the reference algorithm, measured against the reference
-    itself: (1) the restatement compiled with FMA contraction, (2) the
-    restatement with correctly rounded dot products. On ill-conditioned
-    cases (tiny high-order meshes, distorted geometry) either alone can move
-    r_k by 1e-8 of r_0 and even change the iteration count by one."""
+    """Rounding floor of one problem: how far rounding-only perturbations of the
+    reference algorithm move its residual history (max_k |dr_k|/r_0):
+    (1) the restatement with correctly rounded dot products (always);
+    (2) the restatement compiled with FMA contraction, only when the coarse
+        solve is direct: the FMA build would also perturb the AMG SETUP
+        (aggregation compares |a_ij| ties), i.e. build a different
+        hierarchy, which the product never does (its setup is bit-exact).
+    Tests allow at most 2x this floor (and never less than 1e-10 r_0), and
+    every case whose tolerance exceeds 1e-10 r_0 is also shown bitwise equal
+    to the reference in the bitwise-reference mode (test_gpu_bitwise.py)."""
     import ctypes as C
 
     from oracle import OracleFmaSystem, OracleSystem
     from oracle.ctypes_oracle import _ORC_SO, _load
 
     tol = 1e-8
-    n1 = rounding_noise(ref_result, OracleFmaSystem(cfg, **mesh_kw).pcg(b, tol=tol))
     L = _load(_ORC_SO, "orc_")
     L.orc_set_dot_mode.argtypes = [C.c_int]
     L.orc_set_dot_mode.restype = None
     L.orc_set_dot_mode(1)
     try:
-        n2 = rounding_noise(ref_result, OracleSystem(cfg, **mesh_kw).pcg(b, tol=tol))
+        exact = OracleSystem(cfg, **mesh_kw)
+        n_dot = rounding_noise(ref_result, exact.pcg(b, tol=tol))
     finally:
         L.orc_set_dot_mode(0)
-    return max(n1, n2)
+    if exact.coarse_amg:
+        return n_dot
+    return max(n_dot, rounding_noise(ref_result, OracleFmaSystem(cfg, **mesh_kw).pcg(b, tol=tol)))
+
+
+def record_parity(name: str, achieved: float, tol: float, **extra) -> None:
+    """Append one achieved parity value to gpurun_out/parity_values.jsonl
+    (copied to profiles/ as the round's parity evidence)."""
+    import json
+    import os
+
+    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    if not os.path.isdir(d):
+        return
+    with open(os.path.join(d, "parity_values.jsonl"), "a") as f:
+        f.write(json.dumps({"test": name, "achieved": achieved, "tol": tol, **extra}) + "\n")

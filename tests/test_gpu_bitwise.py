@@ -106,7 +106,14 @@ PCG_CASES = [
     dict(k=2, order=10),
     # on-the-fly operator variant
     dict(k=6, order=5, family="distorted_elements", variant="on_the_fly"),
+    dict(k=6, order=5, family="uniform", variant="on_the_fly"),
+    # the distributed-PCG problems of test_gpu_parity.py
+    dict(k=6, order=3, family="distorted_elements"),
+    dict(k=8, order=5, family="distorted_domain"),
 ]
+# the order sweep of test_gpu_parity.py::test_order_sweep_pcg (cfg4 shape, small)
+SWEEP_K = {1: 8, 2: 6, 3: 5, 4: 4, 5: 3, 6: 3, 7: 3, 8: 2, 9: 2, 10: 2}
+PCG_CASES += [dict(k=SWEEP_K[n], order=n) for n in range(1, 8)]
 
 
 @pytest.mark.parametrize("case", PCG_CASES, ids=lambda c: "-".join(f"{k}{v}" for k, v in c.items()))

@@ -1,0 +1,59 @@
+"""Full-size parity (slow): BASELINE configs[3] (cfg4, polynomial-order sweep
+at ~20M DOF) against the compiled reference on the same box, both the fast
+path (tolerances of SURVEY §8c, per-iteration residuals within 1e-10
+relative) and the bitwise-reference mode (every residual, z.r and u equal).
+
+The reference runs in its fastest legal mode (fine_threads = cores-1, coarse
+concurrent): apply_parallel sums the subdomain contributions in the same
+(e, slot) order as apply (fine.cpp:233-270), so the threaded reference is
+bitwise the sequential one."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_1506_05996_b200 as hx
+from helpers import history_parity, record_parity, rel
+from oracle import RefConfig, RefSystem, ref_available, splitmix_vector
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(not ref_available(), reason="oracle/_ref (compiled reference) not built")]
+
+# cfg4: N=1..10 at ~20M DOF: k per order
+CFG4_K = {1: 270, 2: 135, 3: 90, 4: 68, 5: 54, 6: 45, 7: 39, 8: 34, 9: 30, 10: 27}
+
+
+def _ref(k, order):
+    cores = os.cpu_count() or 2
+    return RefSystem(RefConfig(k=k, order=order, precond="two_scale", concurrent_precond=True,
+                               fine_threads=max(1, cores - 1)))
+
+
+@pytest.mark.parametrize("order", [3, 5, 7, 10])
+def test_cfg4_fullsize_parity(order):
+    k = CFG4_K[order]
+    ref = _ref(k, order)
+    mesh = hx.generate_cube_mesh(k)
+    u = splitmix_vector(ref.N, 12345)
+    r_ref = ref.apply_A(u)
+    b = ref.load_ones()
+    theirs = ref.pcg(b, tol=1e-8, max_iterations=500)
+    with hx.Plan(mesh, order) as plan:
+        assert plan.N == ref.N
+        ax = rel(plan.apply_A(u), r_ref)
+        assert ax <= 1e-13, ax
+        ours = plan.pcg(b, tol=1e-8, max_iterations=500)
+    dr = history_parity(ours, theirs, tol=1e-10, per_rk=True)
+    print(f"cfg4 n={order} k={k} N={ref.N}: Ax rel {ax:.2e}, iterations {ours['iterations']} "
+          f"(ref {theirs['iterations']}), max|dr_k|/r_k {dr:.2e}")
+    record_parity(f"cfg4_fullsize[n={order}]", dr, 1e-10, N=ref.N, ax_rel=ax, iterations=ours["iterations"],
+                  ref_iterations=theirs["iterations"])
+    # bitwise-reference mode on the same problem: the whole run equals the reference's
+    with hx.Plan(mesh, order, bitwise_reference=True) as bw:
+        assert np.array_equal(bw.apply_A(u), r_ref)
+        same = bw.pcg(b, tol=1e-8, max_iterations=500)
+    assert same["iterations"] == theirs["iterations"]
+    assert np.array_equal(same["residual_history"], theirs["residual_history"])
+    assert np.array_equal(same["zr_history"], theirs["zr_history"])
+    assert np.array_equal(same["u"], theirs["u"])
+    record_parity(f"cfg4_fullsize_bitwise[n={order}]", 0.0, 0.0, N=ref.N, iterations=same["iterations"])
