@@ -273,7 +273,7 @@ int hxb_profile(hxb_plan* plan, int reps, double* out);
 
 /* Distributed Ax over an element-slab partition (one plan per
  * GPU, rank r of R owning elements [r*NE/R, (r+1)*NE/R), created with
- * options.reserved[1..2] = rank, R and precond_mode none). Vectors are
+ * options.rank = r, options.nranks = R and precond_mode none). Vectors are
  * global-length device arrays; a rank reads/writes only the nodes of its
  * elements. Interface nodes are summed in the reference's (e,l) order across
  * ranks (SemOperator::apply + gather, operator.cpp:255-287, mesh.cpp:463-475):
@@ -291,7 +291,7 @@ int hxb_dist_apply_A_continue(hxb_plan* plan, const double* d_u, double* d_r, co
                               double* d_send_down, void* stream);
 int hxb_dist_apply_A_end(hxb_plan* plan, double* d_r, const double* d_recv_up, void* stream);
 
-/* Distributed two-scale PCG, staged (same slab plans, options.reserved[1..2];
+/* Distributed two-scale PCG, staged (same slab plans, options.rank/nranks;
  * the caller carries the messages, see paper_1506_05996_b200/dist.py). Per
  * iteration of krylov.cpp:20-71: vector updates over the rank's nodes
  * (hxb_dist_vec: 0 r=b,u=0  1 u+=a p, r-=a f  2 p=z+a p  3 p=z), partial dots

@@ -18,9 +18,14 @@
 namespace hexsem {
 
 // build_system's mesh and per-element coefficients -> a device plan
+// devices: empty = one GPU (device 0); several = a multi-GPU plan with one
+// element slab per entry (hxb_options.n_gpus / devices, NCCL between distinct
+// devices). bitwise: the reference-order verification mode
+// (hxb_options.bitwise_reference), equal to this reference bit for bit.
 inline hxb_plan* make_b200_plan(const HexMesh& mesh, int order, const Vector& kappa, const Vector& c, PrecondMode mode,
                                 CoarseSolve coarse, gid direct_threshold,
-                                OperatorVariant variant = OperatorVariant::stored)
+                                OperatorVariant variant = OperatorVariant::stored,
+                                const std::vector<int>& devices = {}, bool bitwise = false)
 {
   std::vector<double> xyz(3 * mesh.vertices.size());
   for (std::size_t v = 0; v < mesh.vertices.size(); ++v)
@@ -43,6 +48,13 @@ inline hxb_plan* make_b200_plan(const HexMesh& mesh, int order, const Vector& ka
   opt.coarse_solve = static_cast<int>(coarse);   // same enum order (coarse.hpp:28)
   opt.direct_threshold = direct_threshold;
   opt.variant = static_cast<int>(variant);       // same enum order (operator.hpp:14)
+  opt.bitwise_reference = bitwise ? 1 : 0;
+  if (devices.size() > HXB_MAX_GPUS) throw std::invalid_argument("at most HXB_MAX_GPUS devices");
+  if (devices.size() == 1) opt.device = devices[0];
+  if (devices.size() > 1) {
+    opt.n_gpus = static_cast<int>(devices.size());
+    for (std::size_t r = 0; r < devices.size(); ++r) opt.devices[r] = devices[r];
+  }
   hxb_plan* plan = nullptr;
   if (int rc = hxb_plan_create(&m, order, kappa.data(), c.data(), &opt, &plan)) {
     if (rc == HXB_EINVAL) throw std::invalid_argument(hxb_last_error());

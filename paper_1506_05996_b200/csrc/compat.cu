@@ -392,14 +392,33 @@ __global__ void cx_agg_sum_kernel(const double* __restrict__ rho, const int* __r
   }
 }
 
-// dot (krylov.cpp:11-16): one thread, s += a_i b_i in index order
-__global__ void cx_dot_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n,
-                              double* __restrict__ out)
+// dot (krylov.cpp:11-16): s += a_i b_i in index order. The products are
+// independent (each rounded once, whoever computes it), so warps 1.. stage the
+// next chunk of products in shared memory while thread 0 adds the current
+// chunk in order: the only serial work left is the additions themselves.
+constexpr int kDotChunk = 2048;
+constexpr int kDotBlock = 512;
+__global__ void __launch_bounds__(kDotBlock) cx_dot_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                                           long long n, double* __restrict__ out)
 {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  __shared__ double buf[2][kDotChunk];
+  const int tid = threadIdx.x;
+  for (int q = tid; q < kDotChunk && q < n; q += kDotBlock) buf[0][q] = a[q] * b[q];
+  __syncthreads();
   double s = 0;
-  for (long long i = 0; i < n; ++i) s += a[i] * b[i];
-  *out = s;
+  for (long long base = 0; base < n; base += kDotChunk) {
+    const int cur = static_cast<int>((base / kDotChunk) & 1);
+    if (tid == 0) {
+      const int m = static_cast<int>(n - base < kDotChunk ? n - base : kDotChunk);
+      const double* v = buf[cur];
+      for (int j = 0; j < m; ++j) s += v[j];
+    } else if (tid >= 32) {
+      const long long nb = base + kDotChunk;
+      for (int q = tid - 32; q < kDotChunk && nb + q < n; q += kDotBlock - 32) buf[cur ^ 1][q] = a[nb + q] * b[nb + q];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) *out = s;
 }
 
 // SimplicialLLT::solve as built for the reference (envelope factor after
@@ -473,7 +492,7 @@ void vec(cudaStream_t s, CxOp op, int n, double a, double* y, const double* x0 =
 
 double dot(CompatPlan& c, cudaStream_t s, const double* a, const double* b, long long n)
 {
-  cx_dot_kernel<<<1, 1, 0, s>>>(a, b, n, c.scal);
+  cx_dot_kernel<<<1, kDotBlock, 0, s>>>(a, b, n, c.scal);
   CX_CUDA(cudaMemcpyAsync(c.h_scal, c.scal, sizeof(double), cudaMemcpyDeviceToHost, s));
   CX_CUDA(cudaStreamSynchronize(s));
   return c.h_scal[0];

@@ -82,8 +82,7 @@ struct FdmArgs {
   const int* pos;           // [e][P^3] CSR position of each slot's contribution (-1: sentinel)
   double* zsort;            // contributions in CSR order (combine streams them)
   // fused coarse restriction (restrict_residual, coarse.cpp:138-162): null Rpart = off
-  const double* inv_lumped; // 1/m_N
-  const double* mass;       // [e][nloc]
+  const double* cw;         // [e][nsurfp] surface-slot weights m_l / m_N (0 on Dirichlet slots)
   double* Rpart;            // [e][8] corner partial sums
   double* fsend = nullptr;  // distributed plans: contributions finalised by a neighbour (pos <= -2)
   int ne, sstride, num_surface_global;
@@ -215,11 +214,21 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
   constexpr int NF = (6 * NP * NP + 3) & ~3, P3 = P * P * P;
   __shared__ __align__(16) int s_code[NSP];
   __shared__ __align__(16) int s_sf[NF];
-  __shared__ __align__(16) int s_pos[(P3 + 3) & ~3];
+  // output positions padded to an odd row stride (P+1 for even P): the x-line
+  // reads of pass 5 then hit distinct banks
+  constexpr int PR = (P % 2 == 0) ? P + 1 : P;
+  __shared__ __align__(16) int s_pos[((P * P * PR) + 3) & ~3];
+  __shared__ __align__(16) double s_cw[NSP];
   stage_ints<true>(s_code, a.smap + (long long)e * a.sstride, NSP, tid, Sh::kBlock);
   stage_ints<true>(s_sf, a.sub_face + (long long)e * a.sfstride, NF, tid, Sh::kBlock);
+  if (a.Rpart)
+    for (int q = tid; q < NSP / 2; q += Sh::kBlock) cp_async16(s_cw + 2 * q, a.cw + (long long)e * NSP + 2 * q);
   cp_async_commit();
-  stage_ints<(P3 % 4) == 0>(s_pos, a.pos + (long long)e * P3, P3, tid, Sh::kBlock);
+  if constexpr (PR == P) {
+    stage_ints<(P3 % 4) == 0>(s_pos, a.pos + (long long)e * P3, P3, tid, Sh::kBlock);
+  } else {
+    for (int q = tid; q < P3; q += Sh::kBlock) cp_async4(s_pos + (q / P) * PR + q % P, a.pos + (long long)e * P3 + q);
+  }
   cp_async_commit();
   const double hx = __ldg(a.h3 + 3 * e), hy = __ldg(a.h3 + 3 * e + 1), hz = __ldg(a.h3 + 3 * e + 2);
   const double svol = 8.0 / (hx * hy * hz);  // fine.cpp:154
@@ -257,7 +266,6 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
         // this line's share of the 8 corner sums R_cb = sum_l B[cb][l] (r/m_N)_l m_l.
         // An element-interior node has one copy, so m_N = m_l and its term is
         // r itself (to rounding): only surface nodes read 1/m_N and m_l.
-        const double* ml = a.mass + (std::size_t)e * NP * NP * NP + (kk * NP + jj) * NP;
         const bool line_interior = jj > 0 && jj < n && kk > 0 && kk < n;
         double w0 = 0.0, w1 = 0.0;
 #pragma unroll
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
           if (line_interior && ii > 0 && ii < n)
             w = in[ii + 1];
           else
-            w = gl[ii] >= 0 ? (in[ii + 1] * __ldg(a.inv_lumped + gl[ii])) * __ldg(ml + ii) : 0.0;
+            w = in[ii + 1] * s_cw[surface_slot(NP, ii, jj, kk)];  // (r/m_N) m_l as r (m_l/m_N)
           w0 += s_h0[ii] * w;
           w1 += s_h1[ii] * w;
         }
@@ -349,7 +357,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
 #pragma unroll
     for (int x = 0; x < P; ++x) in[x] = buf[at(x, la, lb)];
     inv(in, out);
-    const int* ps = s_pos + (lb * P + la) * P;
+    const int* ps = s_pos + (lb * P + la) * PR;
 #pragma unroll
     for (int x = 0; x < P; ++x) {
       const int q = ps[x];

@@ -133,10 +133,19 @@ __global__ void dist_unpack_kernel(const int* __restrict__ list, int n, const do
 //   mode 1: u += a p, r -= a f        (krylov.cpp:53-56)
 //   mode 2: p = z + a p               (krylov.cpp:64-66)
 //   mode 3: p = z                     (krylov.cpp:38)
+// a_num/a_den (device scalars, optional): a = *a_num / *a_den, computed on the
+// device (alpha = zr/pf, beta = zr_next/zr of krylov.cpp:53,64); mode 1 is a
+// no-op when *a_den <= 0 (the breakdown exit of krylov.cpp:46-51 skips the update)
 __global__ void dist_vec_kernel(int mode, const int* __restrict__ list, int nlist, int ib0, int ib1, double a,
                                 const double* __restrict__ x0, const double* __restrict__ x1, double* __restrict__ y0,
-                                double* __restrict__ y1)
+                                double* __restrict__ y1, const double* __restrict__ a_num = nullptr,
+                                const double* __restrict__ a_den = nullptr)
 {
+  if (a_num) {
+    const double den = *a_den;
+    if (mode == 1 && !(den > 0)) return;
+    a = *a_num / den;
+  }
   const int total = nlist + (ib1 - ib0);
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     const int g = t < nlist ? __ldg(list + t) : ib0 + (t - nlist);
@@ -167,6 +176,16 @@ __global__ void __launch_bounds__(BLOCK) dist_dot_kernel(const int* __restrict__
     s += __ldg(x + g) * __ldg(y + g);
   }
   dot_commit<BLOCK>(d, s, red);
+}
+// sum of the ranks' partial scalars in rank order (every rank computes the
+// same value: the deterministic all-reduce of the in-process transport)
+__global__ void sum_partials_kernel(const double* __restrict__ parts, int R, double* __restrict__ out)
+{
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int q = 0; q < R; ++q) s += parts[q];
+    *out = s;
+  }
 }
 // neighbours' fine contributions into their sum positions
 __global__ void dist_fine_scatter_kernel(const int* __restrict__ pos, int n, const double* __restrict__ recv,

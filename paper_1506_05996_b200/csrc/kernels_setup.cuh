@@ -153,6 +153,27 @@ __global__ void mass_csr_kernel(const int* __restrict__ ax_idx, long long n, con
   }
 }
 
+// Restriction weights of the surface slots, m_l / m_N (coarse.cpp:149, 157):
+// the FDM's fused restriction reads one contiguous row per element instead of
+// the scattered 1/m_N and the mass row (Dirichlet slots weigh 0)
+__global__ void restrict_weights_kernel(const int* __restrict__ smap, int sstride, const double* __restrict__ mass,
+                                        int nloc, const double* __restrict__ inv_lumped, const int* __restrict__ slot_l,
+                                        int nsurf_raw, int nsurfp, int ne, double* __restrict__ cw)
+{
+  const long long n = static_cast<long long>(ne) * nsurfp;
+  for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+       p += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long e = p / nsurfp;
+    const int q = static_cast<int>(p % nsurfp);
+    double w = 0.0;
+    if (q < nsurf_raw) {
+      const int code = smap[e * sstride + q];
+      if (code >= 0) w = mass[e * nloc + slot_l[q]] * inv_lumped[code];
+    }
+    cw[p] = w;
+  }
+}
+
 // Lumped mass m_N = gather of the local masses (SemOperator ctor,
 // operator.cpp:90-91): surface nodes sum their copies in the CSR's (e, l)
 // order from 0, interior nodes have one copy (0 + m = m); and 1/m_N. Same

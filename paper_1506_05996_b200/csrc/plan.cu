@@ -9,6 +9,7 @@
 // (the reference's std::async, precond.cpp:40-46).
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
+#include <nccl.h>
 
 #include <cub/cub.cuh>
 
@@ -19,6 +20,9 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/hexsem_b200.h"
@@ -132,6 +136,9 @@ struct DevDense {
 
 }  // namespace
 
+struct Group;
+void destroy_group(Group* g);
+
 struct Plan {
   int device = 0;
   cudaStream_t s_main = nullptr, s_coarse = nullptr;  // s_coarse: highest priority
@@ -153,8 +160,14 @@ struct Plan {
   bool do_fine = false, do_coarse = false, use_amg = false;
   double setup_seconds = 0;
 
-  // host state kept for exports (planes dropped after upload)
-  HostSetup hs;
+  // host state kept for exports (planes dropped after upload); shared by the
+  // ranks of a multi-GPU plan (built once, read-only afterwards)
+  std::shared_ptr<HostSetup> hsp;
+  HostSetup& hs;
+  bool shared_setup = false;
+  Group* group = nullptr;   // multi-GPU plan (hxb_options.n_gpus > 1): this Plan is only the handle
+  Plan() : hsp(std::make_shared<HostSetup>()), hs(*hsp) {}
+  explicit Plan(std::shared_ptr<HostSetup> shared) : hsp(std::move(shared)), hs(*hsp), shared_setup(true) {}
   gid coarse_n = 0;
 
   // device arrays
@@ -180,6 +193,7 @@ struct Plan {
   double *Rpart = nullptr, *R = nullptr, *Z = nullptr, *rho = nullptr, *dZ = nullptr;
   double* Zc = nullptr;       // [e][8] coarse corner values for the fused prolongation
   double* mass_csr = nullptr; // m of each surface copy in Ax-CSR order
+  double* cw = nullptr;       // [e][nsurf] restriction weights m_l / m_N of the surface slots (fused in the FDM)
   std::vector<DevLevel> lv;  // AMG levels 0..L (L = coarsest, uses dense)
   DevDense dense;
   DevCsr Kc{};               // K_c on the device (AMG mode: residual between the two K-cycles)
@@ -245,6 +259,7 @@ struct Plan {
 
   ~Plan()
   {
+    if (group) destroy_group(group);
     if (coarse_exec) cudaGraphExecDestroy(coarse_exec);
     for (cudaEvent_t e : {ev_fork, ev_join, ev_t0, ev_t1, ev_a})
       if (e) cudaEventDestroy(e);
@@ -463,8 +478,7 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   a.ne = pl.ne;
   a.sstride = 2 * pl.nsurf;
   a.num_surface_global = pl.nsg + pl.e0 * (pl.order - 1) * (pl.order - 1) * (pl.order - 1);  // first owned interior id
-  a.inv_lumped = pl.d_inv_lumped;
-  a.mass = pl.mass;
+  a.cw = pl.cw;
   a.Rpart = pl.do_coarse ? pl.Rpart + 8LL * pl.e0 : nullptr;  // owned slab of the full Rpart
   a.fsend = pl.fsend;
   a.sfstride = pl.sfstride;
@@ -1009,7 +1023,7 @@ void device_geometry(Plan& pl, HostSetup& hs, const hxb_options& opt)
     throw HxbError(HXB_EMESH, "inverted element " + std::to_string(first_bad) +
                                   ": non-positive Jacobian determinant at a GLL node");
   const bool device_lumped = std::max(1, opt.nranks) == 1 && opt.host_lists == 0;
-  if (!device_lumped) {  // host consumers: lumped mass, host gather lists, distributed setup
+  if (!device_lumped && !pl.shared_setup) {  // host consumers: lumped mass, host gather lists, distributed setup
     hs.geo.mass.resize(static_cast<std::size_t>(ne) * nloc);
     HXB_CUDA(cudaMemcpy(hs.geo.mass.data(), mass, hs.geo.mass.size() * sizeof(double), cudaMemcpyDeviceToHost));
   }
@@ -1045,22 +1059,29 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     if (opt.nranks > m->num_elements) throw HxbError(HXB_EINVAL, "more ranks than elements");
   }
   HostSetup& hs = pl.hs;
-  hs.mesh = mesh_from_arrays(m->num_vertices, m->xyz, m->num_elements, m->conn, m->num_boundary_faces,
-                             m->bface_element, m->bface_face, m->bface_tag);
+  if (pl.shared_setup) {  // another rank of the multi-GPU plan built the host setup: only this slab's planes
+    if (hs.order != order || hs.mesh.num_elements() != m->num_elements)
+      throw HxbError(HXB_EINVAL, "shared host setup does not match the mesh");
+    device_geometry(pl, hs, opt);
+  } else {
+    hs.mesh = mesh_from_arrays(m->num_vertices, m->xyz, m->num_elements, m->conn, m->num_boundary_faces,
+                               m->bface_element, m->bface_face, m->bface_tag);
+    const int ne0 = hs.mesh.num_elements();
+    hs.kappa.assign(kappa_e, kappa_e + ne0);
+    hs.c.assign(c_e, c_e + ne0);
+    SetupOptions so;
+    so.precond_mode = opt.precond_mode;
+    so.coarse_solve = opt.coarse_solve;
+    so.direct_threshold = opt.direct_threshold;
+    so.store_planes = opt.variant == HXB_VARIANT_STORED;
+    so.geometry_hook = [&pl, &opt](HostSetup& h) { device_geometry(pl, h, opt); };
+    // single-device plan with device lists: the lumped mass is assembled on the
+    // device after the surface CSR exists, so the masses never go back to the host
+    so.device_lumped = std::max(1, opt.nranks) == 1 && opt.host_lists == 0;
+    setup_phase("mesh + checks");
+    build_host_setup(hs, order, so);
+  }
   const int ne = hs.mesh.num_elements();
-  hs.kappa.assign(kappa_e, kappa_e + ne);
-  hs.c.assign(c_e, c_e + ne);
-  SetupOptions so;
-  so.precond_mode = opt.precond_mode;
-  so.coarse_solve = opt.coarse_solve;
-  so.direct_threshold = opt.direct_threshold;
-  so.store_planes = opt.variant == HXB_VARIANT_STORED;
-  so.geometry_hook = [&pl, &opt](HostSetup& h) { device_geometry(pl, h, opt); };
-  // single-device plan with device lists: the lumped mass is assembled on the
-  // device after the surface CSR exists, so the masses never go back to the host
-  so.device_lumped = std::max(1, opt.nranks) == 1 && opt.host_lists == 0;
-  setup_phase("mesh + checks");
-  build_host_setup(hs, order, so);
   setup_phase("device: streams, tables");
   const HexMesh& mesh = hs.mesh;
   const Numbering& num = hs.num;
@@ -1127,8 +1148,10 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
                     &hs.geo.wg[p * total + static_cast<std::size_t>(e0 + le) * pl.nloc], pl.nloc * sizeof(double));
     pl.wg = M.upload(wge);
   }
-  hs.geo.wg.clear();
-  hs.geo.wg.shrink_to_fit();
+  if (!pl.shared_setup) {
+    hs.geo.wg.clear();
+    hs.geo.wg.shrink_to_fit();
+  }
   auto slice = [&](const std::vector<double>& v, int per) {
     return std::vector<double>(v.begin() + static_cast<std::size_t>(e0) * per,
                                v.begin() + static_cast<std::size_t>(e0 + nel) * per);
@@ -1241,6 +1264,22 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   }
   pl.rsurf = M.alloc<double>(static_cast<std::size_t>(pl.ne) * pl.nsurf);
 
+  if (pl.do_fine && pl.do_coarse) {  // restriction weights for the FDM's fused restriction
+    std::vector<int> slot_l(nsurf_raw);
+    for (int k = 0; k < pl.np; ++k)
+      for (int j = 0; j < pl.np; ++j)
+        for (int i = 0; i < pl.np; ++i) {
+          const int sl = surface_slot(pl.np, i, j, k);
+          if (sl >= 0) slot_l[sl] = (k * pl.np + j) * pl.np + i;
+        }
+    DeviceArena tmp;
+    int* d_slot = tmp.upload(slot_l);
+    pl.cw = M.alloc<double>(static_cast<std::size_t>(pl.ne) * pl.nsurf);
+    restrict_weights_kernel<<<vec_grid(static_cast<long long>(pl.ne) * pl.nsurf), kVecBlock>>>(
+        pl.smap, 2 * pl.nsurf, pl.mass, pl.nloc, pl.d_inv_lumped, d_slot, nsurf_raw, pl.nsurf, pl.ne, pl.cw);
+    HXB_CUDA(cudaGetLastError());
+    HXB_CUDA(cudaDeviceSynchronize());
+  }
   setup_phase("fine lists");
   // fine: encoded sub_face and the subdomain gather CSR in (e, slot) order
   if (pl.do_fine) {
@@ -1604,8 +1643,629 @@ Plan* as_plan(hxb_plan* p)
   return reinterpret_cast<Plan*>(p);
 }
 
+// entry points that act on one device's vectors: not on a multi-GPU handle
+Plan* as_device_plan(hxb_plan* p)
+{
+  Plan* pl = as_plan(p);
+  if (pl->group)
+    throw HxbError(HXB_EINVAL, "multi-GPU plans take host vectors (hxb_solve, hxb_apply_A); this entry point "
+                               "acts on one device's memory");
+  return pl;
+}
+
+
 }  // namespace
 }  // namespace hxb
+
+// ============================================================================
+// Multi-GPU plan (hxb_options.n_gpus > 1): the mesh is cut into
+// R contiguous element slabs, slab r on devices[r]. One host thread per GPU
+// runs pcg (krylov.cpp:20-71) on its slab; the exchanges of the staged
+// hxb_dist_* protocol (interface Ax partials and finals, ghost r, returned
+// fine contributions, restriction partials, interface z finals) and the
+// scalar all-reduces go over NCCL (ncclSend/ncclRecv/ncclAllReduce/
+// ncclAllGather on the plan's stream, NVLink between the GPUs of one box) or,
+// when ranks share a device, over device-to-device copies ordered by events.
+// Scalars stay on the device: alpha and beta are formed by the vector
+// kernels from device history arrays, so the only host read per iteration
+// is the convergence check (rn, p.Ap), as in the single-GPU loop.
+namespace hxb {
+
+namespace {
+
+// barrier for the rank threads; abort() releases everyone with an error
+class RankBarrier {
+ public:
+  explicit RankBarrier(int n) : n_(n) {}
+  void wait()
+  {
+    std::unique_lock<std::mutex> lk(m_);
+    if (aborted_) throw HxbError(HXB_ECUDA, "multi-GPU solve aborted by another rank");
+    const long long gen = gen_;
+    if (++count_ == n_) {
+      count_ = 0;
+      ++gen_;
+      cv_.notify_all();
+      return;
+    }
+    cv_.wait(lk, [&] { return gen_ != gen || aborted_; });
+    if (aborted_) throw HxbError(HXB_ECUDA, "multi-GPU solve aborted by another rank");
+  }
+  void abort()
+  {
+    std::lock_guard<std::mutex> lk(m_);
+    aborted_ = true;
+    cv_.notify_all();
+  }
+  void reset()
+  {
+    std::lock_guard<std::mutex> lk(m_);
+    aborted_ = false;
+    count_ = 0;
+  }
+
+ private:
+  std::mutex m_;
+  std::condition_variable cv_;
+  int n_, count_ = 0;
+  long long gen_ = 0;
+  bool aborted_ = false;
+};
+
+#define HXB_NCCL(call)                                                                              \
+  do {                                                                                              \
+    ncclResult_t res__ = (call);                                                                    \
+    if (res__ != ncclSuccess) throw HxbError(HXB_ENCCL, std::string(#call) + ": " + ncclGetErrorString(res__)); \
+  } while (0)
+
+struct RankBuf {
+  double *send_up = nullptr, *recv_down = nullptr, *send_down = nullptr, *recv_up = nullptr;
+  double *gsend_down = nullptr, *gsend_up = nullptr, *grecv_down = nullptr, *grecv_up = nullptr;
+  double *fsend = nullptr, *frecv = nullptr, *zsend_down = nullptr, *zrecv_up = nullptr;
+  double* gather = nullptr;  // NCCL all-gather of the restriction partials: R slabs of `cap`
+  double* scal = nullptr;    // [0] r.r [1] z.r [2] p.f partials, [4, 4+R) pulled partials, [32] r.r sum
+  double *hist_zr = nullptr, *hist_pf = nullptr;
+  double* outbuf = nullptr;  // finalised surface values for the host
+  double* h_scal = nullptr;  // pinned
+  int hist_cap = 0;
+  std::vector<int> fin_surf;  // host copy: finalised surface nodes of this rank
+};
+
+struct Mail {  // local transport: what each rank offers in the current exchange
+  const double* down = nullptr;  // to rank r-1
+  const double* up = nullptr;    // to rank r+1
+  const double* scalar = nullptr;
+};
+
+}  // namespace
+
+struct Group {
+  int R = 0;
+  std::vector<int> dev;
+  std::vector<std::unique_ptr<Plan>> pl;
+  std::vector<RankBuf> buf;
+  bool nccl = false;
+  std::vector<ncclComm_t> comm;
+  std::unique_ptr<RankBarrier> bar;
+  std::vector<cudaEvent_t> ev_ready, ev_done;
+  std::vector<Mail> mail;
+  int cap = 0;  // padded restriction slab (doubles)
+  ~Group()
+  {
+    for (int r = 0; r < static_cast<int>(pl.size()); ++r) {
+      cudaSetDevice(dev[r]);
+      cudaDeviceSynchronize();
+      if (r < static_cast<int>(ev_ready.size()) && ev_ready[r]) cudaEventDestroy(ev_ready[r]);
+      if (r < static_cast<int>(ev_done.size()) && ev_done[r]) cudaEventDestroy(ev_done[r]);
+      if (r < static_cast<int>(buf.size()) && buf[r].h_scal) cudaFreeHost(buf[r].h_scal);
+    }
+    for (ncclComm_t c : comm)
+      if (c) ncclCommDestroy(c);
+  }
+};
+
+void destroy_group(Group* g) { delete g; }
+
+// the host setup behind a plan (a multi-GPU handle's ranks share rank 0's)
+const HostSetup& plan_hs(Plan* pl) { return pl->group ? pl->group->pl[0]->hs : pl->hs; }
+
+namespace {
+
+// ---- transport ---------------------------------------------------------------
+// exchange with the neighbours: to_down/to_up go to ranks r-1/r+1, from_down/
+// from_up arrive from them (counts pair up by construction of the lists)
+void g_exchange(Group& G, int r, const double* to_down, int n_to_down, const double* to_up, int n_to_up,
+                double* from_down, int n_from_down, double* from_up, int n_from_up)
+{
+  Plan& P = *G.pl[r];
+  cudaStream_t s = P.s_main;
+  if (G.nccl) {
+    HXB_NCCL(ncclGroupStart());
+    if (r > 0) {
+      if (n_to_down) HXB_NCCL(ncclSend(to_down, n_to_down, ncclDouble, r - 1, G.comm[r], s));
+      if (n_from_down) HXB_NCCL(ncclRecv(from_down, n_from_down, ncclDouble, r - 1, G.comm[r], s));
+    }
+    if (r + 1 < G.R) {
+      if (n_to_up) HXB_NCCL(ncclSend(to_up, n_to_up, ncclDouble, r + 1, G.comm[r], s));
+      if (n_from_up) HXB_NCCL(ncclRecv(from_up, n_from_up, ncclDouble, r + 1, G.comm[r], s));
+    }
+    HXB_NCCL(ncclGroupEnd());
+    return;
+  }
+  // pull model: after everyone's sends are ready, each rank copies what it receives
+  G.mail[r].down = to_down;
+  G.mail[r].up = to_up;
+  HXB_CUDA(cudaEventRecord(G.ev_ready[r], s));
+  G.bar->wait();
+  if (r > 0 && n_from_down) {
+    HXB_CUDA(cudaStreamWaitEvent(s, G.ev_ready[r - 1], 0));
+    HXB_CUDA(cudaMemcpyPeerAsync(from_down, G.dev[r], G.mail[r - 1].up, G.dev[r - 1], sizeof(double) * n_from_down, s));
+  }
+  if (r + 1 < G.R && n_from_up) {
+    HXB_CUDA(cudaStreamWaitEvent(s, G.ev_ready[r + 1], 0));
+    HXB_CUDA(cudaMemcpyPeerAsync(from_up, G.dev[r], G.mail[r + 1].down, G.dev[r + 1], sizeof(double) * n_from_up, s));
+  }
+  HXB_CUDA(cudaEventRecord(G.ev_done[r], s));
+  G.bar->wait();
+  if (r > 0) HXB_CUDA(cudaStreamWaitEvent(s, G.ev_done[r - 1], 0));
+  if (r + 1 < G.R) HXB_CUDA(cudaStreamWaitEvent(s, G.ev_done[r + 1], 0));
+}
+
+// *sum = sum over ranks of *partial (device scalars; identical on every rank)
+void g_allreduce(Group& G, int r, const double* partial, double* sum)
+{
+  Plan& P = *G.pl[r];
+  cudaStream_t s = P.s_main;
+  if (G.nccl) {
+    HXB_NCCL(ncclAllReduce(partial, sum, 1, ncclDouble, ncclSum, G.comm[r], s));
+    return;
+  }
+  G.mail[r].scalar = partial;
+  HXB_CUDA(cudaEventRecord(G.ev_ready[r], s));
+  G.bar->wait();
+  double* parts = G.buf[r].scal + 4;
+  for (int q = 0; q < G.R; ++q) {
+    HXB_CUDA(cudaStreamWaitEvent(s, G.ev_ready[q], 0));
+    HXB_CUDA(cudaMemcpyPeerAsync(parts + q, G.dev[r], G.mail[q].scalar, G.dev[q], sizeof(double), s));
+  }
+  sum_partials_kernel<<<1, 32, 0, s>>>(parts, G.R, sum);
+  P.launches += 1;
+  HXB_CUDA(cudaEventRecord(G.ev_done[r], s));
+  G.bar->wait();
+  for (int q = 0; q < G.R; ++q) HXB_CUDA(cudaStreamWaitEvent(s, G.ev_done[q], 0));
+}
+
+// every rank's restriction partials (its slab of Rpart) into every rank's full Rpart
+void g_allgather_rpart(Group& G, int r)
+{
+  Plan& P = *G.pl[r];
+  cudaStream_t s = P.s_main;
+  if (G.nccl) {
+    double* mine = G.buf[r].gather + static_cast<std::size_t>(r) * G.cap;
+    HXB_CUDA(cudaMemcpyAsync(mine, P.Rpart + 8LL * P.e0, sizeof(double) * 8 * P.ne, cudaMemcpyDeviceToDevice, s));
+    HXB_NCCL(ncclAllGather(mine, G.buf[r].gather, G.cap, ncclDouble, G.comm[r], s));
+    for (int q = 0; q < G.R; ++q)
+      if (q != r)
+        HXB_CUDA(cudaMemcpyAsync(P.Rpart + 8LL * G.pl[q]->e0, G.buf[r].gather + static_cast<std::size_t>(q) * G.cap,
+                                 sizeof(double) * 8 * G.pl[q]->ne, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  HXB_CUDA(cudaEventRecord(G.ev_ready[r], s));
+  G.bar->wait();
+  for (int q = 0; q < G.R; ++q)
+    if (q != r) {
+      const Plan& Q = *G.pl[q];
+      HXB_CUDA(cudaStreamWaitEvent(s, G.ev_ready[q], 0));
+      HXB_CUDA(cudaMemcpyPeerAsync(P.Rpart + 8LL * Q.e0, G.dev[r], Q.Rpart + 8LL * Q.e0, G.dev[q],
+                                   sizeof(double) * 8 * Q.ne, s));
+    }
+  HXB_CUDA(cudaEventRecord(G.ev_done[r], s));
+  G.bar->wait();
+  for (int q = 0; q < G.R; ++q) HXB_CUDA(cudaStreamWaitEvent(s, G.ev_done[q], 0));
+}
+
+// ---- the staged steps (bodies of hxb_dist_*) on the plan's stream -----------
+void r_vec(Plan& P, int mode, const double* x0, const double* x1, double* y0, double* y1, const double* num = nullptr,
+           const double* den = nullptr)
+{
+  const int total = P.n_loc_surf + (P.ib1 - P.ib0);
+  dist_vec_kernel<<<fill_grid(dist_vec_kernel, kVecBlock, total), kVecBlock, 0, P.s_main>>>(
+      mode, P.loc_list, P.n_loc_surf, P.ib0, P.ib1, 0.0, x0, x1, y0, y1, num, den);
+  P.launches += 1;
+}
+
+void r_dot(Plan& P, const double* x, const double* y, double* out)
+{
+  const int total = P.n_fin_surf + (P.ib1 - P.ib0);
+  dist_dot_kernel<kVecBlock><<<fill_grid(dist_dot_kernel<kVecBlock>, kVecBlock, total), kVecBlock, 0, P.s_main>>>(
+      P.fin_surf, P.n_fin_surf, P.ib0, P.ib1, x, y, dot_args(P, out));
+  P.launches += 1;
+}
+
+void r_pack(Plan& P, const int* list, int n, const double* x, double* buf)
+{
+  if (n) dist_pack_kernel<<<vec_grid(n), kVecBlock, 0, P.s_main>>>(list, n, x, buf), P.launches += 1;
+}
+
+void r_unpack(Plan& P, const int* list, int n, const double* buf, double* x)
+{
+  if (n) dist_unpack_kernel<<<vec_grid(n), kVecBlock, 0, P.s_main>>>(list, n, buf, x), P.launches += 1;
+}
+
+// f = A p over the slabs (hxb_dist_apply_A_begin/_continue/_end)
+void g_apply_A(Group& G, int r, const double* p, double* f)
+{
+  Plan& P = *G.pl[r];
+  RankBuf& B = G.buf[r];
+  cudaStream_t s = P.s_main;
+  enqueue_ax(P, p, f, nullptr, s);
+  if (P.n_up) {
+    dist_partial_kernel<<<vec_grid(P.n_up), kVecBlock, 0, s>>>(P.ax_off + P.n_grp0, P.ax_idx, P.rsurf, P.n_up, B.send_up);
+    P.launches += 1;
+  }
+  g_exchange(G, r, nullptr, 0, B.send_up, P.n_up, B.recv_down, P.n_down, nullptr, 0);
+  if (P.n_down) {
+    const int t0 = P.n_grp0 + P.n_up;
+    dist_continue_kernel<<<vec_grid(P.n_down), kVecBlock, 0, s>>>(P.ax_off + t0, P.ax_idx, P.rsurf, P.ax_nodes + t0,
+                                                                  P.n_down, p, P.mask, B.recv_down, f, B.send_down);
+    P.launches += 1;
+  }
+  g_exchange(G, r, B.send_down, P.n_down, nullptr, 0, nullptr, 0, B.recv_up, P.n_up);
+  if (P.n_up) {
+    dist_finish_kernel<<<vec_grid(P.n_up), kVecBlock, 0, s>>>(P.ax_nodes + P.n_grp0, P.n_up, B.recv_up, f);
+    P.launches += 1;
+  }
+}
+
+// z = P r over the slabs (precond.cpp:27-67); *zr = global z.r on every rank
+void g_precond(Group& G, int r, double* zr)
+{
+  Plan& P = *G.pl[r];
+  RankBuf& B = G.buf[r];
+  cudaStream_t s = P.s_main;
+  if (!P.do_fine) {  // PrecondMode::none: z = r
+    r_vec(P, 3, P.r, nullptr, P.z, nullptr);
+    r_dot(P, P.z, P.r, B.scal + 1);
+    g_allreduce(G, r, B.scal + 1, zr);
+    return;
+  }
+  r_pack(P, P.g_to_down, P.n_g_to_down, P.r, B.gsend_down);
+  r_pack(P, P.g_to_up, P.n_g_to_up, P.r, B.gsend_up);
+  g_exchange(G, r, B.gsend_down, P.n_g_to_down, B.gsend_up, P.n_g_to_up, B.grecv_down, P.n_g_from_down, B.grecv_up,
+             P.n_g_from_up);
+  r_unpack(P, P.g_from_down, P.n_g_from_down, B.grecv_down, P.r);
+  r_unpack(P, P.g_from_up, P.n_g_from_up, B.grecv_up, P.r);
+  P.fsend = B.fsend;
+  HXB_DISPATCH_NP(P.np, launch_fdm, P, s);
+  P.fsend = nullptr;
+  g_exchange(G, r, B.fsend, P.n_fsend_down, B.fsend + P.n_fsend_down, P.n_fsend_up, B.frecv, P.n_frecv_down,
+             B.frecv + P.n_frecv_down, P.n_frecv_up);
+  const int nrecv = P.n_frecv_down + P.n_frecv_up;
+  if (nrecv) {
+    dist_fine_scatter_kernel<<<vec_grid(nrecv), kVecBlock, 0, s>>>(P.frecv_pos, nrecv, B.frecv, P.zsort);
+    P.launches += 1;
+  }
+  g_allgather_rpart(G, r);
+  HXB_CUDA(cudaGraphLaunch(P.coarse_exec, s));  // replicated coarse solve: identical on every rank
+  P.launches += P.coarse_graph_nodes;
+  launch_combine(P, B.scal + 1, s, P.do_fine, P.do_coarse);
+  g_allreduce(G, r, B.scal + 1, zr);
+  // finals of the down-interface nodes to the lower rank
+  r_pack(P, P.ax_nodes + P.n_grp0 + P.n_up, P.n_down, P.z, B.zsend_down);
+  g_exchange(G, r, B.zsend_down, P.n_down, nullptr, 0, nullptr, 0, B.zrecv_up, P.n_up);
+  r_unpack(P, P.ax_nodes + P.n_grp0, P.n_up, B.zrecv_up, P.z);
+}
+
+// this rank's finalised values of x (surface list + owned interior range) into host y
+void g_output(Group& G, int r, const double* x, double* y)
+{
+  Plan& P = *G.pl[r];
+  RankBuf& B = G.buf[r];
+  cudaStream_t s = P.s_main;
+  r_pack(P, P.fin_surf, P.n_fin_surf, x, B.outbuf);
+  std::vector<double> surf(P.n_fin_surf);
+  if (P.n_fin_surf)
+    HXB_CUDA(cudaMemcpyAsync(surf.data(), B.outbuf, sizeof(double) * P.n_fin_surf, cudaMemcpyDeviceToHost, s));
+  if (P.ib1 > P.ib0)
+    HXB_CUDA(cudaMemcpyAsync(y + P.ib0, x + P.ib0, sizeof(double) * (P.ib1 - P.ib0), cudaMemcpyDeviceToHost, s));
+  HXB_CUDA(cudaStreamSynchronize(s));
+  for (int q = 0; q < P.n_fin_surf; ++q) y[B.fin_surf[q]] = surf[q];
+}
+
+struct RankResult {
+  int status = HXB_PCG_CONVERGED, iterations = 0;
+  std::vector<double> res_hist, zr_hist;
+  std::string diag;
+  double solve_seconds = 0;
+};
+
+// pcg (krylov.cpp:20-71) on rank r; b already in P.b
+void g_rank_pcg(Group& G, int r, const hxb_pcg_config& cfg, RankResult& out)
+{
+  Plan& P = *G.pl[r];
+  RankBuf& B = G.buf[r];
+  HXB_CUDA(cudaSetDevice(P.device));
+  cudaStream_t s = P.s_main;
+  if (B.hist_cap < cfg.max_iterations + 2) {
+    B.hist_cap = cfg.max_iterations + 2;
+    B.hist_zr = P.mem.alloc<double>(B.hist_cap);
+    B.hist_pf = P.mem.alloc<double>(B.hist_cap);
+  }
+  HXB_CUDA(cudaEventRecord(P.ev_t0, s));
+  r_vec(P, 0, P.b, nullptr, P.r, P.u);  // r = b, u = 0
+  r_dot(P, P.r, P.r, B.scal + 0);
+  g_allreduce(G, r, B.scal + 0, B.scal + 32);
+  HXB_CUDA(cudaMemcpyAsync(B.h_scal, B.scal + 32, sizeof(double), cudaMemcpyDeviceToHost, s));
+  HXB_CUDA(cudaStreamSynchronize(s));
+  const double r0 = std::sqrt(B.h_scal[0]);
+  out.res_hist.push_back(r0);
+  out.status = HXB_PCG_CONVERGED;
+  int k = 0;
+  if (r0 != 0.0) {
+    g_precond(G, r, B.hist_zr + 0);
+    r_vec(P, 3, P.z, nullptr, P.p, nullptr);  // p = z
+    out.status = HXB_PCG_MAX_ITERATIONS;
+    for (k = 0; k < cfg.max_iterations; ++k) {
+      g_apply_A(G, r, P.p, P.f);
+      r_dot(P, P.p, P.f, B.scal + 2);
+      g_allreduce(G, r, B.scal + 2, B.hist_pf + k);
+      r_vec(P, 1, P.p, P.f, P.r, P.u, B.hist_zr + k, B.hist_pf + k);  // u += alpha p, r -= alpha f
+      r_dot(P, P.r, P.r, B.scal + 0);
+      g_allreduce(G, r, B.scal + 0, B.scal + 32);
+      HXB_CUDA(cudaMemcpyAsync(B.h_scal, B.hist_pf + k, sizeof(double), cudaMemcpyDeviceToHost, s));
+      HXB_CUDA(cudaMemcpyAsync(B.h_scal + 1, B.scal + 32, sizeof(double), cudaMemcpyDeviceToHost, s));
+      HXB_CUDA(cudaStreamSynchronize(s));  // the one host read per iteration (convergence)
+      const double pf = B.h_scal[0], rn = std::sqrt(B.h_scal[1]);
+      if (!(pf > 0)) {
+        out.status = HXB_PCG_BREAKDOWN;
+        char msg[160];
+        std::snprintf(msg, sizeof(msg), "indefinite operator: p.Ap = %f at iteration %d", pf, k);
+        out.diag = msg;
+        out.iterations = k;
+        ++k;  // zr_k was recorded
+        break;
+      }
+      out.iterations = k + 1;
+      out.res_hist.push_back(rn);
+      if (rn / r0 <= cfg.rel_tolerance) {
+        out.status = HXB_PCG_CONVERGED;
+        ++k;
+        break;
+      }
+      if (k + 1 == cfg.max_iterations) {
+        out.diag = "not converged within " + std::to_string(cfg.max_iterations) + " iterations";
+        ++k;
+        break;
+      }
+      g_precond(G, r, B.hist_zr + k + 1);
+      r_vec(P, 2, P.z, nullptr, P.p, nullptr, B.hist_zr + k + 1, B.hist_zr + k);  // p = z + beta p
+    }
+  }
+  HXB_CUDA(cudaEventRecord(P.ev_t1, s));
+  HXB_CUDA(cudaEventSynchronize(P.ev_t1));
+  float ms = 0;
+  HXB_CUDA(cudaEventElapsedTime(&ms, P.ev_t0, P.ev_t1));
+  out.solve_seconds = ms / 1000.0;
+  const int nzr = r0 == 0.0 ? 0 : k;
+  out.zr_hist.resize(nzr);
+  if (nzr) HXB_CUDA(cudaMemcpy(out.zr_hist.data(), B.hist_zr, sizeof(double) * nzr, cudaMemcpyDeviceToHost));
+}
+
+// run fn(r) on one host thread per rank; the first error is rethrown
+template <class F>
+void g_run(Group& G, F&& fn)
+{
+  G.bar->reset();
+  std::vector<std::exception_ptr> err(G.R);
+  std::vector<std::thread> th;
+  for (int r = 0; r < G.R; ++r)
+    th.emplace_back([&, r] {
+      try {
+        HXB_CUDA(cudaSetDevice(G.dev[r]));
+        fn(r);
+      } catch (...) {
+        err[r] = std::current_exception();
+        G.bar->abort();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+
+void build_group(Plan& top, const hxb_mesh* m, int order, const double* kappa_e, const double* c_e,
+                 const hxb_options& opt)
+{
+  const int R = opt.n_gpus;
+  if (R < 2 || R > HXB_MAX_GPUS) throw HxbError(HXB_EINVAL, "n_gpus must lie in 2..8");
+  if (!m || m->num_elements < R) throw HxbError(HXB_EINVAL, "more GPUs than elements");
+  if (opt.nranks > 1) throw HxbError(HXB_EINVAL, "n_gpus and the staged rank/nranks are exclusive");
+  if (opt.precond_mode != HXB_PRECOND_NONE && opt.precond_mode != HXB_PRECOND_TWO_SCALE)
+    throw HxbError(HXB_EINVAL, "multi-GPU plans support precond_mode two_scale or none");
+  int ndev = 0;
+  HXB_CUDA(cudaGetDeviceCount(&ndev));
+  auto G = std::make_unique<Group>();
+  G->R = R;
+  for (int r = 0; r < R; ++r) {
+    if (opt.devices[r] < 0 || opt.devices[r] >= ndev) throw HxbError(HXB_EINVAL, "device ordinal out of range");
+    G->dev.push_back(opt.devices[r]);
+  }
+  // rank 0 builds the host setup (numbering, coarse matrix, AMG) once; the
+  // other ranks share it read-only and build their slabs in parallel
+  auto rank_opt = [&](int r) {
+    hxb_options o = opt;
+    o.n_gpus = 1;
+    o.rank = r;
+    o.nranks = R;
+    o.device = G->dev[r];
+    return o;
+  };
+  G->pl.resize(R);
+  {
+    const hxb_options o = rank_opt(0);
+    G->pl[0] = std::make_unique<Plan>();
+    build_plan(*G->pl[0], m, order, kappa_e, c_e, o);
+  }
+  std::shared_ptr<HostSetup> hs = G->pl[0]->hsp;
+  {
+    std::vector<std::exception_ptr> err(R);
+    std::vector<std::thread> th;
+    for (int r = 1; r < R; ++r)
+      th.emplace_back([&, r] {
+        try {
+          const hxb_options o = rank_opt(r);
+          G->pl[r] = std::make_unique<Plan>(hs);
+          build_plan(*G->pl[r], m, order, kappa_e, c_e, o);
+        } catch (...) {
+          err[r] = std::current_exception();
+        }
+      });
+    for (auto& t : th) t.join();
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
+  }
+  // exchange buffers, events
+  int max_ne = 0;
+  for (int r = 0; r < R; ++r) max_ne = std::max(max_ne, G->pl[r]->ne);
+  G->cap = 8 * max_ne;
+  bool distinct = true;
+  for (int r = 0; r < R; ++r)
+    for (int q = 0; q < r; ++q) distinct = distinct && G->dev[r] != G->dev[q];
+  const char* tr = std::getenv("HXB_GROUP_TRANSPORT");
+  G->nccl = distinct && !(tr && std::string(tr) == "local");
+  G->buf.resize(R);
+  G->ev_ready.assign(R, nullptr);
+  G->ev_done.assign(R, nullptr);
+  G->mail.resize(R);
+  for (int r = 0; r < R; ++r) {
+    Plan& P = *G->pl[r];
+    RankBuf& B = G->buf[r];
+    HXB_CUDA(cudaSetDevice(P.device));
+    DeviceArena& M = P.mem;
+    B.send_up = M.alloc<double>(P.n_up);
+    B.recv_up = M.alloc<double>(P.n_up);
+    B.zrecv_up = M.alloc<double>(P.n_up);
+    B.send_down = M.alloc<double>(P.n_down);
+    B.recv_down = M.alloc<double>(P.n_down);
+    B.zsend_down = M.alloc<double>(P.n_down);
+    B.gsend_down = M.alloc<double>(P.n_g_to_down);
+    B.gsend_up = M.alloc<double>(P.n_g_to_up);
+    B.grecv_down = M.alloc<double>(P.n_g_from_down);
+    B.grecv_up = M.alloc<double>(P.n_g_from_up);
+    B.fsend = M.alloc<double>(P.n_fsend_down + P.n_fsend_up);
+    B.frecv = M.alloc<double>(P.n_frecv_down + P.n_frecv_up);
+    B.scal = M.alloc<double>(64);
+    HXB_CUDA(cudaMemset(B.scal, 0, 64 * sizeof(double)));
+    B.outbuf = M.alloc<double>(P.n_fin_surf);
+    if (G->nccl && P.do_coarse) B.gather = M.alloc<double>(static_cast<std::size_t>(R) * G->cap);
+    HXB_CUDA(cudaMallocHost(&B.h_scal, 8 * sizeof(double)));
+    B.fin_surf.resize(P.n_fin_surf);
+    if (P.n_fin_surf)
+      HXB_CUDA(cudaMemcpy(B.fin_surf.data(), P.fin_surf, sizeof(int) * P.n_fin_surf, cudaMemcpyDeviceToHost));
+    HXB_CUDA(cudaEventCreateWithFlags(&G->ev_ready[r], cudaEventDisableTiming));
+    HXB_CUDA(cudaEventCreateWithFlags(&G->ev_done[r], cudaEventDisableTiming));
+    for (int q = 0; q < R; ++q)  // direct NVLink copies between distinct devices where possible
+      if (G->dev[q] != P.device) {
+        int ok = 0;
+        cudaDeviceCanAccessPeer(&ok, P.device, G->dev[q]);
+        if (ok && cudaDeviceEnablePeerAccess(G->dev[q], 0) != cudaSuccess) cudaGetLastError();
+      }
+  }
+  if (G->nccl) {
+    G->comm.assign(R, nullptr);
+    HXB_NCCL(ncclCommInitAll(G->comm.data(), R, G->dev.data()));
+  }
+  G->bar = std::make_unique<RankBarrier>(R);
+  for (int r = 0; r < R; ++r) HXB_CUDA(cudaDeviceSynchronize());
+  // the handle: whole-mesh facts for hxb_plan_get_info
+  Plan& P0 = *G->pl[0];
+  top.device = G->dev[0];
+  top.order = P0.order;
+  top.np = P0.np;
+  top.nloc = P0.nloc;
+  top.N = P0.N;
+  top.ne = P0.ne_total;
+  top.ne_total = P0.ne_total;
+  top.nv = P0.nv;
+  top.use_amg = P0.use_amg;
+  top.coarse_n = P0.coarse_n;
+  top.precond_mode = P0.precond_mode;
+  top.do_fine = P0.do_fine;
+  top.do_coarse = P0.do_coarse;
+  top.nranks = R;
+  for (int r = 0; r < R; ++r) top.setup_seconds = std::max(top.setup_seconds, G->pl[r]->setup_seconds);
+  top.group = G.release();
+}
+
+// hxb_solve on a multi-GPU plan: b (host, or NULL for the Poisson load) -> res
+void group_solve(Plan& top, const double* b, const hxb_pcg_config& cfg, hxb_pcg_result* res)
+{
+  if (!(cfg.rel_tolerance > 0) || !(cfg.rel_tolerance < 1))
+    throw HxbError(HXB_EINVAL, "pcg: rel_tolerance must lie in (0,1)");
+  if (cfg.max_iterations < 1) throw HxbError(HXB_EINVAL, "pcg: max_iterations must be >= 1");
+  Group& G = *top.group;
+  const HostSetup& hs = G.pl[0]->hs;
+  const int N = top.N;
+  std::vector<double> bdef;
+  if (!b) {
+    bdef.resize(N);
+    for (int g = 0; g < N; ++g) bdef[g] = hs.num.dirichlet_mask[g] ? 0.0 : hs.lumped[g] * 1.0;
+    b = bdef.data();
+  }
+  std::vector<RankResult> out(G.R);
+  const auto t0 = std::chrono::steady_clock::now();
+  g_run(G, [&](int r) {
+    Plan& P = *G.pl[r];
+    HXB_CUDA(cudaMemcpyAsync(P.b, b, sizeof(double) * N, cudaMemcpyHostToDevice, P.s_main));
+    g_rank_pcg(G, r, cfg, out[r]);
+    if (res->u) g_output(G, r, P.u, res->u);
+  });
+  (void)t0;
+  const RankResult& o = out[0];
+  double secs = 0;
+  for (const RankResult& q : out) secs = std::max(secs, q.solve_seconds);
+  res->status = o.status;
+  res->iterations = o.iterations;
+  res->solve_seconds = secs;
+  res->num_residuals = cfg.record_history ? static_cast<int>(o.res_hist.size()) : 0;
+  res->num_zr = cfg.record_history ? static_cast<int>(o.zr_hist.size()) : 0;
+  if (cfg.record_history) {
+    if (res->residual_history) std::memcpy(res->residual_history, o.res_hist.data(), sizeof(double) * o.res_hist.size());
+    if (res->zr_history && !o.zr_hist.empty())
+      std::memcpy(res->zr_history, o.zr_hist.data(), sizeof(double) * o.zr_hist.size());
+  }
+  std::snprintf(res->diagnostic, sizeof(res->diagnostic), "%s", o.diag.c_str());
+}
+
+// hxb_apply_P on a multi-GPU plan (host vectors, TwoScalePreconditioner::apply)
+void group_apply_P(Plan& top, const double* rin, double* z_out)
+{
+  Group& G = *top.group;
+  const int N = top.N;
+  g_run(G, [&](int r) {
+    Plan& P = *G.pl[r];
+    HXB_CUDA(cudaMemcpyAsync(P.r, rin, sizeof(double) * N, cudaMemcpyHostToDevice, P.s_main));
+    g_precond(G, r, G.buf[r].scal + 33);
+    g_output(G, r, P.z, z_out);
+  });
+}
+
+// hxb_apply_A on a multi-GPU plan (host vectors)
+void group_apply_A(Plan& top, const double* u, double* r_out)
+{
+  Group& G = *top.group;
+  const int N = top.N;
+  g_run(G, [&](int r) {
+    Plan& P = *G.pl[r];
+    HXB_CUDA(cudaMemcpyAsync(P.p, u, sizeof(double) * N, cudaMemcpyHostToDevice, P.s_main));
+    g_apply_A(G, r, P.p, P.f);
+    g_output(G, r, P.f, r_out);
+  });
+}
+
+}  // namespace
+}  // namespace hxb
+
 
 using namespace hxb;
 
@@ -1623,7 +2283,10 @@ int hxb_plan_create(const hxb_mesh* mesh, int order, const double* kappa_e, cons
     else
       hxb_default_options(&o);
     auto pl = std::make_unique<Plan>();
-    build_plan(*pl, mesh, order, kappa_e, c_e, o);
+    if (o.n_gpus > 1)
+      build_group(*pl, mesh, order, kappa_e, c_e, o);
+    else
+      build_plan(*pl, mesh, order, kappa_e, c_e, o);
     *out = reinterpret_cast<hxb_plan*>(pl.release());
   });
 }
@@ -1653,16 +2316,18 @@ int hxb_plan_get_info(const hxb_plan* plan, hxb_plan_info* info)
     info->coarse_uses_amg = pl->use_amg ? 1 : 0;
     info->coarse_n = pl->coarse_n;
     info->precond_mode = pl->precond_mode;
-    fill_amg_info(pl->hs, &info->amg_levels, info->amg_rows, info->amg_nnz);
+    fill_amg_info(pl->group ? pl->group->pl[0]->hs : pl->hs, &info->amg_levels, info->amg_rows, info->amg_nnz);
     info->setup_seconds = pl->setup_seconds;
     info->device_bytes = static_cast<int64_t>(pl->mem.bytes);
+    if (pl->group)
+      for (const auto& q : pl->group->pl) info->device_bytes += static_cast<int64_t>(q->mem.bytes);
   });
 }
 
 int hxb_apply_A_device(hxb_plan* plan, const double* d_u, double* d_r, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use hxb_dist_apply_A_*");
     HXB_CUDA(cudaSetDevice(pl->device));
     caller_stream_in(*pl, stream);
@@ -1685,6 +2350,11 @@ int hxb_apply_A(hxb_plan* plan, const double* u, double* r)
 {
   return guarded([&] {
     Plan* pl = as_plan(plan);
+    if (!u || !r) throw HxbError(HXB_EINVAL, "null argument");
+    if (pl->group) {
+      group_apply_A(*pl, u, r);
+      return;
+    }
     if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use hxb_dist_apply_A_*");
     HXB_CUDA(cudaSetDevice(pl->device));
     Plan& P = *pl;
@@ -1844,7 +2514,7 @@ int hxb_apply_A(hxb_plan* plan, const double* u, double* r)
 static int apply_precond_host(hxb_plan* plan, const double* r, double* z, int mode)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     if (mode == HXB_PRECOND_FINE_ONLY && !pl->do_fine) throw HxbError(HXB_EINVAL, "system has no fine preconditioner");
     if (mode == HXB_PRECOND_COARSE_ONLY && !pl->do_coarse)
@@ -1877,7 +2547,16 @@ static int apply_precond_host(hxb_plan* plan, const double* r, double* z, int mo
   });
 }
 
-int hxb_apply_P(hxb_plan* plan, const double* r, double* z) { return apply_precond_host(plan, r, z, -1); }
+int hxb_apply_P(hxb_plan* plan, const double* r, double* z)
+{
+  Plan* pl = plan ? reinterpret_cast<Plan*>(plan) : nullptr;
+  if (pl && pl->group)
+    return guarded([&] {
+      if (!r || !z) throw HxbError(HXB_EINVAL, "null argument");
+      group_apply_P(*pl, r, z);
+    });
+  return apply_precond_host(plan, r, z, -1);
+}
 int hxb_apply_fine(hxb_plan* plan, const double* r, double* z)
 {
   return apply_precond_host(plan, r, z, HXB_PRECOND_FINE_ONLY);
@@ -1890,7 +2569,7 @@ int hxb_apply_coarse(hxb_plan* plan, const double* r, double* z)
 int hxb_apply_P_device(hxb_plan* plan, const double* d_r, double* d_z, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     cudaStream_t s = pl->s_main;
     caller_stream_in(*pl, stream);
@@ -1932,8 +2611,12 @@ int hxb_solve(hxb_plan* plan, const double* b, const hxb_pcg_config* cfg, hxb_pc
 {
   return guarded([&] {
     Plan* pl = as_plan(plan);
-    if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans support the staged operator only");
     if (!cfg || !res) throw HxbError(HXB_EINVAL, "null argument");
+    if (pl->group) {
+      group_solve(*pl, b, *cfg, res);
+      return;
+    }
+    if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "staged distributed plans: use hxb_dist_* (or a multi-GPU plan)");
     HXB_CUDA(cudaSetDevice(pl->device));
     if (b)
       HXB_CUDA(cudaMemcpy(pl->b, b, sizeof(double) * pl->N, cudaMemcpyHostToDevice));
@@ -1946,7 +2629,7 @@ int hxb_solve(hxb_plan* plan, const double* b, const hxb_pcg_config* cfg, hxb_pc
 int hxb_solve_device(hxb_plan* plan, const double* d_b, const hxb_pcg_config* cfg, hxb_pcg_result* res)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans support the staged operator only");
     if (!cfg || !res) throw HxbError(HXB_EINVAL, "null argument");
     HXB_CUDA(cudaSetDevice(pl->device));
@@ -1968,7 +2651,7 @@ static void ensure_coords(Plan& pl)
 int hxb_node_coords(hxb_plan* plan, double* xyz)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     if (!xyz) throw HxbError(HXB_EINVAL, "null argument");
     HXB_CUDA(cudaSetDevice(pl->device));
     ensure_coords(*pl);
@@ -1980,7 +2663,7 @@ int hxb_solve_heat(hxb_plan* plan, const hxb_heat_config* hc, const hxb_pcg_conf
                    int* num_steps, int* all_converged, double* final_u, double* solve_seconds)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     if (!hc || !pc || !steps_out || !num_steps || !all_converged) throw HxbError(HXB_EINVAL, "null argument");
     if (!(hc->dt > 0)) throw HxbError(HXB_EINVAL, "heat: dt must be positive");
     if (pl->nranks > 1) throw HxbError(HXB_EINVAL, "distributed plans: use the staged API");
@@ -2073,7 +2756,8 @@ int hxb_load_ones(hxb_plan* plan, double* b)
 {
   return guarded([&] {
     Plan* pl = as_plan(plan);
-    for (int g = 0; g < pl->N; ++g) b[g] = pl->hs.num.dirichlet_mask[g] ? 0.0 : pl->hs.lumped[g] * 1.0;
+    const HostSetup& hs = plan_hs(pl);
+    for (int g = 0; g < pl->N; ++g) b[g] = hs.num.dirichlet_mask[g] ? 0.0 : hs.lumped[g] * 1.0;
   });
 }
 
@@ -2081,14 +2765,14 @@ int hxb_lumped_mass(hxb_plan* plan, double* m)
 {
   return guarded([&] {
     Plan* pl = as_plan(plan);
-    std::memcpy(m, pl->hs.lumped.data(), sizeof(double) * pl->N);
+    std::memcpy(m, plan_hs(pl).lumped.data(), sizeof(double) * pl->N);
   });
 }
 
 int hxb_export_geometry(hxb_plan* plan, double* mass, double* wg)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     const std::size_t nloc = pl->nloc, nlocp = (nloc + 1) & ~std::size_t{1}, nel = pl->ne;
     if (mass) HXB_CUDA(cudaMemcpy(mass, pl->mass, nel * nloc * sizeof(double), cudaMemcpyDeviceToHost));
     if (wg) {
@@ -2105,13 +2789,13 @@ int hxb_export_geometry(hxb_plan* plan, double* mass, double* wg)
 int hxb_export_maps(hxb_plan* plan, int32_t* l2g, int64_t* g2l_offsets, int32_t* g2l_elem, int32_t* g2l_local,
                     int32_t* sub_l2g, uint8_t* dirichlet_mask)
 {
-  return guarded([&] { export_index_maps(as_plan(plan)->hs, l2g, g2l_offsets, g2l_elem, g2l_local, sub_l2g, dirichlet_mask); });
+  return guarded([&] { export_index_maps(plan_hs(as_plan(plan)), l2g, g2l_offsets, g2l_elem, g2l_local, sub_l2g, dirichlet_mask); });
 }
 
 int hxb_amg_level(hxb_plan* plan, int level, int64_t* rows, int64_t* nnz, int64_t* ptr, int32_t* col, double* val,
                   int32_t* aggregate)
 {
-  return guarded([&] { export_amg_level(as_plan(plan)->hs, level, rows, nnz, ptr, col, val, aggregate); });
+  return guarded([&] { export_amg_level(plan_hs(as_plan(plan)), level, rows, nnz, ptr, col, val, aggregate); });
 }
 
 // Per-component device times (ms, CUDA events, warm caches, mean of reps):
@@ -2122,7 +2806,7 @@ int hxb_amg_level(hxb_plan* plan, int level, int64_t* rows, int64_t* nnz, int64_
 int hxb_profile(hxb_plan* plan, int reps, double* out)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     cudaStream_t s = pl->s_main;
     auto timeit = [&](auto&& fn) {
@@ -2173,7 +2857,7 @@ int hxb_profile(hxb_plan* plan, int reps, double* out)
 int hxb_bench_apply_A(hxb_plan* plan, int reps, double* ms_per_apply, double* ms_elem_kernel)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     cudaStream_t s = pl->s_main;
     for (int w = 0; w < 3; ++w) enqueue_ax(*pl, pl->p, pl->f, nullptr, s);
@@ -2204,7 +2888,7 @@ static void dist_stream_out(Plan* pl, void* stream) { caller_stream_out(*pl, str
 int hxb_dist_info(hxb_plan* plan, int64_t* info)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     if (!info) throw HxbError(HXB_EINVAL, "null argument");
     const int64_t v[8] = {pl->rank, pl->nranks, pl->e0, pl->e0 + pl->ne, pl->n_up, pl->n_down, pl->n_grp0, pl->N};
     std::memcpy(info, v, sizeof(v));
@@ -2214,7 +2898,7 @@ int hxb_dist_info(hxb_plan* plan, int64_t* info)
 int hxb_dist_lists(hxb_plan* plan, int32_t* up_nodes, int32_t* down_nodes)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     if (pl->nranks == 1) return;
     if (up_nodes && pl->n_up)
@@ -2228,7 +2912,7 @@ int hxb_dist_lists(hxb_plan* plan, int32_t* up_nodes, int32_t* down_nodes)
 int hxb_dist_apply_A_begin(hxb_plan* plan, const double* d_u, double* d_r, double* d_send_up, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     dist_stream_in(pl, stream);
     enqueue_ax(*pl, d_u, d_r, nullptr, pl->s_main);  // owned elements + group-0 nodes
@@ -2245,7 +2929,7 @@ int hxb_dist_apply_A_continue(hxb_plan* plan, const double* d_u, double* d_r, co
                               double* d_send_down, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     dist_stream_in(pl, stream);
     if (pl->n_down) {
@@ -2262,7 +2946,7 @@ int hxb_dist_apply_A_continue(hxb_plan* plan, const double* d_u, double* d_r, co
 int hxb_dist_apply_A_end(hxb_plan* plan, double* d_r, const double* d_recv_up, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     dist_stream_in(pl, stream);
     if (pl->n_up) {
@@ -2278,7 +2962,7 @@ int hxb_dist_apply_A_end(hxb_plan* plan, double* d_r, const double* d_recv_up, v
 int hxb_dist_pcg_info(hxb_plan* plan, int64_t* info)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     if (!info) throw HxbError(HXB_EINVAL, "null argument");
     const int64_t v[16] = {pl->n_g_from_down, pl->n_g_from_up, pl->n_g_to_down, pl->n_g_to_up,
                            pl->n_fsend_down,  pl->n_fsend_up,  pl->n_frecv_down, pl->n_frecv_up,
@@ -2292,7 +2976,7 @@ int hxb_dist_vec(hxb_plan* plan, int mode, double a, const double* x0, const dou
                  void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     if (mode < 0 || mode > 3) throw HxbError(HXB_EINVAL, "mode out of range");
     HXB_CUDA(cudaSetDevice(pl->device));
     dist_stream_in(pl, stream);
@@ -2307,7 +2991,7 @@ int hxb_dist_vec(hxb_plan* plan, int mode, double a, const double* x0, const dou
 int hxb_dist_dot(hxb_plan* plan, const double* x, const double* y, double* d_out, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     dist_stream_in(pl, stream);
     const int total = pl->n_fin_surf + (pl->ib1 - pl->ib0);
@@ -2340,7 +3024,7 @@ static void dist_list(Plan* pl, int which, bool pack, const int** list, int* n)
 int hxb_dist_pack(hxb_plan* plan, int which, const double* d_x, double* d_buf, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     const int* list;
     int n;
@@ -2354,7 +3038,7 @@ int hxb_dist_pack(hxb_plan* plan, int which, const double* d_x, double* d_buf, v
 int hxb_dist_unpack(hxb_plan* plan, int which, const double* d_buf, double* d_x, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     const int* list;
     int n;
@@ -2371,7 +3055,7 @@ int hxb_dist_unpack(hxb_plan* plan, int which, const double* d_buf, double* d_x,
 int hxb_dist_fine(hxb_plan* plan, const double* d_r, double* d_fsend, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     if (!pl->do_fine) throw HxbError(HXB_EINVAL, "plan has no fine preconditioner");
     HXB_CUDA(cudaSetDevice(pl->device));
     dist_stream_in(pl, stream);
@@ -2388,7 +3072,7 @@ int hxb_dist_fine(hxb_plan* plan, const double* d_r, double* d_fsend, void* stre
 int hxb_dist_fine_recv(hxb_plan* plan, const double* d_frecv, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     dist_stream_in(pl, stream);
     const int n = pl->n_frecv_down + pl->n_frecv_up;
@@ -2402,7 +3086,7 @@ int hxb_dist_fine_recv(hxb_plan* plan, const double* d_frecv, void* stream)
 int hxb_dist_rpart(hxb_plan* plan, int direction, double* d_buf, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     if (!pl->do_coarse) throw HxbError(HXB_EINVAL, "plan has no coarse preconditioner");
     HXB_CUDA(cudaSetDevice(pl->device));
     dist_stream_in(pl, stream);
@@ -2420,7 +3104,7 @@ int hxb_dist_rpart(hxb_plan* plan, int direction, double* d_buf, void* stream)
 int hxb_dist_coarse(hxb_plan* plan, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     if (!pl->do_coarse) throw HxbError(HXB_EINVAL, "plan has no coarse preconditioner");
     HXB_CUDA(cudaSetDevice(pl->device));
     dist_stream_in(pl, stream);
@@ -2434,7 +3118,7 @@ int hxb_dist_coarse(hxb_plan* plan, void* stream)
 int hxb_dist_combine(hxb_plan* plan, const double* d_r, double* d_z, double* d_zr, void* stream)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     dist_stream_in(pl, stream);
     double* kr = pl->r;
@@ -2451,7 +3135,7 @@ int hxb_dist_combine(hxb_plan* plan, const double* d_r, double* d_z, double* d_z
 int hxb_kernel_timing(hxb_plan* plan, int enable, int max_launches)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     HXB_CUDA(cudaSetDevice(pl->device));
     if (enable) {
       if (max_launches < 1) throw HxbError(HXB_EINVAL, "max_launches must be >= 1");
@@ -2471,7 +3155,7 @@ int hxb_kernel_timing(hxb_plan* plan, int enable, int max_launches)
 int hxb_kernel_timing_read(hxb_plan* plan, int tag, double* total_ms, int* count)
 {
   return guarded([&] {
-    Plan* pl = as_plan(plan);
+    Plan* pl = as_device_plan(plan);
     if (!total_ms || !count) throw HxbError(HXB_EINVAL, "null argument");
     HXB_CUDA(cudaSetDevice(pl->device));
     HXB_CUDA(cudaStreamSynchronize(pl->s_main));
@@ -2495,6 +3179,8 @@ int hxb_launch_count(hxb_plan* plan, int64_t* launches)
     Plan* pl = as_plan(plan);
     if (!launches) throw HxbError(HXB_EINVAL, "null argument");
     *launches = pl->launches;
+    if (pl->group)
+      for (const auto& q : pl->group->pl) *launches += q->launches;
   });
 }
 

@@ -155,7 +155,6 @@ def test_cfg3_bitwise(coarse_solve):
         assert_pcg_bitwise(plan.pcg(b, tol=1e-8), ref.pcg(b, tol=1e-8), f"cfg3 {coarse_solve}")
 
 
-@pytest.mark.slow
 def test_cfg2_bitwise_against_golden():
     """cfg2 (52^3, N=7, 48.6M DOF, AMG coarse path): the bitwise-reference plan
     reproduces the reference's committed run (tests/golden/cfg2_pcg.json) bit
@@ -169,12 +168,15 @@ def test_cfg2_bitwise_against_golden():
             d = gold["ax_digest_seed12345"]
             s = d["stride"]
             assert_bitwise(r[::s][:len(d["sample"])], np.array(d["sample"]), "cfg2 Ax sample")
-        assert float(np.linalg.norm(r)) == gold["ax_norm_seed12345"]
+        # (numpy's norm itself rounds differently on different host CPUs: 1e-14)
+        assert abs(np.linalg.norm(r) - gold["ax_norm_seed12345"]) <= 1e-14 * gold["ax_norm_seed12345"]
         res = plan.pcg(None, tol=1e-8, max_iterations=500)
     assert res["iterations"] == gold["iterations"]
     assert_bitwise(res["residual_history"], np.array(gold["residual_history"]), "cfg2 residual_history")
     assert_bitwise(res["zr_history"], np.array(gold["zr_history"]), "cfg2 zr_history")
-    assert float(np.linalg.norm(res["u"])) == gold["u_norm2"]
-    if "u_digest" in gold:
-        d = gold["u_digest"]
-        assert_bitwise(res["u"][::d["stride"]][:len(d["sample"])], np.array(d["sample"]), "cfg2 u sample")
+    d = gold["u_digest"]
+    assert_bitwise(res["u"][::d["stride"]][:len(d["sample"])], np.array(d["sample"]), "cfg2 u sample")
+    nb = res["u"].size
+    blk = np.array([np.linalg.norm(res["u"][b * nb // 64:(b + 1) * nb // 64]) for b in range(64)])
+    assert np.max(np.abs(blk - np.array(d["block_norms"])) / np.array(d["block_norms"])) <= 1e-14
+    assert abs(np.linalg.norm(res["u"]) - gold["u_norm2"]) <= 1e-14 * gold["u_norm2"]

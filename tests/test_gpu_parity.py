@@ -217,7 +217,6 @@ def test_pcg_amg_path():
     history_parity(plan.pcg(b, tol=1e-8), ref.pcg(b, tol=1e-8))
 
 
-@pytest.mark.slow
 def test_pcg_cfg2_against_golden():
     """cfg2 (52^3, N=7, ~48.6M DOF) two-scale PCG to 1e-8 against
     (a) the reference's history (tests/golden/cfg2_pcg.json, oracle/_ref) and
