@@ -257,6 +257,13 @@ int hxb_setup_export_geometry(const hxb_setup* setup, double* mass, double* wg);
  * (optional) = local node ids [group0 | up | down]. */
 int hxb_setup_dist_lists(const hxb_setup* setup, int rank, int nranks, int64_t* counts, int32_t* nodes);
 
+/* GPU-free check of the sparse direct coarse factor (nested dissection +
+ * supernodal Cholesky of the coupled block of K_c, the device replacement of
+ * SimplicialLLT, coarse.cpp:112-127): relative residual of a solve with b = 1,
+ * number of stored factor entries, separator-tree levels. */
+int hxb_setup_coarse_direct_check(const hxb_setup* setup, double* rel_residual, int64_t* factor_entries,
+                                  int32_t* levels);
+
 /* GllBasis (gll.hpp:17-31) and PencilFactorization (fine.hpp:18-26) tables. */
 int hxb_gll(int order, double* nodes, double* weights, double* deriv);
 int hxb_pencil(int order, double* K, double* M, double* V, double* V_inv, double* lambda);

@@ -1,6 +1,7 @@
 // Host-only part of the C-ABI (include/hexsem_b200.h): mesh generators,
 // the GPU-free setup object used by the bit-exactness tests, counter models.
 // Compiled with g++ (no CUDA); the device plan lives in plan.cu.
+#include <cmath>
 #include <cstring>
 #include <memory>
 
@@ -304,6 +305,54 @@ int hxb_setup_dist_lists(const hxb_setup* setup, int rank, int nranks, int64_t* 
     const int64_t v[6] = {d.e0, d.e1, d.n_grp0, d.n_up, d.n_down, static_cast<int64_t>(d.nodes.size())};
     std::memcpy(counts, v, sizeof(v));
     if (nodes) std::memcpy(nodes, d.nodes.data(), d.nodes.size() * sizeof(int32_t));
+  });
+}
+
+// GPU-free check of the sparse direct coarse factor (setup_nd.cpp) on the
+// setup's coupled coarse block: relative residual |A x - b| / |b| of a
+// factor solve with b = 1, factor entries, separator-tree levels.
+int hxb_setup_coarse_direct_check(const hxb_setup* setup, double* rel_residual, int64_t* factor_entries,
+                                  int32_t* levels)
+{
+  return guarded([&] {
+    const HostSetup& hs = *reinterpret_cast<const HostSetup*>(setup);
+    if (!hs.do_coarse) throw HxbError(HXB_EINVAL, "setup has no coarse preconditioner");
+    const Csr& K = hs.Kc;
+    std::vector<int> pos(K.n, -1), coupled;
+    for (int i = 0; i < K.n; ++i)
+      for (std::int64_t q = K.ptr[i]; q < K.ptr[i + 1]; ++q)
+        if (K.col[q] != i) {
+          pos[i] = static_cast<int>(coupled.size());
+          coupled.push_back(i);
+          break;
+        }
+    Csr B;
+    B.n = static_cast<gid>(coupled.size());
+    B.ptr.assign(1, 0);
+    for (int i : coupled) {
+      for (std::int64_t q = K.ptr[i]; q < K.ptr[i + 1]; ++q) {
+        B.col.push_back(pos[K.col[q]]);
+        B.val.push_back(K.val[q]);
+      }
+      B.ptr.push_back(static_cast<std::int64_t>(B.col.size()));
+    }
+    std::vector<std::array<double, 3>> xyz(B.n);
+    for (int q = 0; q < B.n; ++q) xyz[q] = hs.mesh.vertices[coupled[q]];
+    const NdFactor F = nd_cholesky(B, xyz);
+    std::vector<double> b(B.n, 1.0);
+    const std::vector<double> x = nd_solve_host(F, b);
+    double rn = 0, bn = 0;
+    for (int i = 0; i < B.n; ++i) {
+      double ax = 0;
+      for (std::int64_t q = B.ptr[i]; q < B.ptr[i + 1]; ++q) ax += B.val[q] * x[B.col[q]];
+      rn += (ax - b[i]) * (ax - b[i]);
+      bn += b[i] * b[i];
+    }
+    if (rel_residual) *rel_residual = std::sqrt(rn / bn);
+    std::int64_t e = 0;
+    for (const NdSupernode& S : F.sn) e += static_cast<std::int64_t>(S.linv.size() + S.l21.size());
+    if (factor_entries) *factor_entries = e;
+    if (levels) *levels = F.levels;
   });
 }
 

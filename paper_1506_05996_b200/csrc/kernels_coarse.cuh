@@ -411,4 +411,136 @@ __global__ void dense_tile_reduce_kernel(const double* __restrict__ rowpart, con
   }
 }
 
+// ---------------------------------------------------------------------------
+// Sparse direct coarse solve (setup_nd.cpp): nested-dissection supernodal
+// factor P A P^T = L L^T of the coupled block, solved level by level over the
+// separator tree. Per supernode s (columns [c0, c0+m), below-diagonal rows
+// rows[0..r)):
+//   forward   ye = y_s - (children's propagated L z contributions to V_s)
+//             z_s = L11^-1 ye                                  (nd_fwd_diag)
+//             acc_s = L21 z_s + (children's contributions to rows(s))  (nd_fwd_upd)
+//   backward  t_s = z_s - L21^T x(rows(s))                      (nd_bwd_upd)
+//             x_s = L11^-T t_s                                  (nd_bwd_diag)
+// Each dot product is a warp reduction in a fixed tree; the children's
+// contributions are summed in child order from per-position lists, so the
+// solve is deterministic. One CTA handles one task (supernode, block of rows).
+struct NdDev {
+  int n = 0;                       // coupled unknowns
+  const int* perm = nullptr;       // permuted index -> coupled index
+  const int* c0 = nullptr;
+  const int* m = nullptr;
+  const int* r = nullptr;
+  const long long* linv_off = nullptr;  // also the offsets of linvT (m x m each)
+  const long long* l21_off = nullptr;   // also the offsets of l21T (r x m / m x r)
+  const double *linv = nullptr, *linvT = nullptr, *l21 = nullptr, *l21T = nullptr;
+  const long long* rows_off = nullptr;  // rows and acc of supernode s at rows_off[s]
+  const int* rows = nullptr;
+  const long long* inc_base = nullptr;  // position (s, p) -> inc_base[s] + p in inc_ptr
+  const int* inc_ptr = nullptr;
+  const int* inc_idx = nullptr;         // acc entries contributing to that position, child order
+  double *y = nullptr, *z = nullptr, *t = nullptr, *x = nullptr, *acc = nullptr;
+};
+struct NdTask {
+  int s, row0, nrows;
+};
+constexpr int kNdRowsPerTask = 32;
+constexpr int kNdBlock = 256;
+
+__device__ __forceinline__ double nd_warp_sum(double v)
+{
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ double nd_incoming(const NdDev& d, int s, int p)
+{
+  const long long q = d.inc_base[s] + p;
+  double sum = 0.0;
+  for (int k = d.inc_ptr[q]; k < d.inc_ptr[q + 1]; ++k) sum += d.acc[d.inc_idx[k]];
+  return sum;
+}
+
+__global__ void __launch_bounds__(kNdBlock) nd_fwd_diag_kernel(NdDev d, const NdTask* __restrict__ tasks)
+{
+  extern __shared__ double ye[];
+  const NdTask T = tasks[blockIdx.x];
+  const int s = T.s, m = d.m[s], c0 = d.c0[s];
+  for (int j = threadIdx.x; j < m; j += blockDim.x) ye[j] = d.y[c0 + j] - nd_incoming(d, s, j);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* L = d.linv + d.linv_off[s];
+  for (int j = T.row0 + warp; j < T.row0 + T.nrows; j += kNdBlock / 32) {
+    const double* row = L + static_cast<long long>(j) * m;
+    double v = 0.0;
+    for (int k = lane; k <= j; k += 32) v += row[k] * ye[k];
+    v = nd_warp_sum(v);
+    if (lane == 0) d.z[c0 + j] = v;
+  }
+}
+
+__global__ void __launch_bounds__(kNdBlock) nd_fwd_upd_kernel(NdDev d, const NdTask* __restrict__ tasks)
+{
+  const NdTask T = tasks[blockIdx.x];
+  const int s = T.s, m = d.m[s], c0 = d.c0[s];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* L = d.l21 + d.l21_off[s];
+  for (int i = T.row0 + warp; i < T.row0 + T.nrows; i += kNdBlock / 32) {
+    const double* row = L + static_cast<long long>(i) * m;
+    double v = 0.0;
+    for (int k = lane; k < m; k += 32) v += row[k] * d.z[c0 + k];
+    v = nd_warp_sum(v);
+    if (lane == 0) d.acc[d.rows_off[s] + i] = v + nd_incoming(d, s, m + i);
+  }
+}
+
+__global__ void __launch_bounds__(kNdBlock) nd_bwd_upd_kernel(NdDev d, const NdTask* __restrict__ tasks)
+{
+  const NdTask T = tasks[blockIdx.x];
+  const int s = T.s, m = d.m[s], r = d.r[s], c0 = d.c0[s];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* L = d.l21T + d.l21_off[s];
+  const int* rows = d.rows + d.rows_off[s];
+  for (int j = T.row0 + warp; j < T.row0 + T.nrows; j += kNdBlock / 32) {
+    const double* row = L + static_cast<long long>(j) * r;
+    double v = 0.0;
+    for (int k = lane; k < r; k += 32) v += row[k] * d.x[rows[k]];
+    v = nd_warp_sum(v);
+    if (lane == 0) d.t[c0 + j] = d.z[c0 + j] - v;
+  }
+  (void)m;
+}
+
+__global__ void __launch_bounds__(kNdBlock) nd_bwd_diag_kernel(NdDev d, const NdTask* __restrict__ tasks)
+{
+  const NdTask T = tasks[blockIdx.x];
+  const int s = T.s, m = d.m[s], c0 = d.c0[s];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* L = d.linvT + d.linv_off[s];  // row j of L11^-T: entries k >= j
+  for (int j = T.row0 + warp; j < T.row0 + T.nrows; j += kNdBlock / 32) {
+    const double* row = L + static_cast<long long>(j) * m;
+    double v = 0.0;
+    for (int k = j + lane; k < m; k += 32) v += row[k] * d.t[c0 + k];
+    v = nd_warp_sum(v);
+    if (lane == 0) d.x[c0 + j] = v;
+  }
+}
+
+// y = P b on the coupled rows; decoupled rows solved directly (1/a_ii)
+__global__ void nd_permute_in_kernel(const int* __restrict__ perm, const int* __restrict__ coupled, int m,
+                                     const double* __restrict__ inv_diag, const double* __restrict__ b,
+                                     double* __restrict__ y, double* __restrict__ out, int n)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n || i < m; i += gridDim.x * blockDim.x) {
+    if (i < m) y[i] = b[coupled[perm[i]]];
+    if (i < n && inv_diag[i] != 0.0) out[i] = b[i] * inv_diag[i];
+  }
+}
+
+__global__ void nd_permute_out_kernel(const int* __restrict__ perm, const int* __restrict__ coupled, int m,
+                                      const double* __restrict__ x, double* __restrict__ out)
+{
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) out[coupled[perm[i]]] = x[i];
+}
+
 }  // namespace hxb

@@ -123,6 +123,12 @@ struct DevLevel {
 };
 
 struct DevDense {
+  // nested-dissection supernodal factor (large coupled blocks with vertex coordinates)
+  bool nd = false;
+  NdDev ndd;
+  int nd_levels = 0, nd_max_m = 0;
+  std::vector<std::pair<NdTask*, int>> nd_fwd_diag, nd_fwd_upd, nd_bwd_upd, nd_bwd_diag;  // per level
+  std::int64_t nd_factor_bytes = 0;
   int n = 0, m = 0;
   double* ainv = nullptr;  // full row-major inverse (small blocks)
   int* coupled = nullptr;
@@ -566,9 +572,15 @@ void launch_restrict(Plan& pl, cudaStream_t s)
 }
 
 // ---- AMG enqueue (captured into the coarse graph) --------------------------
+void enqueue_nd(Plan& pl, const DevDense& d, const double* b, double* x, cudaStream_t s);
+
 void enqueue_dense(Plan& pl, const double* b, double* x, cudaStream_t s)
 {
   const DevDense& d = pl.dense;
+  if (d.nd) {
+    enqueue_nd(pl, d, b, x, s);
+    return;
+  }
   if (d.tiles) {  // packed symmetric tiles (large coupled block)
     const int mp = d.nt * kDenseTile;
     dense_gather_x_kernel<<<vec_grid(mp), kVecBlock, 0, s>>>(b, d.coupled, d.m, mp, d.xg);
@@ -799,7 +811,144 @@ struct GatherCsr {
   std::vector<int> idx;
 };
 
-DevDense dense_to_device(Plan& pl, const Csr& A)
+// Upload a nested-dissection factor of the coupled block (setup_nd.cpp) and
+// its per-level task lists.
+void nd_to_device(Plan& pl, DevDense& d, const NdFactor& F)
+{
+  DeviceArena& M = pl.mem;
+  const int ns = static_cast<int>(F.sn.size());
+  std::vector<int> c0(ns), mm(ns), rr(ns);
+  std::vector<long long> linv_off(ns), l21_off(ns), rows_off(ns), inc_base(ns);
+  long long nlinv = 0, nl21 = 0, nrows = 0, npos = 0;
+  for (int s = 0; s < ns; ++s) {
+    const NdSupernode& S = F.sn[s];
+    c0[s] = S.c0;
+    mm[s] = S.c1 - S.c0;
+    rr[s] = static_cast<int>(S.rows.size());
+    linv_off[s] = nlinv;
+    l21_off[s] = nl21;
+    rows_off[s] = nrows;
+    inc_base[s] = npos;
+    nlinv += static_cast<long long>(mm[s]) * mm[s];
+    nl21 += static_cast<long long>(mm[s]) * rr[s];
+    nrows += rr[s];
+    npos += mm[s] + rr[s];
+    d.nd_max_m = std::max(d.nd_max_m, mm[s]);
+  }
+  std::vector<double> linv(nlinv), linvT(nlinv), l21(nl21), l21T(nl21);
+  std::vector<int> rows(nrows);
+  for (int s = 0; s < ns; ++s) {
+    const NdSupernode& S = F.sn[s];
+    const int m = mm[s], r = rr[s];
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) {
+        linv[linv_off[s] + static_cast<long long>(i) * m + j] = S.linv[static_cast<std::size_t>(i) * m + j];
+        linvT[linv_off[s] + static_cast<long long>(j) * m + i] = S.linv[static_cast<std::size_t>(i) * m + j];
+      }
+    for (int i = 0; i < r; ++i)
+      for (int j = 0; j < m; ++j) {
+        l21[l21_off[s] + static_cast<long long>(i) * m + j] = S.l21[static_cast<std::size_t>(i) * m + j];
+        l21T[l21_off[s] + static_cast<long long>(j) * r + i] = S.l21[static_cast<std::size_t>(i) * m + j];
+      }
+    std::copy(S.rows.begin(), S.rows.end(), rows.begin() + rows_off[s]);
+  }
+  // incoming contributions of each front position: children's acc entries, child order
+  std::vector<int> cnt(npos + 1, 0);
+  std::vector<std::vector<std::pair<long long, int>>> lists(ns);
+  for (int s = 0; s < ns; ++s) {
+    const NdSupernode& S = F.sn[s];
+    for (int c : S.children) {
+      const NdSupernode& C = F.sn[c];
+      for (int i = 0; i < rr[c]; ++i) {
+        const int g = C.rows[i];
+        int p;
+        if (g < S.c1) {
+          p = g - S.c0;
+        } else {
+          p = mm[s] + static_cast<int>(std::lower_bound(S.rows.begin(), S.rows.end(), g) - S.rows.begin());
+        }
+        lists[s].push_back({inc_base[s] + p, static_cast<int>(rows_off[c] + i)});
+      }
+    }
+    for (const auto& e : lists[s]) cnt[e.first + 1]++;
+  }
+  for (long long q = 0; q < npos; ++q) cnt[q + 1] += cnt[q];
+  std::vector<int> idx(cnt[npos]);
+  {
+    std::vector<int> cur(cnt.begin(), cnt.end() - 1);
+    for (int s = 0; s < ns; ++s)
+      for (const auto& e : lists[s]) idx[cur[e.first]++] = e.second;  // stable: child order, row order
+  }
+  NdDev& D = d.ndd;
+  D.n = F.n;
+  D.perm = M.upload(F.perm);
+  D.c0 = M.upload(c0);
+  D.m = M.upload(mm);
+  D.r = M.upload(rr);
+  D.linv_off = M.upload(linv_off);
+  D.l21_off = M.upload(l21_off);
+  D.linv = M.upload(linv);
+  D.linvT = M.upload(linvT);
+  D.l21 = M.upload(l21);
+  D.l21T = M.upload(l21T);
+  D.rows_off = M.upload(rows_off);
+  D.rows = M.upload(rows);
+  D.inc_base = M.upload(inc_base);
+  D.inc_ptr = M.upload(cnt);
+  D.inc_idx = M.upload(idx);
+  for (double** v : {&D.y, &D.z, &D.t, &D.x}) *v = M.alloc<double>(std::max(1, F.n));
+  D.acc = M.alloc<double>(std::max<long long>(1, nrows));
+  d.nd_factor_bytes = static_cast<std::int64_t>(sizeof(double)) * 2 * (nlinv + nl21);
+  // per-level task lists (blocks of kNdRowsPerTask rows)
+  d.nd_levels = F.levels;
+  std::vector<std::vector<NdTask>> fd(F.levels), fu(F.levels), bu(F.levels), bd(F.levels);
+  for (int s = 0; s < ns; ++s) {
+    const int lv = F.sn[s].level;
+    for (int r0 = 0; r0 < mm[s]; r0 += kNdRowsPerTask) {
+      const NdTask t{s, r0, std::min(kNdRowsPerTask, mm[s] - r0)};
+      fd[lv].push_back(t);
+      bu[lv].push_back(t);
+      bd[lv].push_back(t);
+    }
+    for (int r0 = 0; r0 < rr[s]; r0 += kNdRowsPerTask) fu[lv].push_back(NdTask{s, r0, std::min(kNdRowsPerTask, rr[s] - r0)});
+  }
+  auto up = [&](const std::vector<std::vector<NdTask>>& v, std::vector<std::pair<NdTask*, int>>& out) {
+    out.clear();
+    for (const auto& l : v) out.push_back({l.empty() ? nullptr : M.upload(l), static_cast<int>(l.size())});
+  };
+  up(fd, d.nd_fwd_diag);
+  up(fu, d.nd_fwd_upd);
+  up(bu, d.nd_bwd_upd);
+  up(bd, d.nd_bwd_diag);
+  const int smem = static_cast<int>(sizeof(double) * std::max(1, d.nd_max_m));
+  if (smem > 200 * 1024) throw HxbError(HXB_EINVAL, "coarse separator too large for the supernodal solve");
+  HXB_CUDA(cudaFuncSetAttribute(nd_fwd_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  d.nd = true;
+}
+
+void enqueue_nd(Plan& pl, const DevDense& d, const double* b, double* x, cudaStream_t s)
+{
+  const NdDev& D = d.ndd;
+  nd_permute_in_kernel<<<vec_grid(std::max(d.n, d.m)), kVecBlock, 0, s>>>(D.perm, d.coupled, d.m, d.inv_diag, b, D.y,
+                                                                          x, d.n);
+  const int smem = static_cast<int>(sizeof(double) * std::max(1, d.nd_max_m));
+  for (int lv = 0; lv < d.nd_levels; ++lv) {
+    if (d.nd_fwd_diag[lv].second)
+      nd_fwd_diag_kernel<<<d.nd_fwd_diag[lv].second, kNdBlock, smem, s>>>(D, d.nd_fwd_diag[lv].first);
+    if (d.nd_fwd_upd[lv].second)
+      nd_fwd_upd_kernel<<<d.nd_fwd_upd[lv].second, kNdBlock, 0, s>>>(D, d.nd_fwd_upd[lv].first);
+  }
+  for (int lv = d.nd_levels - 1; lv >= 0; --lv) {
+    if (d.nd_bwd_upd[lv].second)
+      nd_bwd_upd_kernel<<<d.nd_bwd_upd[lv].second, kNdBlock, 0, s>>>(D, d.nd_bwd_upd[lv].first);
+    if (d.nd_bwd_diag[lv].second)
+      nd_bwd_diag_kernel<<<d.nd_bwd_diag[lv].second, kNdBlock, 0, s>>>(D, d.nd_bwd_diag[lv].first);
+  }
+  nd_permute_out_kernel<<<vec_grid(d.m), kVecBlock, 0, s>>>(D.perm, d.coupled, d.m, D.x, x);
+  (void)pl;
+}
+
+DevDense dense_to_device(Plan& pl, const Csr& A, const std::vector<std::array<double, 3>>* coords = nullptr)
 {
   DenseCoarse dc = dense_coarse_setup(A, 1500);
   DevDense d;
@@ -810,6 +959,19 @@ DevDense dense_to_device(Plan& pl, const Csr& A)
   const std::size_t mm = static_cast<std::size_t>(d.m) * d.m;
   if (!dc.ainv.empty() || d.m == 0) {
     d.ainv = pl.mem.upload(dc.ainv);
+    return d;
+  }
+  if (coords && !std::getenv("HXB_DENSE_COARSE")) {  // sparse direct solve of the coupled block
+    Csr B;
+    B.n = d.m;
+    B.ptr = dc.csr_ptr;
+    B.col = dc.csr_col;
+    B.val = dc.csr_val;
+    std::vector<std::array<double, 3>> xyz(d.m);
+    for (int q = 0; q < d.m; ++q) xyz[q] = (*coords)[dc.coupled[q]];
+    setup_phase("coarse ND factor");
+    const NdFactor F = nd_cholesky(B, xyz);
+    nd_to_device(pl, d, F);
     return d;
   }
   // large coupled block: Cholesky on the device (64-bit cuSOLVER API: m^2 may
@@ -1465,7 +1627,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
       else
         pl.Kc = csr_to_device(pl, hs.Kc);
     } else {
-      pl.dense = dense_to_device(pl, hs.Kc);
+      pl.dense = dense_to_device(pl, hs.Kc, &mesh.vertices);  // K_c rows are mesh vertices
     }
   }
 

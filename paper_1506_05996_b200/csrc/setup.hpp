@@ -175,6 +175,25 @@ struct EnvelopeFactor {
 };
 EnvelopeFactor envelope_cholesky(const Csr& A);
 
+// Nested-dissection supernodal Cholesky (setup_nd.cpp) of an SPD matrix whose
+// rows carry vertex coordinates: P A P^T = L L^T, supernodes in postorder,
+// supernode s owning permuted columns [c0, c1) and below-diagonal rows `rows`
+// (permuted ids, ascending); linv = L11^-1 (m x m), l21 (r x m), row-major.
+struct NdSupernode {
+  std::vector<int> verts;     // original row ids (the separator or leaf)
+  std::vector<int> children;
+  int parent = -1, level = 0, c0 = 0, c1 = 0;
+  std::vector<int> rows;
+  std::vector<double> linv, l21;
+};
+struct NdFactor {
+  int n = 0, levels = 0;
+  std::vector<int> perm;      // permuted index -> original row
+  std::vector<NdSupernode> sn;
+};
+NdFactor nd_cholesky(const Csr& A, const std::vector<std::array<double, 3>>& xyz);
+std::vector<double> nd_solve_host(const NdFactor& F, const std::vector<double>& b);
+
 // Setup phase timer: HXB_SETUP_TIMING=1 prints each phase's wall time to stderr.
 void setup_phase(const char* name);  // closes the running phase, opens `name` (nullptr: close and print)
 

@@ -142,6 +142,7 @@ SIGNATURES = {
     "hxb_setup_export_maps": (C.c_int, [P, P, P, P, P, P, P]),
     "hxb_setup_amg_level": (C.c_int, [P, C.c_int, P, P, P, P, P, P]),
     "hxb_setup_lumped_mass": (C.c_int, [P, P]),
+    "hxb_setup_coarse_direct_check": (C.c_int, [P, P, P, P]),
     "hxb_setup_export_geometry": (C.c_int, [P, P, P]),
     "hxb_setup_dist_lists": (C.c_int, [P, C.c_int, C.c_int, P, P]),
     "hxb_gll": (C.c_int, [C.c_int, P, P, P]),
@@ -675,6 +676,14 @@ class HostSetup:
         m = np.empty(self.N)
         _check(lib().hxb_setup_lumped_mass(self._h, _ptr(m)))
         return m
+
+    def coarse_direct_check(self) -> dict:
+        """Sparse direct coarse factor (nested dissection + supernodal Cholesky,
+        the device replacement of SimplicialLLT) checked on the host: relative
+        residual of a solve with b = 1, stored factor entries, tree levels."""
+        res, ent, lv = C.c_double(), C.c_int64(), C.c_int32()
+        _check(lib().hxb_setup_coarse_direct_check(self._h, C.byref(res), C.byref(ent), C.byref(lv)))
+        return {"rel_residual": res.value, "factor_entries": ent.value, "levels": lv.value}
 
     def geometry(self) -> dict:
         """Host restatement of compute_factors + kappa*mass scaling (setup_mesh.cpp)."""
