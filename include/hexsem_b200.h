@@ -105,11 +105,15 @@ typedef struct hxb_options {
    *   half running concurrently with the coarse graph;
    * fdm_element_order: FDM subdomains in element order instead of Morton order;
    * host_lists: fine-solve gather lists by the host counting sort instead of
-   *   the device radix sort. */
+   *   the device radix sort;
+   * restrict_in_fdm: coarse restriction fused into the FDM kernel and the
+   *   coarse solve overlapped with the fine half of a split combine, instead
+   *   of a restriction pass first and the coarse solve concurrent with the FDM. */
   int fused_combine;
   int fdm_element_order;
   int host_lists;
-  int reserved[4];
+  int restrict_in_fdm;
+  int reserved[3];
 } hxb_options;
 
 /* PcgConfig (krylov.hpp:15-19) */

@@ -422,26 +422,49 @@ __global__ void __launch_bounds__(kDotBlock) cx_dot_kernel(const double* __restr
 }
 
 // SimplicialLLT::solve as built for the reference (envelope factor after
-// RCM): y = P b, L y' = y (row sweep), L^T x' = y' (column sweep), x = P^T x'
-__global__ void cx_envelope_solve_kernel(CompatEnvelope f, const double* __restrict__ b, double* __restrict__ x)
+// RCM): y = P b, L y' = y (row sweep), L^T x' = y' (column sweep), x = P^T x'.
+// Row sweep: the products L_ik y_k of a row are independent (each rounded
+// once), so the block forms them in shared memory and thread 0 subtracts
+// them in k order. Column sweep: for a fixed i the updates of different y_k
+// are independent, and each y_k still receives its updates in descending i.
+constexpr int kEnvChunk = 2048;
+__global__ void __launch_bounds__(256) cx_envelope_solve_kernel(CompatEnvelope f, const double* __restrict__ b,
+                                                                double* __restrict__ x)
 {
-  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  __shared__ double prod[kEnvChunk];
+  __shared__ double yi_s;
+  const int tid = threadIdx.x;
   const long long n = f.n;
   double* y = f.y;
-  for (long long i = 0; i < n; ++i) y[i] = b[f.perm[i]];
+  for (long long i = tid; i < n; i += blockDim.x) y[i] = b[f.perm[i]];
+  __syncthreads();
   for (long long i = 0; i < n; ++i) {
     const double* Li = f.env + f.start[i] - f.first[i];
-    double s = y[i];
-    for (long long k = f.first[i]; k < i; ++k) s -= Li[k] * y[k];
-    y[i] = s / Li[i];
+    double s = 0;
+    if (tid == 0) s = y[i];
+    for (long long k0 = f.first[i]; k0 < i; k0 += kEnvChunk) {
+      const int len = static_cast<int>(i - k0 < kEnvChunk ? i - k0 : kEnvChunk);
+      for (int q = tid; q < len; q += blockDim.x) prod[q] = Li[k0 + q] * y[k0 + q];
+      __syncthreads();
+      if (tid == 0)
+        for (int q = 0; q < len; ++q) s -= prod[q];
+      __syncthreads();
+    }
+    if (tid == 0) y[i] = s / Li[i];
+    __syncthreads();
   }
   for (long long i = n - 1; i >= 0; --i) {
     const double* Li = f.env + f.start[i] - f.first[i];
-    y[i] /= Li[i];
-    const double yi = y[i];
-    for (long long k = f.first[i]; k < i; ++k) y[k] -= Li[k] * yi;
+    if (tid == 0) {
+      y[i] /= Li[i];
+      yi_s = y[i];
+    }
+    __syncthreads();
+    const double yi = yi_s;
+    for (long long k = f.first[i] + tid; k < i; k += blockDim.x) y[k] -= Li[k] * yi;
+    __syncthreads();
   }
-  for (long long i = 0; i < n; ++i) x[f.perm[i]] = y[i];
+  for (long long i = tid; i < n; i += blockDim.x) x[f.perm[i]] = y[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -505,7 +528,7 @@ void spmv(cudaStream_t s, const CompatLevel& L, const double* x, double* y)
 
 void direct_solve(CompatPlan& c, cudaStream_t s, const double* b, double* x)
 {
-  cx_envelope_solve_kernel<<<1, 1, 0, s>>>(c.coarsest, b, x);
+  cx_envelope_solve_kernel<<<1, 256, 0, s>>>(c.coarsest, b, x);
 }
 
 void ksolve(CompatPlan& c, cudaStream_t s, std::size_t l, const double* b, double* x);

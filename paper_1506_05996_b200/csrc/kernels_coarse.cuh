@@ -110,6 +110,82 @@ __global__ void __launch_bounds__(256) restrict_warp_kernel(const double* __rest
   }
 }
 
+// The same restriction with precomputed surface-slot weights cw = m_l / m_N
+// (restrict_weights_kernel): w_l = r_l cw_l on surface slots, w_l = r_l on
+// element-interior nodes (one copy: m_N = m_l). No mass or 1/m_N loads, so it
+// runs as a cheap standalone pass before the FDM and the coarse solve can
+// start concurrently with the fine solves.
+template <int NP>
+__global__ void __launch_bounds__(256) restrict_cw_kernel(const double* __restrict__ r, const int* __restrict__ smap,
+                                                          const double* __restrict__ cw, double* __restrict__ Rpart,
+                                                          int ne, int sstride, int nsurfp, int nsg)
+{
+  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NL = NP * NP, LPL = (NL + 31) / 32;
+  constexpr int CH = LPL < 2 ? LPL : 2;
+  __shared__ double h0[NP], h1[NP];
+  if (threadIdx.x < NP) {
+    h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
+    h1[threadIdx.x] = c_tab[NP].hat1[threadIdx.x];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne; e += warps) {
+    const int* surf = smap + (long long)e * sstride;
+    const double* we = cw + (long long)e * nsurfp;
+    const long long ibase = (long long)nsg + (long long)e * NI;
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 1
+    for (int q0 = 0; q0 < LPL; q0 += CH) {
+      double wv[CH][NP];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int line = lane + 32 * (q0 + q);
+        const int j = (line < NL ? line : 0) % NP, k = (line < NL ? line : 0) / NP;
+        const bool face = (j == 0 || j == n || k == 0 || k == n);
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          if (line >= NL) {
+            wv[q][i] = 0.0;
+          } else if (face || i == 0 || i == n) {
+            const int s = surface_slot(NP, i, j, k);
+            const int code = __ldg(surf + s);
+            wv[q][i] = code >= 0 ? __ldg(r + code) * __ldg(we + s) : 0.0;  // Dirichlet: masked (precond.cpp:35)
+          } else {
+            wv[q][i] = __ldg(r + ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1));
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const int line = lane + 32 * (q0 + q);
+        const int j = (line < NL ? line : 0) % NP, k = (line < NL ? line : 0) / NP;
+        double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          w0 += h0[i] * wv[q][i];
+          w1 += h1[i] * wv[q][i];
+        }
+        if (line < NL) {
+          const double hj[2] = {h0[j], h1[j]}, hk[2] = {h0[k], h1[k]};
+#pragma unroll
+          for (int cb = 0; cb < 8; ++cb) acc[cb] += (hj[(cb >> 1) & 1] * hk[cb >> 2]) * ((cb & 1) ? w1 : w0);
+        }
+      }
+    }
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb)
+      for (int o = 16; o > 0; o >>= 1) acc[cb] += __shfl_xor_sync(0xffffffffu, acc[cb], o);
+    if (lane < 8) {
+      double v = acc[0];
+#pragma unroll
+      for (int cb = 1; cb < 8; ++cb)
+        if (lane == cb) v = acc[cb];
+      Rpart[8 * (long long)e + lane] = v;
+    }
+  }
+}
+
 // Zc[8e + cb] = Z[vertex of corner cb of e] (the 8 coarse values each element
 // prolongates, coarse.cpp:170-171), so the fused combine reads one 64-byte
 // block per element copy instead of 8 dependent gathers.

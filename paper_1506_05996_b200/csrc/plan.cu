@@ -149,6 +149,11 @@ struct Plan {
   int device = 0;
   cudaStream_t s_main = nullptr, s_coarse = nullptr;  // s_coarse: highest priority
   bool split_combine = true;
+  // restriction as its own pass before the FDM, so the coarse solve runs
+  // concurrently with the fine solves and one combine follows (default for
+  // single-device two-scale plans); false: restriction fused into the FDM and
+  // the combine split around the coarse solve (hxb_options.restrict_in_fdm)
+  bool restrict_first = false;
   int* fdm_order = nullptr;  // FDM CTA -> element: Morton order of element centroids (neighbours close in time)
   bool host_lists = false;  // build the fine gather lists on the host (A/B checks of the device sort)
   bool bitwise = false;     // hxb_options.bitwise_reference: every apply/solve through compat.cu
@@ -485,7 +490,7 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   a.sstride = 2 * pl.nsurf;
   a.num_surface_global = pl.nsg + pl.e0 * (pl.order - 1) * (pl.order - 1) * (pl.order - 1);  // first owned interior id
   a.cw = pl.cw;
-  a.Rpart = pl.do_coarse ? pl.Rpart + 8LL * pl.e0 : nullptr;  // owned slab of the full Rpart
+  a.Rpart = pl.do_coarse && !pl.restrict_first ? pl.Rpart + 8LL * pl.e0 : nullptr;  // owned slab of the full Rpart
   a.fsend = pl.fsend;
   a.sfstride = pl.sfstride;
   a.order = pl.fdm_order;
@@ -566,6 +571,11 @@ void launch_prolong(Plan& pl, cudaStream_t s)
 template <int NP>
 void launch_restrict(Plan& pl, cudaStream_t s)
 {
+  if (pl.cw) {
+    const int grid = fill_grid(restrict_cw_kernel<NP>, 256, 32LL * pl.ne);
+    restrict_cw_kernel<NP><<<grid, 256, 0, s>>>(pl.r, pl.smap, pl.cw, pl.Rpart, pl.ne, 2 * pl.nsurf, pl.nsurf, pl.nsg);
+    return;
+  }
   const int grid = fill_grid(restrict_warp_kernel<NP>, 256, 32LL * pl.ne);
   restrict_warp_kernel<NP><<<grid, 256, 0, s>>>(pl.r, pl.d_lumped, pl.smap, pl.mass, pl.Rpart, pl.ne, 2 * pl.nsurf,
                                                pl.nsg);
@@ -705,6 +715,25 @@ bool enqueue_precond(Plan& pl, double* zr_result, const PcgUArgs* ua = nullptr)
     copy_dot_kernel<kVecBlock><<<fill_grid(copy_dot_kernel<kVecBlock>, kVecBlock, pl.N), kVecBlock, 0, s>>>(pl.r, pl.r, pl.z, pl.N,
                                                                      zr_result ? dot_args(pl, zr_result) : DotArgs{});
     pl.launches += 1;
+    return false;
+  }
+  if (pl.restrict_first) {
+    // restriction pass, then the coarse solve (a latency-bound chain on a few
+    // SMs, high-priority stream) concurrently with the fine solves; one
+    // combine sums both, applies the mask and forms z.r
+    HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s);
+    pl.launches += 1;
+    HXB_CUDA(cudaEventRecord(pl.ev_fork, s));
+    HXB_CUDA(cudaStreamWaitEvent(pl.s_coarse, pl.ev_fork, 0));
+    {
+      KtScope kt(pl, HXB_KT_COARSE, pl.s_coarse);
+      HXB_CUDA(cudaGraphLaunch(pl.coarse_exec, pl.s_coarse));
+    }
+    pl.launches += pl.coarse_graph_nodes;
+    HXB_CUDA(cudaEventRecord(pl.ev_join, pl.s_coarse));
+    HXB_DISPATCH_NP(pl.np, launch_fdm, pl, s);
+    HXB_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
+    launch_combine(pl, zr_result, s, true, true);
     return false;
   }
   // fine FDM solves with the coarse restriction fused in (one pass over r),
@@ -1426,7 +1455,8 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   }
   pl.rsurf = M.alloc<double>(static_cast<std::size_t>(pl.ne) * pl.nsurf);
 
-  if (pl.do_fine && pl.do_coarse) {  // restriction weights for the FDM's fused restriction
+  pl.restrict_first = pl.do_fine && pl.do_coarse && pl.nranks == 1 && opt.restrict_in_fdm == 0;
+  if (pl.do_coarse) {  // restriction weights m_l / m_N of the surface slots (restriction pass / fused in the FDM)
     std::vector<int> slot_l(nsurf_raw);
     for (int k = 0; k < pl.np; ++k)
       for (int j = 0; j < pl.np; ++j)

@@ -30,15 +30,23 @@ int surface_slot_count(int np) { return np * np * np - (np - 2) * (np - 2) * (np
 // local-index order ((k*np+j)*np+i); -1 for element-interior nodes.
 int surface_slot_of(int np, int i, int j, int k)
 {
-  const int n = np - 1;
-  const int mid = 4 * np - 4;  // surface nodes per interior k-layer
-  if (k == 0) return j * np + i;
-  if (k == n) return np * np + (np - 2) * mid + j * np + i;
-  const int base = np * np + (k - 1) * mid;
-  if (j == 0) return base + i;
-  if (j == n) return base + np + 2 * (np - 2) + i;
-  if (i == 0) return base + np + 2 * (j - 1);
-  if (i == n) return base + np + 2 * (j - 1) + 1;
+  // entity-grouped slots: 8 vertices, 12 edges x (n-1), 6 faces x (n-1)^2
+  // (same mapping as surface_slot in kernels_common.cuh)
+  const int n = np - 1, m = n - 1;
+  const bool bi = i == 0 || i == n, bj = j == 0 || j == n, bk = k == 0 || k == n;
+  const int nb = bi + bj + bk;
+  if (nb == 3) return (i == n) + 2 * (j == n) + 4 * (k == n);
+  if (nb == 2) {
+    if (!bi) return 8 + ((j == n) + 2 * (k == n)) * m + (i - 1);
+    if (!bj) return 8 + (4 + (i == n) + 2 * (k == n)) * m + (j - 1);
+    return 8 + (8 + (i == n) + 2 * (j == n)) * m + (k - 1);
+  }
+  if (nb == 1) {
+    const int fb = 8 + 12 * m;
+    if (bi) return fb + (i == n) * m * m + (k - 1) * m + (j - 1);
+    if (bj) return fb + (2 + (j == n)) * m * m + (k - 1) * m + (i - 1);
+    return fb + (4 + (k == n)) * m * m + (j - 1) * m + (i - 1);
+  }
   return -1;
 }
 

@@ -53,7 +53,7 @@ class _Options(C.Structure):
                 ("variant", C.c_int), ("device", C.c_int), ("bitwise_reference", C.c_int),
                 ("n_gpus", C.c_int), ("devices", C.c_int * 8), ("rank", C.c_int), ("nranks", C.c_int),
                 ("fused_combine", C.c_int), ("fdm_element_order", C.c_int), ("host_lists", C.c_int),
-                ("reserved", C.c_int * 4)]
+                ("restrict_in_fdm", C.c_int), ("reserved", C.c_int * 3)]
 
 
 class _PcgConfig(C.Structure):
@@ -335,7 +335,7 @@ class Plan:
                  coarse_solve: str = "automatic", direct_threshold: int = 64000, variant: str = "stored",
                  device: int = 0, rank: int = 0, nranks: int = 1, split_combine: bool = True,
                  host_lists: bool = False, fdm_morton: bool = True, bitwise_reference: bool = False,
-                 devices=None):
+                 devices=None, restrict_in_fdm: bool = False):
         L = lib()
         ne = mesh.num_elements
         self.mesh = mesh
@@ -354,6 +354,7 @@ class Plan:
         opt.host_lists = 1 if host_lists else 0
         opt.fdm_element_order = 0 if fdm_morton else 1
         opt.bitwise_reference = 1 if bitwise_reference else 0
+        opt.restrict_in_fdm = 1 if restrict_in_fdm else 0
         if devices is not None:  # multi-GPU plan: one element slab per entry (a device may repeat)
             if not 1 <= len(devices) <= 8:
                 raise ValueError("devices: 1..8 entries")

@@ -201,14 +201,19 @@ def test_split_combine_matches_fused(k, order, coarse):
     coarse half reading it back) sums in the same order as the fused kernel:
     z and the whole PCG history are bitwise equal."""
     mesh = hx.generate_cube_mesh(k, "distorted_elements" if k <= 8 else "uniform")
-    a = hx.Plan(mesh, order, coarse_solve=coarse)
-    b = hx.Plan(mesh, order, coarse_solve=coarse, split_combine=False)
+    a = hx.Plan(mesh, order, coarse_solve=coarse, restrict_in_fdm=True)
+    b = hx.Plan(mesh, order, coarse_solve=coarse, restrict_in_fdm=True, split_combine=False)
     r = splitmix_vector(a.N, 6)
     assert np.array_equal(a.apply_P(r), b.apply_P(r))
     ha, hb = a.pcg(None, tol=1e-10), b.pcg(None, tol=1e-10)
     assert ha["iterations"] == hb["iterations"]
     assert np.array_equal(ha["residual_history"], hb["residual_history"])
     assert np.array_equal(ha["u"], hb["u"])
+    # the default schedule (restriction pass first, coarse solve concurrent with
+    # the FDM, one combine) differs only in the restriction's rounding
+    c = hx.Plan(mesh, order, coarse_solve=coarse)
+    assert rel(c.apply_P(r), a.apply_P(r)) <= 1e-13
+    assert np.array_equal(c.apply_P(r), c.apply_P(r))
 
 
 def test_pcg_amg_path():

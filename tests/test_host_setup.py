@@ -97,3 +97,17 @@ def test_per_element_coefficients():
         a, b = hs.amg_level(lvl), ref.amg_level(lvl)
         assert np.array_equal(a["val"], b["val"]) and np.array_equal(a["aggregate"], b["aggregate"])
     assert ne == 64
+
+
+@pytest.mark.parametrize("k,family", [(8, "uniform"), (6, "distorted_elements"), (12, "distorted_domain"), (20, "uniform")])
+def test_sparse_direct_coarse_factor(k, family):
+    """Nested dissection + supernodal Cholesky of the coupled coarse block
+    (setup_nd.cpp), the replacement of the dense coarse inverse behind the
+    reference's SimplicialLLT path (coarse.cpp:112-127): a solve with the
+    factor reproduces b to rounding, and the factor stays O(n^{4/3})."""
+    hs = hx.HostSetup(hx.generate_cube_mesh(k, family), 2, coarse_solve="direct")
+    r = hs.coarse_direct_check()
+    m = (k - 1) ** 3
+    assert r["rel_residual"] <= 1e-12, r
+    assert r["factor_entries"] <= 40 * m ** (4 / 3), r
+    assert r["levels"] >= 2

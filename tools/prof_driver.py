@@ -5,7 +5,7 @@ import sys
 
 sys.path.insert(0, ".")
 import paper_1506_05996_b200 as hx
-from oracle import splitmix_vector
+splitmix_vector = hx.synthetic_vector
 
 k = int(sys.argv[1]) if len(sys.argv) > 1 else 30
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 7
