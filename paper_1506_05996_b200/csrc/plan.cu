@@ -9,7 +9,8 @@
 // (the reference's std::async, precond.cpp:40-46).
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
-#include <nccl.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types and enums only: the functions are resolved by dlopen (NcclApi)
 
 #include <cub/cub.cuh>
 
@@ -23,6 +24,7 @@
 #include <condition_variable>
 #include <mutex>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/hexsem_b200.h"
@@ -1904,10 +1906,56 @@ class RankBarrier {
   bool aborted_ = false;
 };
 
+// NCCL is resolved at run time (dlopen), only when a multi-GPU plan with
+// distinct devices is built: an NCCL already loaded into the process (e.g.
+// torch's) is reused, and merely loading libhexsem_b200.so never pulls a
+// second libnccl into a process that has its own.
+struct NcclApi {
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api()
+{
+  static NcclApi api;
+  static std::once_flag once;
+  static std::string err;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) {
+      err = std::string("libnccl.so.2 not found: ") + dlerror();
+      return;
+    }
+    auto get = [&](auto& fp, const char* name) {
+      fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
+      if (!fp && err.empty()) err = std::string("NCCL symbol missing: ") + name;
+    };
+    get(api.CommInitAll, "ncclCommInitAll");
+    get(api.CommDestroy, "ncclCommDestroy");
+    get(api.GroupStart, "ncclGroupStart");
+    get(api.GroupEnd, "ncclGroupEnd");
+    get(api.Send, "ncclSend");
+    get(api.Recv, "ncclRecv");
+    get(api.AllReduce, "ncclAllReduce");
+    get(api.AllGather, "ncclAllGather");
+    get(api.GetErrorString, "ncclGetErrorString");
+  });
+  if (!err.empty()) throw HxbError(HXB_ENCCL, err);
+  return api;
+}
+
 #define HXB_NCCL(call)                                                                              \
   do {                                                                                              \
     ncclResult_t res__ = (call);                                                                    \
-    if (res__ != ncclSuccess) throw HxbError(HXB_ENCCL, std::string(#call) + ": " + ncclGetErrorString(res__)); \
+    if (res__ != ncclSuccess) throw HxbError(HXB_ENCCL, std::string(#call) + ": " + nccl_api().GetErrorString(res__)); \
   } while (0)
 
 struct RankBuf {
@@ -1952,7 +2000,7 @@ struct Group {
       if (r < static_cast<int>(buf.size()) && buf[r].h_scal) cudaFreeHost(buf[r].h_scal);
     }
     for (ncclComm_t c : comm)
-      if (c) ncclCommDestroy(c);
+      if (c) nccl_api().CommDestroy(c);
   }
 };
 
@@ -1972,16 +2020,16 @@ void g_exchange(Group& G, int r, const double* to_down, int n_to_down, const dou
   Plan& P = *G.pl[r];
   cudaStream_t s = P.s_main;
   if (G.nccl) {
-    HXB_NCCL(ncclGroupStart());
+    HXB_NCCL(nccl_api().GroupStart());
     if (r > 0) {
-      if (n_to_down) HXB_NCCL(ncclSend(to_down, n_to_down, ncclDouble, r - 1, G.comm[r], s));
-      if (n_from_down) HXB_NCCL(ncclRecv(from_down, n_from_down, ncclDouble, r - 1, G.comm[r], s));
+      if (n_to_down) HXB_NCCL(nccl_api().Send(to_down, n_to_down, ncclDouble, r - 1, G.comm[r], s));
+      if (n_from_down) HXB_NCCL(nccl_api().Recv(from_down, n_from_down, ncclDouble, r - 1, G.comm[r], s));
     }
     if (r + 1 < G.R) {
-      if (n_to_up) HXB_NCCL(ncclSend(to_up, n_to_up, ncclDouble, r + 1, G.comm[r], s));
-      if (n_from_up) HXB_NCCL(ncclRecv(from_up, n_from_up, ncclDouble, r + 1, G.comm[r], s));
+      if (n_to_up) HXB_NCCL(nccl_api().Send(to_up, n_to_up, ncclDouble, r + 1, G.comm[r], s));
+      if (n_from_up) HXB_NCCL(nccl_api().Recv(from_up, n_from_up, ncclDouble, r + 1, G.comm[r], s));
     }
-    HXB_NCCL(ncclGroupEnd());
+    HXB_NCCL(nccl_api().GroupEnd());
     return;
   }
   // pull model: after everyone's sends are ready, each rank copies what it receives
@@ -2009,7 +2057,7 @@ void g_allreduce(Group& G, int r, const double* partial, double* sum)
   Plan& P = *G.pl[r];
   cudaStream_t s = P.s_main;
   if (G.nccl) {
-    HXB_NCCL(ncclAllReduce(partial, sum, 1, ncclDouble, ncclSum, G.comm[r], s));
+    HXB_NCCL(nccl_api().AllReduce(partial, sum, 1, ncclDouble, ncclSum, G.comm[r], s));
     return;
   }
   G.mail[r].scalar = partial;
@@ -2035,7 +2083,7 @@ void g_allgather_rpart(Group& G, int r)
   if (G.nccl) {
     double* mine = G.buf[r].gather + static_cast<std::size_t>(r) * G.cap;
     HXB_CUDA(cudaMemcpyAsync(mine, P.Rpart + 8LL * P.e0, sizeof(double) * 8 * P.ne, cudaMemcpyDeviceToDevice, s));
-    HXB_NCCL(ncclAllGather(mine, G.buf[r].gather, G.cap, ncclDouble, G.comm[r], s));
+    HXB_NCCL(nccl_api().AllGather(mine, G.buf[r].gather, G.cap, ncclDouble, G.comm[r], s));
     for (int q = 0; q < G.R; ++q)
       if (q != r)
         HXB_CUDA(cudaMemcpyAsync(P.Rpart + 8LL * G.pl[q]->e0, G.buf[r].gather + static_cast<std::size_t>(q) * G.cap,
@@ -2365,7 +2413,7 @@ void build_group(Plan& top, const hxb_mesh* m, int order, const double* kappa_e,
   }
   if (G->nccl) {
     G->comm.assign(R, nullptr);
-    HXB_NCCL(ncclCommInitAll(G->comm.data(), R, G->dev.data()));
+    HXB_NCCL(nccl_api().CommInitAll(G->comm.data(), R, G->dev.data()));
   }
   G->bar = std::make_unique<RankBarrier>(R);
   for (int r = 0; r < R; ++r) HXB_CUDA(cudaDeviceSynchronize());

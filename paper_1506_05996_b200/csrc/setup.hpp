@@ -86,7 +86,7 @@ struct Numbering {
   gid num_surface_global = 0;  // NVu + NEd(n-1) + NF(n-1)^2
   std::vector<gid> vertex_rank;  // vertex id -> global id (or -1 if unreferenced)
   // per element: global ids of its element-surface local nodes in ascending
-  // surface-slot order (surface_slot_of: vertices, edges, faces), NE * nsurf
+  // local index order (the "surface slots"), NE * nsurf
   std::vector<gid> l2g_surf;
   std::vector<std::uint8_t> dirichlet_mask;  // per global node
   // face adjacency: for element e and face f, neighbor element (or -1) and its face

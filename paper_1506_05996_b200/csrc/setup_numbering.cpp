@@ -30,23 +30,15 @@ int surface_slot_count(int np) { return np * np * np - (np - 2) * (np - 2) * (np
 // local-index order ((k*np+j)*np+i); -1 for element-interior nodes.
 int surface_slot_of(int np, int i, int j, int k)
 {
-  // entity-grouped slots: 8 vertices, 12 edges x (n-1), 6 faces x (n-1)^2
-  // (same mapping as surface_slot in kernels_common.cuh)
-  const int n = np - 1, m = n - 1;
-  const bool bi = i == 0 || i == n, bj = j == 0 || j == n, bk = k == 0 || k == n;
-  const int nb = bi + bj + bk;
-  if (nb == 3) return (i == n) + 2 * (j == n) + 4 * (k == n);
-  if (nb == 2) {
-    if (!bi) return 8 + ((j == n) + 2 * (k == n)) * m + (i - 1);
-    if (!bj) return 8 + (4 + (i == n) + 2 * (k == n)) * m + (j - 1);
-    return 8 + (8 + (i == n) + 2 * (j == n)) * m + (k - 1);
-  }
-  if (nb == 1) {
-    const int fb = 8 + 12 * m;
-    if (bi) return fb + (i == n) * m * m + (k - 1) * m + (j - 1);
-    if (bj) return fb + (2 + (j == n)) * m * m + (k - 1) * m + (i - 1);
-    return fb + (4 + (k == n)) * m * m + (j - 1) * m + (i - 1);
-  }
+  const int n = np - 1;
+  const int mid = 4 * np - 4;  // surface nodes per interior k-layer
+  if (k == 0) return j * np + i;
+  if (k == n) return np * np + (np - 2) * mid + j * np + i;
+  const int base = np * np + (k - 1) * mid;
+  if (j == 0) return base + i;
+  if (j == n) return base + np + 2 * (np - 2) + i;
+  if (i == 0) return base + np + 2 * (j - 1);
+  if (i == n) return base + np + 2 * (j - 1) + 1;
   return -1;
 }
 
@@ -151,6 +143,36 @@ void parallel_for(gid n, F&& f)
   for (auto& th : pool) th.join();
 }
 
+// std::sort on host threads: sorted chunks merged pairwise. Used only where
+// the order is total (or equal keys are identical values), so the result is
+// exactly std::sort's.
+template <class T, class C>
+void parallel_sort(std::vector<T>& v, C comp)
+{
+  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const std::size_t n = v.size();
+  if (n < (1u << 16) || hw == 1) {
+    std::sort(v.begin(), v.end(), comp);
+    return;
+  }
+  std::vector<std::size_t> cut(hw + 1);
+  for (unsigned t = 0; t <= hw; ++t) cut[t] = n * t / hw;
+  {
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < hw; ++t)
+      pool.emplace_back([&, t] { std::sort(v.begin() + cut[t], v.begin() + cut[t + 1], comp); });
+    for (auto& th : pool) th.join();
+  }
+  for (std::size_t w = 1; w < hw; w *= 2) {
+    std::vector<std::thread> pool;
+    for (std::size_t t = 0; t + w < hw; t += 2 * w) {
+      const std::size_t a = cut[t], m = cut[t + w], b = cut[std::min<std::size_t>(hw, t + 2 * w)];
+      pool.emplace_back([&, a, m, b] { std::inplace_merge(v.begin() + a, v.begin() + m, v.begin() + b, comp); });
+    }
+    for (auto& th : pool) th.join();
+  }
+}
+
 }  // namespace
 
 Numbering build_numbering(const HexMesh& mesh, int order)
@@ -175,12 +197,14 @@ Numbering build_numbering(const HexMesh& mesh, int order)
 
   // (1) unique edges ordered by (min id, max id)
   std::vector<std::uint64_t> edges(static_cast<std::size_t>(ne) * 12);
-  for (gid e = 0; e < ne; ++e)
-    for (int q = 0; q < 12; ++q)
-      edges[static_cast<std::size_t>(e) * 12 + q] =
-          edge_key(mesh.elements[e][kEdges[q].lo_corner], mesh.elements[e][kEdges[q].hi_corner]);
+  parallel_for(ne, [&](gid b, gid en) {
+    for (gid e = b; e < en; ++e)
+      for (int q = 0; q < 12; ++q)
+        edges[static_cast<std::size_t>(e) * 12 + q] =
+            edge_key(mesh.elements[e][kEdges[q].lo_corner], mesh.elements[e][kEdges[q].hi_corner]);
+  });
   std::vector<std::uint64_t> uedges = edges;
-  std::sort(uedges.begin(), uedges.end());
+  parallel_sort(uedges, std::less<std::uint64_t>());
   uedges.erase(std::unique(uedges.begin(), uedges.end()), uedges.end());
   num.num_edges = static_cast<gid>(uedges.size());
   std::vector<gid> erank(edges.size());
@@ -193,11 +217,13 @@ Numbering build_numbering(const HexMesh& mesh, int order)
 
   // (2) unique faces ordered by canonical frame (origin, xn, yn)
   std::vector<FaceFrame> frames(static_cast<std::size_t>(ne) * 6);
-  for (gid e = 0; e < ne; ++e)
-    for (int f = 0; f < 6; ++f) frames[static_cast<std::size_t>(e) * 6 + f] = face_frame(mesh.elements[e], f / 2, f % 2);
+  parallel_for(ne, [&](gid b, gid en) {
+    for (gid e = b; e < en; ++e)
+      for (int f = 0; f < 6; ++f) frames[static_cast<std::size_t>(e) * 6 + f] = face_frame(mesh.elements[e], f / 2, f % 2);
+  });
   std::vector<std::pair<FaceKey, std::int64_t>> fk(frames.size());
   for (std::size_t i = 0; i < frames.size(); ++i) fk[i] = {frames[i].key, static_cast<std::int64_t>(i)};
-  std::sort(fk.begin(), fk.end(), [](const auto& x, const auto& y) {
+  parallel_sort(fk, [](const std::pair<FaceKey, std::int64_t>& x, const std::pair<FaceKey, std::int64_t>& y) {
     if (x.first == y.first) return x.second < y.second;
     return x.first < y.first;
   });

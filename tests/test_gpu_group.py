@@ -18,7 +18,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("R,k,order,family", [(2, 6, 7, "uniform"), (3, 6, 4, "distorted_elements"),
-                                              (4, 8, 3, "distorted_domain")])
+                                              (4, 8, 3, "distorted_domain"), (2, 5, 3, "uniform"),
+                                              (3, 5, 2, "uniform")])
 def test_group_ax_bitwise_equals_single_plan(R, k, order, family):
     mesh = hx.generate_cube_mesh(k, family)
     single = hx.Plan(mesh, order, precond="none")
@@ -67,6 +68,9 @@ def test_group_precond_none_and_reuse():
     mesh = hx.generate_cube_mesh(5)
     single = hx.Plan(mesh, 3, precond="none")
     group = hx.Plan(mesh, 3, precond="none", devices=[0, 0])
+    r = splitmix_vector(single.N, 9)
+    assert np.array_equal(group.apply_P(r), r)
+    assert np.array_equal(group.apply_A(r), single.apply_A(r))
     for seed in (1, 2):
         b = splitmix_vector(single.N, seed) * single.load_ones()
         one, many = single.pcg(b, tol=1e-8), group.pcg(b, tol=1e-8)
