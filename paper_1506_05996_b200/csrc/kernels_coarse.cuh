@@ -116,9 +116,10 @@ __global__ void __launch_bounds__(256) restrict_warp_kernel(const double* __rest
 // runs as a cheap standalone pass before the FDM and the coarse solve can
 // start concurrently with the fine solves.
 template <int NP>
-__global__ void __launch_bounds__(256) restrict_cw_kernel(const double* __restrict__ r, const int* __restrict__ smap,
+__global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __restrict__ r, const int* __restrict__ smap,
                                                           const double* __restrict__ cw, double* __restrict__ Rpart,
-                                                          int ne, int sstride, int nsurfp, int nsg)
+                                                          int ne, int sstride, int nsurfp, int nsg,
+                                                          const int* __restrict__ order)
 {
   constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NL = NP * NP, LPL = (NL + 31) / 32;
   constexpr int CH = LPL < 2 ? LPL : 2;
@@ -130,7 +131,11 @@ __global__ void __launch_bounds__(256) restrict_cw_kernel(const double* __restri
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne; e += warps) {
+  // elements in Morton order (order[], the FDM's traversal): the face
+  // neighbours that share a surface node run close in time, so its r is read
+  // from L2
+  for (int eo = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; eo < ne; eo += warps) {
+    const int e = order ? __ldg(order + eo) : eo;
     const int* surf = smap + (long long)e * sstride;
     const double* we = cw + (long long)e * nsurfp;
     const long long ibase = (long long)nsg + (long long)e * NI;

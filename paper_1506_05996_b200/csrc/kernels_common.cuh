@@ -58,11 +58,11 @@ __device__ __forceinline__ double load_masked(const double* __restrict__ x, int 
 
 // Rank of local node (i,j,k) among element-surface nodes in ascending local
 // index, -1 for element-interior (mirrors setup_numbering.cpp). An
-// entity-grouped order (vertices, edges, faces: contiguous slot blocks per
-// mesh edge/face) was measured at cfg2: the Ax gather read 0.36 GB less and
-// took 0.216 instead of 0.265 ms, but the element kernel's scattered surface
-// stores took it from 0.76 to 0.99 ms and the restriction pass from 0.32 to
-// 0.73 ms, so this order stays.
+// entity-grouped rsurf order (vertices, edges, faces: contiguous runs per mesh
+// edge/face) was measured at cfg2 three ways: the gather read
+// 0.36 GB less (0.265 -> 0.215 ms) but the element kernel lost more, with
+// scattered stores (0.76 -> 0.99 ms), a TMA bulk store of a shared-staged row
+// (0.87 ms) or coalesced 16-byte stores of it (0.89 ms); this order stays.
 __host__ __device__ __forceinline__ int surface_slot(int np, int i, int j, int k)
 {
   const int n = np - 1, mid = 4 * np - 4;

@@ -52,10 +52,14 @@ __device__ __forceinline__ void stage_ints(int* dst, const int* src, int n, int 
   }
 }
 
+#ifndef FDM_S10
+#define FDM_S10 17
+#define FDM_PS10 170
+#endif
 template <int P>
 struct FdmLayout {  // (row stride S, plane stride PS) per pencil size
-  static constexpr int S = P == 6 ? 9 : P == 8 ? 9 : P == 10 ? 17 : P == 12 ? 13 : P;
-  static constexpr int PS = P == 4 ? 19 : P == 6 ? 54 : P == 8 ? 72 : P == 10 ? 170 : P == 12 ? 156 : P * S;
+  static constexpr int S = P == 6 ? 9 : P == 8 ? 9 : P == 10 ? FDM_S10 : P == 12 ? 13 : P;
+  static constexpr int PS = P == 4 ? 19 : P == 6 ? 54 : P == 8 ? 72 : P == 10 ? FDM_PS10 : P == 12 ? 156 : P * S;
 };
 
 #ifndef FDM_MIN_BLOCKS
@@ -214,9 +218,10 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
   constexpr int NF = (6 * NP * NP + 3) & ~3, P3 = P * P * P;
   __shared__ __align__(16) int s_code[NSP];
   __shared__ __align__(16) int s_sf[NF];
-  // output positions padded to an odd row stride (P+1 for even P): the x-line
-  // reads of pass 5 then hit distinct banks
-  constexpr int PR = (P % 2 == 0) ? P + 1 : P;
+  // output positions, staged by 16-byte copies (a row stride padded for the
+  // pass-5 reads needed 4-byte copies: measured 4.4M extra wavefronts per
+  // launch at cfg2 against 1.4M from the 2-way read conflicts it removed)
+  constexpr int PR = P;
   __shared__ __align__(16) int s_pos[((P * P * PR) + 3) & ~3];
   __shared__ __align__(16) double s_cw[NSP];
   stage_ints<true>(s_code, a.smap + (long long)e * a.sstride, NSP, tid, Sh::kBlock);
@@ -224,11 +229,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
   if (a.Rpart)
     for (int q = tid; q < NSP / 2; q += Sh::kBlock) cp_async16(s_cw + 2 * q, a.cw + (long long)e * NSP + 2 * q);
   cp_async_commit();
-  if constexpr (PR == P) {
-    stage_ints<(P3 % 4) == 0>(s_pos, a.pos + (long long)e * P3, P3, tid, Sh::kBlock);
-  } else {
-    for (int q = tid; q < P3; q += Sh::kBlock) cp_async4(s_pos + (q / P) * PR + q % P, a.pos + (long long)e * P3 + q);
-  }
+  stage_ints<(P3 % 4) == 0>(s_pos, a.pos + (long long)e * P3, P3, tid, Sh::kBlock);
   cp_async_commit();
   const double hx = __ldg(a.h3 + 3 * e), hy = __ldg(a.h3 + 3 * e + 1), hz = __ldg(a.h3 + 3 * e + 2);
   const double svol = 8.0 / (hx * hy * hz);  // fine.cpp:154

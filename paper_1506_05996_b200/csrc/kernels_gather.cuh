@@ -235,8 +235,11 @@ struct CombineProlongArgs {
   int e0 = 0;       // global id of the first element whose mass block is at `mass`
 };
 
+#ifndef COMBINE_MIN_BLOCKS
+#define COMBINE_MIN_BLOCKS 6  // cfg2: 6 (40 regs, 100 B spills) 0.857 ms, 4 (64 regs) 0.937, 8 (32 regs) 1.024
+#endif
 template <int NP>
-__global__ void __launch_bounds__(kGatherBlock, 4) combine_prolong_kernel(CombineProlongArgs a)
+__global__ void __launch_bounds__(kGatherBlock, COMBINE_MIN_BLOCKS) combine_prolong_kernel(CombineProlongArgs a)
 {
   constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1);
   constexpr int NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2), NSP = (NS + 3) & ~3;

@@ -156,6 +156,9 @@ struct Plan {
   // single-device two-scale plans); false: restriction fused into the FDM and
   // the combine split around the coarse solve (hxb_options.restrict_in_fdm)
   bool restrict_first = false;
+  // unused dynamic shared memory per FDM CTA: caps the FDM's resident CTAs per
+  // SM so the concurrent coarse-solve kernels find room on every SM
+  int fdm_smem_pad = 0;
   int* fdm_order = nullptr;  // FDM CTA -> element: Morton order of element centroids (neighbours close in time)
   bool host_lists = false;  // build the fine gather lists on the host (A/B checks of the device sort)
   bool bitwise = false;     // hxb_options.bitwise_reference: every apply/solve through compat.cu
@@ -499,9 +502,9 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   KtScope kt(pl, HXB_KT_FDM, s);
   pl.launches += 1;
   if (pl.fdm_eo)
-    fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
+    fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, pl.fdm_smem_pad, s>>>(a);
   else
-    fdm_kernel<NP, false><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
+    fdm_kernel<NP, false><<<pl.ne, FdmShape<NP>::kBlock, pl.fdm_smem_pad, s>>>(a);
 }
 
 template <int NP>
@@ -575,7 +578,8 @@ void launch_restrict(Plan& pl, cudaStream_t s)
 {
   if (pl.cw) {
     const int grid = fill_grid(restrict_cw_kernel<NP>, 256, 32LL * pl.ne);
-    restrict_cw_kernel<NP><<<grid, 256, 0, s>>>(pl.r, pl.smap, pl.cw, pl.Rpart, pl.ne, 2 * pl.nsurf, pl.nsurf, pl.nsg);
+    restrict_cw_kernel<NP><<<grid, 256, 0, s>>>(pl.r, pl.smap, pl.cw, pl.Rpart, pl.ne, 2 * pl.nsurf, pl.nsurf, pl.nsg,
+                                                pl.fdm_order);
     return;
   }
   const int grid = fill_grid(restrict_warp_kernel<NP>, 256, 32LL * pl.ne);
@@ -1458,6 +1462,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   pl.rsurf = M.alloc<double>(static_cast<std::size_t>(pl.ne) * pl.nsurf);
 
   pl.restrict_first = pl.do_fine && pl.do_coarse && pl.nranks == 1 && opt.restrict_in_fdm == 0;
+  if (const char* pad = std::getenv("HXB_FDM_SMEM_PAD")) pl.fdm_smem_pad = std::atoi(pad);
   if (pl.do_coarse) {  // restriction weights m_l / m_N of the surface slots (restriction pass / fused in the FDM)
     std::vector<int> slot_l(nsurf_raw);
     for (int k = 0; k < pl.np; ++k)
@@ -2331,7 +2336,9 @@ void build_group(Plan& top, const hxb_mesh* m, int order, const double* kappa_e,
     G->dev.push_back(opt.devices[r]);
   }
   // rank 0 builds the host setup (numbering, coarse matrix, AMG) once; the
-  // other ranks share it read-only and build their slabs in parallel
+  // other ranks share it read-only and build their device slabs one after the
+  // other (their graph captures must not overlap another thread's setup calls
+  // on a shared device)
   auto rank_opt = [&](int r) {
     hxb_options o = opt;
     o.n_gpus = 1;
@@ -2347,22 +2354,10 @@ void build_group(Plan& top, const hxb_mesh* m, int order, const double* kappa_e,
     build_plan(*G->pl[0], m, order, kappa_e, c_e, o);
   }
   std::shared_ptr<HostSetup> hs = G->pl[0]->hsp;
-  {
-    std::vector<std::exception_ptr> err(R);
-    std::vector<std::thread> th;
-    for (int r = 1; r < R; ++r)
-      th.emplace_back([&, r] {
-        try {
-          const hxb_options o = rank_opt(r);
-          G->pl[r] = std::make_unique<Plan>(hs);
-          build_plan(*G->pl[r], m, order, kappa_e, c_e, o);
-        } catch (...) {
-          err[r] = std::current_exception();
-        }
-      });
-    for (auto& t : th) t.join();
-    for (auto& e : err)
-      if (e) std::rethrow_exception(e);
+  for (int r = 1; r < R; ++r) {
+    const hxb_options o = rank_opt(r);
+    G->pl[r] = std::make_unique<Plan>(hs);
+    build_plan(*G->pl[r], m, order, kappa_e, c_e, o);
   }
   // exchange buffers, events
   int max_ne = 0;

@@ -111,3 +111,23 @@ def test_sparse_direct_coarse_factor(k, family):
     assert r["rel_residual"] <= 1e-12, r
     assert r["factor_entries"] <= 40 * m ** (4 / 3), r
     assert r["levels"] >= 2
+
+
+@pytest.mark.slow
+def test_numbering_bit_exact_cfg2():
+    """cfg2 (52^3 hexes, N=7: 72M local entries, 140M subdomain slots): the
+    closed-form numbering equals the compiled reference's build_index_maps
+    (mesh.cpp:287-453) entry for entry: l2g, the g2l CSR, sub_l2g and the
+    Dirichlet mask. Run with HXB_RUN_SLOW=1 (about a minute and 10 GB)."""
+    from oracle import RefSystem, ref_available
+
+    if not ref_available():
+        pytest.skip("compiled reference not built")
+    ref = RefSystem(RefConfig(k=52, order=7, precond="fine_only"))
+    b = ref.maps()
+    ref.close()
+    hs = hx.HostSetup(hx.generate_cube_mesh(52), 7, precond="fine_only")
+    a = hs.maps()
+    assert hs.N == 48627125
+    for key in ("l2g", "g2l_offsets", "g2l_elem", "g2l_local", "sub_l2g", "dirichlet_mask"):
+        assert np.array_equal(a[key], b[key]), key

@@ -38,7 +38,8 @@ def test_reference_pcg_with_b200_operators(k, order, family, precond):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k,order,family,precond,mode", [(8, 4, 0, 0, "0,0"), (6, 3, 1, 0, "0,0,0"), (5, 3, 0, 3, "0,0")])
+@pytest.mark.parametrize("k,order,family,precond,mode", [(8, 4, 0, 0, "0,0"), (6, 3, 1, 0, "0,0,0"), (5, 3, 0, 0, "0,0"),
+                                                        (5, 3, 0, 3, "0,0")])
 def test_reference_pcg_with_multi_gpu_plan(k, order, family, precond, mode):
     """The adapter's multi-GPU plan (hxb_options.n_gpus, element slabs, the
     in-library distributed PCG): here the slabs share device 0, so the
@@ -53,13 +54,16 @@ def test_reference_pcg_with_multi_gpu_plan(k, order, family, precond, mode):
     assert res["plug_status"] == res["ref_status"] == res["solve_status"] == 0
     assert abs(res["plug_iterations"] - res["ref_iterations"]) <= 1
     assert abs(res["solve_iterations"] - res["ref_iterations"]) <= 1
-    tol = 1e-10 if family == 0 else 1e-8
+    # unpreconditioned CG (precond 3) amplifies the FMA rounding of Ax over its
+    # 47 iterations (the bitwise plan, test below, shows the arithmetic is the
+    # reference's): 1e-8 there
+    tol = 1e-10 if family == 0 and precond != 3 else 1e-8
     assert res["plug_max_dr_over_r0"] <= tol and res["solve_max_dr_over_r0"] <= tol, res
     assert res["plug_u_rel"] <= 1e-8 and res["solve_u_rel"] <= 1e-8, res
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k,order,family,precond", [(8, 4, 0, 0), (4, 5, 2, 0), (6, 3, 1, 1)])
+@pytest.mark.parametrize("k,order,family,precond", [(8, 4, 0, 0), (4, 5, 2, 0), (6, 3, 1, 1), (5, 3, 0, 3)])
 def test_reference_pcg_with_bitwise_plan(k, order, family, precond):
     """Through the same adapter, the bitwise-reference plan reproduces the
     reference's own solve exactly: zero residual-history and u differences,
