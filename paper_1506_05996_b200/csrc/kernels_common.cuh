@@ -110,6 +110,15 @@ __device__ __forceinline__ void surface_ijk(int s, int& i, int& j, int& k)
   }
 }
 
+// optional u += alpha_k p_k of the PCG (krylov.cpp:54) riding along another pass
+struct PcgUArgs {
+  double* u = nullptr;
+  const double* p = nullptr;
+  const double* zr = nullptr;
+  const double* pf = nullptr;
+  int k = 0;
+};
+
 // ---------------------------------------------------------------------------
 // TMA bulk copies (cp.async.bulk, 1-D, no tensor map) completing on an
 // mbarrier: global -> shared staging for streamed per-element data.

@@ -335,13 +335,6 @@ __global__ void __launch_bounds__(kGatherBlock, COMBINE_MIN_BLOCKS) combine_prol
 // half then reads z back (fine_in_z), so the result is bit-identical to the
 // fused kernel. One item per thread, no persistent loop, so the coarse
 // kernels on the high-priority stream are scheduled as soon as CTAs retire.
-struct PcgUArgs {  // optional u += alpha_k p_k of the PCG (krylov.cpp:54) riding along
-  double* u = nullptr;
-  const double* p = nullptr;
-  const double* zr = nullptr;
-  const double* pf = nullptr;
-  int k = 0;
-};
 
 __global__ void __launch_bounds__(kGatherBlock) combine_fine_kernel(const double* __restrict__ zsort,
                                                                     const unsigned* __restrict__ fine_off,
