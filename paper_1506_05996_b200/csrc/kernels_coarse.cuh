@@ -119,7 +119,7 @@ template <int NP>
 __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __restrict__ r, const int* __restrict__ smap,
                                                           const double* __restrict__ cw, double* __restrict__ Rpart,
                                                           int ne, int sstride, int nsurfp, int nsg,
-                                                          const int* __restrict__ order, PcgUArgs ua, int nnodes)
+                                                          const int* __restrict__ order)
 {
   constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NL = NP * NP, LPL = (NL + 31) / 32;
   constexpr int CH = LPL < 2 ? LPL : 2;
@@ -188,12 +188,6 @@ __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __res
         if (lane == cb) v = acc[cb];
       Rpart[8 * (long long)e + lane] = v;
     }
-  }
-  // the PCG's u += alpha_k p_k streams while other warps wait on their gathers
-  if (ua.u) {
-    const double alpha = ua.zr[ua.k] / ua.pf[ua.k];
-    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < nnodes; g += gridDim.x * blockDim.x)
-      ua.u[g] += alpha * ua.p[g];
   }
 }
 

@@ -156,11 +156,6 @@ struct Plan {
   // single-device two-scale plans); false: restriction fused into the FDM and
   // the combine split around the coarse solve (hxb_options.restrict_in_fdm)
   bool restrict_first = false;
-  // unused dynamic shared memory per FDM CTA: caps the FDM's resident CTAs per
-  // SM so the concurrent coarse-solve kernels find room on every SM
-  int fdm_smem_pad = 0;
-  bool restrict_on_coarse = false;  // A/B: restriction on the coarse stream, concurrent with the FDM
-  bool u_in_restrict = false;       // A/B: u += alpha p inside the restriction pass
   int* fdm_order = nullptr;  // FDM CTA -> element: Morton order of element centroids (neighbours close in time)
   bool host_lists = false;  // build the fine gather lists on the host (A/B checks of the device sort)
   bool bitwise = false;     // hxb_options.bitwise_reference: every apply/solve through compat.cu
@@ -504,9 +499,9 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   KtScope kt(pl, HXB_KT_FDM, s);
   pl.launches += 1;
   if (pl.fdm_eo)
-    fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, pl.fdm_smem_pad, s>>>(a);
+    fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
   else
-    fdm_kernel<NP, false><<<pl.ne, FdmShape<NP>::kBlock, pl.fdm_smem_pad, s>>>(a);
+    fdm_kernel<NP, false><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
 }
 
 template <int NP>
@@ -576,12 +571,12 @@ void launch_prolong(Plan& pl, cudaStream_t s)
 }
 
 template <int NP>
-void launch_restrict(Plan& pl, cudaStream_t s, const PcgUArgs& ua = {})
+void launch_restrict(Plan& pl, cudaStream_t s)
 {
   if (pl.cw) {
     const int grid = fill_grid(restrict_cw_kernel<NP>, 256, 32LL * pl.ne);
     restrict_cw_kernel<NP><<<grid, 256, 0, s>>>(pl.r, pl.smap, pl.cw, pl.Rpart, pl.ne, 2 * pl.nsurf, pl.nsurf, pl.nsg,
-                                                pl.fdm_order, ua, pl.N);
+                                                pl.fdm_order);
     return;
   }
   const int grid = fill_grid(restrict_warp_kernel<NP>, 256, 32LL * pl.ne);
@@ -729,17 +724,9 @@ bool enqueue_precond(Plan& pl, double* zr_result, const PcgUArgs* ua = nullptr)
     // restriction pass, then the coarse solve (a latency-bound chain on a few
     // SMs, high-priority stream) concurrently with the fine solves; one
     // combine sums both, applies the mask and forms z.r
-    // the PCG's u += alpha p rides along the latency-bound restriction pass
-    const bool with_u = ua && pl.u_in_restrict && !pl.restrict_on_coarse;
-    if (pl.restrict_on_coarse) {  // the restriction heads the coarse branch; the FDM starts at once
-      HXB_CUDA(cudaEventRecord(pl.ev_fork, s));
-      HXB_CUDA(cudaStreamWaitEvent(pl.s_coarse, pl.ev_fork, 0));
-      HXB_DISPATCH_NP(pl.np, launch_restrict, pl, pl.s_coarse);
-    } else {
-      HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s, with_u ? *ua : PcgUArgs{});
-      HXB_CUDA(cudaEventRecord(pl.ev_fork, s));
-      HXB_CUDA(cudaStreamWaitEvent(pl.s_coarse, pl.ev_fork, 0));
-    }
+    HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s);
+    HXB_CUDA(cudaEventRecord(pl.ev_fork, s));
+    HXB_CUDA(cudaStreamWaitEvent(pl.s_coarse, pl.ev_fork, 0));
     pl.launches += 1;
     {
       KtScope kt(pl, HXB_KT_COARSE, pl.s_coarse);
@@ -750,7 +737,7 @@ bool enqueue_precond(Plan& pl, double* zr_result, const PcgUArgs* ua = nullptr)
     HXB_DISPATCH_NP(pl.np, launch_fdm, pl, s);
     HXB_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
     launch_combine(pl, zr_result, s, true, true);
-    return with_u;
+    return false;
   }
   // fine FDM solves with the coarse restriction fused in (one pass over r),
   // then the coarse graph; the combine sums both and applies the mask
@@ -1472,9 +1459,6 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   pl.rsurf = M.alloc<double>(static_cast<std::size_t>(pl.ne) * pl.nsurf);
 
   pl.restrict_first = pl.do_fine && pl.do_coarse && pl.nranks == 1 && opt.restrict_in_fdm == 0;
-  if (const char* pad = std::getenv("HXB_FDM_SMEM_PAD")) pl.fdm_smem_pad = std::atoi(pad);
-  if (const char* rc = std::getenv("HXB_RESTRICT_ON_COARSE")) pl.restrict_on_coarse = std::atoi(rc) != 0;
-  if (const char* uc = std::getenv("HXB_U_IN_RESTRICT")) pl.u_in_restrict = std::atoi(uc) != 0;
   if (pl.do_coarse) {  // restriction weights m_l / m_N of the surface slots (restriction pass / fused in the FDM)
     std::vector<int> slot_l(nsurf_raw);
     for (int k = 0; k < pl.np; ++k)
