@@ -167,29 +167,56 @@ __device__ __forceinline__ void pencil_inv_eo(const double* __restrict__ IE, con
   if constexpr (mid) out[h] = E[h];
 }
 
-template <int NP, bool EO>
-__global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks) fdm_kernel(FdmArgs a)
+// EPB subdomains per CTA: lines of consecutive elements packed into the same
+// warps (P^2 lines per element: at P = 6 one element per CTA leaves 28 of
+// 64 lanes idle). Used when the restriction is not fused (the Rpart/fsend
+// paths reduce per element over whole warps and keep EPB = 1), and only where
+// one subdomain per CTA leaves most lanes idle: measured at cfg4 sizes
+// (profiles/r02_ab_experiments.jsonl, A/B 10), packing took n=3 (P=6) from
+// 1.89 to 1.62 ms but lost at n=4..8 (e.g. n=7: 1.23 -> 1.34 ms), where the
+// extra shared memory per CTA costs more occupancy than the idle lanes.
+template <int NP>
+struct FdmEPB {
+  static constexpr int kP = NP + 2;
+  static constexpr int value = (kP == 4 || kP == 6) ? 256 / (kP * kP) : 1;
+};
+template <int NP, int EPB>
+struct FdmShapeE {
+  static constexpr int kLines = (NP + 2) * (NP + 2);
+  static constexpr int kBlock = ((EPB * kLines + 31) / 32) * 32;
+  static constexpr int kMinBlocks =
+      EPB == 1 ? FDM_MIN_BLOCKS : ((FDM_MIN_BLOCKS * 128) / kBlock > 0 ? (FDM_MIN_BLOCKS * 128) / kBlock : 1);
+};
+
+template <int NP, bool EO, int EPB = 1>
+__global__ void __launch_bounds__(FdmShapeE<NP, EPB>::kBlock, FdmShapeE<NP, EPB>::kMinBlocks) fdm_kernel(FdmArgs a)
 {
   using Sh = FdmShape<NP>;
+  constexpr int kBlk = FdmShapeE<NP, EPB>::kBlock;
   constexpr int P = Sh::kP, S = Sh::kS, PS = Sh::kPS, n = NP - 1;
   constexpr int kTab = EO ? 1 : 2 * P * P;
-  __shared__ double buf[Sh::kBuf];
+  __shared__ double buf_all[EPB * Sh::kBuf];
   __shared__ double tab[kTab];  // dense fallback only: V^T, V^-T as warp-uniform broadcasts
   const OrderTables& T = c_tab[NP];
   const FdmConst& C = c_fdm[NP];  // even/odd tables, lambda, 1/M: constant bank
-  const int e = a.order ? __ldg(a.order + blockIdx.x) : static_cast<int>(blockIdx.x);
   const int tid = threadIdx.x;
-  const bool lt = tid < Sh::kLines;
-  const int la = tid % P, lb = tid / P;
+  const int es = min(tid / (P * P), EPB - 1);  // this thread's subdomain in the CTA
+  const int tl = tid - es * P * P;
+  const long long eidx = static_cast<long long>(blockIdx.x) * EPB + es;
+  const bool ev = eidx < a.ne;
+  const int e = ev ? (a.order ? __ldg(a.order + eidx) : static_cast<int>(eidx)) : 0;
+  const bool lt = tid < EPB * P * P && ev;
+  const int la = tl % P, lb = tl / P;
+  double* buf = buf_all + es * Sh::kBuf;
   auto at = [](int x, int y, int z) { return z * PS + y * S + x; };
   if constexpr (!EO) {
-    for (int q = tid; q < P * P; q += Sh::kBlock) {
+    for (int q = tid; q < P * P; q += kBlk) {
       tab[q] = T.VT[q];
       tab[P * P + q] = T.ViT[q];
     }
   }
   __shared__ double s_lam[P], s_invM[P];  // indexed per thread (non-uniform): shared, not constant
-  for (int q = tid; q < P; q += Sh::kBlock) {
+  for (int q = tid; q < P; q += kBlk) {
     s_lam[q] = C.lam[q];
     s_invM[q] = C.invM[q];
   }
@@ -207,8 +234,8 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
   };
 
   __shared__ double s_h0[NP], s_h1[NP];   // coarse hats 0.5(1 -+ t) (gll.cpp:92)
-  __shared__ double s_red[Sh::kBlock / 32][8];
-  for (int q = tid; q < NP; q += Sh::kBlock) {
+  __shared__ double s_red[kBlk / 32][8];
+  for (int q = tid; q < NP; q += kBlk) {
     s_h0[q] = T.hat0[q];
     s_h1[q] = T.hat1[q];
   }
@@ -216,20 +243,38 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
   // output positions (needed last) are staged by coalesced cp.async copies
   constexpr int NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2), NSP = (NS + 3) & ~3;
   constexpr int NF = (6 * NP * NP + 3) & ~3, P3 = P * P * P;
-  __shared__ __align__(16) int s_code[NSP];
-  __shared__ __align__(16) int s_sf[NF];
+  __shared__ __align__(16) int s_code_all[EPB][NSP];
+  __shared__ __align__(16) int s_sf_all[EPB][NF];
   // output positions, staged by 16-byte copies (a row stride padded for the
   // pass-5 reads needed 4-byte copies: measured 4.4M extra wavefronts per
   // launch at cfg2 against 1.4M from the 2-way read conflicts it removed)
   constexpr int PR = P;
-  __shared__ __align__(16) int s_pos[((P * P * PR) + 3) & ~3];
-  __shared__ __align__(16) double s_cw[NSP];
-  stage_ints<true>(s_code, a.smap + (long long)e * a.sstride, NSP, tid, Sh::kBlock);
-  stage_ints<true>(s_sf, a.sub_face + (long long)e * a.sfstride, NF, tid, Sh::kBlock);
-  if (a.Rpart)
-    for (int q = tid; q < NSP / 2; q += Sh::kBlock) cp_async16(s_cw + 2 * q, a.cw + (long long)e * NSP + 2 * q);
+  constexpr int P3P = ((P * P * PR) + 3) & ~3;
+  __shared__ __align__(16) int s_pos_all[EPB][P3P];
+  __shared__ __align__(16) double s_cw[EPB == 1 ? NSP : 2];
+  const int* s_code = s_code_all[es];
+  const int* s_sf = s_sf_all[es];
+  const int* s_pos = s_pos_all[es];
+#pragma unroll 1
+  for (int q = 0; q < EPB; ++q) {  // every subdomain's rows, staged by the whole CTA
+    const long long ei = static_cast<long long>(blockIdx.x) * EPB + q;
+    if (ei >= a.ne) break;
+    const int eq = a.order ? __ldg(a.order + ei) : static_cast<int>(ei);
+    stage_ints<true>(s_code_all[q], a.smap + (long long)eq * a.sstride, NSP, tid, kBlk);
+    stage_ints<true>(s_sf_all[q], a.sub_face + (long long)eq * a.sfstride, NF, tid, kBlk);
+  }
+  if constexpr (EPB == 1) {
+    if (a.Rpart)
+      for (int q = tid; q < NSP / 2; q += kBlk) cp_async16(s_cw + 2 * q, a.cw + (long long)e * NSP + 2 * q);
+  }
   cp_async_commit();
-  stage_ints<(P3 % 4) == 0>(s_pos, a.pos + (long long)e * P3, P3, tid, Sh::kBlock);
+#pragma unroll 1
+  for (int q = 0; q < EPB; ++q) {
+    const long long ei = static_cast<long long>(blockIdx.x) * EPB + q;
+    if (ei >= a.ne) break;
+    const int eq = a.order ? __ldg(a.order + ei) : static_cast<int>(ei);
+    stage_ints<(P3 % 4) == 0>(s_pos_all[q], a.pos + (long long)eq * P3, P3, tid, kBlk);
+  }
   cp_async_commit();
   const double hx = __ldg(a.h3 + 3 * e), hy = __ldg(a.h3 + 3 * e + 1), hz = __ldg(a.h3 + 3 * e + 2);
   const double svol = 8.0 / (hx * hy * hz);  // fine.cpp:154
@@ -263,7 +308,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
       }
 #pragma unroll
       for (int ii = 0; ii <= n; ++ii) in[ii + 1] = gl[ii] >= 0 ? __ldg(a.r + gl[ii]) : 0.0;
-      if (a.Rpart) {
+      if (EPB == 1 && a.Rpart) {
         // this line's share of the 8 corner sums R_cb = sum_l B[cb][l] (r/m_N)_l m_l.
         // An element-interior node has one copy, so m_N = m_l and its term is
         // r itself (to rounding): only surface nodes read 1/m_N and m_l.
@@ -300,7 +345,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
 #pragma unroll
     for (int x = 0; x < P; ++x) buf[at(x, y, z)] = out[x];
   }
-  if (a.Rpart) {  // fixed-tree reduction of the corner sums over the CTA's lines
+  if (EPB == 1 && a.Rpart) {  // fixed-tree reduction of the corner sums over the CTA's lines
 #pragma unroll
     for (int cb = 0; cb < 8; ++cb)
       for (int o = 16; o > 0; o >>= 1) racc[cb] += __shfl_xor_sync(0xffffffffu, racc[cb], o);
@@ -309,10 +354,10 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
       for (int cb = 0; cb < 8; ++cb) s_red[tid >> 5][cb] = racc[cb];
   }
   __syncthreads();
-  if (a.Rpart && tid < 8) {
+  if (EPB == 1 && a.Rpart && tid < 8) {
     double v = 0.0;
 #pragma unroll
-    for (int w = 0; w < Sh::kBlock / 32; ++w) v += s_red[w][tid];
+    for (int w = 0; w < kBlk / 32; ++w) v += s_red[w][tid];
     a.Rpart[8 * (long long)e + tid] = v;
   }
 
@@ -364,7 +409,7 @@ __global__ void __launch_bounds__(FdmShape<NP>::kBlock, FdmShape<NP>::kMinBlocks
       const int q = ps[x];
       if (q >= 0)
         a.zsort[q] = out[x];
-      else if (q <= -2)  // finalised by a neighbour rank (distributed plans)
+      else if (EPB == 1 && q <= -2)  // finalised by a neighbour rank (distributed plans)
         a.fsend[-2 - q] = out[x];
     }
   }

@@ -156,6 +156,7 @@ struct Plan {
   // single-device two-scale plans); false: restriction fused into the FDM and
   // the combine split around the coarse solve (hxb_options.restrict_in_fdm)
   bool restrict_first = false;
+  bool fdm_one_per_cta = false;  // A/B (HXB_FDM_ONE_PER_CTA=1): one subdomain per FDM CTA at every order
   int* fdm_order = nullptr;  // FDM CTA -> element: Morton order of element centroids (neighbours close in time)
   bool host_lists = false;  // build the fine gather lists on the host (A/B checks of the device sort)
   bool bitwise = false;     // hxb_options.bitwise_reference: every apply/solve through compat.cu
@@ -498,7 +499,10 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   a.order = pl.fdm_order;
   KtScope kt(pl, HXB_KT_FDM, s);
   pl.launches += 1;
-  if (pl.fdm_eo)
+  constexpr int EPB = FdmEPB<NP>::value;
+  if (pl.fdm_eo && EPB > 1 && !a.Rpart && !a.fsend && !pl.fdm_one_per_cta)  // several subdomains per CTA
+    fdm_kernel<NP, true, EPB><<<(pl.ne + EPB - 1) / EPB, FdmShapeE<NP, EPB>::kBlock, 0, s>>>(a);
+  else if (pl.fdm_eo)
     fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
   else
     fdm_kernel<NP, false><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
@@ -1459,6 +1463,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   pl.rsurf = M.alloc<double>(static_cast<std::size_t>(pl.ne) * pl.nsurf);
 
   pl.restrict_first = pl.do_fine && pl.do_coarse && pl.nranks == 1 && opt.restrict_in_fdm == 0;
+  if (const char* o = std::getenv("HXB_FDM_ONE_PER_CTA")) pl.fdm_one_per_cta = std::atoi(o) != 0;
   if (pl.do_coarse) {  // restriction weights m_l / m_N of the surface slots (restriction pass / fused in the FDM)
     std::vector<int> slot_l(nsurf_raw);
     for (int k = 0; k < pl.np; ++k)

@@ -12,7 +12,8 @@
 // (mesh.cpp:260-281): o = min corner id, xn = the smaller of o's two in-face
 // neighbours. Only the entity lists are sorted (12 edges + 6 faces per
 // element instead of (n+1)^3 48-byte keys), so this is O(NE log NE + N).
-// Bit-exactness against the reference is checked in tests/test_numbering.py.
+// Bit-exactness against the reference is checked in tests/test_host_setup.py
+// (108 meshes, and cfg2 entry for entry in the slow test_numbering_bit_exact_cfg2).
 //
 // Also derived here: the Dirichlet mask (mesh.cpp:369-383) and the face slots
 // of the extended (n+3)^3 subdomain numbering (sub_l2g, mesh.cpp:385-451).

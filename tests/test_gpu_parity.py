@@ -427,3 +427,19 @@ def test_direct_coarse_device_factorization(k, order):
     assert rel(plan.apply_P(r), ref.apply_P(r)) <= 1e-11
     b = ref.load_ones()
     history_parity(plan.pcg(b, tol=1e-8), ref.pcg(b, tol=1e-8), tol=1e-10)
+
+
+@pytest.mark.parametrize("k,order", [(6, 2), (5, 3), (4, 5), (3, 7), (3, 9)])
+def test_fdm_subdomains_per_cta_bitwise_neutral(k, order, monkeypatch):
+    """Several subdomains per FDM CTA (lines of consecutive elements packed
+    into full warps) performs each subdomain's arithmetic unchanged: the fine
+    preconditioner and the PCG history are bitwise equal to one subdomain per
+    CTA."""
+    mesh = hx.generate_cube_mesh(k, "distorted_elements")
+    a = hx.Plan(mesh, order)
+    monkeypatch.setenv("HXB_FDM_ONE_PER_CTA", "1")
+    b = hx.Plan(mesh, order)
+    r = splitmix_vector(a.N, 17)
+    assert np.array_equal(a.apply_fine(r), b.apply_fine(r))
+    ha, hb = a.pcg(None, tol=1e-10), b.pcg(None, tol=1e-10)
+    assert np.array_equal(ha["residual_history"], hb["residual_history"])
