@@ -616,6 +616,16 @@ void enqueue_dense(Plan& pl, const double* b, double* x, cudaStream_t s)
 
 void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s);
 
+// grid of a coarse-graph kernel (grid-stride loops). Capping it so the
+// graph's kernels need fewer CTA slots next to the concurrent FDM was measured
+// slower at every cap (cfg2: 148 CTAs 4.44, 74 CTAs 4.60 ms per iteration
+// against 4.35 uncapped, profiles/r02_ab_experiments.jsonl A/B 11).
+int coarse_grid(const Plan& pl, long long n, int block = kVecBlock)
+{
+  (void)pl;
+  return static_cast<int>(std::max(1LL, std::min((n + block - 1) / block, 148LL * 4)));
+}
+
 // Fusions used when the cycle runs inside ksolve(l): the K-solve's init
 // (r_copy = r, x = 0) in the first kernel, its z.r (and p = z) in the last.
 struct CycleFuse {
@@ -635,10 +645,10 @@ void enqueue_cycle(Plan& pl, int l, const double* r, double* zout, cudaStream_t 
   }
   DevLevel& v = pl.lv[l];
   DevLevel& c = pl.lv[l + 1];
-  const int g = vec_grid(v.n);
+  const int g = coarse_grid(pl, v.n);
   amg_jacobi2_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, fu.r_copy, fu.x_zero, fu.ks_init);
   amg_resid_kernel<<<g, kVecBlock, 0, s>>>(v.A, r, v.zA, v.kf);  // kf is free during the cycle
-  amg_agg_sum_kernel<<<vec_grid(v.nc), kVecBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
+  amg_agg_sum_kernel<<<coarse_grid(pl, v.nc), kVecBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
   enqueue_ksolve(pl, l + 1, c.b, c.x, s);
   amg_prolong_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
   if (fu.dot)
@@ -655,7 +665,7 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
     return;
   }
   DevLevel& v = pl.lv[l];
-  const int g = vec_grid(v.n);
+  const int g = coarse_grid(pl, v.n);
   {  // init fused into the first cycle's Jacobi kernel, z.r and p = z into its last smoother
     const DotArgs d0 = cdot_args(pl, &v.ks->zr);
     CycleFuse fu;
@@ -685,14 +695,14 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
 // restrict_warp_kernel launched just before the graph.
 void enqueue_coarse(Plan& pl, cudaStream_t s)
 {
-  vertex_gather_kernel<<<gather_grid(pl.nv), kGatherBlock, 0, s>>>(pl.Rpart, pl.vtx_off, pl.vtx_idx, pl.vmask, pl.R, pl.nv);
+  vertex_gather_kernel<<<coarse_grid(pl, pl.nv, kGatherBlock), kGatherBlock, 0, s>>>(pl.Rpart, pl.vtx_off, pl.vtx_idx, pl.vmask, pl.R, pl.nv);
   if (pl.use_amg) {
     enqueue_cycle(pl, 0, pl.R, pl.Z, s);
     // two composed K-cycles: Z = B R + B (R - K_c B R)  (coarse.cpp:193-200)
     const DevCsr K = pl.Kc;
-    amg_resid_kernel<<<vec_grid(K.n), kVecBlock, 0, s>>>(K, pl.R, pl.Z, pl.rho);
+    amg_resid_kernel<<<coarse_grid(pl, K.n), kVecBlock, 0, s>>>(K, pl.R, pl.Z, pl.rho);
     enqueue_cycle(pl, 0, pl.rho, pl.dZ, s);
-    axpy1_kernel<<<vec_grid(K.n), kVecBlock, 0, s>>>(pl.Z, pl.dZ, K.n);
+    axpy1_kernel<<<coarse_grid(pl, K.n), kVecBlock, 0, s>>>(pl.Z, pl.dZ, K.n);
   } else {
     enqueue_dense(pl, pl.R, pl.Z, s);
   }
