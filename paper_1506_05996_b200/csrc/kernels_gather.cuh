@@ -16,15 +16,7 @@ namespace hxb {
 
 constexpr int kGatherBlock = 256;
 constexpr int kGatherCap = 320;  // staged values per warp (avg ~1.5-2.6 per node)
-#ifdef GATHER_SKEW
-// staged value c at c + c/16: lanes whose segments start 16 values apart
-// (8 nodes of 2 copies) land in different banks for the per-lane sums
-__device__ __forceinline__ unsigned gskew(unsigned c) { return c + (c >> 4); }
-constexpr int kGatherStage = kGatherCap + kGatherCap / 16;
-#else
-__device__ __forceinline__ unsigned gskew(unsigned c) { return c; }
-constexpr int kGatherStage = kGatherCap;
-#endif
+
 
 // Sums for a warp's 32 consecutive nodes of values scattered in an E-vector: src(idx[q]) gathered by the warp
 // (coalesced index segment, parallel value loads), then per-lane sequential sums.
@@ -42,9 +34,9 @@ __device__ __forceinline__ double warp_csr_sum(const unsigned* __restrict__ off,
   double s = 0.0;
   if (cnt <= static_cast<unsigned>(kGatherCap)) {
 #pragma unroll 4
-    for (unsigned c = lane; c < cnt; c += 32) stage[gskew(c)] = src(__ldg(idx + base + c));
+    for (unsigned c = lane; c < cnt; c += 32) stage[c] = src(__ldg(idx + base + c));
     __syncwarp();
-    for (unsigned q = my0 - base; q < my1 - base; ++q) s += stage[gskew(q)];
+    for (unsigned q = my0 - base; q < my1 - base; ++q) s += stage[q];
     __syncwarp();
   } else {
     for (unsigned q = my0; q < my1; ++q) s += src(__ldg(idx + q));
@@ -71,7 +63,7 @@ struct AxGatherArgs {
 __global__ void __launch_bounds__(kGatherBlock) ax_gather_kernel(AxGatherArgs a)
 {
   __shared__ double red[kGatherBlock / 32];
-  __shared__ double stage[kGatherBlock / 32][kGatherStage];
+  __shared__ double stage[kGatherBlock / 32][kGatherCap];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = gridDim.x * (kGatherBlock / 32);
   double dot = 0.0;

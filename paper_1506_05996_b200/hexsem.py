@@ -361,6 +361,8 @@ class Plan:
             opt.n_gpus = len(devices)
             for r, d in enumerate(devices):
                 opt.devices[r] = int(d)
+            if len(devices) == 1:
+                opt.device = int(devices[0])
         cm = mesh._c()
         h = C.c_void_p()
         _check(L.hxb_plan_create(C.byref(cm), order, _ptr(self.kappa_e), _ptr(self.c_e), C.byref(opt), C.byref(h)))
