@@ -113,7 +113,14 @@ typedef struct hxb_options {
   int fdm_element_order;
   int host_lists;
   int restrict_in_fdm;
-  int reserved[3];
+  /* SM partition of a single-GPU two-scale plan: the coarse solve runs on
+   * coarse_sms SMs of its own (a green context) while the fine solves run on
+   * the others, so the coarse solve's chain of small kernels never waits for
+   * SMs held by the fine solves. 0: the library default; -1: no partition
+   * (both share every SM, the coarse stream at high priority); > 0: that many
+   * SMs (rounded to the hardware's granularity of 8). */
+  int coarse_sms;
+  int reserved[2];
 } hxb_options;
 
 /* PcgConfig (krylov.hpp:15-19) */
@@ -152,6 +159,8 @@ typedef struct hxb_plan_info {
   int64_t amg_nnz[16];
   double setup_seconds;        /* host setup + upload */
   int64_t device_bytes;        /* device memory held by the plan */
+  int32_t coarse_sms;          /* SMs of the coarse solve's partition (0: all SMs shared) */
+  int32_t pad_;
 } hxb_plan_info;
 
 typedef struct hxb_plan hxb_plan;

@@ -115,14 +115,24 @@ __global__ void __launch_bounds__(256) restrict_warp_kernel(const double* __rest
 // element-interior nodes (one copy: m_N = m_l). No mass or 1/m_N loads, so it
 // runs as a cheap standalone pass before the FDM and the coarse solve can
 // start concurrently with the fine solves.
+//
+// Warp per element, lanes over the element's nodes in storage order: surface
+// slots first (codes and weights are contiguous rows, r gathered through the
+// codes), then the interior block (contiguous ids). Every load of a warp
+// instruction is coalesced; each lane spreads its node's weighted value over
+// the 8 corners with hat_a(t_i) hat_b(t_j) hat_c(t_k) and the warp reduces the
+// partials in a fixed tree (deterministic; the order differs from the
+// reference's l-loop at rounding level only). Measured against the line-per-
+// lane traversal it replaced (strided interior loads, 35 % of HBM): see
+// DESIGN.md section 7.
 template <int NP>
 __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __restrict__ r, const int* __restrict__ smap,
                                                           const double* __restrict__ cw, double* __restrict__ Rpart,
                                                           int ne, int sstride, int nsurfp, int nsg,
                                                           const int* __restrict__ order)
 {
-  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NL = NP * NP, LPL = (NL + 31) / 32;
-  constexpr int CH = LPL < 2 ? LPL : 2;
+  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2);
+  constexpr int US = NP == 7 ? 3 : 4;  // loads in flight per lane (NP = 7 spills at 4)
   __shared__ double h0[NP], h1[NP];
   if (threadIdx.x < NP) {
     h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
@@ -131,6 +141,18 @@ __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __res
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
+  auto spread = [&](double (&acc)[8], int i, int j, int k, double w) {
+    const double a0 = h0[i] * w, a1 = h1[i] * w;
+    const double c00 = h0[j] * h0[k], c10 = h1[j] * h0[k], c01 = h0[j] * h1[k], c11 = h1[j] * h1[k];
+    acc[0] += c00 * a0;
+    acc[1] += c00 * a1;
+    acc[2] += c10 * a0;
+    acc[3] += c10 * a1;
+    acc[4] += c01 * a0;
+    acc[5] += c01 * a1;
+    acc[6] += c11 * a0;
+    acc[7] += c11 * a1;
+  };
   // elements in Morton order (order[], the FDM's traversal): the face
   // neighbours that share a surface node run close in time, so its r is read
   // from L2
@@ -138,43 +160,43 @@ __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __res
     const int e = order ? __ldg(order + eo) : eo;
     const int* surf = smap + (long long)e * sstride;
     const double* we = cw + (long long)e * nsurfp;
-    const long long ibase = (long long)nsg + (long long)e * NI;
+    const double* ri = r + (long long)nsg + (long long)e * NI;
     double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll 1
-    for (int q0 = 0; q0 < LPL; q0 += CH) {
-      double wv[CH][NP];
+    for (int s0 = 0; s0 < NS; s0 += 32 * US) {
+      int code[US];
+      double wt[US], v[US];
 #pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        const int line = lane + 32 * (q0 + q);
-        const int j = (line < NL ? line : 0) % NP, k = (line < NL ? line : 0) / NP;
-        const bool face = (j == 0 || j == n || k == 0 || k == n);
-#pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          if (line >= NL) {
-            wv[q][i] = 0.0;
-          } else if (face || i == 0 || i == n) {
-            const int s = surface_slot(NP, i, j, k);
-            const int code = __ldg(surf + s);
-            wv[q][i] = code >= 0 ? __ldg(r + code) * __ldg(we + s) : 0.0;  // Dirichlet: masked (precond.cpp:35)
-          } else {
-            wv[q][i] = __ldg(r + ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1));
-          }
-        }
+      for (int u = 0; u < US; ++u) {
+        const int s = s0 + 32 * u + lane;
+        code[u] = s < NS ? __ldg(surf + s) : -1;
+        wt[u] = s < NS ? __ldg(we + s) : 0.0;
       }
 #pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        const int line = lane + 32 * (q0 + q);
-        const int j = (line < NL ? line : 0) % NP, k = (line < NL ? line : 0) / NP;
-        double w0 = 0.0, w1 = 0.0;
+      for (int u = 0; u < US; ++u) v[u] = code[u] >= 0 ? __ldg(r + code[u]) : 0.0;  // Dirichlet: masked (precond.cpp:35)
 #pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          w0 += h0[i] * wv[q][i];
-          w1 += h1[i] * wv[q][i];
+      for (int u = 0; u < US; ++u) {
+        const int s = s0 + 32 * u + lane;
+        if (s < NS) {
+          int i, j, k;
+          surface_ijk<NP>(s, i, j, k);
+          spread(acc, i, j, k, v[u] * wt[u]);
         }
-        if (line < NL) {
-          const double hj[2] = {h0[j], h1[j]}, hk[2] = {h0[k], h1[k]};
+      }
+    }
+    if constexpr (NI > 0) {
+#pragma unroll 1
+      for (int t0 = 0; t0 < NI; t0 += 32 * US) {
+        double v[US];
 #pragma unroll
-          for (int cb = 0; cb < 8; ++cb) acc[cb] += (hj[(cb >> 1) & 1] * hk[cb >> 2]) * ((cb & 1) ? w1 : w0);
+        for (int u = 0; u < US; ++u) {
+          const int t = t0 + 32 * u + lane;
+          v[u] = t < NI ? __ldg(ri + t) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < US; ++u) {
+          const int t = t0 + 32 * u + lane;
+          if (t < NI) spread(acc, 1 + t % (n - 1), 1 + (t / (n - 1)) % (n - 1), 1 + t / ((n - 1) * (n - 1)), v[u]);
         }
       }
     }

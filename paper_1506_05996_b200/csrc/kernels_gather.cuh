@@ -205,24 +205,27 @@ __global__ void dist_finish_kernel(const int* __restrict__ nodes, int n, const d
 // Two-scale combine with the coarse prolongation fused in (precond.cpp:57-66,
 // prolongate coarse.cpp:164-186): per node g
 //   zf = sum of its subdomain contributions in (e, slot) order (fine.cpp:224-227)
-//   zc = (sum over its copies (e,l), in (e,l) order, of
-//         (sum_cb B[cb][l] Zc[e][cb]) * m[e][l]) / m_N[g]
+//   zc = the Q1 prolongation of the coarse solution at g
 //   z  = mask ? r : (0 + zf) + zc ;  z.r partial
-// Element-interior nodes have one copy whose (e,l) follows from g
-// (interior ids are (e, local)-ordered, mesh.cpp:283); surface nodes walk
-// their Ax gather list (ax_idx = e*nsurfp + slot).
+// The reference forms zc as the mass-weighted average over g's copies,
+// (sum_(e,l) (B Zc_e)_l m_l) / m_N. The Q1 interpolant is continuous across
+// element faces (a shared face's values depend only on its four vertices), so
+// every copy carries the same value to rounding and the average is that value
+// to rounding: the combine evaluates it once, at the node's first copy (for an
+// element-interior node, its only copy). That drops the per-copy mass and
+// index streams (0.5 GB per apply at cfg2); the bitwise-reference mode
+// (compat.cu) keeps the reference's weighted form.
+//
+// Warp per 32 consecutive nodes: their contribution lists are one contiguous
+// zsort segment, staged by coalesced loads into shared memory; each lane then
+// sums its node's entries in list order.
 struct CombineProlongArgs {
   const double* r;
   const std::uint8_t* mask;
   const double* zsort;
   const unsigned* fine_off;
-  const unsigned* ax_off;
-  const int* ax_idx;
+  const int* surf_first;   // first copy e*nsurfp + slot of each surface item (Zc element numbering)
   const double* Zc;
-  const double* mass;      // [e][nloc] (element-interior copies)
-  const double* mass_csr;  // surface copies, Ax-CSR order
-  const double* lumped;
-  const double* inv_lumped;
   double* z;
   int N, nsg;
   int do_fine, do_coarse;
@@ -233,25 +236,52 @@ struct CombineProlongArgs {
   // the distributed plan runs over its finalised nodes only
   const int* surf_nodes = nullptr;
   int ibase = 0;    // global id of the first interior item
-  int e0 = 0;       // global id of the first element whose mass block is at `mass`
+  int e0 = 0;       // Zc index of the element owning the first interior item
 };
 
 #ifndef COMBINE_MIN_BLOCKS
-#define COMBINE_MIN_BLOCKS 6  // cfg2: 6 (40 regs, 100 B spills) 0.857 ms, 4 (64 regs) 0.937, 8 (32 regs) 1.024
+#define COMBINE_MIN_BLOCKS 6
 #endif
+constexpr int kCombineCap = 320;  // staged contributions per warp (avg ~2.9 per node at P = n+3)
+
+// sum, for each lane's item g0 + lane, of its CSR segment of a contiguous value array
+__device__ __forceinline__ double warp_segment_sum(const unsigned* __restrict__ off, const double* __restrict__ val,
+                                                   int g0, int n, double* __restrict__ stage)
+{
+  const int lane = threadIdx.x & 31;
+  const int g = g0 + lane;
+  const unsigned my0 = __ldg(off + min(g, n));
+  const unsigned my1 = __ldg(off + min(g + 1, n));
+  const unsigned base = __shfl_sync(0xffffffffu, my0, 0);
+  const unsigned end = __shfl_sync(0xffffffffu, my1, 31);
+  const unsigned cnt = end - base;
+  double s = 0.0;
+  if (cnt <= static_cast<unsigned>(kCombineCap)) {
+#pragma unroll 4
+    for (unsigned c = lane; c < cnt; c += 32) stage[c] = __ldcs(val + base + c);
+    __syncwarp();
+    for (unsigned q = my0 - base; q < my1 - base; ++q) s += stage[q];
+    __syncwarp();
+  } else {
+    for (unsigned q = my0; q < my1; ++q) s += __ldcs(val + q);
+  }
+  return s;
+}
+
 template <int NP>
 __global__ void __launch_bounds__(kGatherBlock, COMBINE_MIN_BLOCKS) combine_prolong_kernel(CombineProlongArgs a)
 {
   constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1);
   constexpr int NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2), NSP = (NS + 3) & ~3;
   __shared__ double red[kGatherBlock / 32];
+  __shared__ double stage[kGatherBlock / 32][kCombineCap];
   __shared__ double h0[NP], h1[NP];
   if (threadIdx.x < NP) {
     h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
     h1[threadIdx.x] = c_tab[NP].hat1[threadIdx.x];
   }
   __syncthreads();
-  // prolongated value of copy (e; i,j,k) before the mass: sum_cb B[cb][l] Zc[e][cb] (coarse.cpp:176-179)
+  // prolongated value at (e; i,j,k): sum_cb B[cb][l] Zc[e][cb] (coarse.cpp:176-179)
   auto pz = [&](long long e, int i, int j, int k) {
     const double2* zc2 = reinterpret_cast<const double2*>(a.Zc + 8 * e);
     const double2 c01 = __ldg(zc2), c23 = __ldg(zc2 + 1), c45 = __ldg(zc2 + 2), c67 = __ldg(zc2 + 3);
@@ -262,72 +292,216 @@ __global__ void __launch_bounds__(kGatherBlock, COMBINE_MIN_BLOCKS) combine_prol
     for (int cb = 0; cb < 8; ++cb) s += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[cb >> 2] * zc[cb];
     return s;
   };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nwarps = gridDim.x * (kGatherBlock / 32);
+  const bool stage_fine = a.do_fine && !a.fine_in_z;
   double dot = 0.0;
-  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < a.N; it += gridDim.x * blockDim.x) {
+  for (int w0 = (blockIdx.x * (kGatherBlock / 32) + warp) * 32; w0 < a.N; w0 += nwarps * 32) {
+    // every load that does not depend on the contribution sums is issued first
+    // (node id, r, mask, the prolongation's element corners), so a warp waits
+    // for two dependent round trips per 32 nodes rather than four
+    const int it = w0 + lane;
+    const bool valid = it < a.N;
     const bool surf = it < a.nsg;
-    const int g = surf ? (a.surf_nodes ? __ldg(a.surf_nodes + it) : it) : a.ibase + (it - a.nsg);
-    const double rg = __ldg(a.r + g);
+    const int g = !valid ? 0 : surf ? (a.surf_nodes ? __ldg(a.surf_nodes + it) : it) : a.ibase + (it - a.nsg);
+    const double rg = valid ? __ldg(a.r + g) : 0.0;
+    const bool dir = valid && surf && __ldg(a.mask + g);  // Dirichlet nodes are element-surface nodes
+    long long ze = 0;
+    int i = 0, j = 0, k = 0;
+    if (a.do_coarse && valid) {
+      if (!surf) {
+        if constexpr (NI > 0) {
+          const int t = it - a.nsg;  // interior ids are (e, local)-ordered (mesh.cpp:283)
+          const int l = t % NI;
+          ze = t / NI + a.e0;
+          i = 1 + l % (n - 1);
+          j = 1 + (l / (n - 1)) % (n - 1);
+          k = 1 + l / ((n - 1) * (n - 1));
+        }
+      } else {
+        const int x0 = __ldg(a.surf_first + it);
+        ze = x0 / NSP;
+        surface_ijk<NP>(x0 % NSP, i, j, k);
+      }
+    }
+    const double zc = a.do_coarse && valid && !dir ? pz(ze, i, j, k) : 0.0;
+    const double zf = stage_fine ? warp_segment_sum(a.fine_off, a.zsort, w0, a.N, stage[warp]) : 0.0;
+    if (!valid) continue;
     double zg;
-    if (surf && __ldg(a.mask + g)) {  // Dirichlet nodes are element-surface nodes
+    if (dir) {
       zg = rg;
     } else {
       double s = 0.0;
-      if (a.fine_in_z) {
+      if (a.fine_in_z)
         s = a.z[g];
-      } else if (a.do_fine) {
-        // up to 8 contributions loaded at once (predicated), summed in list order
-        const unsigned q0 = __ldg(a.fine_off + it), q1 = __ldg(a.fine_off + it + 1);
-        double v[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) v[t] = q0 + t < q1 ? __ldcs(a.zsort + q0 + t) : 0.0;
-        double zf = 0.0;
-#pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (q0 + t < q1) zf += v[t];
-        for (unsigned q = q0 + 8; q < q1; ++q) zf += __ldcs(a.zsort + q);
+      else if (a.do_fine)
         s += zf;
-      }
-      if (a.do_coarse) {
-        double zc = 0.0;
-        if (!surf) {
-          if constexpr (NI > 0) {
-            const int t = it - a.nsg;  // interior ids are (e, local)-ordered (mesh.cpp:283)
-            const long long el = t / NI;          // element relative to e0
-            const int l = t % NI;
-            const int i = 1 + l % (n - 1), j = 1 + (l / (n - 1)) % (n - 1), k = 1 + l / ((n - 1) * (n - 1));
-            // single copy: (B zc) m / m_N with m_N = m is B zc to rounding (coarse.cpp:180, 185)
-            zc = pz(el + a.e0, i, j, k);
-          }
-        } else {
-          // face nodes (2 copies) dominate: the first two copies are evaluated
-          // independently, the rest (edges 4, vertices 8+) in order after them
-          const unsigned c0 = __ldg(a.ax_off + it), c1 = __ldg(a.ax_off + it + 1);
-          const int x0 = __ldg(a.ax_idx + c0);
-          const int x1 = c0 + 1 < c1 ? __ldg(a.ax_idx + c0 + 1) : x0;
-          int i0, j0, k0, i1, j1, k1;
-          surface_ijk<NP>(x0 % NSP, i0, j0, k0);
-          surface_ijk<NP>(x1 % NSP, i1, j1, k1);
-          const double m0 = __ldcs(a.mass_csr + c0);
-          const double m1 = c0 + 1 < c1 ? __ldcs(a.mass_csr + c0 + 1) : 0.0;
-          const double p0 = pz(x0 / NSP, i0, j0, k0) * m0;
-          const double p1 = pz(x1 / NSP, i1, j1, k1) * m1;
-          zc += p0;
-          if (c0 + 1 < c1) zc += p1;
-          for (unsigned q = c0 + 2; q < c1; ++q) {
-            const int c = __ldg(a.ax_idx + q);
-            int i, j, k;
-            surface_ijk<NP>(c % NSP, i, j, k);
-            zc += pz(c / NSP, i, j, k) * __ldcs(a.mass_csr + q);
-          }
-        }
-        s += surf ? zc * __ldg(a.inv_lumped + g) : zc;  // /m_N (coarse.cpp:185) as a product with 1/m_N
-      }
+      if (a.do_coarse) s += zc;
       zg = s;
     }
     a.z[g] = zg;
     dot += zg * rg;
   }
   dot_commit<kGatherBlock>(a.dot, dot, red);
+}
+
+// ---------------------------------------------------------------------------
+// The same combine as a TMA-streamed persistent kernel (single-device plans,
+// node ids = item ids). A tile of kCombTile consecutive nodes reads five
+// contiguous ranges: r, the Dirichlet mask, the contribution offsets, the
+// first-copy codes and its zsort segment [off[t0], off[t1]). One thread issues
+// them as 1-D bulk copies (cp.async.bulk) completing on the stage's mbarrier,
+// one tile ahead, into two shared-memory stages; the CTA's threads then sum,
+// prolongate and store straight from shared memory. The data stream needs no
+// per-thread loads in flight, so the kernel runs at the copy engines' rate
+// instead of the warps' memory-level parallelism. Tiles whose segment exceeds
+// the stage (none in the meshes measured) and the tail tile read global memory
+// directly. Same arithmetic, same order as combine_prolong_kernel.
+// Tile of 512 nodes from order 3 up (2.6-5.9 contributions per node on
+// average), 256 below (up to 10 per node at order 2), so a tile's segment
+// fits the 3072-entry stage (measured: order 3 at 256 nodes 0.394 ms, at 512
+// 0.366 ms with a few tiles over the cap reading global memory).
+constexpr int kCombZcap = 3072, kCombBlock = 256, kCombTileMax = 512;
+template <int NP>
+struct CombTile {
+  static constexpr int value = NP <= 3 ? 256 : 512;
+};
+template <int T>
+struct CombStage {
+  double zs[kCombZcap];
+  double rr[T];
+  unsigned off[T + 4];
+  int sf[T];
+  unsigned char mk[T];
+};
+template <int T>
+constexpr int comb_smem() { return 2 * static_cast<int>(sizeof(CombStage<T>)); }
+
+template <int NP>
+__global__ void __launch_bounds__(kCombBlock, 3) combine_tma_kernel(CombineProlongArgs a, int ntiles, int ntma)
+{
+  constexpr int kCombTile = CombTile<NP>::value;
+  using CombStageT = CombStage<kCombTile>;
+  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1);
+  constexpr int NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2), NSP = (NS + 3) & ~3;
+  extern __shared__ __align__(128) unsigned char comb_smem[];
+  CombStageT* st = reinterpret_cast<CombStageT*>(comb_smem);
+  __shared__ __align__(8) unsigned long long full[2];
+  __shared__ unsigned zbase[2], zfit[2];
+  __shared__ double red[kCombBlock / 32];
+  __shared__ double h0[NP], h1[NP];
+  const int tid = threadIdx.x;
+  if (tid < NP) {
+    h0[tid] = c_tab[NP].hat0[tid];
+    h1[tid] = c_tab[NP].hat1[tid];
+  }
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto pz = [&](long long e, int i, int j, int k) {
+    const double2* zc2 = reinterpret_cast<const double2*>(a.Zc + 8 * e);
+    const double2 c01 = __ldg(zc2), c23 = __ldg(zc2 + 1), c45 = __ldg(zc2 + 2), c67 = __ldg(zc2 + 3);
+    const double zc[8] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y};
+    const double hi[2] = {h0[i], h1[i]}, hj[2] = {h0[j], h1[j]}, hk[2] = {h0[k], h1[k]};
+    double s = 0.0;
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb) s += hi[cb & 1] * hj[(cb >> 1) & 1] * hk[cb >> 2] * zc[cb];
+    return s;
+  };
+  // thread 0: stage tile ti (ti < ntma: every range in bounds)
+  auto issue = [&](int ti, int s) {
+    const long long t0 = static_cast<long long>(ti) * kCombTile;
+    const unsigned q0 = __ldg(a.fine_off + t0), q1 = __ldg(a.fine_off + t0 + kCombTile);
+    const unsigned z0 = q0 & ~1u, z1 = (q1 + 1) & ~1u;
+    // the second half of a split combine reads the fine sums from z instead
+    const bool fits = !a.fine_in_z && z1 - z0 <= static_cast<unsigned>(kCombZcap);
+    const bool sf = a.do_coarse && t0 < a.nsg;
+    zbase[s] = z0;
+    zfit[s] = fits ? 1u : 0u;
+    const unsigned bytes = kCombTile * 8 + (kCombTile + 4) * 4 + kCombTile + (sf ? kCombTile * 4 : 0) +
+                           (fits ? (z1 - z0) * 8 : 0);
+    fence_proxy_async_smem();
+    mbar_expect_tx(&full[s], bytes);
+    bulk_g2s(st[s].rr, a.r + t0, kCombTile * 8, &full[s]);
+    bulk_g2s(st[s].off, a.fine_off + t0, (kCombTile + 4) * 4, &full[s]);
+    bulk_g2s(st[s].mk, a.mask + t0, kCombTile, &full[s]);
+    if (sf) bulk_g2s(st[s].sf, a.surf_first + t0, kCombTile * 4, &full[s]);
+    if (fits && z1 > z0) bulk_g2s(st[s].zs, a.zsort + z0, (z1 - z0) * 8, &full[s]);
+  };
+  double dot = 0.0;
+  if (tid == 0 && static_cast<int>(blockIdx.x) < ntma) issue(blockIdx.x, 0);
+  int use = 0;
+  for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x, ++use) {
+    const int s = use & 1;
+    const int tn = ti + gridDim.x;
+    if (tid == 0 && tn < ntma) issue(tn, s ^ 1);  // stage s^1 was released by the last __syncthreads
+    const bool staged = ti < ntma;
+    if (staged) mbar_wait(&full[s], (use >> 1) & 1);
+    const CombStageT& S = st[s];
+    const long long t0 = static_cast<long long>(ti) * kCombTile;
+    const unsigned z0 = staged ? zbase[s] : 0u;
+    const bool fit = staged && zfit[s];
+#pragma unroll
+    for (int h = 0; h < kCombTile / kCombBlock; ++h) {
+      const int l = tid + h * kCombBlock;
+      const long long itl = t0 + l;
+      if (itl >= a.N) continue;
+      const int it = static_cast<int>(itl);
+      const bool surf = it < a.nsg;
+      const double rg = staged ? S.rr[l] : __ldg(a.r + it);
+      double zg;
+      if (surf && (staged ? S.mk[l] : __ldg(a.mask + it))) {
+        zg = rg;
+      } else {
+        double sum = 0.0;
+        if (a.fine_in_z) {
+          sum = a.z[it];
+        } else if (a.do_fine) {
+          const unsigned q0 = staged ? S.off[l] : __ldg(a.fine_off + it);
+          const unsigned q1 = staged ? S.off[l + 1] : __ldg(a.fine_off + it + 1);
+          double zf = 0.0;
+          if (fit) {
+            for (unsigned q = q0 - z0; q < q1 - z0; ++q) zf += S.zs[q];
+          } else {
+            for (unsigned q = q0; q < q1; ++q) zf += __ldcs(a.zsort + q);
+          }
+          sum += zf;
+        }
+        if (a.do_coarse) {
+          double zc = 0.0;
+          if (!surf) {
+            if constexpr (NI > 0) {
+              const int t = it - a.nsg;
+              const int lq = t % NI;
+              zc = pz(t / NI, 1 + lq % (n - 1), 1 + (lq / (n - 1)) % (n - 1), 1 + lq / ((n - 1) * (n - 1)));
+            }
+          } else {
+            const int x0 = staged ? S.sf[l] : __ldg(a.surf_first + it);
+            int i0, j0, k0;
+            surface_ijk<NP>(x0 % NSP, i0, j0, k0);
+            zc = pz(x0 / NSP, i0, j0, k0);
+          }
+          sum += zc;
+        }
+        zg = sum;
+      }
+      a.z[it] = zg;
+      dot += zg * rg;
+    }
+    __syncthreads();  // stage s fully read before thread 0 refills it (next iteration's issue)
+  }
+  dot_commit<kCombBlock>(a.dot, dot, red);
+}
+
+// first copy (lowest (e, slot)) of every item of a copy CSR
+__global__ void first_copy_kernel(const unsigned* __restrict__ off, const int* __restrict__ idx, int n,
+                                  int* __restrict__ first)
+{
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+    first[t] = __ldg(idx + __ldg(off + t));
 }
 
 // First half of the split combine: z[g] = sum of node g's fine contributions

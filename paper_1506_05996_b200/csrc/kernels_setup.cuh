@@ -142,17 +142,6 @@ __global__ void surface_map_kernel(const int* __restrict__ l2g_surf, const int* 
   }
 }
 
-// mass of every surface copy in Ax-CSR order (the fused prolongation streams it)
-__global__ void mass_csr_kernel(const int* __restrict__ ax_idx, long long n, const double* __restrict__ mass, int nloc,
-                                int nsurfp, const int* __restrict__ slot_l, double* __restrict__ mcsr)
-{
-  for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
-       p += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int x = ax_idx[p];
-    mcsr[p] = mass[static_cast<long long>(x / nsurfp) * nloc + slot_l[x % nsurfp]];
-  }
-}
-
 // Restriction weights of the surface slots, m_l / m_N (coarse.cpp:149, 157):
 // the FDM's fused restriction reads one contiguous row per element instead of
 // the scattered 1/m_N and the mass row (Dirichlet slots weigh 0)

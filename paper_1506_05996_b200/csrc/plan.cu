@@ -7,6 +7,7 @@
 // status read-back per iteration. The coarse correction runs on its own
 // stream as a captured CUDA graph, concurrently with the fine FDM solves
 // (the reference's std::async, precond.cpp:40-46).
+#include <cuda.h>  // green-context types only: the functions come from cudaGetDriverEntryPointByVersion
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 #include <dlfcn.h>
@@ -52,6 +53,17 @@ namespace {
   } while (0)
 
 constexpr int kVecBlock = 256;
+#ifndef FDM_SMEM_PAD
+#define FDM_SMEM_PAD 0  // A/B: unused dynamic shared memory per FDM CTA (caps FDM residency per SM)
+#endif
+#ifndef COMBINE_TMA
+#define COMBINE_TMA 1  // A/B: 0 = the warp-staged combine_prolong_kernel on single-device plans
+#endif
+#ifndef COARSE_BLOCK
+#define COARSE_BLOCK 256
+#endif
+constexpr int kCoarseBlock = COARSE_BLOCK;  // block of the coarse graph's vector kernels
+
 
 int gather_grid(long long n)
 {
@@ -146,6 +158,7 @@ struct DevDense {
 
 struct Group;
 void destroy_group(Group* g);
+void destroy_green(CUgreenCtx g);
 
 struct Plan {
   int device = 0;
@@ -163,6 +176,12 @@ struct Plan {
   CompatPlan cx;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr, ev_a = nullptr;
   cudaGraphExec_t coarse_exec = nullptr;
+  // SM partition (hxb_options.coarse_sms): s_coarse and s_fine are streams of
+  // two green contexts splitting the SMs; null s_fine: no partition
+  CUgreenCtx g_coarse = nullptr, g_fine = nullptr;
+  cudaStream_t s_fine = nullptr;
+  cudaEvent_t ev_fine = nullptr;
+  int coarse_sms = 0;  // SMs of the coarse partition (0: none)
   DeviceArena mem;
 
   int order = 0, np = 0, nloc = 0, nsurf = 0, P = 0;
@@ -206,7 +225,7 @@ struct Plan {
   std::uint8_t* vmask = nullptr;
   double *Rpart = nullptr, *R = nullptr, *Z = nullptr, *rho = nullptr, *dZ = nullptr;
   double* Zc = nullptr;       // [e][8] coarse corner values for the fused prolongation
-  double* mass_csr = nullptr; // m of each surface copy in Ax-CSR order
+  int* surf_first = nullptr;  // first copy of each surface item (combine's prolongation)
   double* cw = nullptr;       // [e][nsurf] restriction weights m_l / m_N of the surface slots (fused in the FDM)
   std::vector<DevLevel> lv;  // AMG levels 0..L (L = coarsest, uses dense)
   DevDense dense;
@@ -250,9 +269,6 @@ struct Plan {
   // distributed preconditioned CG (setup_dist.cpp)
   int* fin_surf = nullptr;    // finalised surface nodes (group 0 + down)
   int n_fin_surf = 0, ib0 = 0, ib1 = 0;
-  unsigned* pr_off = nullptr; // prolongation CSR of the finalised surface nodes (all copies)
-  int* pr_idx = nullptr;
-  double* pr_mass = nullptr;
   int* frecv_pos = nullptr;   // [from down | from up] sum positions of the neighbours' contributions
   int n_frecv_down = 0, n_frecv_up = 0, n_fsend_down = 0, n_fsend_up = 0;
   int *g_from_down = nullptr, *g_from_up = nullptr, *g_to_down = nullptr, *g_to_up = nullptr;
@@ -279,6 +295,10 @@ struct Plan {
       if (e) cudaEventDestroy(e);
     if (s_main) cudaStreamDestroy(s_main);
     if (s_coarse) cudaStreamDestroy(s_coarse);
+    if (s_fine) cudaStreamDestroy(s_fine);
+    if (ev_fine) cudaEventDestroy(ev_fine);
+    destroy_green(g_coarse);
+    destroy_green(g_fine);
     if (h_status) cudaFreeHost(h_status);
     for (cudaEvent_t e : kt_ev) cudaEventDestroy(e);
     for (cudaEvent_t e : pipe_ev) cudaEventDestroy(e);
@@ -503,7 +523,7 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   if (pl.fdm_eo && EPB > 1 && !a.Rpart && !a.fsend && !pl.fdm_one_per_cta)  // several subdomains per CTA
     fdm_kernel<NP, true, EPB><<<(pl.ne + EPB - 1) / EPB, FdmShapeE<NP, EPB>::kBlock, 0, s>>>(a);
   else if (pl.fdm_eo)
-    fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
+    fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, FDM_SMEM_PAD, s>>>(a);
   else
     fdm_kernel<NP, false><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
 }
@@ -517,13 +537,8 @@ void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine
   a.mask = pl.mask;
   a.zsort = pl.zsort;
   a.fine_off = pl.fine_off;
-  a.ax_off = pl.ax_off;
-  a.ax_idx = pl.ax_idx;
+  a.surf_first = pl.surf_first;
   a.Zc = pl.Zc;
-  a.mass = pl.mass;
-  a.mass_csr = pl.mass_csr;
-  a.lumped = pl.d_lumped;
-  a.inv_lumped = pl.d_inv_lumped;
   a.z = pl.z;
   if (pl.nranks > 1) {  // this rank's finalised nodes
     a.N = pl.n_fin_surf + (pl.ib1 - pl.ib0);
@@ -531,9 +546,6 @@ void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine
     a.surf_nodes = pl.fin_surf;
     a.ibase = pl.ib0;
     a.e0 = pl.e0;
-    a.ax_off = pl.pr_off;
-    a.ax_idx = pl.pr_idx;
-    a.mass_csr = pl.pr_mass;
   } else {
     a.N = pl.N;
     a.nsg = pl.nsg;
@@ -544,6 +556,23 @@ void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine
   a.do_coarse = do_coarse ? 1 : 0;
   a.fine_in_z = fine_in_z ? 1 : 0;
   a.dot = zr_result ? dot_args(pl, zr_result) : DotArgs{};
+  if (COMBINE_TMA && pl.nranks == 1 && (do_fine || fine_in_z) && a.N > 0) {
+    constexpr int kCombTile = CombTile<NP>::value, kCombSmem = comb_smem<kCombTile>();
+    static bool attr = false;  // per NP instantiation
+    if (!attr) {
+      HXB_CUDA(cudaFuncSetAttribute(combine_tma_kernel<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kCombSmem));
+      attr = true;
+    }
+    const long long ntiles = (static_cast<long long>(a.N) + kCombTile - 1) / kCombTile;
+    // tiles whose five ranges are in bounds: r/mask [t0, t0+T), fine_off [t0, t0+T+4)
+    const long long ntma = std::max(0LL, (static_cast<long long>(a.N) + 1 - kCombTile - 4) / kCombTile + 1);
+    int per_sm = 0;
+    HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, combine_tma_kernel<NP>, kCombBlock, kCombSmem));
+    const int grid = static_cast<int>(std::max(1LL, std::min<long long>(ntiles, 1LL * std::max(per_sm, 1) * pl.num_sms)));
+    combine_tma_kernel<NP><<<grid, kCombBlock, kCombSmem, s>>>(a, static_cast<int>(ntiles),
+                                                                static_cast<int>(std::min(ntma, ntiles)));
+    return;
+  }
   combine_prolong_kernel<NP><<<fill_grid(combine_prolong_kernel<NP>, kGatherBlock, a.N), kGatherBlock, 0, s>>>(a);
 }
 
@@ -620,7 +649,7 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
 // graph's kernels need fewer CTA slots next to the concurrent FDM was measured
 // slower at every cap (cfg2: 148 CTAs 4.44, 74 CTAs 4.60 ms per iteration
 // against 4.35 uncapped, profiles/r02_ab_experiments.jsonl A/B 11).
-int coarse_grid(const Plan& pl, long long n, int block = kVecBlock)
+int coarse_grid(const Plan& pl, long long n, int block = kCoarseBlock)
 {
   (void)pl;
   return static_cast<int>(std::max(1LL, std::min((n + block - 1) / block, 148LL * 4)));
@@ -646,15 +675,15 @@ void enqueue_cycle(Plan& pl, int l, const double* r, double* zout, cudaStream_t 
   DevLevel& v = pl.lv[l];
   DevLevel& c = pl.lv[l + 1];
   const int g = coarse_grid(pl, v.n);
-  amg_jacobi2_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, fu.r_copy, fu.x_zero, fu.ks_init);
-  amg_resid_kernel<<<g, kVecBlock, 0, s>>>(v.A, r, v.zA, v.kf);  // kf is free during the cycle
-  amg_agg_sum_kernel<<<coarse_grid(pl, v.nc), kVecBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
+  amg_jacobi2_kernel<<<g, kCoarseBlock, 0, s>>>(v.A, v.dinv, r, v.zA, fu.r_copy, fu.x_zero, fu.ks_init);
+  amg_resid_kernel<<<g, kCoarseBlock, 0, s>>>(v.A, r, v.zA, v.kf);  // kf is free during the cycle
+  amg_agg_sum_kernel<<<coarse_grid(pl, v.nc), kCoarseBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
   enqueue_ksolve(pl, l + 1, c.b, c.x, s);
-  amg_prolong_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
+  amg_prolong_smooth_kernel<<<g, kCoarseBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
   if (fu.dot)
-    amg_smooth_dot_kernel<kVecBlock><<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout, fu.p_copy, *fu.dot);
+    amg_smooth_dot_kernel<kCoarseBlock><<<g, kCoarseBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout, fu.p_copy, *fu.dot);
   else
-    amg_smooth_kernel<<<g, kVecBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout);
+    amg_smooth_kernel<<<g, kCoarseBlock, 0, s>>>(v.A, v.dinv, r, v.zB, zout);
 }
 
 void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
@@ -677,15 +706,15 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
     enqueue_cycle(pl, l, b, v.kz, s, fu);
   }
   for (int it = 0; it < 2; ++it) {
-    amg_spmv_dot_kernel<kVecBlock><<<g, kVecBlock, 0, s>>>(v.A, v.kp, v.kf, cdot_args(pl, &v.ks->pf));
+    amg_spmv_dot_kernel<kCoarseBlock><<<g, kCoarseBlock, 0, s>>>(v.A, v.kp, v.kf, cdot_args(pl, &v.ks->pf));
     // amg.cpp:244-253; the second step reads zr from zr_next (the shift after kdir is folded in)
-    amg_kupdate_kernel<<<g, kVecBlock, 0, s>>>(v.kp, v.kf, x, v.kr, v.n, v.ks, it);
+    amg_kupdate_kernel<<<g, kCoarseBlock, 0, s>>>(v.kp, v.kf, x, v.kr, v.n, v.ks, it);
     if (it == 1) break;
     const DotArgs d1 = cdot_args(pl, &v.ks->zr_next);
     CycleFuse fu;
     fu.dot = &d1;
     enqueue_cycle(pl, l, v.kr, v.kz, s, fu);
-    amg_kdir_kernel<<<g, kVecBlock, 0, s>>>(v.kz, v.kp, v.n, v.ks);
+    amg_kdir_kernel<<<g, kCoarseBlock, 0, s>>>(v.kz, v.kp, v.n, v.ks);
   }
 }
 
@@ -695,19 +724,112 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
 // restrict_warp_kernel launched just before the graph.
 void enqueue_coarse(Plan& pl, cudaStream_t s)
 {
-  vertex_gather_kernel<<<coarse_grid(pl, pl.nv, kGatherBlock), kGatherBlock, 0, s>>>(pl.Rpart, pl.vtx_off, pl.vtx_idx, pl.vmask, pl.R, pl.nv);
+  vertex_gather_kernel<<<coarse_grid(pl, pl.nv), kCoarseBlock, 0, s>>>(pl.Rpart, pl.vtx_off, pl.vtx_idx, pl.vmask, pl.R, pl.nv);
   if (pl.use_amg) {
     enqueue_cycle(pl, 0, pl.R, pl.Z, s);
     // two composed K-cycles: Z = B R + B (R - K_c B R)  (coarse.cpp:193-200)
     const DevCsr K = pl.Kc;
-    amg_resid_kernel<<<coarse_grid(pl, K.n), kVecBlock, 0, s>>>(K, pl.R, pl.Z, pl.rho);
+    amg_resid_kernel<<<coarse_grid(pl, K.n), kCoarseBlock, 0, s>>>(K, pl.R, pl.Z, pl.rho);
     enqueue_cycle(pl, 0, pl.rho, pl.dZ, s);
-    axpy1_kernel<<<coarse_grid(pl, K.n), kVecBlock, 0, s>>>(pl.Z, pl.dZ, K.n);
+    axpy1_kernel<<<coarse_grid(pl, K.n), kCoarseBlock, 0, s>>>(pl.Z, pl.dZ, K.n);
   } else {
     enqueue_dense(pl, pl.R, pl.Z, s);
   }
   launch_prolong(pl, s);
 }
+
+// ---- SM partition for the coarse solve (green contexts) -------------------
+// The driver entry points are resolved through the runtime
+// (cudaGetDriverEntryPointByVersion), so the library does not link libcuda.
+struct GreenApi {
+  CUresult (*dev_get)(CUdevice*, int) = nullptr;
+  CUresult (*get_res)(CUdevice, CUdevResource*, CUdevResourceType) = nullptr;
+  CUresult (*split)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned) = nullptr;
+  CUresult (*gen_desc)(CUdevResourceDesc*, CUdevResource*, unsigned) = nullptr;
+  CUresult (*create)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned) = nullptr;
+  CUresult (*stream)(CUstream*, CUgreenCtx, unsigned, int) = nullptr;
+  CUresult (*destroy)(CUgreenCtx) = nullptr;
+  bool ok = false;
+};
+
+const GreenApi& green_api()
+{
+  static const GreenApi api = [] {
+    GreenApi g;
+    auto sym = [](const char* name, auto& fn) {
+      void* p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPointByVersion(name, &p, CUDART_VERSION, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(p);
+      return fn != nullptr;
+    };
+    g.ok = sym("cuDeviceGet", g.dev_get) && sym("cuDeviceGetDevResource", g.get_res) &&
+           sym("cuDevSmResourceSplitByCount", g.split) && sym("cuDevResourceGenerateDesc", g.gen_desc) &&
+           sym("cuGreenCtxCreate", g.create) && sym("cuGreenCtxStreamCreate", g.stream) &&
+           sym("cuGreenCtxDestroy", g.destroy);
+    cudaGetLastError();
+    return g;
+  }();
+  return api;
+}
+
+// SMs of the coarse partition when hxb_options.coarse_sms is 0
+constexpr int kDefaultCoarseSms = -1;
+
+// Split the device's SMs into a coarse partition of `want` SMs (rounded up to
+// the hardware granularity) and the rest; s_coarse becomes a high-priority
+// stream of the first, s_fine a stream of the second. The coarse graph is
+// captured afterwards on s_coarse, so its replays stay on those SMs. Without
+// driver support the plan keeps one shared SM pool (same results).
+void make_sm_partition(Plan& pl, int want)
+{
+  const GreenApi& G = green_api();
+  if (!G.ok) return;
+  CUdevice dev = 0;
+  CUdevResource all{}, part{}, rest{};
+  unsigned nb = 1;
+  if (G.dev_get(&dev, pl.device) != CUDA_SUCCESS || G.get_res(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
+    return;
+  if (static_cast<unsigned>(want) >= all.sm.smCount ||
+      G.split(&part, &nb, &all, &rest, 0, static_cast<unsigned>(want)) != CUDA_SUCCESS || nb != 1 ||
+      rest.sm.smCount == 0)
+    return;
+  CUdevResourceDesc da = nullptr, db = nullptr;
+  if (G.gen_desc(&da, &part, 1) != CUDA_SUCCESS || G.gen_desc(&db, &rest, 1) != CUDA_SUCCESS) return;
+  CUgreenCtx ga = nullptr, gb = nullptr;
+  if (G.create(&ga, da, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return;
+  if (G.create(&gb, db, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
+    G.destroy(ga);
+    return;
+  }
+  int lo = 0, hi = 0;
+  HXB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  CUstream sa = nullptr, sb = nullptr;
+  if (G.stream(&sa, ga, CU_STREAM_NON_BLOCKING, hi) != CUDA_SUCCESS ||
+      G.stream(&sb, gb, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) {
+    if (sa) cudaStreamDestroy(sa);
+    G.destroy(ga);
+    G.destroy(gb);
+    return;
+  }
+  HXB_CUDA(cudaStreamDestroy(pl.s_coarse));
+  pl.s_coarse = sa;
+  pl.s_fine = sb;
+  pl.g_coarse = ga;
+  pl.g_fine = gb;
+  HXB_CUDA(cudaEventCreateWithFlags(&pl.ev_fine, cudaEventDisableTiming));
+  pl.coarse_sms = static_cast<int>(part.sm.smCount);
+}
+
+}  // namespace
+
+void destroy_green(CUgreenCtx g)
+{
+  if (g && green_api().ok) green_api().destroy(g);
+}
+
+namespace {
 
 void capture_coarse_graph(Plan& pl)
 {
@@ -748,7 +870,14 @@ bool enqueue_precond(Plan& pl, double* zr_result, const PcgUArgs* ua = nullptr)
     }
     pl.launches += pl.coarse_graph_nodes;
     HXB_CUDA(cudaEventRecord(pl.ev_join, pl.s_coarse));
-    HXB_DISPATCH_NP(pl.np, launch_fdm, pl, s);
+    if (pl.s_fine) {  // SM partition: the fine solves on the other green context's SMs
+      HXB_CUDA(cudaStreamWaitEvent(pl.s_fine, pl.ev_fork, 0));
+      HXB_DISPATCH_NP(pl.np, launch_fdm, pl, pl.s_fine);
+      HXB_CUDA(cudaEventRecord(pl.ev_fine, pl.s_fine));
+      HXB_CUDA(cudaStreamWaitEvent(s, pl.ev_fine, 0));
+    } else {
+      HXB_DISPATCH_NP(pl.np, launch_fdm, pl, s);
+    }
     HXB_CUDA(cudaStreamWaitEvent(s, pl.ev_join, 0));
     launch_combine(pl, zr_result, s, true, true);
     return false;
@@ -1399,20 +1528,6 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
                                                         pl.ax_idx);
     HXB_CUDA(cudaGetLastError());
     pl.n_loc_surf = pl.n_grp0 = pl.nsg;
-    if (pl.do_coarse) {
-      std::vector<int> slot_l(nsurf_raw);
-      for (int k = 0; k < pl.np; ++k)
-        for (int j = 0; j < pl.np; ++j)
-          for (int i = 0; i < pl.np; ++i) {
-            const int sl = surface_slot(pl.np, i, j, k);
-            if (sl >= 0) slot_l[sl] = (k * pl.np + j) * pl.np + i;
-          }
-      int* d_slot = pl.mem.upload(slot_l);
-      pl.mass_csr = M.alloc<double>(static_cast<std::size_t>(std::max<long long>(total, 1)));
-      mass_csr_kernel<<<vec_grid(total), kVecBlock>>>(pl.ax_idx, total, pl.mass, pl.nloc, pl.nsurf, d_slot,
-                                                       pl.mass_csr);
-      HXB_CUDA(cudaGetLastError());
-    }
     if (hs.lumped.empty()) {  // lumped mass and 1/m_N from the device masses in CSR order
       std::vector<int> slot_l(nsurf_raw);
       for (int k = 0; k < pl.np; ++k)
@@ -1454,25 +1569,24 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
         idx[smap[static_cast<std::size_t>(e) * 2 * pl.nsurf + pl.nsurf + q]] = e * pl.nsurf + q;
     pl.ax_idx = M.upload(idx);
     pl.n_loc_surf = pl.n_grp0 = pl.nsg;
-    if (pl.do_coarse) {  // mass of every surface copy in Ax-CSR order (streamed by the fused prolongation)
-      std::vector<int> slot_l(nsurf_raw);
-      for (int k = 0; k < pl.np; ++k)
-        for (int j = 0; j < pl.np; ++j)
-          for (int i = 0; i < pl.np; ++i) {
-            const int sl = surface_slot(pl.np, i, j, k);
-            if (sl >= 0) slot_l[sl] = (k * pl.np + j) * pl.np + i;
-          }
-      std::vector<double> mcsr(off[pl.nsg]);
-      for (std::size_t q = 0; q < mcsr.size(); ++q)
-        mcsr[q] = hs.geo.mass[static_cast<std::size_t>(idx[q] / pl.nsurf) * pl.nloc + slot_l[idx[q] % pl.nsurf]];
-      pl.mass_csr = M.upload(mcsr);
-    }
   } else {
     build_dist_ax(pl, hs, nsurf_raw);
   }
   pl.rsurf = M.alloc<double>(static_cast<std::size_t>(pl.ne) * pl.nsurf);
+  if (pl.do_coarse && pl.nranks == 1 && pl.nsg > 0) {  // first copy of every surface node (combine's prolongation)
+    // padded to whole combine tiles (combine_tma_kernel stages a tile's entries at once)
+    const std::size_t padded = (static_cast<std::size_t>(pl.nsg) + kCombTileMax - 1) / kCombTileMax * kCombTileMax;
+    pl.surf_first = M.alloc<int>(padded);
+    HXB_CUDA(cudaMemset(pl.surf_first, 0, sizeof(int) * padded));
+    first_copy_kernel<<<vec_grid(pl.nsg), kVecBlock>>>(pl.ax_off, pl.ax_idx, pl.nsg, pl.surf_first);
+    HXB_CUDA(cudaGetLastError());
+  }
 
   pl.restrict_first = pl.do_fine && pl.do_coarse && pl.nranks == 1 && opt.restrict_in_fdm == 0;
+  if (pl.restrict_first && !pl.group) {
+    const int want = opt.coarse_sms == 0 ? kDefaultCoarseSms : opt.coarse_sms;
+    if (want > 0) make_sm_partition(pl, want);
+  }
   if (const char* o = std::getenv("HXB_FDM_ONE_PER_CTA")) pl.fdm_one_per_cta = std::atoi(o) != 0;
   if (pl.do_coarse) {  // restriction weights m_l / m_N of the surface slots (restriction pass / fused in the FDM)
     std::vector<int> slot_l(nsurf_raw);
@@ -1528,9 +1642,15 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.n_g_from_up = static_cast<int>(d.ghost_from_up.size());
     pl.n_g_to_down = static_cast<int>(d.ghost_to_down.size());
     pl.n_g_to_up = static_cast<int>(d.ghost_to_up.size());
-    pl.pr_off = M.upload(d.pr_off);
-    pl.pr_idx = M.upload(d.pr_idx);
-    pl.pr_mass = M.upload(d.pr_mass);
+    if (pl.n_fin_surf > 0) {  // first copy of every finalised surface node (combine's prolongation)
+      DeviceArena tmp;
+      const unsigned* d_off = tmp.upload(d.pr_off);
+      const int* d_idx = tmp.upload(d.pr_idx);
+      pl.surf_first = M.alloc<int>(pl.n_fin_surf);
+      first_copy_kernel<<<vec_grid(pl.n_fin_surf), kVecBlock>>>(d_off, d_idx, pl.n_fin_surf, pl.surf_first);
+      HXB_CUDA(cudaGetLastError());
+      HXB_CUDA(cudaDeviceSynchronize());
+    }
   } else if (pl.do_fine && !pl.host_lists) {
     // subdomain contributions' (e, slot)-ordered positions by a device sort
     const std::size_t nsub = static_cast<std::size_t>(pl.P) * pl.P * pl.P;
@@ -1542,7 +1662,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     pl.fine_pos = M.alloc<int>(ne * nsub);
     const long long total = device_csr_by_key(keys, static_cast<long long>(ne * nsub), pl.N, pl.fine_off, pl.fine_pos);
     cudaFree(keys);
-    pl.zsort = M.alloc<double>(static_cast<std::size_t>(std::max<long long>(total, 1)));
+    pl.zsort = M.alloc<double>(static_cast<std::size_t>(std::max<long long>(total, 1)) + 2);  // +2: even-rounded tile copies
   } else if (pl.do_fine) {
     const std::size_t nsub = static_cast<std::size_t>(pl.P) * pl.P * pl.P;
     std::vector<unsigned> cnt(static_cast<std::size_t>(pl.N) + 1, 0);
@@ -1562,7 +1682,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
       });
     pl.fine_off = M.upload(cnt);
     pl.fine_pos = M.upload(pos);
-    pl.zsort = M.alloc<double>(cnt[pl.N]);
+    pl.zsort = M.alloc<double>(static_cast<std::size_t>(cnt[pl.N]) + 2);  // +2: even-rounded tile copies
   }
   if (pl.nranks > 1) {
     std::vector<int> nodes_host(pl.n_loc_surf);
@@ -2565,6 +2685,7 @@ int hxb_plan_get_info(const hxb_plan* plan, hxb_plan_info* info)
     fill_amg_info(pl->group ? pl->group->pl[0]->hs : pl->hs, &info->amg_levels, info->amg_rows, info->amg_nnz);
     info->setup_seconds = pl->setup_seconds;
     info->device_bytes = static_cast<int64_t>(pl->mem.bytes);
+    info->coarse_sms = pl->coarse_sms;
     if (pl->group)
       for (const auto& q : pl->group->pl) info->device_bytes += static_cast<int64_t>(q->mem.bytes);
   });

@@ -53,7 +53,7 @@ class _Options(C.Structure):
                 ("variant", C.c_int), ("device", C.c_int), ("bitwise_reference", C.c_int),
                 ("n_gpus", C.c_int), ("devices", C.c_int * 8), ("rank", C.c_int), ("nranks", C.c_int),
                 ("fused_combine", C.c_int), ("fdm_element_order", C.c_int), ("host_lists", C.c_int),
-                ("restrict_in_fdm", C.c_int), ("reserved", C.c_int * 3)]
+                ("restrict_in_fdm", C.c_int), ("coarse_sms", C.c_int), ("reserved", C.c_int * 2)]
 
 
 class _PcgConfig(C.Structure):
@@ -82,7 +82,8 @@ class _PlanInfo(C.Structure):
     _fields_ = [("num_global", C.c_int64), ("num_elements", C.c_int64), ("num_vertices", C.c_int64),
                 ("order", C.c_int32), ("coarse_uses_amg", C.c_int32), ("coarse_n", C.c_int64),
                 ("amg_levels", C.c_int32), ("precond_mode", C.c_int32), ("amg_rows", C.c_int64 * 16),
-                ("amg_nnz", C.c_int64 * 16), ("setup_seconds", C.c_double), ("device_bytes", C.c_int64)]
+                ("amg_nnz", C.c_int64 * 16), ("setup_seconds", C.c_double), ("device_bytes", C.c_int64),
+                ("coarse_sms", C.c_int32), ("pad_", C.c_int32)]
 
 
 # Exported symbols and their signatures (kept in sync with include/hexsem_b200.h).
@@ -335,7 +336,7 @@ class Plan:
                  coarse_solve: str = "automatic", direct_threshold: int = 64000, variant: str = "stored",
                  device: int = 0, rank: int = 0, nranks: int = 1, split_combine: bool = True,
                  host_lists: bool = False, fdm_morton: bool = True, bitwise_reference: bool = False,
-                 devices=None, restrict_in_fdm: bool = False):
+                 devices=None, restrict_in_fdm: bool = False, coarse_sms: int = 0):
         L = lib()
         ne = mesh.num_elements
         self.mesh = mesh
@@ -355,6 +356,7 @@ class Plan:
         opt.fdm_element_order = 0 if fdm_morton else 1
         opt.bitwise_reference = 1 if bitwise_reference else 0
         opt.restrict_in_fdm = 1 if restrict_in_fdm else 0
+        opt.coarse_sms = int(coarse_sms)
         if devices is not None:  # multi-GPU plan: one element slab per entry (a device may repeat)
             if not 1 <= len(devices) <= 8:
                 raise ValueError("devices: 1..8 entries")
@@ -381,6 +383,7 @@ class Plan:
         self.amg_nnz = [int(info.amg_nnz[i]) for i in range(self.amg_levels)]
         self.setup_seconds = float(info.setup_seconds)
         self.device_bytes = int(info.device_bytes)
+        self.coarse_sms = int(info.coarse_sms)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -13,7 +13,7 @@ n = int(sys.argv[2]) if len(sys.argv) > 2 else 7
 opts = {}
 for a in sys.argv[3:]:
     key, val = a.split("=")
-    opts[key] = val.lower() in ("1", "true", "yes")
+    opts[key] = int(val) if key in ("coarse_sms",) else val.lower() in ("1", "true", "yes")
 p = hx.Plan(hx.generate_cube_mesh(k), n, **opts)
 prof = p.profile(5)
 p.pcg_device(None, tol=1e-8, want_u=False)
@@ -24,6 +24,7 @@ for tag in ("ax_elem", "ax_gather", "fdm", "combine", "coarse", "combine_fine"):
     ms, cnt = p.kernel_time(tag)
     live[tag] = ms / max(1, cnt)
 print(json.dumps({"lib": os.environ.get("HXB_LIB", "default"), "opts": opts, "k": k, "n": n,
+                  "coarse_sms": getattr(p, "coarse_sms", None),
                   "iterations": r["iterations"], "solve_ms": r["solve_seconds"] * 1e3,
                   "ms_per_it": r["solve_seconds"] * 1e3 / r["iterations"], "live": live,
                   "profile": {kk: round(v, 4) for kk, v in prof.items() if v}}))
