@@ -37,25 +37,6 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem)
 {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
-// The fine solves run concurrently with the coarse solve, whose hierarchy
-// (~60 MB at cfg2) is re-read by every smoother sweep: the FDM's read-once
-// streams (gather codes, face ids, output positions) and its zsort stores are
-// marked evict-first in L2 so they do not push the coarse matrices out.
-#ifndef FDM_L2_HINTS
-#define FDM_L2_HINTS 1
-#endif
-__device__ __forceinline__ unsigned long long l2_evict_first_policy()
-{
-  unsigned long long pol = 0;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, unsigned long long pol)
-{
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(smem)), "l"(gmem),
-               "l"(pol)
-               : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
@@ -65,12 +46,7 @@ template <bool V16>
 __device__ __forceinline__ void stage_ints(int* dst, const int* src, int n, int tid, int nthreads)
 {
   if constexpr (V16) {
-#if FDM_L2_HINTS
-    const unsigned long long pol = l2_evict_first_policy();
-    for (int q = tid; q < n / 4; q += nthreads) cp_async16_hint(dst + 4 * q, src + 4 * q, pol);
-#else
     for (int q = tid; q < n / 4; q += nthreads) cp_async16(dst + 4 * q, src + 4 * q);
-#endif
   } else {
     for (int q = tid; q < n; q += nthreads) cp_async4(dst + q, src + q);
   }
@@ -432,11 +408,7 @@ __global__ void __launch_bounds__(FdmShapeE<NP, EPB>::kBlock, FdmShapeE<NP, EPB>
     for (int x = 0; x < P; ++x) {
       const int q = ps[x];
       if (q >= 0)
-#if FDM_L2_HINTS
-        __stcs(a.zsort + q, out[x]);  // streamed: the combine reads it once, after the coarse solve
-#else
         a.zsort[q] = out[x];
-#endif
       else if (EPB == 1 && q <= -2)  // finalised by a neighbour rank (distributed plans)
         a.fsend[-2 - q] = out[x];
     }

@@ -53,9 +53,6 @@ namespace {
   } while (0)
 
 constexpr int kVecBlock = 256;
-#ifndef FDM_SMEM_PAD
-#define FDM_SMEM_PAD 0  // A/B: unused dynamic shared memory per FDM CTA (caps FDM residency per SM)
-#endif
 #ifndef COMBINE_TMA
 #define COMBINE_TMA 1  // A/B: 0 = the warp-staged combine_prolong_kernel on single-device plans
 #endif
@@ -523,7 +520,7 @@ void launch_fdm(Plan& pl, cudaStream_t s)
   if (pl.fdm_eo && EPB > 1 && !a.Rpart && !a.fsend && !pl.fdm_one_per_cta)  // several subdomains per CTA
     fdm_kernel<NP, true, EPB><<<(pl.ne + EPB - 1) / EPB, FdmShapeE<NP, EPB>::kBlock, 0, s>>>(a);
   else if (pl.fdm_eo)
-    fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, FDM_SMEM_PAD, s>>>(a);
+    fdm_kernel<NP, true><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
   else
     fdm_kernel<NP, false><<<pl.ne, FdmShape<NP>::kBlock, 0, s>>>(a);
 }

@@ -16,6 +16,7 @@
 #include <cmath>
 
 #include "setup.hpp"
+#include "setup_parallel.hpp"
 
 namespace hxb {
 
@@ -132,7 +133,8 @@ using RefTrip = std::pair<std::pair<gid, gid>, double>;
 
 Csr csr_from_reftrips(gid n, std::vector<RefTrip> trips)
 {
-  std::sort(trips.begin(), trips.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+  // the reference's std::sort (amg.cpp:28), equal keys left in its order (setup_parallel.hpp)
+  std_sort_threads(trips.begin(), trips.end(), [](const RefTrip& a, const RefTrip& b) { return a.first < b.first; });
   Csr m;
   m.n = n;
   m.ptr.assign(static_cast<std::size_t>(n) + 1, 0);
@@ -173,9 +175,12 @@ Csr assemble_coarse_matrix(const HexMesh& mesh, const std::vector<double>& kappa
                            const std::vector<std::uint8_t>& vmask)
 {
   const gid nv = mesh.num_vertices();
-  std::vector<RefTrip> trips;
-  trips.reserve(static_cast<std::size_t>(mesh.num_elements()) * 64);
-  for (gid e = 0; e < mesh.num_elements(); ++e) {
+  const gid ne = mesh.num_elements();
+  // element matrices on host threads (independent), then the triplets in
+  // element order exactly as the reference's single loop appends them
+  std::vector<double> kall(static_cast<std::size_t>(ne) * 64);
+  parallel_for(ne, [&](gid e_begin, gid e_end) {
+  for (gid e = e_begin; e < e_end; ++e) {
     double ke[8][8] = {};
     for (int qb = 0; qb < 8; ++qb) {
       const double xi = (qb & 1) ? 1.0 : -1.0;
@@ -213,12 +218,19 @@ Csr assemble_coarse_matrix(const HexMesh& mesh, const std::vector<double>& kappa
           ke[ab][bb] += mq * s;
         }
     }
+    std::copy(&ke[0][0], &ke[0][0] + 64, kall.begin() + static_cast<std::size_t>(e) * 64);
+  }
+  });
+  std::vector<RefTrip> trips;
+  trips.reserve(static_cast<std::size_t>(ne) * 64);
+  for (gid e = 0; e < ne; ++e) {
+    const double* ke = kall.data() + static_cast<std::size_t>(e) * 64;
     for (int ab = 0; ab < 8; ++ab) {
       const gid ga = mesh.elements[e][hex_corner(ab & 1, (ab >> 1) & 1, (ab >> 2) & 1)];
       for (int bb = 0; bb < 8; ++bb) {
         const gid gb = mesh.elements[e][hex_corner(bb & 1, (bb >> 1) & 1, (bb >> 2) & 1)];
         if (vmask[ga] || vmask[gb]) continue;
-        trips.push_back({{ga, gb}, ke[ab][bb]});
+        trips.push_back({{ga, gb}, ke[ab * 8 + bb]});
       }
     }
   }

@@ -22,6 +22,7 @@
 #include <thread>
 
 #include "setup.hpp"
+#include "setup_parallel.hpp"
 
 namespace hxb {
 
@@ -127,53 +128,6 @@ inline int edge_index(int a, int bit_a1, int bit_a2)
   return a * 4 + bit_a2 * 2 + bit_a1;
 }
 
-template <class F>
-void parallel_for(gid n, F&& f)
-{
-  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  if (n < 4096 || hw == 1) {
-    f(0, n);
-    return;
-  }
-  std::vector<std::thread> pool;
-  const gid chunk = (n + hw - 1) / hw;
-  for (unsigned t = 0; t < hw; ++t) {
-    const gid b = static_cast<gid>(t) * chunk, e = std::min<gid>(n, b + chunk);
-    if (b < e) pool.emplace_back([&f, b, e] { f(b, e); });
-  }
-  for (auto& th : pool) th.join();
-}
-
-// std::sort on host threads: sorted chunks merged pairwise. Used only where
-// the order is total (or equal keys are identical values), so the result is
-// exactly std::sort's.
-template <class T, class C>
-void parallel_sort(std::vector<T>& v, C comp)
-{
-  const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  const std::size_t n = v.size();
-  if (n < (1u << 16) || hw == 1) {
-    std::sort(v.begin(), v.end(), comp);
-    return;
-  }
-  std::vector<std::size_t> cut(hw + 1);
-  for (unsigned t = 0; t <= hw; ++t) cut[t] = n * t / hw;
-  {
-    std::vector<std::thread> pool;
-    for (unsigned t = 0; t < hw; ++t)
-      pool.emplace_back([&, t] { std::sort(v.begin() + cut[t], v.begin() + cut[t + 1], comp); });
-    for (auto& th : pool) th.join();
-  }
-  for (std::size_t w = 1; w < hw; w *= 2) {
-    std::vector<std::thread> pool;
-    for (std::size_t t = 0; t + w < hw; t += 2 * w) {
-      const std::size_t a = cut[t], m = cut[t + w], b = cut[std::min<std::size_t>(hw, t + 2 * w)];
-      pool.emplace_back([&, a, m, b] { std::inplace_merge(v.begin() + a, v.begin() + m, v.begin() + b, comp); });
-    }
-    for (auto& th : pool) th.join();
-  }
-}
-
 }  // namespace
 
 Numbering build_numbering(const HexMesh& mesh, int order)
@@ -197,6 +151,7 @@ Numbering build_numbering(const HexMesh& mesh, int order)
   num.num_vertex_nodes = nvu;
 
   // (1) unique edges ordered by (min id, max id)
+  setup_phase("numbering: edges");
   std::vector<std::uint64_t> edges(static_cast<std::size_t>(ne) * 12);
   parallel_for(ne, [&](gid b, gid en) {
     for (gid e = b; e < en; ++e)
@@ -217,6 +172,7 @@ Numbering build_numbering(const HexMesh& mesh, int order)
   edges.shrink_to_fit();
 
   // (2) unique faces ordered by canonical frame (origin, xn, yn)
+  setup_phase("numbering: faces");
   std::vector<FaceFrame> frames(static_cast<std::size_t>(ne) * 6);
   parallel_for(ne, [&](gid b, gid en) {
     for (gid e = b; e < en; ++e)
@@ -260,6 +216,7 @@ Numbering build_numbering(const HexMesh& mesh, int order)
   num.num_global = static_cast<gid>(total);
 
   // (3) per-element surface slots
+  setup_phase("numbering: surface ids");
   const int nsurf = surface_slot_count(np);
   num.l2g_surf.assign(static_cast<std::size_t>(ne) * nsurf, -1);
   parallel_for(ne, [&](gid b, gid en) {
@@ -307,6 +264,7 @@ Numbering build_numbering(const HexMesh& mesh, int order)
   });
 
   // (4) Dirichlet mask from tagged faces (mesh.cpp:369-383)
+  setup_phase("numbering: dirichlet mask");
   num.dirichlet_mask.assign(num.num_global, 0);
   for (const auto& bf : mesh.boundary_faces) {
     if (bf.tag != 0) continue;
@@ -325,47 +283,47 @@ Numbering build_numbering(const HexMesh& mesh, int order)
   }
 
   // (5) sub_l2g face slots (mesh.cpp:419-450): neighbour's first interior layer
+  setup_phase("numbering: sub_face");
+  // The shared face's canonical frame (step 2) is the same in both elements,
+  // so a face node's coordinates in the neighbour follow from the two frames:
+  // e's (u, v) -> canonical (ss, tt) -> the neighbour's (u2, v2), then one
+  // layer inward. Each mapped face node is checked against the neighbour's
+  // copy of it (same global id).
   const std::size_t fs = static_cast<std::size_t>(np) * np;
   num.sub_face.assign(static_cast<std::size_t>(ne) * 6 * fs, -1);
   parallel_for(ne, [&](gid b, gid en) {
-    std::vector<gid> full(static_cast<std::size_t>(np) * np * np);
-    std::vector<std::pair<gid, int>> nb(fs);
+    auto node_gid = [&](gid el, const int (&ijk)[3]) -> gid {
+      const int sl = surface_slot_of(np, ijk[0], ijk[1], ijk[2]);
+      if (sl >= 0) return num.l2g_surf[static_cast<std::size_t>(el) * nsurf + sl];
+      return static_cast<gid>(num.num_surface_global + static_cast<std::int64_t>(el) * nm1 * nm1 * nm1 +
+                              ((ijk[2] - 1) * nm1 + (ijk[1] - 1)) * nm1 + (ijk[0] - 1));
+    };
     for (gid e = b; e < en; ++e) {
       for (int f = 0; f < 6; ++f) {
         const gid e2 = num.face_nbr_elem[static_cast<std::size_t>(e) * 6 + f];
         if (e2 < 0) continue;
         const int f2 = num.face_nbr_face[static_cast<std::size_t>(e) * 6 + f];
-        element_l2g(num, ne, e2, full.data());
-        const int a2 = f2 / 2, s2 = f2 % 2;
-        // neighbour face nodes: global id -> local index in e2
-        int q = 0;
-        for (int v = 0; v < np; ++v)
-          for (int u = 0; u < np; ++u) {
-            int ijk[3];
-            ijk[a2] = s2 ? n : 0;
-            ijk[(a2 + 1) % 3] = u;
-            ijk[(a2 + 2) % 3] = v;
-            const int l = (ijk[2] * np + ijk[1]) * np + ijk[0];
-            nb[q++] = {full[l], l};
-          }
-        std::sort(nb.begin(), nb.end());
-        const int a = f / 2, s = f % 2;
+        const FaceFrame& fr = frames[static_cast<std::size_t>(e) * 6 + f];
+        const FaceFrame& fr2 = frames[static_cast<std::size_t>(e2) * 6 + f2];
+        const int a = f / 2, s = f % 2, a2 = f2 / 2, s2 = f2 % 2;
         gid* out = num.sub_face.data() + (static_cast<std::size_t>(e) * 6 + f) * fs;
         for (int v = 0; v < np; ++v)
           for (int u = 0; u < np; ++u) {
-            int ijk[3];
+            const int pp = fr.x0 ? n - u : u, qq = fr.y0 ? n - v : v;
+            const int ss = fr.swap ? qq : pp, tt = fr.swap ? pp : qq;
+            const int pp2 = fr2.swap ? tt : ss, qq2 = fr2.swap ? ss : tt;
+            const int u2 = fr2.x0 ? n - pp2 : pp2, v2 = fr2.y0 ? n - qq2 : qq2;
+            int ijk[3], ijk2[3];
             ijk[a] = s ? n : 0;
             ijk[(a + 1) % 3] = u;
             ijk[(a + 2) % 3] = v;
-            const gid g = num.l2g_surf[static_cast<std::size_t>(e) * nsurf +
-                                       surface_slot_of(np, ijk[0], ijk[1], ijk[2])];
-            auto it = std::lower_bound(nb.begin(), nb.end(), std::make_pair(g, -1));
-            if (it == nb.end() || it->first != g)
+            ijk2[a2] = s2 ? n : 0;
+            ijk2[(a2 + 1) % 3] = u2;
+            ijk2[(a2 + 2) % 3] = v2;
+            if (node_gid(e, ijk) != node_gid(e2, ijk2))
               throw HxbError(2, "global node has no copy in expected neighbor element");
-            const int l2 = it->second;
-            int ijk2[3] = {l2 % np, (l2 / np) % np, l2 / (np * np)};
             ijk2[a2] += s2 ? -1 : 1;
-            out[v * np + u] = full[(ijk2[2] * np + ijk2[1]) * np + ijk2[0]];
+            out[v * np + u] = node_gid(e2, ijk2);
           }
       }
     }
