@@ -142,6 +142,32 @@ __global__ void surface_map_kernel(const int* __restrict__ l2g_surf, const int* 
   }
 }
 
+// sub_face rows [e][6 np^2] -> padded [e][nfp], Dirichlet-encoded (-1: no neighbour)
+__global__ void encode_sub_face_kernel(const int* __restrict__ raw, const std::uint8_t* __restrict__ mask, int ne,
+                                       int nf, int nfp, int* __restrict__ enc)
+{
+  const long long n = static_cast<long long>(ne) * nfp;
+  for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+       p += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long e = p / nfp;
+    const int q = static_cast<int>(p % nfp);
+    int v = -1;
+    if (q < nf) {
+      const int g = raw[e * nf + q];
+      v = g < 0 ? -1 : (mask[g] ? encode_dirichlet(g) : g);
+    }
+    enc[p] = v;
+  }
+}
+
+// b[g] = mask ? 0 : m_N * 1 (assemble_load with s = 1, problem.cpp:38-46)
+__global__ void load_ones_kernel(const std::uint8_t* __restrict__ mask, const double* __restrict__ lumped, int n,
+                                 double* __restrict__ b)
+{
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n; g += gridDim.x * blockDim.x)
+    b[g] = mask[g] ? 0.0 : lumped[g] * 1.0;
+}
+
 // Restriction weights of the surface slots, m_l / m_N (coarse.cpp:149, 157):
 // the FDM's fused restriction reads one contiguous row per element instead of
 // the scattered 1/m_N and the mass row (Dirichlet slots weigh 0)

@@ -223,6 +223,7 @@ struct Plan {
   double *Rpart = nullptr, *R = nullptr, *Z = nullptr, *rho = nullptr, *dZ = nullptr;
   double* Zc = nullptr;       // [e][8] coarse corner values for the fused prolongation
   int* surf_first = nullptr;  // first copy of each surface item (combine's prolongation)
+  double* r_alt = nullptr;    // second residual buffer (restriction with the fused r update writes it)
   double* cw = nullptr;       // [e][nsurf] restriction weights m_l / m_N of the surface slots (fused in the FDM)
   std::vector<DevLevel> lv;  // AMG levels 0..L (L = coarsest, uses dense)
   DevDense dense;
@@ -562,7 +563,8 @@ void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine
     }
     const long long ntiles = (static_cast<long long>(a.N) + kCombTile - 1) / kCombTile;
     // tiles whose five ranges are in bounds: r/mask [t0, t0+T), fine_off [t0, t0+T+4)
-    const long long ntma = std::max(0LL, (static_cast<long long>(a.N) + 1 - kCombTile - 4) / kCombTile + 1);
+    const long long span = static_cast<long long>(a.N) + 1 - kCombTile - 4;  // last in-bounds tile start
+    const long long ntma = span < 0 ? 0 : span / kCombTile + 1;
     int per_sm = 0;
     HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, combine_tma_kernel<NP>, kCombBlock, kCombSmem));
     const int grid = static_cast<int>(std::max(1LL, std::min<long long>(ntiles, 1LL * std::max(per_sm, 1) * pl.num_sms)));
@@ -601,8 +603,14 @@ void launch_prolong(Plan& pl, cudaStream_t s)
 }
 
 template <int NP>
-void launch_restrict(Plan& pl, cudaStream_t s)
+void launch_restrict(Plan& pl, cudaStream_t s, const RestrictUpd* up = nullptr)
 {
+  if (up) {  // PCG r update fused in: reads pl.r, writes up->r_out (fixed grid: deterministic norm)
+    const int grid = fill_grid(restrict_cw_kernel<NP, true>, 256, 32LL * pl.ne);
+    restrict_cw_kernel<NP, true><<<grid, 256, 0, s>>>(pl.r, pl.smap, pl.cw, pl.Rpart, pl.ne, 2 * pl.nsurf, pl.nsurf,
+                                                      pl.nsg, pl.fdm_order, *up);
+    return;
+  }
   if (pl.cw) {
     const int grid = fill_grid(restrict_cw_kernel<NP>, 256, 32LL * pl.ne);
     restrict_cw_kernel<NP><<<grid, 256, 0, s>>>(pl.r, pl.smap, pl.cw, pl.Rpart, pl.ne, 2 * pl.nsurf, pl.nsurf, pl.nsg,
@@ -844,7 +852,7 @@ void capture_coarse_graph(Plan& pl)
 // z = P r (reads pl.r, writes pl.z); optional z.r into *zr_result. With ua,
 // the PCG's u += alpha_k p_k runs inside the fine half of the combine (in the
 // shadow of the coarse solve); returns whether it did.
-bool enqueue_precond(Plan& pl, double* zr_result, const PcgUArgs* ua = nullptr)
+bool enqueue_precond(Plan& pl, double* zr_result, const PcgUArgs* ua = nullptr, bool restricted = false)
 {
   cudaStream_t s = pl.s_main;
   if (pl.precond_mode == HXB_PRECOND_NONE) {
@@ -856,8 +864,9 @@ bool enqueue_precond(Plan& pl, double* zr_result, const PcgUArgs* ua = nullptr)
   if (pl.restrict_first) {
     // restriction pass, then the coarse solve (a latency-bound chain on a few
     // SMs, high-priority stream) concurrently with the fine solves; one
-    // combine sums both, applies the mask and forms z.r
-    HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s);
+    // combine sums both, applies the mask and forms z.r. restricted: the PCG
+    // already ran the restriction (fused with its r update)
+    if (!restricted) HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s);
     HXB_CUDA(cudaEventRecord(pl.ev_fork, s));
     HXB_CUDA(cudaStreamWaitEvent(pl.s_coarse, pl.ev_fork, 0));
     pl.launches += 1;
@@ -1538,8 +1547,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
       pl.d_inv_lumped = M.alloc<double>(pl.N);
       HXB_DISPATCH_NP(pl.np, launch_lumped, pl, d_slot);
       HXB_CUDA(cudaGetLastError());
-      hs.lumped.resize(pl.N);  // host copy for the load vector and exports
-      HXB_CUDA(cudaMemcpy(hs.lumped.data(), pl.d_lumped, sizeof(double) * pl.N, cudaMemcpyDeviceToHost));
+      // the host copy (load vector, exports) is made on first use: host_lumped()
     }
     HXB_CUDA(cudaDeviceSynchronize());
     cudaFree(keys);
@@ -1606,13 +1614,17 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
   if (pl.do_fine) {
     const int nf = 6 * pl.np * pl.np, nfp = (nf + 3) & ~3;  // rows padded for 16-byte TMA copies
     pl.sfstride = nfp;
-    std::vector<int> enc(static_cast<std::size_t>(pl.ne) * nfp, -1);
-    for (int le = 0; le < pl.ne; ++le)
-      for (int q = 0; q < nf; ++q) {
-        const gid g = num.sub_face[static_cast<std::size_t>(pl.e0 + le) * nf + q];
-        enc[static_cast<std::size_t>(le) * nfp + q] = g < 0 ? -1 : (num.dirichlet_mask[g] ? encode_dirichlet(g) : g);
-      }
-    pl.sub_face = M.upload(enc);
+    // raw rows uploaded, Dirichlet-encoded and padded on the device
+    DeviceArena tmp;
+    const std::size_t nrow = static_cast<std::size_t>(pl.ne) * nf;
+    int* raw = tmp.alloc<int>(nrow);
+    HXB_CUDA(cudaMemcpy(raw, num.sub_face.data() + static_cast<std::size_t>(pl.e0) * nf, sizeof(int) * nrow,
+                        cudaMemcpyHostToDevice));
+    pl.sub_face = M.alloc<int>(static_cast<std::size_t>(pl.ne) * nfp);
+    encode_sub_face_kernel<<<vec_grid(static_cast<long long>(pl.ne) * nfp), kVecBlock>>>(raw, pl.mask, pl.ne, nf, nfp,
+                                                                                       pl.sub_face);
+    HXB_CUDA(cudaGetLastError());
+    HXB_CUDA(cudaDeviceSynchronize());
   }
   if (pl.do_fine && pl.nranks > 1) {
     const DistLists dl = dist_partition(hs, pl.rank, pl.nranks, pl.nsurf);
@@ -1798,6 +1810,10 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
 
   setup_phase("vectors + graph");
   // PCG vectors and reduction scratch
+  if (pl.restrict_first) {
+    pl.r_alt = M.alloc<double>(pl.N);
+    HXB_CUDA(cudaMemset(pl.r_alt, 0, sizeof(double) * pl.N));
+  }
   for (double** v : {&pl.u, &pl.r, &pl.z, &pl.p, &pl.f, &pl.b}) {
     *v = M.alloc<double>(pl.N);
     HXB_CUDA(cudaMemset(*v, 0, sizeof(double) * pl.N));
@@ -1874,10 +1890,26 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
     copy_dot_kernel<kVecBlock><<<fill_grid(copy_dot_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(pl.z, pl.r, pl.p, n, dot_args(pl, pl.zr_hist));
     pl.launches += 1;
     status = HXB_PCG_MAX_ITERATIONS;
+    // restriction-first schedule: the r update and its norm run inside the
+    // restriction pass (restrict_cw_kernel<NP, true>), which then starts the
+    // next preconditioner application; r alternates between two buffers
+    const bool fused_update = pl.restrict_first && pl.r_alt && pl.surf_first;
     for (int k = 0; k < cfg.max_iterations; ++k) {
       enqueue_ax(pl, pl.p, pl.f, pl.pf_hist + k, s);
-      pcg_update_kernel<kVecBlock><<<fill_grid(pcg_update_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(pl.f, pl.r, n, pl.zr_hist, pl.pf_hist, k,
-                                                                     dot_args(pl, pl.res2));
+      if (fused_update) {
+        RestrictUpd up;
+        up.f = pl.f;
+        up.r_out = pl.r_alt;
+        up.surf_first = pl.surf_first;
+        up.zr = pl.zr_hist;
+        up.pf = pl.pf_hist;
+        up.k = k;
+        up.nrm = dot_args(pl, pl.res2);
+        HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s, &up);
+      } else {
+        pcg_update_kernel<kVecBlock><<<fill_grid(pcg_update_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(
+            pl.f, pl.r, n, pl.zr_hist, pl.pf_hist, k, dot_args(pl, pl.res2));
+      }
       sqrt_store_kernel<<<1, 1, 0, s>>>(pl.res2, pl.res_hist + k + 1);
       pl.launches += 2;
       HXB_CUDA(cudaMemcpyAsync(pl.h_status, pl.pf_hist + k, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1912,7 +1944,8 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
       ua.zr = pl.zr_hist;
       ua.pf = pl.pf_hist;
       ua.k = k;
-      if (enqueue_precond(pl, pl.zr_hist + k + 1, &ua))
+      if (fused_update) std::swap(pl.r, pl.r_alt);  // the updated residual
+      if (enqueue_precond(pl, pl.zr_hist + k + 1, &ua, fused_update))
         pcg_dir_p_kernel<<<fill_grid(pcg_dir_p_kernel, kVecBlock, n), kVecBlock, 0, s>>>(pl.z, pl.p, n, pl.zr_hist, k);
       else
         pcg_dir_kernel<<<fill_grid(pcg_dir_kernel, kVecBlock, n), kVecBlock, 0, s>>>(pl.z, pl.p, pl.u, n, pl.zr_hist,
@@ -2141,6 +2174,21 @@ void destroy_group(Group* g) { delete g; }
 
 // the host setup behind a plan (a multi-GPU handle's ranks share rank 0's)
 const HostSetup& plan_hs(Plan* pl) { return pl->group ? pl->group->pl[0]->hs : pl->hs; }
+
+// host copy of the lumped mass: single-device plans assemble it on the device
+// and copy it back on first use (3 GB at cfg5, not needed by a device solve)
+const std::vector<double>& host_lumped(Plan* pl)
+{
+  if (pl->group) return pl->group->pl[0]->hs.lumped;
+  HostSetup& hs = pl->hs;
+  if (hs.lumped.empty() && pl->N > 0) {
+    if (!pl->d_lumped) throw HxbError(HXB_EINVAL, "plan has no lumped mass");
+    HXB_CUDA(cudaSetDevice(pl->device));
+    hs.lumped.resize(pl->N);
+    HXB_CUDA(cudaMemcpy(hs.lumped.data(), pl->d_lumped, sizeof(double) * pl->N, cudaMemcpyDeviceToHost));
+  }
+  return hs.lumped;
+}
 
 namespace {
 
@@ -2964,11 +3012,12 @@ static void solve_dispatch(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* 
   if (res->u) HXB_CUDA(cudaMemcpy(res->u, pl.cx.u, sizeof(double) * pl.N, cudaMemcpyDeviceToHost));
 }
 
+// b = assemble_load(s = 1) (problem.cpp:38-46): m_N * 1 off the Dirichlet nodes, on the device
 static void fill_default_b(Plan& pl)
 {
-  std::vector<double> b(pl.N);
-  for (int g = 0; g < pl.N; ++g) b[g] = pl.hs.num.dirichlet_mask[g] ? 0.0 : pl.hs.lumped[g] * 1.0;
-  HXB_CUDA(cudaMemcpy(pl.b, b.data(), sizeof(double) * pl.N, cudaMemcpyHostToDevice));
+  load_ones_kernel<<<vec_grid(pl.N), kVecBlock, 0, pl.s_main>>>(pl.mask, pl.d_lumped, pl.N, pl.b);
+  HXB_CUDA(cudaGetLastError());
+  HXB_CUDA(cudaStreamSynchronize(pl.s_main));
 }
 
 int hxb_solve(hxb_plan* plan, const double* b, const hxb_pcg_config* cfg, hxb_pcg_result* res)
@@ -3066,7 +3115,8 @@ int hxb_solve_heat(hxb_plan* plan, const hxb_heat_config* hc, const hxb_pcg_conf
     const double r2 = hc->source_radius * hc->source_radius;
     const double total_time = hc->dt * hc->steps;
     double mass_total = 0;
-    for (int g = 0; g < n; ++g) mass_total += P.hs.lumped[g];
+    const std::vector<double>& lumped = host_lumped(&P);
+    for (int g = 0; g < n; ++g) mass_total += lumped[g];
     if (!P.heat_u) P.heat_u = P.mem.alloc<double>(n);
     {
       std::vector<double> u0(n);
@@ -3121,7 +3171,8 @@ int hxb_load_ones(hxb_plan* plan, double* b)
   return guarded([&] {
     Plan* pl = as_plan(plan);
     const HostSetup& hs = plan_hs(pl);
-    for (int g = 0; g < pl->N; ++g) b[g] = hs.num.dirichlet_mask[g] ? 0.0 : hs.lumped[g] * 1.0;
+    const std::vector<double>& lumped = host_lumped(pl);
+    for (int g = 0; g < pl->N; ++g) b[g] = hs.num.dirichlet_mask[g] ? 0.0 : lumped[g] * 1.0;
   });
 }
 
@@ -3129,7 +3180,7 @@ int hxb_lumped_mass(hxb_plan* plan, double* m)
 {
   return guarded([&] {
     Plan* pl = as_plan(plan);
-    std::memcpy(m, plan_hs(pl).lumped.data(), sizeof(double) * pl->N);
+    std::memcpy(m, host_lumped(pl).data(), sizeof(double) * pl->N);
   });
 }
 
