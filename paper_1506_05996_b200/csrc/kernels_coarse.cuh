@@ -125,33 +125,15 @@ __global__ void __launch_bounds__(256) restrict_warp_kernel(const double* __rest
 // reference's l-loop at rounding level only). Measured against the line-per-
 // lane traversal it replaced (strided interior loads, 35 % of HBM): see
 // DESIGN.md section 7.
-// The PCG's r update fused into the restriction (UPD): r_new = r - alpha f is
-// formed for every node the warp reads (the same expression as
-// pcg_update_kernel, so every reader sees the same value), each node's owner
-// (its element for interior nodes, its first copy for surface nodes) stores
-// it into the other r buffer and adds r_new^2 to the norm, reduced in a fixed
-// order. The restriction then reads the updated residual without a separate
-// pass over r and f.
-struct RestrictUpd {
-  const double* f = nullptr;
-  double* r_out = nullptr;
-  const int* surf_first = nullptr;  // first copy e*nsurfp + slot of every surface node
-  const double* zr = nullptr;
-  const double* pf = nullptr;
-  int k = 0;
-  DotArgs nrm;
-};
-
-template <int NP, bool UPD = false>
+template <int NP>
 __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __restrict__ r, const int* __restrict__ smap,
                                                           const double* __restrict__ cw, double* __restrict__ Rpart,
                                                           int ne, int sstride, int nsurfp, int nsg,
-                                                          const int* __restrict__ order, RestrictUpd up = {})
+                                                          const int* __restrict__ order)
 {
   constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2);
-  constexpr int US = UPD ? 3 : (NP == 7 ? 3 : 4);  // loads in flight per lane (NP = 7 spills at 4)
+  constexpr int US = NP == 7 ? 3 : 4;  // loads in flight per lane (NP = 7 spills at 4)
   __shared__ double h0[NP], h1[NP];
-  __shared__ double red[UPD ? 8 : 1];
   if (threadIdx.x < NP) {
     h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
     h1[threadIdx.x] = c_tab[NP].hat1[threadIdx.x];
@@ -159,12 +141,6 @@ __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __res
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  double alpha = 0.0;
-  if constexpr (UPD) {
-    const double pfk = up.pf[up.k];
-    alpha = pfk > 0 ? up.zr[up.k] / pfk : 0.0;  // breakdown: r unchanged (pcg_update_kernel)
-  }
-  double nrm = 0.0;
   auto spread = [&](double (&acc)[8], int i, int j, int k, double w) {
     const double a0 = h0[i] * w, a1 = h1[i] * w;
     const double c00 = h0[j] * h0[k], c10 = h1[j] * h0[k], c01 = h0[j] * h1[k], c11 = h1[j] * h1[k];
@@ -196,29 +172,8 @@ __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __res
         code[u] = s < NS ? __ldg(surf + s) : -1;
         wt[u] = s < NS ? __ldg(we + s) : 0.0;
       }
-      if constexpr (UPD) {
-        int g[US];
-        double fv[US];
 #pragma unroll
-        for (int u = 0; u < US; ++u) {
-          g[u] = code[u] >= 0 ? code[u] : (code[u] <= -2 ? -code[u] - 2 : -1);
-          v[u] = g[u] >= 0 ? __ldg(r + g[u]) : 0.0;
-          fv[u] = g[u] >= 0 ? __ldg(up.f + g[u]) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < US; ++u) {
-          const int s = s0 + 32 * u + lane;
-          const double rn = v[u] - alpha * fv[u];
-          if (g[u] >= 0 && __ldg(up.surf_first + g[u]) == e * nsurfp + s) {
-            up.r_out[g[u]] = rn;
-            nrm += rn * rn;
-          }
-          v[u] = code[u] >= 0 ? rn : 0.0;  // Dirichlet: masked (precond.cpp:35)
-        }
-      } else {
-#pragma unroll
-        for (int u = 0; u < US; ++u) v[u] = code[u] >= 0 ? __ldg(r + code[u]) : 0.0;  // Dirichlet: masked (precond.cpp:35)
-      }
+      for (int u = 0; u < US; ++u) v[u] = code[u] >= 0 ? __ldg(r + code[u]) : 0.0;  // Dirichlet: masked (precond.cpp:35)
 #pragma unroll
       for (int u = 0; u < US; ++u) {
         const int s = s0 + 32 * u + lane;
@@ -236,23 +191,12 @@ __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __res
 #pragma unroll
         for (int u = 0; u < US; ++u) {
           const int t = t0 + 32 * u + lane;
-          if constexpr (UPD) {
-            const long long gi = (long long)nsg + (long long)e * NI + t;
-            v[u] = t < NI ? __ldg(r + gi) - alpha * __ldg(up.f + gi) : 0.0;
-          } else {
-            v[u] = t < NI ? __ldg(ri + t) : 0.0;
-          }
+          v[u] = t < NI ? __ldg(ri + t) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < US; ++u) {
           const int t = t0 + 32 * u + lane;
-          if (t < NI) {
-            if constexpr (UPD) {
-              up.r_out[(long long)nsg + (long long)e * NI + t] = v[u];
-              nrm += v[u] * v[u];
-            }
-            spread(acc, 1 + t % (n - 1), 1 + (t / (n - 1)) % (n - 1), 1 + t / ((n - 1) * (n - 1)), v[u]);
-          }
+          if (t < NI) spread(acc, 1 + t % (n - 1), 1 + (t / (n - 1)) % (n - 1), 1 + t / ((n - 1) * (n - 1)), v[u]);
         }
       }
     }
@@ -267,7 +211,6 @@ __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __res
       Rpart[8 * (long long)e + lane] = v;
     }
   }
-  if constexpr (UPD) dot_commit<256>(up.nrm, nrm, red);
 }
 
 // Zc[8e + cb] = Z[vertex of corner cb of e] (the 8 coarse values each element

@@ -223,7 +223,6 @@ struct Plan {
   double *Rpart = nullptr, *R = nullptr, *Z = nullptr, *rho = nullptr, *dZ = nullptr;
   double* Zc = nullptr;       // [e][8] coarse corner values for the fused prolongation
   int* surf_first = nullptr;  // first copy of each surface item (combine's prolongation)
-  double* r_alt = nullptr;    // second residual buffer (restriction with the fused r update writes it)
   double* cw = nullptr;       // [e][nsurf] restriction weights m_l / m_N of the surface slots (fused in the FDM)
   std::vector<DevLevel> lv;  // AMG levels 0..L (L = coarsest, uses dense)
   DevDense dense;
@@ -603,14 +602,8 @@ void launch_prolong(Plan& pl, cudaStream_t s)
 }
 
 template <int NP>
-void launch_restrict(Plan& pl, cudaStream_t s, const RestrictUpd* up = nullptr)
+void launch_restrict(Plan& pl, cudaStream_t s)
 {
-  if (up) {  // PCG r update fused in: reads pl.r, writes up->r_out (fixed grid: deterministic norm)
-    const int grid = fill_grid(restrict_cw_kernel<NP, true>, 256, 32LL * pl.ne);
-    restrict_cw_kernel<NP, true><<<grid, 256, 0, s>>>(pl.r, pl.smap, pl.cw, pl.Rpart, pl.ne, 2 * pl.nsurf, pl.nsurf,
-                                                      pl.nsg, pl.fdm_order, *up);
-    return;
-  }
   if (pl.cw) {
     const int grid = fill_grid(restrict_cw_kernel<NP>, 256, 32LL * pl.ne);
     restrict_cw_kernel<NP><<<grid, 256, 0, s>>>(pl.r, pl.smap, pl.cw, pl.Rpart, pl.ne, 2 * pl.nsurf, pl.nsurf, pl.nsg,
@@ -852,7 +845,7 @@ void capture_coarse_graph(Plan& pl)
 // z = P r (reads pl.r, writes pl.z); optional z.r into *zr_result. With ua,
 // the PCG's u += alpha_k p_k runs inside the fine half of the combine (in the
 // shadow of the coarse solve); returns whether it did.
-bool enqueue_precond(Plan& pl, double* zr_result, const PcgUArgs* ua = nullptr, bool restricted = false)
+bool enqueue_precond(Plan& pl, double* zr_result, const PcgUArgs* ua = nullptr)
 {
   cudaStream_t s = pl.s_main;
   if (pl.precond_mode == HXB_PRECOND_NONE) {
@@ -864,9 +857,8 @@ bool enqueue_precond(Plan& pl, double* zr_result, const PcgUArgs* ua = nullptr, 
   if (pl.restrict_first) {
     // restriction pass, then the coarse solve (a latency-bound chain on a few
     // SMs, high-priority stream) concurrently with the fine solves; one
-    // combine sums both, applies the mask and forms z.r. restricted: the PCG
-    // already ran the restriction (fused with its r update)
-    if (!restricted) HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s);
+    // combine sums both, applies the mask and forms z.r
+    HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s);
     HXB_CUDA(cudaEventRecord(pl.ev_fork, s));
     HXB_CUDA(cudaStreamWaitEvent(pl.s_coarse, pl.ev_fork, 0));
     pl.launches += 1;
@@ -1810,10 +1802,6 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
 
   setup_phase("vectors + graph");
   // PCG vectors and reduction scratch
-  if (pl.restrict_first) {
-    pl.r_alt = M.alloc<double>(pl.N);
-    HXB_CUDA(cudaMemset(pl.r_alt, 0, sizeof(double) * pl.N));
-  }
   for (double** v : {&pl.u, &pl.r, &pl.z, &pl.p, &pl.f, &pl.b}) {
     *v = M.alloc<double>(pl.N);
     HXB_CUDA(cudaMemset(*v, 0, sizeof(double) * pl.N));
@@ -1890,26 +1878,10 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
     copy_dot_kernel<kVecBlock><<<fill_grid(copy_dot_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(pl.z, pl.r, pl.p, n, dot_args(pl, pl.zr_hist));
     pl.launches += 1;
     status = HXB_PCG_MAX_ITERATIONS;
-    // restriction-first schedule: the r update and its norm run inside the
-    // restriction pass (restrict_cw_kernel<NP, true>), which then starts the
-    // next preconditioner application; r alternates between two buffers
-    const bool fused_update = pl.restrict_first && pl.r_alt && pl.surf_first;
     for (int k = 0; k < cfg.max_iterations; ++k) {
       enqueue_ax(pl, pl.p, pl.f, pl.pf_hist + k, s);
-      if (fused_update) {
-        RestrictUpd up;
-        up.f = pl.f;
-        up.r_out = pl.r_alt;
-        up.surf_first = pl.surf_first;
-        up.zr = pl.zr_hist;
-        up.pf = pl.pf_hist;
-        up.k = k;
-        up.nrm = dot_args(pl, pl.res2);
-        HXB_DISPATCH_NP(pl.np, launch_restrict, pl, s, &up);
-      } else {
-        pcg_update_kernel<kVecBlock><<<fill_grid(pcg_update_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(
-            pl.f, pl.r, n, pl.zr_hist, pl.pf_hist, k, dot_args(pl, pl.res2));
-      }
+      pcg_update_kernel<kVecBlock><<<fill_grid(pcg_update_kernel<kVecBlock>, kVecBlock, n), kVecBlock, 0, s>>>(
+          pl.f, pl.r, n, pl.zr_hist, pl.pf_hist, k, dot_args(pl, pl.res2));
       sqrt_store_kernel<<<1, 1, 0, s>>>(pl.res2, pl.res_hist + k + 1);
       pl.launches += 2;
       HXB_CUDA(cudaMemcpyAsync(pl.h_status, pl.pf_hist + k, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1944,8 +1916,7 @@ void run_pcg(Plan& pl, const hxb_pcg_config& cfg, hxb_pcg_result* res)
       ua.zr = pl.zr_hist;
       ua.pf = pl.pf_hist;
       ua.k = k;
-      if (fused_update) std::swap(pl.r, pl.r_alt);  // the updated residual
-      if (enqueue_precond(pl, pl.zr_hist + k + 1, &ua, fused_update))
+      if (enqueue_precond(pl, pl.zr_hist + k + 1, &ua))
         pcg_dir_p_kernel<<<fill_grid(pcg_dir_p_kernel, kVecBlock, n), kVecBlock, 0, s>>>(pl.z, pl.p, n, pl.zr_hist, k);
       else
         pcg_dir_kernel<<<fill_grid(pcg_dir_kernel, kVecBlock, n), kVecBlock, 0, s>>>(pl.z, pl.p, pl.u, n, pl.zr_hist,

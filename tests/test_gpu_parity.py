@@ -459,4 +459,13 @@ def test_tiny_meshes_default_load(k, order, family):
     assert a["status"] == e["status"] == "converged"
     assert np.array_equal(a["residual_history"], e["residual_history"])
     theirs = ref.pcg(b, tol=1e-8)
-    history_parity(a, theirs, tol=1e-10)
+    # order 9 on 8 elements amplifies rounding past 1e-10 r_0: judged against
+    # the problem's own floor (helpers.reference_noise), as every such case
+    from helpers import reference_noise
+
+    tol = max(1e-10, 2 * reference_noise(theirs, b, RefConfig(k=k, order=order, family=family)))
+    dr = history_parity(a, theirs, tol=tol)
+    record_parity(f"tiny_default_load[k={k},n={order},{family}]", dr, tol)
+    with hx.Plan(hx.generate_cube_mesh(k, family), order, bitwise_reference=True) as bw:
+        same = bw.pcg(None, tol=1e-8)
+    assert np.array_equal(same["residual_history"], theirs["residual_history"])
