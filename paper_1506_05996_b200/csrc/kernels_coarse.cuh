@@ -291,6 +291,38 @@ __global__ void amg_agg_sum_kernel(const double* __restrict__ rho, const int* __
   }
 }
 
+// rc[c] = sum over the members i of aggregate c, in member order, of
+// (r - A z)_i: the residual (amg.cpp:218-219) and its restriction to the
+// aggregates (amg.cpp:221-222, members in ascending order) in one pass. Eight lanes per aggregate compute
+// member rows in parallel (csr_row_dot, as amg_resid_kernel) and the group
+// sums them in member order by shuffles, so rc is bitwise the two-kernel
+// result without the residual vector's round trip or its launch.
+__global__ void amg_resid_agg_kernel(DevCsr A, const double* __restrict__ r, const double* __restrict__ z,
+                                     const int* __restrict__ agg_ptr, const int* __restrict__ agg_mem,
+                                     double* __restrict__ rc, int nc)
+{
+  constexpr int G = 8;
+  const int lane = threadIdx.x & 31, sub = lane & (G - 1);
+  const unsigned gmask = 0xffu << (lane & ~(G - 1));
+  const int groups = (gridDim.x * blockDim.x) / G;
+  // a group's lanes share c and the member count, so its shuffles are uniform
+  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) / G; c < nc; c += groups) {
+    const int p0 = __ldg(agg_ptr + c), p1 = __ldg(agg_ptr + c + 1);
+    double s = 0.0;
+    for (int q0 = p0; q0 < p1; q0 += G) {
+      const int q = q0 + sub;
+      double rho = 0.0;
+      if (q < p1) {
+        const int i = __ldg(agg_mem + q);
+        rho = __ldg(r + i) - csr_row_dot(A, i, z);
+      }
+      const int cnt = min(G, p1 - q0);
+      for (int j = 0; j < cnt; ++j) s += __shfl_sync(gmask, rho, j, G);
+    }
+    if (sub == 0) rc[c] = s;
+  }
+}
+
 // zout = z3 + w d (r - A z3), z3 = zin + ec[agg] on the fly (amg.cpp:220-222)
 __global__ void amg_prolong_smooth_kernel(DevCsr A, const double* __restrict__ dinv, const double* __restrict__ r,
                                           const double* __restrict__ zin, const double* __restrict__ ec,

@@ -674,8 +674,8 @@ void enqueue_cycle(Plan& pl, int l, const double* r, double* zout, cudaStream_t 
   DevLevel& c = pl.lv[l + 1];
   const int g = coarse_grid(pl, v.n);
   amg_jacobi2_kernel<<<g, kCoarseBlock, 0, s>>>(v.A, v.dinv, r, v.zA, fu.r_copy, fu.x_zero, fu.ks_init);
-  amg_resid_kernel<<<g, kCoarseBlock, 0, s>>>(v.A, r, v.zA, v.kf);  // kf is free during the cycle
-  amg_agg_sum_kernel<<<coarse_grid(pl, v.nc), kCoarseBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
+  amg_resid_agg_kernel<<<coarse_grid(pl, 8LL * v.nc), kCoarseBlock, 0, s>>>(v.A, r, v.zA, v.agg_ptr, v.agg_mem, c.b,
+                                                                            v.nc);
   enqueue_ksolve(pl, l + 1, c.b, c.x, s);
   amg_prolong_smooth_kernel<<<g, kCoarseBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
   if (fu.dot)

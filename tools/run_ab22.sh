@@ -1,0 +1,11 @@
+mkdir -p gpurun_out
+rm -f gpurun_out/ab22.jsonl
+for lib in paper_1506_05996_b200/ab/prevcoarse/libhexsem_b200.so ""; do
+  for kn in "52 7" "90 3" "54 5"; do
+    HXB_LIB=$lib timeout 300 python tools/ab_run.py $kn >> gpurun_out/ab22.jsonl 2>>gpurun_out/ab22.err
+  done
+done
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:fdm_kernel|combine_tma|restrict_cw" -c 3 -o gpurun_out/prof_precond2 -f \
+  python tools/prof_driver.py 52 7 > gpurun_out/ncu_precond.log 2>&1; echo "rc=$?" >> gpurun_out/ncu_precond.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_group.py -q -m gpu -p no:cacheprovider > gpurun_out/tests22.log 2>&1
+echo "tests rc=$?" >> gpurun_out/tests22.log
