@@ -291,38 +291,6 @@ __global__ void amg_agg_sum_kernel(const double* __restrict__ rho, const int* __
   }
 }
 
-// rc[c] = sum over the members i of aggregate c, in member order, of
-// (r - A z)_i: the residual (amg.cpp:218-219) and its restriction to the
-// aggregates (amg.cpp:221-222, members in ascending order) in one pass. Eight lanes per aggregate compute
-// member rows in parallel (csr_row_dot, as amg_resid_kernel) and the group
-// sums them in member order by shuffles, so rc is bitwise the two-kernel
-// result without the residual vector's round trip or its launch.
-__global__ void amg_resid_agg_kernel(DevCsr A, const double* __restrict__ r, const double* __restrict__ z,
-                                     const int* __restrict__ agg_ptr, const int* __restrict__ agg_mem,
-                                     double* __restrict__ rc, int nc)
-{
-  constexpr int G = 8;
-  const int lane = threadIdx.x & 31, sub = lane & (G - 1);
-  const unsigned gmask = 0xffu << (lane & ~(G - 1));
-  const int groups = (gridDim.x * blockDim.x) / G;
-  // a group's lanes share c and the member count, so its shuffles are uniform
-  for (int c = (blockIdx.x * blockDim.x + threadIdx.x) / G; c < nc; c += groups) {
-    const int p0 = __ldg(agg_ptr + c), p1 = __ldg(agg_ptr + c + 1);
-    double s = 0.0;
-    for (int q0 = p0; q0 < p1; q0 += G) {
-      const int q = q0 + sub;
-      double rho = 0.0;
-      if (q < p1) {
-        const int i = __ldg(agg_mem + q);
-        rho = __ldg(r + i) - csr_row_dot(A, i, z);
-      }
-      const int cnt = min(G, p1 - q0);
-      for (int j = 0; j < cnt; ++j) s += __shfl_sync(gmask, rho, j, G);
-    }
-    if (sub == 0) rc[c] = s;
-  }
-}
-
 // zout = z3 + w d (r - A z3), z3 = zin + ec[agg] on the fly (amg.cpp:220-222)
 __global__ void amg_prolong_smooth_kernel(DevCsr A, const double* __restrict__ dinv, const double* __restrict__ r,
                                           const double* __restrict__ zin, const double* __restrict__ ec,
@@ -382,6 +350,31 @@ __global__ void __launch_bounds__(BLOCK) amg_spmv_dot_kernel(DevCsr A, const dou
     const double fi = csr_row_dot(A, i, p);
     f[i] = fi;
     s += p[i] * fi;
+  }
+  dot_commit<BLOCK>(d, s, red);
+}
+
+// The K-solve's second step: p_new = z + beta p (amg.cpp:256-260, beta =
+// zr_next / zr; p unchanged once the solve stopped) formed on the fly for
+// every row the SpMV reads, f = A p_new, p_new.f: amg_kdir_kernel and
+// amg_spmv_dot_kernel in one pass (p_new goes to a second buffer, since
+// other rows still read the old p).
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) amg_spmv_dir_dot_kernel(DevCsr A, const double* __restrict__ z,
+                                                                const double* __restrict__ p, double* __restrict__ pn,
+                                                                double* __restrict__ f, const KScalars* ks, DotArgs d)
+{
+  __shared__ double red[BLOCK / 32];
+  const bool stop = ks->stopped;
+  const double beta = stop ? 0.0 : ks->zr_next / ks->zr;
+  auto pv = [&](int c) { return stop ? __ldg(p + c) : __ldg(z + c) + beta * __ldg(p + c); };
+  double s = 0.0;
+  for (int i = blockIdx.x * BLOCK + threadIdx.x; i < A.n; i += gridDim.x * BLOCK) {
+    const double fi = csr_row_sum(A.ptr, A.col, A.val, i, pv);
+    const double pi = pv(i);
+    pn[i] = pi;
+    f[i] = fi;
+    s += pi * fi;
   }
   dot_commit<BLOCK>(d, s, red);
 }

@@ -129,6 +129,7 @@ struct DevLevel {
   int* agg_ptr = nullptr;
   int* agg_mem = nullptr;
   double *zA = nullptr, *zB = nullptr, *kr = nullptr, *kz = nullptr, *kp = nullptr, *kf = nullptr;
+  double* kp2 = nullptr;              // the K-solve's second direction (formed inside its SpMV)
   double *b = nullptr, *x = nullptr;  // rc/ec targets from the finer level's cycle
   KScalars* ks = nullptr;
 };
@@ -674,8 +675,8 @@ void enqueue_cycle(Plan& pl, int l, const double* r, double* zout, cudaStream_t 
   DevLevel& c = pl.lv[l + 1];
   const int g = coarse_grid(pl, v.n);
   amg_jacobi2_kernel<<<g, kCoarseBlock, 0, s>>>(v.A, v.dinv, r, v.zA, fu.r_copy, fu.x_zero, fu.ks_init);
-  amg_resid_agg_kernel<<<coarse_grid(pl, 8LL * v.nc), kCoarseBlock, 0, s>>>(v.A, r, v.zA, v.agg_ptr, v.agg_mem, c.b,
-                                                                            v.nc);
+  amg_resid_kernel<<<g, kCoarseBlock, 0, s>>>(v.A, r, v.zA, v.kf);  // kf is free during the cycle
+  amg_agg_sum_kernel<<<coarse_grid(pl, v.nc), kCoarseBlock, 0, s>>>(v.kf, v.agg_ptr, v.agg_mem, c.b, v.nc);
   enqueue_ksolve(pl, l + 1, c.b, c.x, s);
   amg_prolong_smooth_kernel<<<g, kCoarseBlock, 0, s>>>(v.A, v.dinv, r, v.zA, c.x, v.agg, v.zB);
   if (fu.dot)
@@ -704,15 +705,19 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
     enqueue_cycle(pl, l, b, v.kz, s, fu);
   }
   for (int it = 0; it < 2; ++it) {
-    amg_spmv_dot_kernel<kCoarseBlock><<<g, kCoarseBlock, 0, s>>>(v.A, v.kp, v.kf, cdot_args(pl, &v.ks->pf));
-    // amg.cpp:244-253; the second step reads zr from zr_next (the shift after kdir is folded in)
-    amg_kupdate_kernel<<<g, kCoarseBlock, 0, s>>>(v.kp, v.kf, x, v.kr, v.n, v.ks, it);
+    // amg.cpp:244-253; the second step's direction p = z + beta p (amg.cpp:256-260)
+    // is formed inside its SpMV (into kp2) and its zr read from zr_next
+    if (it == 0)
+      amg_spmv_dot_kernel<kCoarseBlock><<<g, kCoarseBlock, 0, s>>>(v.A, v.kp, v.kf, cdot_args(pl, &v.ks->pf));
+    else
+      amg_spmv_dir_dot_kernel<kCoarseBlock><<<g, kCoarseBlock, 0, s>>>(v.A, v.kz, v.kp, v.kp2, v.kf, v.ks,
+                                                                       cdot_args(pl, &v.ks->pf));
+    amg_kupdate_kernel<<<g, kCoarseBlock, 0, s>>>(it == 0 ? v.kp : v.kp2, v.kf, x, v.kr, v.n, v.ks, it);
     if (it == 1) break;
     const DotArgs d1 = cdot_args(pl, &v.ks->zr_next);
     CycleFuse fu;
     fu.dot = &d1;
     enqueue_cycle(pl, l, v.kr, v.kz, s, fu);
-    amg_kdir_kernel<<<g, kCoarseBlock, 0, s>>>(v.kz, v.kp, v.n, v.ks);
   }
 }
 
@@ -1780,7 +1785,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
         for (int i = 0; i < v.n; ++i) amem[cur2[h.aggregate[i]]++] = i;
         v.agg_ptr = M.upload(aptr);
         v.agg_mem = M.upload(amem);
-        for (double** b : {&v.zA, &v.zB, &v.kr, &v.kz, &v.kp, &v.kf}) *b = M.alloc<double>(v.n);
+        for (double** b : {&v.zA, &v.zB, &v.kr, &v.kz, &v.kp, &v.kf, &v.kp2}) *b = M.alloc<double>(v.n);
         v.ks = M.alloc<KScalars>(1);
       }
       pl.lv[L].n = amg.coarsest.n;
