@@ -354,31 +354,6 @@ __global__ void __launch_bounds__(BLOCK) amg_spmv_dot_kernel(DevCsr A, const dou
   dot_commit<BLOCK>(d, s, red);
 }
 
-// The K-solve's second step: p_new = z + beta p (amg.cpp:256-260, beta =
-// zr_next / zr; p unchanged once the solve stopped) formed on the fly for
-// every row the SpMV reads, f = A p_new, p_new.f: amg_kdir_kernel and
-// amg_spmv_dot_kernel in one pass (p_new goes to a second buffer, since
-// other rows still read the old p).
-template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) amg_spmv_dir_dot_kernel(DevCsr A, const double* __restrict__ z,
-                                                                const double* __restrict__ p, double* __restrict__ pn,
-                                                                double* __restrict__ f, const KScalars* ks, DotArgs d)
-{
-  __shared__ double red[BLOCK / 32];
-  const bool stop = ks->stopped;
-  const double beta = stop ? 0.0 : ks->zr_next / ks->zr;
-  auto pv = [&](int c) { return stop ? __ldg(p + c) : __ldg(z + c) + beta * __ldg(p + c); };
-  double s = 0.0;
-  for (int i = blockIdx.x * BLOCK + threadIdx.x; i < A.n; i += gridDim.x * BLOCK) {
-    const double fi = csr_row_sum(A.ptr, A.col, A.val, i, pv);
-    const double pi = pv(i);
-    pn[i] = pi;
-    f[i] = fi;
-    s += pi * fi;
-  }
-  dot_commit<BLOCK>(d, s, red);
-}
-
 // if (!(pf > 0) || !(|zr| > 0)) stop; else x += a p, r -= a f  (amg.cpp:244-253).
 // zr_is_next: the second step reads zr from zr_next (the value the separate
 // shift kernel used to copy into zr after amg_kdir_kernel)

@@ -160,6 +160,35 @@ __global__ void encode_sub_face_kernel(const int* __restrict__ raw, const std::u
   }
 }
 
+__global__ void iota_kernel(int* __restrict__ v, int n)
+{
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) v[t] = t;
+}
+// cnt[t'] = copies of node perm[t'] (cnt[n] = 0 for the exclusive scan)
+__global__ void perm_counts_kernel(const unsigned* __restrict__ off, const int* __restrict__ perm, int n,
+                                   unsigned* __restrict__ cnt)
+{
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= n; t += gridDim.x * blockDim.x) {
+    if (t == n) {
+      cnt[t] = 0;
+    } else {
+      const int g = perm[t];
+      cnt[t] = off[g + 1] - off[g];
+    }
+  }
+}
+// idx2 segments in permuted node order
+__global__ void perm_segments_kernel(const unsigned* __restrict__ off, const int* __restrict__ idx,
+                                     const int* __restrict__ perm, const unsigned* __restrict__ off2, int n,
+                                     int* __restrict__ idx2)
+{
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int g = perm[t];
+    const unsigned a = off[g], b = off[g + 1], d = off2[t];
+    for (unsigned q = a; q < b; ++q) idx2[d + (q - a)] = idx[q];
+  }
+}
+
 // b[g] = mask ? 0 : m_N * 1 (assemble_load with s = 1, problem.cpp:38-46)
 __global__ void load_ones_kernel(const std::uint8_t* __restrict__ mask, const double* __restrict__ lumped, int n,
                                  double* __restrict__ b)

@@ -56,6 +56,9 @@ constexpr int kVecBlock = 256;
 #ifndef COMBINE_TMA
 #define COMBINE_TMA 1  // A/B: 0 = the warp-staged combine_prolong_kernel on single-device plans
 #endif
+#ifndef GATHER_FIRST_COPY_ORDER
+#define GATHER_FIRST_COPY_ORDER 1  // A/B: 0 = the Ax gather walks surface nodes in global-id order
+#endif
 #ifndef COARSE_BLOCK
 #define COARSE_BLOCK 256
 #endif
@@ -129,7 +132,6 @@ struct DevLevel {
   int* agg_ptr = nullptr;
   int* agg_mem = nullptr;
   double *zA = nullptr, *zB = nullptr, *kr = nullptr, *kz = nullptr, *kp = nullptr, *kf = nullptr;
-  double* kp2 = nullptr;              // the K-solve's second direction (formed inside its SpMV)
   double *b = nullptr, *x = nullptr;  // rc/ec targets from the finer level's cycle
   KScalars* ks = nullptr;
 };
@@ -250,6 +252,11 @@ struct Plan {
   int rank = 0, nranks = 1;
   int e0 = 0;                 // first owned element (global id); pl.ne counts owned elements
   int* ax_nodes = nullptr;    // local surface node -> global id (null: identity)
+  // the Ax gather's own order (single-device plans): surface nodes sorted by
+  // their first copy (e, slot), with the CSR permuted to match
+  unsigned* gx_off = nullptr;
+  int* gx_idx = nullptr;
+  int* gx_nodes = nullptr;
   int n_loc_surf = 0;         // local surface nodes = [group0 | up | down]
   int n_grp0 = 0, n_up = 0, n_down = 0;
   int sfstride = 0;           // sub_face row stride (ints)
@@ -487,6 +494,11 @@ void enqueue_ax(Plan& pl, const double* u, double* r, double* dot_result, cudaSt
   g.r = r;
   g.num_surface_global = pl.nranks > 1 ? pl.n_grp0 : pl.nsg;  // distributed: interface nodes go through dist_*
   g.nodes = pl.ax_nodes;
+  if (pl.gx_off) {  // first-copy order: rsurf rows are read while they are still in L2
+    g.off = pl.gx_off;
+    g.idx = pl.gx_idx;
+    g.nodes = pl.gx_nodes;
+  }
   g.dot = d2;
   {
     KtScope kt(pl, HXB_KT_AX_GATHER, s);
@@ -705,19 +717,15 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
     enqueue_cycle(pl, l, b, v.kz, s, fu);
   }
   for (int it = 0; it < 2; ++it) {
-    // amg.cpp:244-253; the second step's direction p = z + beta p (amg.cpp:256-260)
-    // is formed inside its SpMV (into kp2) and its zr read from zr_next
-    if (it == 0)
-      amg_spmv_dot_kernel<kCoarseBlock><<<g, kCoarseBlock, 0, s>>>(v.A, v.kp, v.kf, cdot_args(pl, &v.ks->pf));
-    else
-      amg_spmv_dir_dot_kernel<kCoarseBlock><<<g, kCoarseBlock, 0, s>>>(v.A, v.kz, v.kp, v.kp2, v.kf, v.ks,
-                                                                       cdot_args(pl, &v.ks->pf));
-    amg_kupdate_kernel<<<g, kCoarseBlock, 0, s>>>(it == 0 ? v.kp : v.kp2, v.kf, x, v.kr, v.n, v.ks, it);
+    amg_spmv_dot_kernel<kCoarseBlock><<<g, kCoarseBlock, 0, s>>>(v.A, v.kp, v.kf, cdot_args(pl, &v.ks->pf));
+    // amg.cpp:244-253; the second step reads zr from zr_next (the shift after kdir is folded in)
+    amg_kupdate_kernel<<<g, kCoarseBlock, 0, s>>>(v.kp, v.kf, x, v.kr, v.n, v.ks, it);
     if (it == 1) break;
     const DotArgs d1 = cdot_args(pl, &v.ks->zr_next);
     CycleFuse fu;
     fu.dot = &d1;
     enqueue_cycle(pl, l, v.kr, v.kz, s, fu);
+    amg_kdir_kernel<<<g, kCoarseBlock, 0, s>>>(v.kz, v.kp, v.n, v.ks);
   }
 }
 
@@ -1296,6 +1304,41 @@ long long device_csr_by_key(const int* d_keys, long long n, int nkeys, unsigned*
   return total;
 }
 
+// Ax gather order for single-device plans: surface nodes sorted by their
+// first copy e*nsurf + slot (unique keys), the CSR rebuilt in that order. The
+// gather then walks rsurf element by element (first copies contiguous, the
+// other copies in neighbours handled a few rows later), instead of in
+// global-id order, which revisits each rsurf sector from several faces after
+// it may have left L2. Each node's own sum keeps its (e, l) order, so r is
+// unchanged bit for bit; only the fused p.Ap's summation order moves.
+void build_gather_order(Plan& pl)
+{
+  const int n = pl.nsg;
+  DeviceArena tmp;
+  int* key = tmp.alloc<int>(n);
+  int* key2 = tmp.alloc<int>(n);
+  int* val = tmp.alloc<int>(n);
+  unsigned* cnt = tmp.alloc<unsigned>(static_cast<std::size_t>(n) + 1);
+  pl.gx_nodes = pl.mem.alloc<int>(n);
+  first_copy_kernel<<<vec_grid(n), kVecBlock>>>(pl.ax_off, pl.ax_idx, n, key);
+  iota_kernel<<<vec_grid(n), kVecBlock>>>(val, n);
+  int bits = 1;
+  const long long maxkey = static_cast<long long>(pl.ne) * pl.nsurf;
+  while ((1LL << bits) <= maxkey) ++bits;
+  std::size_t b1 = 0, b2 = 0;
+  HXB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b1, key, key2, val, pl.gx_nodes, n, 0, bits));
+  pl.gx_off = pl.mem.alloc<unsigned>(static_cast<std::size_t>(n) + 1);
+  HXB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b2, cnt, pl.gx_off, n + 1));
+  void* work = tmp.alloc<unsigned char>(std::max<std::size_t>({b1, b2, 1}));
+  HXB_CUDA(cub::DeviceRadixSort::SortPairs(work, b1, key, key2, val, pl.gx_nodes, n, 0, bits));
+  perm_counts_kernel<<<vec_grid(n), kVecBlock>>>(pl.ax_off, pl.gx_nodes, n, cnt);
+  HXB_CUDA(cub::DeviceScan::ExclusiveSum(work, b2, cnt, pl.gx_off, n + 1));
+  pl.gx_idx = pl.mem.alloc<int>(std::max<std::size_t>(pl.n_ax_entries, 1));
+  perm_segments_kernel<<<vec_grid(n), kVecBlock>>>(pl.ax_off, pl.ax_idx, pl.gx_nodes, pl.gx_off, n, pl.gx_idx);
+  HXB_CUDA(cudaGetLastError());
+  HXB_CUDA(cudaDeviceSynchronize());
+}
+
 template <int NP>
 void launch_lumped(Plan& pl, const int* d_slot)
 {
@@ -1583,6 +1626,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
     first_copy_kernel<<<vec_grid(pl.nsg), kVecBlock>>>(pl.ax_off, pl.ax_idx, pl.nsg, pl.surf_first);
     HXB_CUDA(cudaGetLastError());
   }
+  if (GATHER_FIRST_COPY_ORDER && pl.nranks == 1 && pl.nsg > 0) build_gather_order(pl);
 
   pl.restrict_first = pl.do_fine && pl.do_coarse && pl.nranks == 1 && opt.restrict_in_fdm == 0;
   if (pl.restrict_first && !pl.group) {
@@ -1785,7 +1829,7 @@ void build_plan(Plan& pl, const hxb_mesh* m, int order, const double* kappa_e, c
         for (int i = 0; i < v.n; ++i) amem[cur2[h.aggregate[i]]++] = i;
         v.agg_ptr = M.upload(aptr);
         v.agg_mem = M.upload(amem);
-        for (double** b : {&v.zA, &v.zB, &v.kr, &v.kz, &v.kp, &v.kf, &v.kp2}) *b = M.alloc<double>(v.n);
+        for (double** b : {&v.zA, &v.zB, &v.kr, &v.kz, &v.kp, &v.kf}) *b = M.alloc<double>(v.n);
         v.ks = M.alloc<KScalars>(1);
       }
       pl.lv[L].n = amg.coarsest.n;
