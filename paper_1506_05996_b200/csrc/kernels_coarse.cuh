@@ -134,14 +134,25 @@ __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __res
   constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2);
   constexpr int US = NP == 7 ? 3 : 4;  // loads in flight per lane (NP = 7 spills at 4)
   __shared__ double h0[NP], h1[NP];
+  // local (i, j, k) of every surface slot and element-interior index, packed i | j << 4 | k << 8
+  __shared__ unsigned short lut_surf[NS], lut_int[NI > 0 ? NI : 1];
   if (threadIdx.x < NP) {
     h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
     h1[threadIdx.x] = c_tab[NP].hat1[threadIdx.x];
   }
+  for (int q = threadIdx.x; q < NS; q += blockDim.x) {
+    int i, j, k;
+    surface_ijk<NP>(q, i, j, k);
+    lut_surf[q] = static_cast<unsigned short>(i | (j << 4) | (k << 8));
+  }
+  for (int q = threadIdx.x; q < NI; q += blockDim.x)
+    lut_int[q] = static_cast<unsigned short>((1 + q % (n - 1)) | ((1 + (q / (n - 1)) % (n - 1)) << 4) |
+                                             ((1 + q / ((n - 1) * (n - 1))) << 8));
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
-  auto spread = [&](double (&acc)[8], int i, int j, int k, double w) {
+  auto spread = [&](double (&acc)[8], unsigned ijk, double w) {
+    const int i = ijk & 15, j = (ijk >> 4) & 15, k = ijk >> 8;
     const double a0 = h0[i] * w, a1 = h1[i] * w;
     const double c00 = h0[j] * h0[k], c10 = h1[j] * h0[k], c01 = h0[j] * h1[k], c11 = h1[j] * h1[k];
     acc[0] += c00 * a0;
@@ -177,11 +188,7 @@ __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __res
 #pragma unroll
       for (int u = 0; u < US; ++u) {
         const int s = s0 + 32 * u + lane;
-        if (s < NS) {
-          int i, j, k;
-          surface_ijk<NP>(s, i, j, k);
-          spread(acc, i, j, k, v[u] * wt[u]);
-        }
+        if (s < NS) spread(acc, lut_surf[s], v[u] * wt[u]);
       }
     }
     if constexpr (NI > 0) {
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __res
 #pragma unroll
         for (int u = 0; u < US; ++u) {
           const int t = t0 + 32 * u + lane;
-          if (t < NI) spread(acc, 1 + t % (n - 1), 1 + (t / (n - 1)) % (n - 1), 1 + t / ((n - 1) * (n - 1)), v[u]);
+          if (t < NI) spread(acc, lut_int[t], v[u]);
         }
       }
     }
