@@ -469,3 +469,20 @@ def test_tiny_meshes_default_load(k, order, family):
     with hx.Plan(hx.generate_cube_mesh(k, family), order, bitwise_reference=True) as bw:
         same = bw.pcg(None, tol=1e-8)
     assert np.array_equal(same["residual_history"], theirs["residual_history"])
+
+
+def test_sm_partition_is_bitwise_neutral():
+    """hxb_options.coarse_sms: the coarse solve on its own green-context SM
+    partition, the fine solves on the rest. Same kernels, grids and
+    reduction trees, so P and the whole PCG are bitwise the shared-SM plan's."""
+    mesh = hx.generate_cube_mesh(12)
+    shared = hx.Plan(mesh, 5, coarse_sms=-1)
+    split = hx.Plan(mesh, 5, coarse_sms=24)
+    assert shared.coarse_sms == 0
+    assert split.coarse_sms in (0, 24)  # 0: the driver offers no green contexts (shared SMs, same results)
+    r = splitmix_vector(shared.N, 17)
+    assert np.array_equal(split.apply_P(r), shared.apply_P(r))
+    a, b = shared.pcg(None, tol=1e-10), split.pcg(None, tol=1e-10)
+    assert a["iterations"] == b["iterations"]
+    assert np.array_equal(a["residual_history"], b["residual_history"])
+    assert np.array_equal(a["u"], b["u"])
