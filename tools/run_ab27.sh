@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+rm -f gpurun_out/ab27.jsonl
+for lib in paper_1506_05996_b200/ab/nocompact/libhexsem_b200.so ""; do
+  for kn in "52 7" "90 3" "54 5" "27 10" "68 4"; do
+    HXB_LIB=$lib timeout 300 python tools/ab_run.py $kn >> gpurun_out/ab27.jsonl 2>>gpurun_out/ab27.err
+  done
+done
+timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/tests27.log 2>&1
+echo "tests rc=$?" >> gpurun_out/tests27.log
