@@ -1,5 +1,5 @@
 // Coarse two-scale component on the device:
-//   restrict_kernel + vertex_gather_kernel   CoarsePreconditioner::restrict_residual
+//   restrict_cw_kernel + vertex_gather_kernel CoarsePreconditioner::restrict_residual
 //                                            (coarse.cpp:138-162) + R[mask]=0 (:191-192)
 //   AMG K-cycle kernels                      AmgHierarchy cycle/ksolve (amg.cpp:198-263)
 //   dense_solve_kernel                       coarsest / direct solve (Eigen LLT in the
@@ -15,102 +15,7 @@ constexpr double kJacobiOmega = 2.0 / 3.0;  // amg.cpp:44
 
 // Restriction, warp per element (restrict_residual, coarse.cpp:138-162, on
 // the masked residual, precond.cpp:35): R_cb(e) = sum_l B[cb][l] y_l m_l with
-// y = r / m_N. B is the tensor product of the two linear hats, so the sum is
-// done separably: each lane owns (j,k) lines, forms the two hat-weighted
-// line sums W_a = sum_i hat_a(t_i) y_i m_i, spreads them over the 8 corners
-// with hat_b(t_j) hat_c(t_k), and the warp reduces the 8 partials in a fixed
-// tree (deterministic; summation order differs from the reference's l-loop
-// at rounding level only). Rpart[8e + cb] feeds vertex_gather_kernel.
-template <int NP>
-__global__ void __launch_bounds__(256) restrict_warp_kernel(const double* __restrict__ r,
-                                                            const double* __restrict__ lumped,
-                                                            const int* __restrict__ smap,
-                                                            const double* __restrict__ mass,
-                                                            double* __restrict__ Rpart, int ne, int sstride, int nsg)
-{
-  constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NL = NP * NP, LPL = (NL + 31) / 32;
-  constexpr int CH = LPL < 2 ? LPL : 2;  // LPL is 1, 2 or 4
-  __shared__ double h0[NP], h1[NP];
-  if (threadIdx.x < NP) {
-    h0[threadIdx.x] = c_tab[NP].hat0[threadIdx.x];
-    h1[threadIdx.x] = c_tab[NP].hat1[threadIdx.x];
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int warps = (gridDim.x * blockDim.x) >> 5;
-  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < ne; e += warps) {
-    const int* surf = smap + (long long)e * sstride;
-    const long long ibase = (long long)nsg + (long long)e * NI;
-    const double* me = mass + (std::size_t)e * NP * NP * NP;
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    // lines in chunks of CH per lane: ids first, then every load of the chunk,
-    // then arithmetic (memory-level parallelism without spilling at large NP)
-#pragma unroll 1
-    for (int q0 = 0; q0 < LPL; q0 += CH) {
-      long long gid[CH][NP];
-#pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        const int line = lane + 32 * (q0 + q);
-        const int j = (line < NL ? line : 0) % NP, k = (line < NL ? line : 0) / NP;
-        const bool face = (j == 0 || j == n || k == 0 || k == n);
-#pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          if (line >= NL) {
-            gid[q][i] = -1;
-          } else if (face || i == 0 || i == n) {
-            const int code = __ldg(surf + surface_slot(NP, i, j, k));
-            gid[q][i] = code >= 0 ? code : -1;  // Dirichlet: masked residual (precond.cpp:35)
-          } else {
-            gid[q][i] = ibase + ((k - 1) * (n - 1) + (j - 1)) * (n - 1) + (i - 1);
-          }
-        }
-      }
-      double rv[CH][NP], lv[CH][NP], mv[CH][NP];
-#pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        const int line = lane + 32 * (q0 + q);
-#pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          const long long g = gid[q][i] < 0 ? 0 : gid[q][i];
-          rv[q][i] = __ldg(r + g);
-          lv[q][i] = __ldg(lumped + g);
-          mv[q][i] = line < NL ? __ldg(me + line * NP + i) : 0.0;
-        }
-      }
-      // line sums W_a = sum_i hat_a(t_i) (r/m_N)_i m_i, spread to the corners
-#pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        const int line = lane + 32 * (q0 + q);
-        const int j = (line < NL ? line : 0) % NP, k = (line < NL ? line : 0) / NP;
-        double w0 = 0.0, w1 = 0.0;
-#pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          const double y = gid[q][i] < 0 ? 0.0 : rv[q][i] / lv[q][i];  // coarse.cpp:144
-          const double w = y * mv[q][i];
-          w0 += h0[i] * w;
-          w1 += h1[i] * w;
-        }
-        if (line < NL) {
-          const double hj[2] = {h0[j], h1[j]}, hk[2] = {h0[k], h1[k]};
-#pragma unroll
-          for (int cb = 0; cb < 8; ++cb) acc[cb] += (hj[(cb >> 1) & 1] * hk[cb >> 2]) * ((cb & 1) ? w1 : w0);
-        }
-      }
-    }
-#pragma unroll
-    for (int cb = 0; cb < 8; ++cb)
-      for (int o = 16; o > 0; o >>= 1) acc[cb] += __shfl_xor_sync(0xffffffffu, acc[cb], o);
-    if (lane < 8) {
-      double v = acc[0];
-#pragma unroll
-      for (int cb = 1; cb < 8; ++cb)
-        if (lane == cb) v = acc[cb];
-      Rpart[8 * (long long)e + lane] = v;
-    }
-  }
-}
-
-// The same restriction with precomputed surface-slot weights cw = m_l / m_N
+// y = r / m_N, using precomputed surface-slot weights cw = m_l / m_N
 // (restrict_weights_kernel): w_l = r_l cw_l on surface slots, w_l = r_l on
 // element-interior nodes (one copy: m_N = m_l). No mass or 1/m_N loads, so it
 // runs as a cheap standalone pass before the FDM and the coarse solve can

@@ -617,15 +617,10 @@ void launch_prolong(Plan& pl, cudaStream_t s)
 template <int NP>
 void launch_restrict(Plan& pl, cudaStream_t s)
 {
-  if (pl.cw) {
-    const int grid = fill_grid(restrict_cw_kernel<NP>, 256, 32LL * pl.ne);
-    restrict_cw_kernel<NP><<<grid, 256, 0, s>>>(pl.r, pl.smap, pl.cw, pl.Rpart, pl.ne, 2 * pl.nsurf, pl.nsurf, pl.nsg,
-                                                pl.fdm_order);
-    return;
-  }
-  const int grid = fill_grid(restrict_warp_kernel<NP>, 256, 32LL * pl.ne);
-  restrict_warp_kernel<NP><<<grid, 256, 0, s>>>(pl.r, pl.d_lumped, pl.smap, pl.mass, pl.Rpart, pl.ne, 2 * pl.nsurf,
-                                               pl.nsg);
+  if (!pl.cw) throw HxbError(HXB_EINVAL, "restriction weights missing (plan without a coarse branch)");
+  const int grid = fill_grid(restrict_cw_kernel<NP>, 256, 32LL * pl.ne);
+  restrict_cw_kernel<NP><<<grid, 256, 0, s>>>(pl.r, pl.smap, pl.cw, pl.Rpart, pl.ne, 2 * pl.nsurf, pl.nsurf, pl.nsg,
+                                              pl.fdm_order);
 }
 
 // ---- AMG enqueue (captured into the coarse graph) --------------------------
@@ -729,10 +724,9 @@ void enqueue_ksolve(Plan& pl, int l, const double* b, double* x, cudaStream_t s)
   }
 }
 
-// restrict -> mask -> coarse solve; leaves Z (coarse.cpp:188-206)
 // Rpart -> R -> coarse solve -> Zc (coarse.cpp:188-206). Rpart comes from
-// the FDM kernel (fused restriction) or, without a fine branch, from
-// restrict_warp_kernel launched just before the graph.
+// restrict_cw_kernel launched just before the graph (or, with
+// restrict_in_fdm, from the FDM kernel's fused restriction).
 void enqueue_coarse(Plan& pl, cudaStream_t s)
 {
   vertex_gather_kernel<<<coarse_grid(pl, pl.nv), kCoarseBlock, 0, s>>>(pl.Rpart, pl.vtx_off, pl.vtx_idx, pl.vmask, pl.R, pl.nv);
