@@ -65,6 +65,25 @@ struct FdmLayout {  // (row stride S, plane stride PS) per pencil size
 #ifndef FDM_MIN_BLOCKS
 #define FDM_MIN_BLOCKS 8
 #endif
+// resident CTAs per SM the register budget is sized for, per order: the high
+// orders spill at 8 (P = 12: 48 registers + 88 B stack, P = 13: 40 + 168 B).
+// Measured alone at cfg4 sizes (profiles/r02_ab_experiments.jsonl, A/B 29):
+// n=8 (NP=9) 8: 0.451, 7: 0.441 ms; n=9 (NP=10) 8: 0.841, 7: 0.755, 6: 0.743,
+// 5: 0.722 ms; n=10 (NP=11) 8: 0.597, 6: 0.439, 5: 0.398, 4: 0.407 ms.
+#ifndef FDM_MB9
+#define FDM_MB9 7
+#endif
+#ifndef FDM_MB10
+#define FDM_MB10 5
+#endif
+#ifndef FDM_MB11
+#define FDM_MB11 5
+#endif
+template <int NP>
+constexpr int fdm_min_blocks()
+{
+  return NP == 9 ? FDM_MB9 : NP == 10 ? FDM_MB10 : NP == 11 ? FDM_MB11 : FDM_MIN_BLOCKS;
+}
 template <int NP>
 struct FdmShape {
   static constexpr int kP = NP + 2;
@@ -73,7 +92,7 @@ struct FdmShape {
   static constexpr int kS = FdmLayout<kP>::S;
   static constexpr int kPS = FdmLayout<kP>::PS;
   static constexpr int kBuf = kP * kPS;
-  static constexpr int kMinBlocks = FDM_MIN_BLOCKS;  // resident CTAs per SM the register budget is sized for
+  static constexpr int kMinBlocks = fdm_min_blocks<NP>();  // resident CTAs per SM the register budget is sized for
 };
 
 struct FdmArgs {
@@ -185,7 +204,7 @@ struct FdmShapeE {
   static constexpr int kLines = (NP + 2) * (NP + 2);
   static constexpr int kBlock = ((EPB * kLines + 31) / 32) * 32;
   static constexpr int kMinBlocks =
-      EPB == 1 ? FDM_MIN_BLOCKS : ((FDM_MIN_BLOCKS * 128) / kBlock > 0 ? (FDM_MIN_BLOCKS * 128) / kBlock : 1);
+      EPB == 1 ? fdm_min_blocks<NP>() : ((FDM_MIN_BLOCKS * 128) / kBlock > 0 ? (FDM_MIN_BLOCKS * 128) / kBlock : 1);
 };
 
 template <int NP, bool EO, int EPB = 1>
