@@ -1079,18 +1079,28 @@ void nd_to_device(Plan& pl, DevDense& d, const NdFactor& F)
   for (double** v : {&D.y, &D.z, &D.t, &D.x}) *v = M.alloc<double>(std::max(1, F.n));
   D.acc = M.alloc<double>(std::max<long long>(1, nrows));
   d.nd_factor_bytes = static_cast<std::int64_t>(sizeof(double)) * 2 * (nlinv + nl21);
-  // per-level task lists (blocks of kNdRowsPerTask rows)
+  // per-level task lists: blocks of kNdRowsPerTask rows, or of 8 rows (one
+  // per warp) on the levels near the root, whose few large supernodes would
+  // otherwise run on a few dozen CTAs (measured at 27^3, n=10: the root-side
+  // backward updates took 35-42 us each on 21-45 CTAs)
   d.nd_levels = F.levels;
+  std::vector<long long> lv_m(F.levels, 0), lv_r(F.levels, 0);
+  for (int s = 0; s < ns; ++s) {
+    lv_m[F.sn[s].level] += mm[s];
+    lv_r[F.sn[s].level] += rr[s];
+  }
+  auto block_rows = [&](long long rows) { return rows / kNdRowsPerTask >= 2LL * pl.num_sms ? kNdRowsPerTask : 8; };
   std::vector<std::vector<NdTask>> fd(F.levels), fu(F.levels), bu(F.levels), bd(F.levels);
   for (int s = 0; s < ns; ++s) {
     const int lv = F.sn[s].level;
-    for (int r0 = 0; r0 < mm[s]; r0 += kNdRowsPerTask) {
-      const NdTask t{s, r0, std::min(kNdRowsPerTask, mm[s] - r0)};
+    const int bm = block_rows(lv_m[lv]), br = block_rows(lv_r[lv]);
+    for (int r0 = 0; r0 < mm[s]; r0 += bm) {
+      const NdTask t{s, r0, std::min(bm, mm[s] - r0)};
       fd[lv].push_back(t);
       bu[lv].push_back(t);
       bd[lv].push_back(t);
     }
-    for (int r0 = 0; r0 < rr[s]; r0 += kNdRowsPerTask) fu[lv].push_back(NdTask{s, r0, std::min(kNdRowsPerTask, rr[s] - r0)});
+    for (int r0 = 0; r0 < rr[s]; r0 += br) fu[lv].push_back(NdTask{s, r0, std::min(br, rr[s] - r0)});
   }
   auto up = [&](const std::vector<std::vector<NdTask>>& v, std::vector<std::pair<NdTask*, int>>& out) {
     out.clear();
