@@ -59,6 +59,9 @@ constexpr int kVecBlock = 256;
 #ifndef GATHER_FIRST_COPY_ORDER
 #define GATHER_FIRST_COPY_ORDER 1  // A/B: 0 = the Ax gather walks surface nodes in global-id order
 #endif
+#ifndef ND_SPLIT_CTAS_PER_SM
+#define ND_SPLIT_CTAS_PER_SM 2  // ND levels with fewer 32-row blocks than this many per SM use 8-row blocks
+#endif
 #ifndef COARSE_BLOCK
 #define COARSE_BLOCK 256
 #endif
@@ -1089,7 +1092,9 @@ void nd_to_device(Plan& pl, DevDense& d, const NdFactor& F)
     lv_m[F.sn[s].level] += mm[s];
     lv_r[F.sn[s].level] += rr[s];
   }
-  auto block_rows = [&](long long rows) { return rows / kNdRowsPerTask >= 2LL * pl.num_sms ? kNdRowsPerTask : 8; };
+  auto block_rows = [&](long long rows) {
+    return rows / kNdRowsPerTask >= static_cast<long long>(ND_SPLIT_CTAS_PER_SM) * pl.num_sms ? kNdRowsPerTask : 8;
+  };
   std::vector<std::vector<NdTask>> fd(F.levels), fu(F.levels), bu(F.levels), bd(F.levels);
   for (int s = 0; s < ns; ++s) {
     const int lv = F.sn[s].level;
