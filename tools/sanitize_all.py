@@ -17,6 +17,9 @@ cases = [
     dict(k=12, order=3, coarse_solve="amg"),              # AMG K-cycles
     dict(k=6, order=2, variant="on_the_fly"),             # low-order kernel, on-the-fly geometry
     dict(k=4, order=5, family="distorted_elements", bitwise_reference=True),
+    dict(k=12, order=7),                                  # TMA-staged combine over many full tiles, gather order
+    dict(k=9, order=2, coarse_solve="amg"),               # 256-node combine tiles
+    dict(k=10, order=4, coarse_sms=16),                   # coarse solve on a green-context SM partition
 ]
 for c in cases:
     c = dict(c)
