@@ -361,10 +361,15 @@ __global__ void __launch_bounds__(kGatherBlock, COMBINE_MIN_BLOCKS) combine_prol
 // average), 256 below (up to 10 per node at order 2), so a tile's segment
 // fits the 3072-entry stage (measured: order 3 at 256 nodes 0.394 ms, at 512
 // 0.366 ms with a few tiles over the cap reading global memory).
-constexpr int kCombZcap = 3072, kCombBlock = 256, kCombTileMax = 512;
+#ifndef COMB_BLOCK
+#define COMB_BLOCK 256
+#endif
+constexpr int kCombZcap = 3072, kCombTileMax = 512;
 template <int NP>
 struct CombTile {
   static constexpr int value = NP <= 3 ? 256 : 512;
+  static constexpr int block = COMB_BLOCK < value ? COMB_BLOCK : value;   // threads per CTA
+  static constexpr int minb = block >= 512 ? 2 : 3;                       // resident CTAs per SM
 };
 template <int T>
 struct CombStage {
@@ -378,9 +383,9 @@ template <int T>
 constexpr int comb_smem() { return 2 * static_cast<int>(sizeof(CombStage<T>)); }
 
 template <int NP>
-__global__ void __launch_bounds__(kCombBlock, 3) combine_tma_kernel(CombineProlongArgs a, int ntiles, int ntma)
+__global__ void __launch_bounds__(CombTile<NP>::block, CombTile<NP>::minb) combine_tma_kernel(CombineProlongArgs a, int ntiles, int ntma)
 {
-  constexpr int kCombTile = CombTile<NP>::value;
+  constexpr int kCombTile = CombTile<NP>::value, kCombBlock = CombTile<NP>::block;
   using CombStageT = CombStage<kCombTile>;
   constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1);
   constexpr int NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2), NSP = (NS + 3) & ~3;

@@ -581,6 +581,7 @@ void launch_combine_np(Plan& pl, double* zr_result, cudaStream_t s, bool do_fine
     const long long span = static_cast<long long>(a.N) + 1 - kCombTile - 4;  // last in-bounds tile start
     const long long ntma = span < 0 ? 0 : span / kCombTile + 1;
     int per_sm = 0;
+    constexpr int kCombBlock = CombTile<NP>::block;
     HXB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, combine_tma_kernel<NP>, kCombBlock, kCombSmem));
     const int grid = static_cast<int>(std::max(1LL, std::min<long long>(ntiles, 1LL * std::max(per_sm, 1) * pl.num_sms)));
     combine_tma_kernel<NP><<<grid, kCombBlock, kCombSmem, s>>>(a, static_cast<int>(ntiles),
