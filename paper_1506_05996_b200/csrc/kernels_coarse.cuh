@@ -30,14 +30,20 @@ constexpr double kJacobiOmega = 2.0 / 3.0;  // amg.cpp:44
 // reference's l-loop at rounding level only). Measured against the line-per-
 // lane traversal it replaced (strided interior loads, 35 % of HBM): see
 // DESIGN.md section 7.
+#ifndef RESTRICT_MINB
+#define RESTRICT_MINB 4
+#endif
+#ifndef RESTRICT_US
+#define RESTRICT_US 4
+#endif
 template <int NP>
-__global__ void __launch_bounds__(256, 4) restrict_cw_kernel(const double* __restrict__ r, const int* __restrict__ smap,
+__global__ void __launch_bounds__(256, RESTRICT_MINB) restrict_cw_kernel(const double* __restrict__ r, const int* __restrict__ smap,
                                                           const double* __restrict__ cw, double* __restrict__ Rpart,
                                                           int ne, int sstride, int nsurfp, int nsg,
                                                           const int* __restrict__ order)
 {
   constexpr int n = NP - 1, NI = (n - 1) * (n - 1) * (n - 1), NS = NP * NP * NP - (NP - 2) * (NP - 2) * (NP - 2);
-  constexpr int US = NP == 7 ? 3 : 4;  // loads in flight per lane (NP = 7 spills at 4)
+  constexpr int US = NP == 7 && RESTRICT_US > 3 && RESTRICT_MINB >= 4 ? 3 : RESTRICT_US;  // loads in flight per lane (NP = 7 spills at 4)
   __shared__ double h0[NP], h1[NP];
   // local (i, j, k) of every surface slot and element-interior index, packed i | j << 4 | k << 8
   __shared__ unsigned short lut_surf[NS], lut_int[NI > 0 ? NI : 1];
