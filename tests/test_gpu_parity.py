@@ -486,3 +486,5 @@ def test_sm_partition_is_bitwise_neutral():
     assert a["iterations"] == b["iterations"]
     assert np.array_equal(a["residual_history"], b["residual_history"])
     assert np.array_equal(a["u"], b["u"])
+    # a partition that leaves nothing for the fine solves is declined (shared SMs)
+    assert hx.Plan(mesh, 5, coarse_sms=1000).coarse_sms == 0
